@@ -1,0 +1,445 @@
+"""Benchmark: PointCNN++ MVMR conv layer forward + backward on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--workload ns|batch64] [--math auto|exact|bf16]
+
+A step = one conv layer forward + backward (dgrad + wgrad) over the cached
+neighbor structure (the PointConvOp cache hit, conv_op.hpp:109-111) on the
+synthetic north-star cloud: 1M uniform points in the unit cube (seed 1+rank),
+r = 1.8 N^(-1/3), t = 3 (27 cells), C_in = C_out = 64, fp32 tensors
+(SURVEY.md §8d).  Multi-GPU (torchrun): every rank owns whole clouds of the
+batch (weak scaling, one 1M cloud per GPU for `ns`; `batch64` shards 64
+scenes x 250K points, strong scaling) and the weight gradient is summed with
+one NCCL all-reduce per step.  Inputs (F_in 256 MB, G_out
+256 MB) exceed the 126 MB L2, so no flush is needed between steps.
+
+Prints ONE JSON line on rank 0 (contract in the task statement).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "MVMR conv fwd+bwd Mpoints/s (C=64, 27 cells), % of roofline; peak memory GB"
+N_POINTS = 1_000_000
+C = 64
+T_RES = 3
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=10)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--workload", default="ns", choices=["ns", "batch64"])
+    p.add_argument("--math", default="auto", choices=["auto", "exact", "bf16"])
+    p.add_argument("--points", type=int, default=N_POINTS)
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile-out", default="")
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        d = json.load(open(path))
+        return d["hbm_gbs"], d["bf16_tflops"], d.get("bf16_tflops_sustained", d["bf16_tflops"]), "measured"
+    return 6650.0, 1590.0, 1400.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.rows = []
+        self.proc = None
+        self.t = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            return
+        self.t = threading.Thread(target=self._read, daemon=True)
+        self.t.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self, t0=None, t1=None):
+        rows = [r for ts, r in self.rows if (t0 is None or ts >= t0 - 0.06) and (t1 is None or ts <= t1 + 0.06)]
+        if not rows:
+            rows = [r for _, r in self.rows]
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            parts = [x.strip() for x in r.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def algorithmic(n_out, n_in, n_t, cin, cout, K):
+    """bytes per pass and flops per pass (fp32 API, u32 SoA triplets)."""
+    b_pass = 4 * (n_in * cin + n_out * cout) + 12 * n_t + 4 * K * cin * cout
+    f_pass = 2 * n_t * cin * cout
+    return b_pass, f_pass
+
+
+# ---------------------------------------------------------------------------
+# reference arm: the reference CPU implementation (oracle/_ref) on host cores
+# ---------------------------------------------------------------------------
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle import Oracle, Reference, reference_available
+    orc = Oracle()
+    if reference_available():
+        impl, kind = Reference(), "reference"
+    else:
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libnpref.so not built"}))
+        return
+    cores = impl.hardware_concurrency()
+    n = 250_000  # bounded sample of the workload per step (same density / neighbor count)
+    xyz = orc.gen_uniform_cube(n, 1.0, 1)
+    r = 1.8 * n ** (-1 / 3)
+    w = orc.make_weights(T_RES, 1, C, C, 2)
+    f = orc.gen_features(n, 1, C, 3)
+    g = orc.gen_features(n, 1, C, 4)
+    times, cache, _ = impl.conv_layer_f32(xyz, r, T_RES, w, f, g, workers=cores, build=True)
+    build_s = float(times[0] + times[1])
+    per = []
+    for s in range(args.warmup + args.steps):
+        times, cache, _ = impl.conv_layer_f32(xyz, r, T_RES, w, f, g, workers=cores, build=False,
+                                              cache=cache)
+        if s >= args.warmup:
+            per.append(float(times[2] + times[3] + times[4]))
+    impl.free_cache(cache)
+    ms = 1e3 * statistics.mean(per)
+    value = n / (ms / 1e3) / 1e6
+    out = {
+        "metric": METRIC, "value": round(value, 4), "unit": "Mpoints/s", "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (gen_uniform_cube seed 1, gen_features seeds 3/4, make_weights seed 2)",
+        "impl": "reference",
+        "config": {"workload": f"{args.workload}: reference CPU fwd+bwd (mvmr + mvmr_transposed"
+                               " + vvor, cached sorted triplets)", "points_per_step": n,
+                   "c_in": C, "c_out": C, "kernel_cells": 27, "radius": r,
+                   "exec": "grouped L=128 deterministic=false"},
+        "cpu_baseline": {"value": round(value, 4), "unit": "Mpoints/s", "cores": cores,
+                         "kind": kind,
+                         "sample": f"{n}-point uniform cloud per step (bounded sample of the 1M "
+                                   f"workload, same r*N^(1/3)); neighbor build {build_s:.2f}s "
+                                   "(1 thread, excluded like the GPU arm's cached structure)"},
+        "e2e": {"value": round(value, 4), "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+
+
+def cpu_baseline_sample():
+    """Reference CPU chain on a bounded sample (c2: 100K points, C=64), rank 0, N=1."""
+    from oracle import Oracle, Reference, reference_available
+    orc = Oracle()
+    if not reference_available():
+        return None
+    ref = Reference()
+    cores = ref.hardware_concurrency()
+    n = 100_000
+    xyz = orc.gen_uniform_cube(n, 1.0, 1)
+    r = 1.8 * n ** (-1 / 3)
+    w = orc.make_weights(T_RES, 1, C, C, 2)
+    f = orc.gen_features(n, 1, C, 3)
+    g = orc.gen_features(n, 1, C, 4)
+    times, cache, _ = ref.conv_layer_f32(xyz, r, T_RES, w, f, g, workers=cores, build=True)
+    build = float(times[0] + times[1])
+    per = []
+    for _ in range(4):
+        times, cache, _ = ref.conv_layer_f32(xyz, r, T_RES, w, f, g, workers=cores, build=False,
+                                             cache=cache)
+        per.append(float(times[2] + times[3] + times[4]))
+    ref.free_cache(cache)
+    s = statistics.median(per[1:])
+    return {"value": round(n / s / 1e6, 4), "unit": "Mpoints/s", "cores": cores,
+            "kind": "reference",
+            "sample": f"100K-point uniform cloud (BASELINE config 2), C=64, fwd+dgrad+wgrad, "
+                      f"median of 3 after 1 warm-up; neighbor build+sort {build:.2f}s on 1 thread"}
+
+
+# ---------------------------------------------------------------------------
+# our arm
+# ---------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from oracle import Oracle
+    from paper_2511_23227_b200 import npconv as npc
+    from paper_2511_23227_b200 import shard
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    orc = Oracle()
+    math = {"auto": npc.Math.auto, "exact": npc.Math.exact, "bf16": npc.Math.bf16}[args.math]
+    cfg = npc.ExecConfig(math=math)
+
+    # ---- this rank's scenes
+    if args.workload == "ns":
+        n_pts = args.points
+        scenes = [rank]          # one 1M cloud per GPU, seed 1 + rank
+        scaling = "weak"
+    else:
+        n_pts = 250_000
+        a, b = shard.scene_range(64, rank, world)
+        scenes = list(range(a, b))
+        scaling = "strong"
+    r = 1.8 * n_pts ** (-1 / 3)
+    w = torch.from_numpy(orc.make_weights(T_RES, 1, C, C, 2)).to(dev)
+    ctx = npc.context(local)
+    data = []
+    n_t_total = 0
+    t_build = []
+    for s in scenes:
+        xyz = orc.gen_uniform_cube(n_pts, 1.0, 1 + s)
+        cl = npc.make_point_cloud(xyz, device=dev)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        nb = npc.build_neighbors(cl, cl, npc.ConvGeometry(radius=r, t=T_RES))
+        nb.prepare(math)
+        torch.cuda.synchronize()
+        t_build.append(time.perf_counter() - t0)
+        f = torch.from_numpy(orc.gen_features(n_pts, 1, C, 3 + 100 * s)).to(dev)
+        g = torch.from_numpy(orc.gen_features(n_pts, 1, C, 4 + 100 * s)).to(dev)
+        fo = torch.empty((n_pts, 1, C), device=dev)
+        gi = torch.empty((n_pts, 1, C), device=dev)
+        gw = torch.empty((27, 1, C, C), device=dev)
+        data.append((cl, nb, f, g, fo, gi, gw))
+        n_t_total += nb.size
+    gw_sum = torch.zeros((27, 1, C, C), device=dev)
+
+    def step():
+        gw_sum.zero_()
+        for (cl, nb, f, g, fo, gi, gw) in data:
+            npc.conv_forward(nb, w, f, cfg, out=fo)
+            npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw)
+            gw_sum.add_(gw)
+        if world > 1:
+            shard.allreduce_weight_grad(gw_sum)
+
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ctx.profile_reset()
+    ctx.profile(True)
+    launches0 = ctx.launch_count()
+    npc.context(local).reset_peak()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
+    e0.record()
+    for _ in range(args.steps):
+        step()
+    e1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    wall1 = time.time()
+    ms = e0.elapsed_time(e1) / args.steps
+    launches = ctx.launch_count() - launches0
+    prof = ctx.profile_dump()
+    ctx.profile(False)
+    _, peak_bytes = ctx.memory()
+    peak_torch = torch.cuda.max_memory_allocated(dev)
+    t_ms = torch.tensor([ms], device=dev, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t_ms, op=dist.ReduceOp.MAX)
+    ms = float(t_ms.item())
+    n_points_total = n_pts * len(scenes) * (world if args.workload == "ns" else 1)
+    if args.workload == "batch64":
+        n_points_total = n_pts * 64
+    value = n_points_total / (ms / 1e3) / 1e6
+
+    # ---- e2e: the same step through the public API with pinned host buffers
+    e2e = None
+    if not args.no_e2e:
+        hf = [torch.empty_like(d[2], device="cpu").pin_memory().copy_(d[2]) for d in data]
+        hg = [torch.empty_like(d[3], device="cpu").pin_memory().copy_(d[3]) for d in data]
+        ho = [torch.empty_like(d[4], device="cpu").pin_memory() for d in data]
+        hi = [torch.empty_like(d[5], device="cpu").pin_memory() for d in data]
+        hw = torch.empty_like(gw_sum, device="cpu").pin_memory()
+
+        def step_e2e():
+            gw_sum.zero_()
+            for s_, (cl, nb, f, g, fo, gi, gw) in enumerate(data):
+                f.copy_(hf[s_], non_blocking=True)
+                g.copy_(hg[s_], non_blocking=True)
+                npc.conv_forward(nb, w, f, cfg, out=fo)
+                npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw)
+                gw_sum.add_(gw)
+                ho[s_].copy_(fo, non_blocking=True)
+                hi[s_].copy_(gi, non_blocking=True)
+            if world > 1:
+                shard.allreduce_weight_grad(gw_sum)
+            hw.copy_(gw_sum, non_blocking=True)
+
+        for _ in range(max(1, args.warmup)):
+            step_e2e()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(args.steps):
+            step_e2e()
+        a1.record()
+        torch.cuda.synchronize()
+        ems = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(ems, op=dist.ReduceOp.MAX)
+        h2d = sum(x.numel() * 4 for x in hf + hg)
+        d2h = sum(x.numel() * 4 for x in ho + hi) + hw.numel() * 4
+        e2e = {"value": round(n_points_total / (float(ems.item()) / 1e3) / 1e6, 3),
+               "unit": "Mpoints/s", "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "ms_per_step": round(float(ems.item()), 4)}
+    if rank == 0:
+        sampler.stop()
+    clocks = sampler.summary(wall0, wall1) if rank == 0 else None
+
+    if world > 1:
+        dist.barrier()
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant kernel (one launch = one pass over one cloud)
+    hbm, bf16_burst, bf16_sus, peak_kind = peaks()
+    n_t = data[0][1].size
+    b_pass, f_pass = algorithmic(n_pts, n_pts, n_t, C, C, 27)
+    top = max(prof.items(), key=lambda kv: kv[1][1]) if prof else ("none", (1, 0.0))
+    name, (cnt, tot) = top
+    per_launch_ms = tot / max(cnt, 1)
+    share = tot / max(sum(v[1] for v in prof.values()), 1e-9)
+    # passes per launch: tc kernels fuse (fwd: 1 pass, bwd: 2 passes)
+    passes = 2 if "bwd" in name else 1
+    if "tc" in name or "umma" in name:
+        achieved = passes * f_pass / (per_launch_ms / 1e3) / 1e12
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": bf16_sus,
+                "unit": "TFLOP/s", "frac": round(achieved / bf16_sus, 4), "traffic": None,
+                "kernel": name, "peak_kind": f"{peak_kind} bf16 sustained",
+                "algorithmic_flop_per_launch": passes * f_pass,
+                "launch_ms": round(per_launch_ms, 4), "share_of_step": round(share, 3)}
+    else:
+        achieved = passes * b_pass / (per_launch_ms / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                "frac": round(achieved / hbm, 4), "traffic": None, "kernel": name,
+                "peak_kind": f"{peak_kind} copy bandwidth",
+                "algorithmic_bytes_per_launch": passes * b_pass,
+                "launch_ms": round(per_launch_ms, 4), "share_of_step": round(share, 3)}
+    # layer-level fractions: both the HBM and tensor views
+    layer_bytes = 3 * b_pass * len(scenes)
+    layer_flops = 3 * f_pass * len(scenes)
+    layer = {"hbm_frac": round(layer_bytes / (ms / 1e3) / 1e9 / hbm, 4),
+             "tensor_frac": round(layer_flops / (ms / 1e3) / 1e12 / bf16_sus, 4),
+             "algorithmic_bytes_per_step": layer_bytes, "algorithmic_flop_per_step": layer_flops}
+
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_sample()
+    dtype = {"auto": "bf16-operand/fp32-accumulate (tcgen05) where supported, else f32",
+             "exact": "f32", "bf16": "bf16-operand/fp32-accumulate (tcgen05)"}[args.math]
+    out = {
+        "metric": METRIC, "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
+        "higher_is_better": True, "scaling": scaling, "vs_baseline": None, "dtype": dtype,
+        "data": "synthetic: gen_uniform_cube (seed 1+scene), features U[-1,1) (seeds 3/4+100s), "
+                "make_weights seed 2",
+        "config": {"workload": ("ns: one 1M-point uniform cloud per GPU, conv layer fwd+bwd "
+                                "(north-star instance)") if args.workload == "ns" else
+                   "batch64: 64 scenes x 250K points sharded across GPUs (config 5)",
+                   "points_per_gpu": n_pts * len(scenes), "triplets_per_gpu": n_t_total,
+                   "c_in": C, "c_out": C, "kernel_cells": 27, "radius": r, "math": args.math,
+                   "parallelism": f"dp{world} (whole clouds per GPU, NCCL dW all-reduce)",
+                   "l2": "inputs (F_in/G_out 256 MB each) exceed the 126 MB L2; no flush",
+                   "neighbor_build_s": round(statistics.mean(t_build), 4)},
+        "roofline": roof,
+        "layer_roofline": layer,
+        "peak_memory_gb": round(max(peak_bytes, peak_torch) / 1e9, 3),
+        "gpu_launches": int(launches),
+        "kernels": {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in prof.items()},
+        "clocks": clocks,
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+    }
+    print(json.dumps(out))
+    if args.profile_out:
+        with open(args.profile_out, "w") as fh:
+            json.dump(out, fh, indent=1)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

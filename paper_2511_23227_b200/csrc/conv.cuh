@@ -1,0 +1,29 @@
+// conv.cuh -- engine entry points shared by the C ABI (api.cu).
+#pragma once
+
+#include "neighbors.cuh"
+
+namespace npcg {
+
+// ---- exact engines (conv_simt.cu) -----------------------------------------
+template <typename T>
+void mvmr_rows(npcg_context* ctx, const CsrView& csr, const T* w, const T* fin, int G, int cin,
+               int cout, T* out);
+template <typename T>
+void transpose_w(npcg_context* ctx, const T* w, int64_t KG, int cin, int cout, T* wt);
+template <typename T>
+void vvor_cells(npcg_context* ctx, const CellPlan& cells, const T* gout, const T* fin, int G,
+                int cin, int cout, T* grad);
+
+// ---- tensor-core engines (conv_tc.cu) --------------------------------------
+// True when the tcgen05 path handles this shape.
+bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t n_kernels);
+// Forward / input-gradient / weight-gradient over a neighbor handle with
+// bf16 operands and fp32 accumulation.  Builds and caches the tile plans.
+void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
+                float* fout);
+void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
+                 const float* gout, float* grad_in, float* grad_w);
+void tc_prepare(npcg_context* ctx, npcg_neighbors* nb);
+
+}  // namespace npcg

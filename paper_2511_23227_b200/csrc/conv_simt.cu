@@ -1,0 +1,228 @@
+// conv_simt.cu -- exact-arithmetic MVMR / VVOR engines on CUDA cores.
+//
+// These run in the API dtype (fp32 or fp64, FMA accumulation) for every
+// shape the reference accepts (any G, C_in, C_out, t).  They are the
+// NPCG_MATH_EXACT path and the narrow-channel path of the north star.
+//
+//   mvmr            engine.cpp:444-455 -> output-stationary: one warp per
+//                   (output row, group), lanes own output channels, the
+//                   row's neighbor entries are walked in CSR order and
+//                   reduced in registers; one plain store per output value
+//                   (no atomics, deterministic).
+//   mvmr_transposed engine.cpp:457-473 -> the same kernel over the
+//                   transposed CSR (rows = input points) with W^T.
+//   vvor            vvor.cpp:102-271 -> per kernel cell, chunks of the cell's
+//                   entries accumulate dW_k tiles in registers (rows staged
+//                   in shared memory); chunk partials are summed in a fixed
+//                   order by a second kernel (deterministic, no atomics).
+#include "neighbors.cuh"
+#include "conv.cuh"
+
+namespace npcg {
+
+// ---------------------------------------------------------------------------
+// mvmr rows
+// ---------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(256) k_mvmr_rows(CsrView csr, const T* __restrict__ w,
+                                                   const T* __restrict__ fin, int G, int cin,
+                                                   int cout, int m_base,
+                                                   T* __restrict__ out) {
+  const int64_t warp = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (warp >= csr.n_rows * G) return;
+  const int64_t row = warp / G;
+  const int g = static_cast<int>(warp - row * G);
+  T acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = T(0);
+  const int64_t e0 = csr.row_ptr[row], e1 = csr.row_ptr[row + 1];
+  for (int64_t e = e0; e < e1; ++e) {
+    const int64_t j = csr.col[e];
+    const int64_t k = csr.k[e];
+    const T* f = fin + (j * G + g) * cin;
+    const T* wm = w + ((k * G + g) * cin) * cout + m_base;
+    for (int c0 = 0; c0 < cin; c0 += 32) {
+      const T fv = (c0 + lane < cin) ? f[c0 + lane] : T(0);
+      const int cn = cin - c0 < 32 ? cin - c0 : 32;
+      for (int cc = 0; cc < cn; ++cc) {
+        const T fc = __shfl_sync(0xffffffffu, fv, cc);
+        const T* wr = wm + static_cast<int64_t>(c0 + cc) * cout;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int m = lane + 32 * r;
+          if (m_base + m < cout) acc[r] = fma(wr[m], fc, acc[r]);
+        }
+      }
+    }
+  }
+  T* o = out + (row * G + g) * cout + m_base;
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int m = lane + 32 * r;
+    if (m_base + m < cout) o[m] = acc[r];
+  }
+}
+
+template <typename T>
+void mvmr_rows(npcg_context* ctx, const CsrView& csr, const T* w, const T* fin, int G, int cin,
+               int cout, T* out) {
+  if (csr.n_rows == 0) return;
+  const unsigned blocks = static_cast<unsigned>(ceil_div(csr.n_rows * G * 32, 256));
+  for (int m_base = 0; m_base < cout; m_base += 256) {
+    const int rem = cout - m_base;
+    if (rem <= 32)
+      launch(ctx, "mvmr_simt", k_mvmr_rows<T, 1>, dim3(blocks), dim3(256), 0, csr, w, fin, G, cin,
+             cout, m_base, out);
+    else if (rem <= 64)
+      launch(ctx, "mvmr_simt", k_mvmr_rows<T, 2>, dim3(blocks), dim3(256), 0, csr, w, fin, G, cin,
+             cout, m_base, out);
+    else if (rem <= 128)
+      launch(ctx, "mvmr_simt", k_mvmr_rows<T, 4>, dim3(blocks), dim3(256), 0, csr, w, fin, G, cin,
+             cout, m_base, out);
+    else
+      launch(ctx, "mvmr_simt", k_mvmr_rows<T, 8>, dim3(blocks), dim3(256), 0, csr, w, fin, G, cin,
+             cout, m_base, out);
+  }
+}
+
+// W (K, G, Cin, Cout) -> W^T (K, G, Cout, Cin)  (tensors.hpp:113-123 transposed())
+template <typename T>
+__global__ void k_transpose_w(const T* __restrict__ w, int64_t KG, int cin, int cout,
+                              T* __restrict__ wt) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t per = static_cast<int64_t>(cin) * cout;
+  if (p >= KG * per) return;
+  const int64_t kg = p / per, r = p - kg * per;
+  const int c = static_cast<int>(r / cout), m = static_cast<int>(r - static_cast<int64_t>(c) * cout);
+  wt[kg * per + static_cast<int64_t>(m) * cin + c] = w[p];
+}
+
+template <typename T>
+void transpose_w(npcg_context* ctx, const T* w, int64_t KG, int cin, int cout, T* wt) {
+  const int64_t n = KG * cin * cout;
+  launch(ctx, "transpose_w", k_transpose_w<T>, dim3(static_cast<unsigned>(ceil_div(n, 256))),
+         dim3(256), 0, w, KG, cin, cout, wt);
+}
+
+// ---------------------------------------------------------------------------
+// vvor: per-cell chunk partials + fixed-order reduction
+// ---------------------------------------------------------------------------
+constexpr int kVvorThreads = 256;
+constexpr int kVvorOutsPerThread = 16;
+constexpr int kVvorOutsPerBlock = kVvorThreads * kVvorOutsPerThread;
+
+template <typename T>
+__global__ void __launch_bounds__(kVvorThreads)
+    k_vvor_chunks(const uint32_t* __restrict__ ci, const uint32_t* __restrict__ cj,
+                  const int64_t* __restrict__ chunk_begin, const int64_t* __restrict__ chunk_end,
+                  const T* __restrict__ gout, const T* __restrict__ fin, int G, int cin,
+                  int cout, int rows_per_batch, T* __restrict__ partial) {
+  extern __shared__ unsigned char smem_raw[];
+  T* gs = reinterpret_cast<T*>(smem_raw);          // [rows][cout]
+  T* fs = gs + static_cast<int64_t>(rows_per_batch) * cout;  // [rows][cin]
+  const int64_t chunk = blockIdx.x;
+  const int g = blockIdx.y;
+  const int64_t o_base = static_cast<int64_t>(blockIdx.z) * kVvorOutsPerBlock;
+  const int64_t per = static_cast<int64_t>(cout) * cin;
+  const int64_t b0 = chunk_begin[chunk], b1 = chunk_end[chunk];
+  T acc[kVvorOutsPerThread];
+  int om[kVvorOutsPerThread], oc[kVvorOutsPerThread];
+#pragma unroll
+  for (int s = 0; s < kVvorOutsPerThread; ++s) {
+    acc[s] = T(0);
+    const int64_t o = o_base + threadIdx.x + static_cast<int64_t>(s) * kVvorThreads;
+    om[s] = o < per ? static_cast<int>(o / cin) : -1;
+    oc[s] = o < per ? static_cast<int>(o % cin) : 0;
+  }
+  for (int64_t e0 = b0; e0 < b1; e0 += rows_per_batch) {
+    const int nr = static_cast<int>(b1 - e0 < rows_per_batch ? b1 - e0 : rows_per_batch);
+    __syncthreads();
+    for (int x = threadIdx.x; x < nr * cout; x += blockDim.x) {
+      const int r = x / cout, m = x - r * cout;
+      gs[x] = gout[(static_cast<int64_t>(ci[e0 + r]) * G + g) * cout + m];
+    }
+    for (int x = threadIdx.x; x < nr * cin; x += blockDim.x) {
+      const int r = x / cin, c = x - r * cin;
+      fs[x] = fin[(static_cast<int64_t>(cj[e0 + r]) * G + g) * cin + c];
+    }
+    __syncthreads();
+    for (int r = 0; r < nr; ++r) {
+#pragma unroll
+      for (int s = 0; s < kVvorOutsPerThread; ++s)
+        if (om[s] >= 0) acc[s] = fma(gs[r * cout + om[s]], fs[r * cin + oc[s]], acc[s]);
+    }
+  }
+  T* p = partial + (chunk * G + g) * per;
+#pragma unroll
+  for (int s = 0; s < kVvorOutsPerThread; ++s) {
+    const int64_t o = o_base + threadIdx.x + static_cast<int64_t>(s) * kVvorThreads;
+    if (o < per) p[o] = acc[s];
+  }
+}
+
+// grad[k][g][o] = sum over chunks c of cell k (ascending) of partial[c][g][o]
+template <typename T>
+__global__ void k_vvor_reduce(const T* __restrict__ partial, const int64_t* __restrict__ kc_ptr,
+                              int64_t K, int G, int64_t per, T* __restrict__ grad) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p >= K * G * per) return;
+  const int64_t k = p / (G * per), rem = p - k * G * per;
+  T s = T(0);
+  for (int64_t c = kc_ptr[k]; c < kc_ptr[k + 1]; ++c) s += partial[c * G * per + rem];
+  grad[p] = s;
+}
+
+template <typename T>
+void vvor_cells(npcg_context* ctx, const CellPlan& cells, const T* gout, const T* fin, int G,
+                int cin, int cout, T* grad) {
+  const int64_t K = cells.n_kernels;
+  const int64_t per = static_cast<int64_t>(cout) * cin;
+  const int64_t chunk_len = 4096;
+  std::vector<int64_t> cb, ce, kc(K + 1, 0);
+  for (int64_t k = 0; k < K; ++k) {
+    kc[k] = static_cast<int64_t>(cb.size());
+    for (int64_t s = cells.k_ptr_host[k]; s < cells.k_ptr_host[k + 1]; s += chunk_len) {
+      cb.push_back(s);
+      ce.push_back(std::min(cells.k_ptr_host[k + 1], s + chunk_len));
+    }
+  }
+  kc[K] = static_cast<int64_t>(cb.size());
+  const int64_t nch = static_cast<int64_t>(cb.size());
+  const int64_t total = K * G * per;
+  if (nch == 0) {
+    NPCG_CUDA(cudaMemsetAsync(grad, 0, total * sizeof(T), ctx->stream));
+    return;
+  }
+  DevBuf<int64_t> d_cb(ctx, nch), d_ce(ctx, nch), d_kc(ctx, K + 1);
+  NPCG_CUDA(cudaMemcpyAsync(d_cb.get(), cb.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
+  NPCG_CUDA(cudaMemcpyAsync(d_ce.get(), ce.data(), nch * 8, cudaMemcpyHostToDevice, ctx->stream));
+  NPCG_CUDA(cudaMemcpyAsync(d_kc.get(), kc.data(), (K + 1) * 8, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  DevBuf<T> partial(ctx, nch * G * per);
+  int rows = static_cast<int>(48 * 1024 / ((cin + cout) * sizeof(T)));
+  rows = rows < 1 ? 1 : (rows > 32 ? 32 : rows);
+  const size_t smem = static_cast<size_t>(rows) * (cin + cout) * sizeof(T);
+  const unsigned oz = static_cast<unsigned>(ceil_div(per, kVvorOutsPerBlock));
+  launch(ctx, "vvor_simt", k_vvor_chunks<T>,
+         dim3(static_cast<unsigned>(nch), static_cast<unsigned>(G), oz), dim3(kVvorThreads), smem,
+         cells.i.get(), cells.j.get(), static_cast<const int64_t*>(d_cb.get()),
+         static_cast<const int64_t*>(d_ce.get()), gout, fin, G, cin, cout, rows, partial.get());
+  launch(ctx, "vvor_reduce", k_vvor_reduce<T>, dim3(static_cast<unsigned>(ceil_div(total, 256))),
+         dim3(256), 0, static_cast<const T*>(partial.get()),
+         static_cast<const int64_t*>(d_kc.get()), K, G, per, grad);
+}
+
+// explicit instantiations
+template void mvmr_rows<float>(npcg_context*, const CsrView&, const float*, const float*, int,
+                               int, int, float*);
+template void mvmr_rows<double>(npcg_context*, const CsrView&, const double*, const double*, int,
+                                int, int, double*);
+template void transpose_w<float>(npcg_context*, const float*, int64_t, int, int, float*);
+template void transpose_w<double>(npcg_context*, const double*, int64_t, int, int, double*);
+template void vvor_cells<float>(npcg_context*, const CellPlan&, const float*, const float*, int,
+                                int, int, float*);
+template void vvor_cells<double>(npcg_context*, const CellPlan&, const double*, const double*,
+                                 int, int, int, double*);
+
+}  // namespace npcg

@@ -1,0 +1,229 @@
+"""GPU parity: neighbor build + kernel-cell assignment + triplet ordering.
+
+Bar: byte-equality with the reference (golden fixtures from the unmodified
+reference, the C oracle, and oracle/_ref when present) -- i, j, k arrays in the
+reference's exact emission order."""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def _cloud(npc, xyz, off=None):
+    return npc.make_point_cloud(np.asarray(xyz, dtype=np.float64), off)
+
+
+def _eq(a, b):
+    return all(np.array_equal(np.asarray(p), np.asarray(q)) for p, q in zip(a, b))
+
+
+def test_known_answers(npc, golden):
+    h = golden("golden_hand.json")
+    c = h["radius_collinear"]
+    cl = _cloud(npc, c["xyz"])
+    nl = npc.radius_search(cl, cl, c["radius"])
+    got = list(zip(nl.out_index.cpu().tolist(), nl.in_index.cpu().tolist()))
+    assert [list(p) for p in got] == c["pairs"]
+    assert nl.radius == 1.5
+    cb = h["closed_ball"]
+    assert npc.radius_search(_cloud(npc, cb["q"]), _cloud(npc, cb["t"]), 1.0).size() == 1
+    bi = h["batch_isolation"]
+    cl = _cloud(npc, bi["xyz"], bi["offsets"])
+    nl = npc.radius_search(cl, cl, 1.0)
+    got = [[a, b] for a, b in zip(nl.out_index.cpu().tolist(), nl.in_index.cpu().tolist())]
+    assert got == bi["pairs"]
+    for center, nbr, r, t, k in h["kernel_index"]["cases"]:
+        assert npc.local_voxel_kernel_index(center, nbr, r, t) == k
+
+
+def test_edge_cases(npc):
+    one = _cloud(npc, [[5, 5, 5]])
+    nl = npc.radius_search(one, one, 0.001)
+    assert nl.size() == 1 and nl.out_index.item() == 0 and nl.in_index.item() == 0
+    assert npc.radius_search(_cloud(npc, [[0, 0, 0]]), _cloud(npc, [[10, 0, 0]]), 1.0).size() == 0
+    empty = _cloud(npc, np.zeros((0, 3)))
+    assert npc.radius_search(empty, one, 1.0).size() == 0
+    assert npc.radius_search(one, empty, 1.0).size() == 0
+    with pytest.raises(npc.RadiusError):
+        npc.radius_search(one, one, 0.0)
+    with pytest.raises(npc.RadiusError):
+        npc.radius_search(one, one, -1.0)
+    two = _cloud(npc, [[0, 0, 0], [1, 1, 1]], [0, 1, 2])
+    with pytest.raises(npc.ShapeError):
+        npc.radius_search(two, one, 1.0)
+    g = npc.ConvGeometry(radius=1.5, t=2)
+    with pytest.raises(npc.ShapeError):
+        npc.build_triplets_native(one, one, g)
+    with pytest.raises(npc.RadiusError):
+        npc.build_triplets_native(one, one, npc.ConvGeometry(radius=0.0, t=3))
+    with pytest.raises(npc.ShapeError):
+        npc.local_voxel_kernel_index([0, 0, 0], [0, 0, 0], 1.0, 4)
+    tl = npc.build_triplets_native(empty, empty, npc.ConvGeometry(radius=1.5, t=3))
+    assert tl.size() == 0 and tl.n_kernels == 27
+
+
+def test_tiny_native_builds(npc):
+    g = npc.ConvGeometry(radius=1.5, t=3)
+    one = _cloud(npc, [[0, 0, 0]])
+    tl = npc.build_triplets_native(one, one, g)
+    i, j, k = tl.numpy()
+    assert list(i) == [0] and list(j) == [0] and list(k) == [13] and tl.sort_axis == 0
+    col = _cloud(npc, [[0, 0, 0], [1, 0, 0], [2, 0, 0]])
+    i, j, k = npc.build_triplets_native(col, col, g).numpy()
+    assert len(i) == 7
+    assert k[[n for n in range(7) if i[n] == 1 and j[n] == 0][0]] == 4
+    e = list(zip(i, j))
+    assert e == sorted(e)
+    tl = npc.build_triplets_native(_cloud(npc, [[0, 0, 0], [1, 0, 0]]),
+                                   _cloud(npc, [[0, 0, 0], [1, 0, 0]]),
+                                   npc.ConvGeometry(radius=1.5, t=1))
+    assert tl.n_kernels == 1 and tl.size() == 4 and set(tl.numpy()[2]) == {0}
+    tl = npc.build_triplets_native(one, one, npc.ConvGeometry(radius=1.5, t=5))
+    assert tl.n_kernels == 125 and tl.numpy()[2][0] == 62
+    out = _cloud(npc, [[0.5, 0, 0]])
+    inn = _cloud(npc, [[0, 0, 0], [1, 0, 0], [9, 9, 9]])
+    tl = npc.build_triplets_native(out, inn, g)
+    assert tl.size() == 2 and tl.n_out == 1 and tl.n_in == 3
+
+
+@pytest.mark.parametrize("name", ["geom_uniform_2000.npz", "geom_multibatch.npz"])
+def test_golden_triplets_bit_exact(npc, golden, name):
+    g = golden(name)
+    off = g.get("offsets")
+    cl = _cloud(npc, g["xyz"], off)
+    geom = npc.ConvGeometry(radius=float(g["radius"]), t=int(g["t"]))
+    tl = npc.build_triplets_native(cl, cl, geom)
+    assert _eq(tl.numpy(), (g["i"], g["j"], g["k"]))
+    if "bk_i" in g:
+        s = npc.sort_triplets(tl, npc.SortAxis.by_k)
+        assert _eq(s.numpy(), (g["bk_i"], g["bk_j"], g["bk_k"]))
+        # the operator's cache export is the same by_k list
+        nb = npc.build_neighbors(cl, cl, geom)
+        assert _eq(nb.export_triplets(npc.SortAxis.by_k).numpy(), (g["bk_i"], g["bk_j"], g["bk_k"]))
+
+
+def test_golden_cross_query(npc, golden):
+    g = golden("geom_cross.npz")
+    q, t = _cloud(npc, g["queries"]), _cloud(npc, g["targets"])
+    nl = npc.radius_search(q, t, float(g["radius"]))
+    assert np.array_equal(nl.out_index.cpu().numpy(), g["out_index"])
+    assert np.array_equal(nl.in_index.cpu().numpy(), g["in_index"])
+    tl = npc.build_triplets_native(q, t, npc.ConvGeometry(radius=float(g["radius"]), t=3))
+    assert _eq(tl.numpy(), (g["i"], g["j"], g["k"]))
+
+
+@pytest.mark.parametrize("seed", list(range(1, 13)))
+def test_random_clouds_match_oracle(npc, orc, seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.integers(50, 3000))
+    kind = seed % 3
+    if kind == 0:
+        xyz = orc.gen_uniform_cube(n, float(rng.uniform(0.5, 8.0)), seed)
+    elif kind == 1:
+        xyz = rng.normal(size=(n, 3)) * rng.uniform(0.1, 3.0) + rng.uniform(-5, 5, 3)
+    else:  # grid-snapped: many exact boundary cases
+        v = 2.0 ** -int(rng.integers(1, 5))
+        xyz = (rng.integers(0, 12, size=(n, 3)) + 0.5 * rng.integers(0, 2, size=(n, 3))) * v
+    nb = int(rng.integers(1, 5))
+    cuts = np.sort(rng.integers(0, n + 1, size=nb - 1))
+    off = np.concatenate([[0], cuts, [n]]).astype(np.int64)
+    t = int(rng.choice([1, 3, 5, 7]))
+    scale = np.ptp(xyz) if n > 1 else 1.0
+    r = float(rng.uniform(0.02, 0.15) * scale + 1e-9)
+    if kind == 2:
+        r = float(rng.choice([v, 2 * v, np.sqrt(2) * v, np.sqrt(3) * v, 1.8 * v]))
+    cl = _cloud(npc, xyz, off)
+    tl = npc.build_triplets_native(cl, cl, npc.ConvGeometry(radius=r, t=t))
+    want = orc.build_triplets(xyz, xyz, r, t, off, off)
+    assert _eq(tl.numpy(), want), (seed, n, t, r)
+    for axis in (1, 2, 3):
+        s = npc.sort_triplets(tl, axis)
+        assert _eq(s.numpy(), orc.sort_triplets(*want, axis, n, n, t ** 3)), axis
+
+
+def test_matches_reference_directly(npc, ref):
+    for seed in (3, 4):
+        n = 5000
+        xyz = ref.gen_uniform_cube(n, 1.0, seed)
+        r = 1.8 * n ** (-1 / 3)
+        cl = _cloud(npc, xyz)
+        tl = npc.build_triplets_native(cl, cl, npc.ConvGeometry(radius=r, t=3))
+        assert _eq(tl.numpy(), ref.build_triplets(xyz, xyz, r, 3, axis=0))
+
+
+def test_complete_graph_and_large_rows(npc, orc):
+    xyz = orc.gen_uniform_cube(60, 1.0, 35)
+    cl = _cloud(npc, xyz)
+    nl = npc.radius_search(cl, cl, 10.0)
+    assert nl.size() == 3600
+    oi, ii = orc.radius_search(xyz, xyz, 10.0)
+    assert np.array_equal(nl.out_index.cpu().numpy(), oi)
+    assert np.array_equal(nl.in_index.cpu().numpy(), ii)
+
+
+def test_sort_triplets_stability(npc, golden):
+    s = golden("golden_hand.json")["sort_by_k"]
+    tl = npc.TripletList.from_numpy(s["i"], s["j"], s["k"], 3, 8, 3)
+    o = npc.sort_triplets(tl, npc.SortAxis.by_k)
+    oi, oj, ok = o.numpy()
+    assert list(ok) == s["sorted_k"] and list(oj) == s["sorted_j"] and o.sort_axis == 3
+    assert tl.sort_axis == 0
+    o2 = npc.sort_triplets(o, npc.SortAxis.by_k)
+    assert _eq(o2.numpy(), o.numpy())
+    u = npc.TripletList.from_numpy(s["stab_i"], [9] * 4, s["stab_k"], 4, 10, 2)
+    assert list(npc.sort_triplets(u, npc.SortAxis.by_k).numpy()[0]) == s["stab_sorted_i"]
+    none = npc.sort_triplets(tl, npc.SortAxis.none)
+    assert _eq(none.numpy(), tl.numpy()) and none.sort_axis == 0
+
+
+def test_sort_multiset_large(npc, orc):
+    rng = np.random.default_rng(61)
+    n = 100000
+    i = rng.integers(0, 500, n).astype(np.uint32)
+    j = rng.integers(0, 400, n).astype(np.uint32)
+    k = rng.integers(0, 27, n).astype(np.uint32)
+    tl = npc.TripletList.from_numpy(i, j, k, 500, 400, 27)
+    for axis in (1, 2, 3):
+        got = npc.sort_triplets(tl, axis).numpy()
+        assert _eq(got, orc.sort_triplets(i, j, k, axis, 500, 400, 27))
+
+
+def test_nonfinite_and_offsets_rejected_by_library(npc):
+    import ctypes as C
+    from paper_2511_23227_b200 import _lib as L
+    ctx = npc.context()
+    xyz = torch.tensor([[0.0, float("inf"), 0.0]], dtype=torch.float64, device="cuda")
+    cl = npc.PointCloud(xyz, np.array([0, 1]))
+    with pytest.raises(npc.NonFiniteError):
+        npc.radius_search(cl, cl, 1.0)
+    bad = npc.PointCloud(torch.zeros((2, 3), dtype=torch.float64, device="cuda"), np.array([0, 1]))
+    with pytest.raises(npc.OffsetError):
+        npc.radius_search(bad, bad, 1.0)
+    assert ctx.launch_count() > 0
+    del C, L
+
+
+def test_voxel_downsample_golden(npc, golden):
+    g = golden("voxel_clusters.npz")
+    cl = _cloud(npc, g["xyz"], g["offsets"])
+    coarse, mp = npc.voxel_downsample(cl, float(g["voxel"]))
+    assert np.array_equal(mp.kept_index.cpu().numpy(), g["kept"])
+    assert np.array_equal(mp.parent_of.cpu().numpy(), g["parent"])
+    assert np.array_equal(coarse.batch_offsets(), g["kept_offsets"])
+    assert np.array_equal(coarse.positions(), g["xyz"][g["kept"]])
+    with pytest.raises(npc.VoxelError):
+        npc.voxel_downsample(cl, 0.0)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_voxel_downsample_random(npc, orc, seed):
+    rng = np.random.default_rng(seed + 50)
+    xyz = rng.normal(size=(4000, 3)) * 2.0
+    off = np.array([0, 1000, 1000, 4000])
+    v = float(rng.uniform(0.2, 1.5))
+    kept, parent, koff = orc.voxel_downsample(xyz, v, off)
+    coarse, mp = npc.voxel_downsample(_cloud(npc, xyz, off), v)
+    assert np.array_equal(mp.kept_index.cpu().numpy(), kept)
+    assert np.array_equal(mp.parent_of.cpu().numpy(), parent)
+    assert np.array_equal(coarse.batch_offsets(), koff)

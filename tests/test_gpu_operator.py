@@ -1,0 +1,128 @@
+"""GPU parity of the operator path (PointConvOp, conv_op.hpp) and the BASELINE
+configs at parity-test sizes:
+  c1: 16K uniform points, C_in = C_out = 32, t = 3, forward        (exact path)
+  c2: 100K uniform points, C = 64, forward + both gradients         (exact + bf16)
+"""
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a = np.asarray(a, np.float64).ravel()
+    b = np.asarray(b, np.float64).ravel()
+    return float(np.max(np.abs(a - b)) / max(float(np.max(np.abs(b))), 1e-30))
+
+
+def T(x, dt=torch.float32):
+    return torch.as_tensor(np.ascontiguousarray(x)).to("cuda", dt)
+
+
+def test_pointconv_state_and_shapes(npc, orc):
+    w = T(orc.make_weights(3, 1, 4, 5, 1))
+    op = npc.PointConvOp(w, npc.ConvGeometry(radius=0.3, t=3))
+    with pytest.raises(npc.StateError):
+        op.backward(T(np.zeros((3, 1, 5))))
+    with pytest.raises(npc.StateError):
+        op.cached_triplets()
+    with pytest.raises(npc.ShapeError):
+        npc.PointConvOp(w, npc.ConvGeometry(radius=0.3, t=5))
+    xyz = orc.gen_uniform_cube(200, 1.0, 3)
+    cl = npc.make_point_cloud(xyz)
+    with pytest.raises(npc.ShapeError):
+        op.forward(cl, T(np.zeros((199, 1, 4))))
+    f = T(orc.gen_features(200, 1, 4, 4))
+    op.forward(cl, f)
+    with pytest.raises(npc.ShapeError):
+        op.backward(T(np.zeros((200, 1, 4))))
+
+
+def test_pointconv_matches_oracle_and_caches(npc, orc, golden):
+    g = golden("conv_small.npz")
+    n = len(g["xyz"])
+    cl = npc.make_point_cloud(g["xyz"])
+    w = T(g["w"], torch.float64)
+    op = npc.PointConvOp(w, npc.ConvGeometry(radius=float(g["radius"]), t=3),
+                         npc.ExecConfig(math=npc.Math.exact))
+    out = op.forward(cl, T(g["fin"], torch.float64))
+    assert rel(out.cpu(), g["fout"]) <= 1e-12
+    res = op.backward(T(g["gout"], torch.float64))
+    assert rel(res.grad_in.cpu(), g["grad_in"]) <= 1e-12
+    assert rel(res.grad_w.cpu(), g["grad_w"]) <= 1e-12
+    ti, tj, tk = op.cached_triplets().numpy()  # by_k (choose_sort_axis)
+    assert np.array_equal(ti, g["i"]) and np.array_equal(tj, g["j"]) and np.array_equal(tk, g["k"])
+    nb = op.neighbors()
+    op.forward(cl, T(g["fin"], torch.float64))
+    assert op.neighbors() is nb  # identity cache hit (conv_op.hpp:109-111)
+    cl2 = npc.make_point_cloud(g["xyz"])
+    op.forward(cl2, T(g["fin"], torch.float64))
+    assert op.neighbors() is not nb
+
+
+def test_pointwise_t1_identity(npc, orc):
+    # test_conv_op.cpp:35-56: t=1, tiny radius -> F_out = W^T f per point
+    xyz = orc.gen_uniform_cube(100, 10.0, 5)
+    cl = npc.make_point_cloud(xyz)
+    w = orc.make_weights(1, 1, 6, 7, 6, np.float64)
+    f = orc.gen_features(100, 1, 6, 7, np.float64)
+    op = npc.PointConvOp(T(w, torch.float64), npc.ConvGeometry(radius=1e-6, t=1))
+    out = op.forward(cl, T(f, torch.float64)).cpu().numpy()
+    want = np.einsum("ngc,gcm->ngm", f, w[0])
+    assert rel(out, want) <= 1e-14
+
+
+def test_strided_two_cloud_forward(npc, orc, ref):
+    # conv_op.hpp:161-175, 219-225 on a clustered cloud (config-3 stand-in, small)
+    xyz = ref.gen_gaussian_clusters(6000, 8, 4.0, 0.3, 17)
+    cl = npc.make_point_cloud(xyz)
+    w = orc.make_weights(3, 1, 16, 24, 8, np.float64)
+    op = npc.PointConvOp(T(w, torch.float64), npc.ConvGeometry(radius=0.25, t=3))
+    f = orc.gen_features(6000, 1, 16, 9, np.float64)
+    sr = npc.strided_block(op, cl, T(f, torch.float64), 0.2)
+    kept, parent, koff = ref.voxel_downsample(xyz, 0.2)
+    assert np.array_equal(sr.map.kept_index.cpu().numpy(), kept)
+    coarse = xyz[kept]
+    ti, tj, tk = ref.build_triplets(coarse, xyz, 0.25, 3, axis=0)
+    fo, _, _ = orc.dense_conv(w, f, ti, tj, tk, len(kept))
+    assert rel(sr.coarse_features.cpu(), fo) <= 1e-12
+    up = npc.upsample(cl, sr.map, sr.coarse_features)
+    assert up.shape[0] == 6000
+
+
+def test_c1_forward_parity(npc, orc):
+    """BASELINE config 1: 16K points, C=32, fp32 exact vs the fp64 oracle."""
+    n = 16384
+    xyz = orc.gen_uniform_cube(n, 1.0, 1)
+    r = 1.8 * n ** (-1 / 3)
+    w = orc.make_weights(3, 1, 32, 32, 2)
+    f = orc.gen_features(n, 1, 32, 3)
+    ti, tj, tk = orc.build_triplets(xyz, xyz, r, 3)
+    assert len(ti) == 385924
+    fo, _, _ = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3))
+    out = op.forward(npc.make_point_cloud(xyz), T(f))
+    assert rel(out.cpu(), fo) <= 1e-5
+
+
+@pytest.mark.slow
+def test_c2_fwd_bwd_parity(npc, orc):
+    """BASELINE config 2: 100K points, C=64, forward + dgrad + wgrad."""
+    n = 100000
+    xyz = orc.gen_uniform_cube(n, 1.0, 1)
+    r = 1.8 * n ** (-1 / 3)
+    w = orc.make_weights(3, 1, 64, 64, 2)
+    f = orc.gen_features(n, 1, 64, 3)
+    go = orc.gen_features(n, 1, 64, 4)
+    ti, tj, tk = orc.build_triplets(xyz, xyz, r, 3)
+    assert len(ti) == 2435886
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
+                                go.astype(np.float64))
+    cl = npc.make_point_cloud(xyz)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.exact))
+    out = op.forward(cl, T(f))
+    res = op.backward(T(go))
+    assert rel(out.cpu(), fo) <= 1e-5
+    assert rel(res.grad_in.cpu(), gi) <= 1e-5
+    assert rel(res.grad_w.cpu(), gw) <= 1e-5
