@@ -232,6 +232,11 @@ npcg_status npcg_conv_backward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype
 /* Builds (and caches in the handle) the compute plans the engines use, so
  * that the first forward / backward does not pay for them.  Optional. */
 npcg_status npcg_neighbors_prepare(npcg_context* ctx, npcg_neighbors* nb, int32_t math);
+/* Tensor-core tile-plan statistics (instrumentation; builds the plans): for
+ * the forward, input-gradient and weight-gradient plans, four values each --
+ * [super-tiles, super-tiles beyond tile capacity (served by the exact engine),
+ *  max halo rows, mean halo rows x 100].  stats: HOST int64[12]. */
+npcg_status npcg_neighbors_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* stats);
 
 /* ---- strided path ------------------------------- */
 /* spatial.hpp:47-48 voxel_downsample.  kept (n_points) / parent (n_points)

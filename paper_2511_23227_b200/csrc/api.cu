@@ -679,6 +679,15 @@ npcg_status npcg_neighbors_prepare(npcg_context* ctx, npcg_neighbors* nb, int32_
   });
 }
 
+npcg_status npcg_neighbors_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* stats) {
+  if (!ctx || !nb || !stats) return NPCG_ERR_INVALID;
+  return guard(ctx, [&] {
+    if (nb->t == 0) fail(NPCG_ERR_STATE, "plan_stats: handle has no kernel cells");
+    if (!tc_supported(1, 64, 64, nb->n_kernels)) fail(NPCG_ERR_UNSUPPORTED, "no tensor-core plan for this K");
+    tc_plan_stats(ctx, nb, stats);
+  });
+}
+
 npcg_status npcg_voxel_downsample(npcg_context* ctx, const npcg_cloud* cloud, double voxel,
                                   int64_t* kept, int64_t* parent, int64_t* out_offsets,
                                   int64_t* n_kept) {

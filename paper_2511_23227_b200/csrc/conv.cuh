@@ -25,5 +25,6 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const flo
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
                  const float* gout, float* grad_in, float* grad_w);
 void tc_prepare(npcg_context* ctx, npcg_neighbors* nb);
+void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12);
 
 }  // namespace npcg

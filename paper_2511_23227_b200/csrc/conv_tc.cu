@@ -1,16 +1,1179 @@
-// conv_tc.cu -- tcgen05 / TMEM tensor-core engines (placeholder).
+// conv_tc.cu -- tcgen05 / TMEM engines for the point-centric convolution
+// (bf16 operands, fp32 accumulate), C_in = C_out = 64, G = 1, K = t^3 <= 32.
+//
+// Formulation (output-stationary cell aggregation):
+//     F_out[i] = sum_k W_k^T A_k[i],   A_k[i] = sum_{j in N_k(i)} F_in[j]
+// Rows are processed in spatial (Morton) order in 128-row sub-tiles grouped
+// into super-tiles.  Per super-tile the union of all neighbor rows (the halo,
+// ~2.6x the rows at 384 rows/super-tile) is bulk-copied into shared memory
+// once; every A_k is then aggregated from shared memory (fp32 accumulate via
+// FHADD.BF16) into a SWIZZLE_128B K-major tile and multiplied on the tensor
+// core against W_k, which is loaded once per super-tile and cell (W traffic
+// amortised over 384 rows).  Accumulators live in TMEM (3 x 64 columns,
+// double-buffered); one epilogue store per output value, no atomics.
+//
+//   forward   : rows = output points, gathered features = F_in, B = W_k
+//   dgrad     : rows = input points (transposed CSR), features = G_out, B = W_k^T
+//   wgrad     : rows = output points, A_k^T (MN-major, two cells stacked to
+//               M = 128) x dense G_out tile (MN-major) into per-cell TMEM
+//               accumulators; per-CTA partials reduced in a fixed order.
+//
+// Warp roles (fwd / dgrad kernel, 448 threads):
+//   warps 0-3  epilogue (TMEM lane quadrant = warp id)
+//   warp 4     producer: halo / W_k / stage-descriptor bulk copies
+//   warp 5     MMA issuer (one elected lane) + TMEM allocator
+//   warps 6-13 aggregation (quarter-warp per row, 4 rows per step)
+#include <cuda_bf16.h>
+
+#include <algorithm>
+#include <cstdio>
+
 #include "conv.cuh"
+#include "tc_common.cuh"
 
 namespace npcg {
-struct TcPlan {};
+using namespace tc;
+
+constexpr int TM = 128;
+constexpr int CH = 64;
+constexpr int KMAX = 32;
+constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sorts in smem
+constexpr int MAX_BLOCK_ENTRIES = 1024;  // entries per (sub-tile, cell) block
+constexpr int BLOCK_MAX_BYTES = 512 + 2 * MAX_BLOCK_ENTRIES;
+constexpr uint32_t kOverflow = 0xFFFFFFFFu;
+
+struct TcDirPlan {
+  int st = 3;
+  int hcap = 1280;
+  int64_t n_rows = 0, n_cols = 0;
+  int n_sub = 0, n_super = 0, K = 0;
+  DevBuf<uint32_t> halo;      // n_super * hcap, permuted column index
+  DevBuf<uint32_t> halo_len;  // n_super (kOverflow marks a super-tile the planner rejected)
+  DevBuf<uint32_t> blk_off;   // n_sub*K + 1 byte offsets of the stage-descriptor blocks
+  DevBuf<uint8_t> blocks;
+  int n_overflow = 0;
+  int max_halo = 0;
+  double mean_halo = 0.0;
+};
+
+struct TcPlan {
+  std::unique_ptr<TcDirPlan> fwd, bwd, wg;
+  DevBuf<uint32_t> inv_perm_out, inv_perm_in;
+  DevBuf<__nv_bfloat16> feat_in;   // bf16 F_in in perm_in order
+  DevBuf<__nv_bfloat16> feat_out;  // bf16 G_out in perm_out order
+  DevBuf<uint8_t> wpack;           // K x 8 KB, SW128 K-major B operand
+  DevBuf<float> partial;           // wgrad per-CTA partials
+};
+
 void destroy_tc_plan(TcPlan* p) { delete p; }
-bool tc_supported(int64_t, int64_t, int64_t, int64_t) { return false; }
-void tc_forward(npcg_context*, npcg_neighbors*, const float*, const float*, float*) {
-  fail(NPCG_ERR_UNSUPPORTED, "tensor-core path not built");
+
+bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K) {
+  return G == 1 && cin == CH && cout == CH && K >= 1 && K <= KMAX;
 }
-void tc_backward(npcg_context*, npcg_neighbors*, const float*, const float*, const float*, float*,
-                 float*) {
-  fail(NPCG_ERR_UNSUPPORTED, "tensor-core path not built");
+
+// ===========================================================================
+// planner
+// ===========================================================================
+__global__ void k_inverse_perm(const uint32_t* __restrict__ perm, int64_t n,
+                               uint32_t* __restrict__ inv) {
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (p < n) inv[perm[p]] = static_cast<uint32_t>(p);
 }
-void tc_prepare(npcg_context*, npcg_neighbors*) {}
+
+// Per sub-tile: entries per (sub-tile, cell) block -> block byte sizes; flags
+// sub-tiles whose blocks exceed the stage-descriptor slot or whose per-(row,
+// cell) counts exceed the 5-bit item field.
+__global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ row_ptr,
+                                                    const uint32_t* __restrict__ kk,
+                                                    const uint32_t* __restrict__ perm_rows,
+                                                    int64_t n_rows, int K,
+                                                    uint32_t* __restrict__ blk_size,
+                                                    uint32_t* __restrict__ sub_bad) {
+  __shared__ uint32_t cnt[KMAX];
+  __shared__ uint8_t rc[TM][KMAX];
+  __shared__ int bad;
+  const int r = threadIdx.x;
+  if (r < KMAX) cnt[r] = 0;
+  if (r == 0) bad = 0;
+  for (int k = 0; k < KMAX; ++k) rc[r][k] = 0;
+  __syncthreads();
+  const int64_t p = static_cast<int64_t>(blockIdx.x) * TM + r;
+  if (p < n_rows) {
+    const uint32_t i = perm_rows[p];
+    for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      const uint32_t k = kk[e];
+      atomicAdd(&cnt[k], 1u);
+      if (rc[r][k] < 255) rc[r][k]++;
+    }
+  }
+  for (int k = 0; k < K; ++k)
+    if (rc[r][k] > 31) bad = 1;
+  __syncthreads();
+  if (r < K) {
+    const uint32_t E = cnt[r];
+    if (E > MAX_BLOCK_ENTRIES) bad = 1;
+    blk_size[static_cast<int64_t>(blockIdx.x) * K + r] = 512u + ((2u * E + 15u) / 16u) * 16u;
+  }
+  __syncthreads();
+  if (r == 0) sub_bad[blockIdx.x] = bad;
+}
+
+// Per super-tile: halo (sorted unique permuted neighbor rows), per-(sub-tile,
+// cell) item lists (rows ordered by entry count, descending) and u16 halo
+// indices of the entries.  Block layout: u32 item[128] | u16 entry[E] (pad 16 B)
+//   item = r | count << 7 | entry_offset << 12
+__global__ void __launch_bounds__(512) k_plan_super(
+    const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+    const uint32_t* __restrict__ kk, const uint32_t* __restrict__ perm_rows,
+    const uint32_t* __restrict__ inv_perm_cols, int64_t n_rows, int K, int n_sub, int st, int hcap,
+    const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ sub_bad,
+    uint32_t* __restrict__ halo_out, uint32_t* __restrict__ halo_len,
+    uint8_t* __restrict__ blocks) {
+  extern __shared__ __align__(16) uint8_t sm[];
+  uint32_t* buf = reinterpret_cast<uint32_t*>(sm);                          // MAXE_ST
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(buf + MAXE_ST);               // st*K*TM
+  uint16_t* eoff = cnt + st * K * TM;                                        // st*K*TM
+  int* rowoff = reinterpret_cast<int*>(eoff + st * K * TM);                  // st*TM + 1
+  __shared__ int s_total, s_bad, s_H;
+  __shared__ int wsum[16];
+
+  const int s = blockIdx.x;
+  const int sub0 = s * st;
+  const int nsub = min(st, n_sub - sub0);
+  const int R = nsub * TM;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (tid == 0) {
+    s_bad = 0;
+    for (int g = 0; g < nsub; ++g) s_bad |= sub_bad[sub0 + g];
+  }
+  for (int x = tid; x < st * K * TM; x += blockDim.x) cnt[x] = 0;
+  __syncthreads();
+  if (s_bad) {
+    if (tid == 0) halo_len[s] = kOverflow;
+    return;
+  }
+  // 1. row lengths -> offsets (block scan over R <= 512 rows)
+  int len = 0;
+  uint32_t row_i = 0;
+  if (tid < R) {
+    const int64_t p = static_cast<int64_t>(sub0) * TM + tid;
+    if (p < n_rows) {
+      row_i = perm_rows[p];
+      len = static_cast<int>(row_ptr[row_i + 1] - row_ptr[row_i]);
+    }
+  }
+  int incl = len;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += n;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int w = 0; w < 16; ++w) {
+      const int v = wsum[w];
+      wsum[w] = acc;
+      acc += v;
+    }
+    s_total = acc;
+  }
+  __syncthreads();
+  const int my_off = incl - len + wsum[warp];
+  if (tid < R) rowoff[tid] = my_off;
+  const int E = s_total;
+  if (E > MAXE_ST) {
+    if (tid == 0) halo_len[s] = kOverflow;
+    return;
+  }
+  // 2. permuted neighbor ids + per-(sub, cell, row) counts
+  if (tid < R && len > 0) {
+    const int g = tid / TM, r = tid % TM;
+    const int64_t e0 = row_ptr[row_i];
+    for (int q = 0; q < len; ++q) {
+      buf[my_off + q] = inv_perm_cols[col[e0 + q]];
+      cnt[(g * K + static_cast<int>(kk[e0 + q])) * TM + r]++;
+    }
+  }
+  int P = 1;
+  while (P < E) P <<= 1;
+  for (int x = E + tid; x < P; x += blockDim.x) buf[x] = 0xFFFFFFFFu;
+  __syncthreads();
+  // 3. bitonic sort buf[0, P)
+  for (int size = 2; size <= P; size <<= 1) {
+    for (int stride = size >> 1; stride > 0; stride >>= 1) {
+      for (int x = tid; x < (P >> 1); x += blockDim.x) {
+        const int lo = 2 * stride * (x / stride) + (x % stride);
+        const int hi = lo + stride;
+        const bool up = (lo & size) == 0;
+        const uint32_t a = buf[lo], b = buf[hi];
+        if ((a > b) == up) {
+          buf[lo] = b;
+          buf[hi] = a;
+        }
+      }
+      __syncthreads();
+    }
+  }
+  // 4. unique (compaction in place, chunked per thread)
+  const int per = (P + blockDim.x - 1) / blockDim.x;
+  const int c0 = tid * per, c1 = min(P, c0 + per);
+  int local = 0;
+  for (int x = c0; x < c1; ++x) {
+    const uint32_t v = buf[x];
+    if (v != 0xFFFFFFFFu && (x == 0 || buf[x - 1] != v)) ++local;
+  }
+  int li = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int n = __shfl_up_sync(0xffffffffu, li, o);
+    if (lane >= o) li += n;
+  }
+  __syncthreads();
+  if (lane == 31) wsum[warp] = li;
+  __syncthreads();
+  if (tid == 0) {
+    int acc = 0;
+    for (int w = 0; w < 16; ++w) {
+      const int v = wsum[w];
+      wsum[w] = acc;
+      acc += v;
+    }
+    s_H = acc;
+  }
+  __syncthreads();
+  const int H = s_H;
+  if (H > hcap) {
+    if (tid == 0) halo_len[s] = kOverflow;
+    return;
+  }
+  // gather my unique values into registers-by-chunk, then write compacted
+  {
+    int w0 = li - local + wsum[warp];
+    uint32_t vals[32];
+    int nv = 0;
+    for (int x = c0; x < c1 && nv < 32; ++x) {
+      const uint32_t v = buf[x];
+      if (v != 0xFFFFFFFFu && (x == 0 || buf[x - 1] != v)) vals[nv++] = v;
+    }
+    __syncthreads();
+    for (int q = 0; q < nv; ++q) {
+      buf[w0 + q] = vals[q];
+      halo_out[static_cast<int64_t>(s) * hcap + w0 + q] = vals[q];
+    }
+  }
+  __syncthreads();
+  // 5. items per (sub, cell) block: rows by count descending (stable in r)
+  const unsigned lt = (1u << lane) - 1u;
+  for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
+    const int g = b / K, k = b % K;
+    const int64_t boff = blk_off[static_cast<int64_t>(sub0 + g) * K + k];
+    uint32_t* items = reinterpret_cast<uint32_t*>(blocks + boff);
+    int pos = 0, ebase = 0;
+    for (int v = 31; v >= 0; --v) {
+      for (int ch = 0; ch < TM / 32; ++ch) {
+        const int r = ch * 32 + lane;
+        const int c = cnt[(g * K + k) * TM + r];
+        const unsigned m = __ballot_sync(0xffffffffu, c == v);
+        if (c == v) {
+          const int before = __popc(m & lt);
+          const int eo = ebase + v * before;
+          items[pos + before] = static_cast<uint32_t>(r) | (static_cast<uint32_t>(c) << 7) |
+                                (static_cast<uint32_t>(eo) << 12);
+          eoff[(g * K + k) * TM + r] = static_cast<uint16_t>(eo);
+        }
+        pos += __popc(m);
+        ebase += v * __popc(m);
+      }
+    }
+  }
+  __syncthreads();
+  for (int x = tid; x < st * K * TM; x += blockDim.x) cnt[x] = 0;
+  __syncthreads();
+  // 6. entries: halo index of each neighbor, written at its item's offset
+  if (tid < R && len > 0) {
+    const int g = tid / TM, r = tid % TM;
+    const int64_t e0 = row_ptr[row_i];
+    for (int q = 0; q < len; ++q) {
+      const int k = static_cast<int>(kk[e0 + q]);
+      const uint32_t pj = inv_perm_cols[col[e0 + q]];
+      int lo = 0, hi = H;
+      while (lo < hi) {
+        const int mid = (lo + hi) >> 1;
+        if (buf[mid] < pj) lo = mid + 1;
+        else hi = mid;
+      }
+      const int idx = (g * K + k) * TM + r;
+      const int pos = eoff[idx] + cnt[idx]++;
+      const int64_t boff = blk_off[static_cast<int64_t>(sub0 + g) * K + k];
+      reinterpret_cast<uint16_t*>(blocks + boff + 512)[pos] = static_cast<uint16_t>(lo);
+    }
+  }
+  if (tid == 0) halo_len[s] = static_cast<uint32_t>(H);
+}
+
+static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_t* row_ptr,
+                                                 const uint32_t* col, const uint32_t* kk,
+                                                 int64_t n_rows, int64_t n_cols,
+                                                 const uint32_t* perm_rows,
+                                                 const uint32_t* inv_perm_cols, int K, int st,
+                                                 int hcap) {
+  auto P = std::make_unique<TcDirPlan>();
+  P->st = st;
+  P->hcap = hcap;
+  P->n_rows = n_rows;
+  P->n_cols = n_cols;
+  P->K = K;
+  P->n_sub = static_cast<int>(ceil_div(n_rows, TM));
+  P->n_super = static_cast<int>(ceil_div(P->n_sub, st));
+  if (P->n_sub == 0) return P;
+  const int64_t nblk = static_cast<int64_t>(P->n_sub) * K;
+  DevBuf<uint32_t> blk_size(ctx, nblk + 1), sub_bad(ctx, P->n_sub);
+  NPCG_CUDA(cudaMemsetAsync(blk_size.get() + nblk, 0, 4, ctx->stream));
+  launch(ctx, "plan_counts", k_plan_counts, dim3(P->n_sub), dim3(TM), 0, row_ptr, kk, perm_rows,
+         n_rows, K, blk_size.get(), sub_bad.get());
+  P->blk_off.alloc(ctx, nblk + 1);
+  uint32_t total = 0;
+  exclusive_scan_u32(ctx, blk_size.get(), P->blk_off.get(), nblk + 1, &total);
+  P->blocks.alloc(ctx, total);
+  P->halo.alloc(ctx, static_cast<int64_t>(P->n_super) * hcap);
+  P->halo_len.alloc(ctx, P->n_super);
+  const size_t smem = MAXE_ST * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
+  NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  launch(ctx, "plan_super", k_plan_super, dim3(P->n_super), dim3(512), smem, row_ptr, col, kk,
+         perm_rows, inv_perm_cols, n_rows, K, P->n_sub, st, hcap,
+         static_cast<const uint32_t*>(P->blk_off.get()), static_cast<const uint32_t*>(sub_bad.get()),
+         P->halo.get(), P->halo_len.get(), P->blocks.get());
+  std::vector<uint32_t> hl(P->n_super);
+  NPCG_CUDA(cudaMemcpyAsync(hl.data(), P->halo_len.get(), hl.size() * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  double sum = 0;
+  for (uint32_t h : hl) {
+    if (h == kOverflow) {
+      P->n_overflow++;
+    } else {
+      P->max_halo = std::max<int>(P->max_halo, static_cast<int>(h));
+      sum += h;
+    }
+  }
+  const int ok = P->n_super - P->n_overflow;
+  P->mean_halo = ok ? sum / ok : 0.0;
+  return P;
+}
+
+// ===========================================================================
+// operand preparation
+// ===========================================================================
+// dst[p][c] = bf16(src[perm[p]][c]), 64 channels, 8 per thread.
+__global__ void k_to_bf16_perm(const float* __restrict__ src, const uint32_t* __restrict__ perm,
+                               int64_t n, __nv_bfloat16* __restrict__ dst) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= n * 8) return;
+  const int64_t p = x >> 3;
+  const int q = static_cast<int>(x & 7);
+  const float4* s = reinterpret_cast<const float4*>(src + static_cast<int64_t>(perm[p]) * CH + q * 8);
+  const float4 a = __ldg(s), b = __ldg(s + 1);
+  uint4 o;
+  o.x = pack_bf16x2(a.x, a.y);
+  o.y = pack_bf16x2(a.z, a.w);
+  o.z = pack_bf16x2(b.x, b.y);
+  o.w = pack_bf16x2(b.z, b.w);
+  reinterpret_cast<uint4*>(dst + p * CH)[q] = o;
+}
+
+// B operand images (SW128 K-major, 8 KB per cell).  transpose=false: N = C_out
+// rows, K = C_in (forward); transpose=true: N = C_in rows, K = C_out (dgrad).
+__global__ void k_pack_w(const float* __restrict__ w, int K, bool transpose,
+                         uint8_t* __restrict__ out) {
+  const int x = blockIdx.x * blockDim.x + threadIdx.x;
+  if (x >= K * CH * CH) return;
+  const int k = x / (CH * CH), rem = x % (CH * CH);
+  const int c = rem / CH, m = rem % CH;  // W[k][c][m]
+  const float v = w[x];
+  const uint32_t off = transpose ? sw128_off(c, m) : sw128_off(m, c);
+  reinterpret_cast<__nv_bfloat16*>(out + static_cast<int64_t>(k) * 8192 + off)[0] = __float2bfloat16_rn(v);
+}
+
+// ===========================================================================
+// forward / dgrad kernel
+// ===========================================================================
+struct FwdArgs {
+  const uint32_t* halo;
+  const uint32_t* halo_len;
+  const uint32_t* blk_off;
+  const uint8_t* blocks;
+  const uint32_t* perm_rows;
+  int64_t n_rows;
+  int n_sub, n_super, st, hcap, K;
+  const __nv_bfloat16* feat;  // bf16 (n_cols, 64), permuted
+  const uint8_t* wpack;       // K x 8 KB
+  float* out;                 // (n_rows, 64), original order
+};
+
+constexpr int FWD_THREADS = 448;
+constexpr int FWD_AGG_WARP0 = 6;
+constexpr int FWD_AGG_WARPS = 8;
+constexpr int NSA = 2;  // A stages (16 KB)
+constexpr int NSW = 2;  // W stages (8 KB)
+constexpr int NSD = 2;  // stage-descriptor slots
+constexpr int FWD_ACC_COLS = 192;  // 3 sub-tiles x 64 fp32 columns
+
+struct FwdSmem {
+  uint32_t halo, a, w, d, bar, tmem_slot;
+  size_t total;
+};
+__host__ __device__ inline FwdSmem fwd_smem_layout(int hcap) {
+  FwdSmem L{};
+  uint32_t o = 0;
+  L.halo = o;
+  o += hcap * 128;
+  o = (o + 1023) & ~1023u;
+  L.a = o;
+  o += NSA * 16384;
+  L.w = o;
+  o += NSW * 8192;
+  L.d = o;
+  o += NSD * BLOCK_MAX_BYTES;
+  o = (o + 7) & ~7u;
+  L.bar = o;
+  o += 32 * 8;
+  L.tmem_slot = o;
+  o += 16;
+  L.total = o + 1024;  // alignment slack
+  return L;
+}
+
+// barrier indices
+enum : int {
+  B_HALO_FULL = 0,
+  B_HALO_EMPTY = 1,
+  B_A_FULL = 2,          // NSA
+  B_A_EMPTY = 4,         // NSA
+  B_W_FULL = 6,          // NSW
+  B_W_EMPTY = 8,         // NSW
+  B_D_FULL = 10,         // NSD
+  B_D_EMPTY = 12,        // NSD
+  B_T_FULL = 14,         // 2
+  B_T_EMPTY = 16,        // 2
+  B_COUNT = 18
+};
+
+__global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const FwdSmem L = fwd_smem_layout(a.hcap);
+  const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_w = base + L.w, s_d = base + L.d;
+  const uint32_t s_bar = base + L.bar;
+  auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
+  const uint8_t* g_halo = gbase + L.halo;
+  uint8_t* g_a = gbase + L.a;
+  const uint8_t* g_d = gbase + L.d;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) {
+    mbar_init(bar(B_HALO_FULL), 1);
+    mbar_init(bar(B_HALO_EMPTY), FWD_AGG_WARPS);
+    for (int i = 0; i < NSA; ++i) {
+      mbar_init(bar(B_A_FULL + i), FWD_AGG_WARPS);
+      mbar_init(bar(B_A_EMPTY + i), 1);
+    }
+    for (int i = 0; i < NSW; ++i) {
+      mbar_init(bar(B_W_FULL + i), 1);
+      mbar_init(bar(B_W_EMPTY + i), 1);
+    }
+    for (int i = 0; i < NSD; ++i) {
+      mbar_init(bar(B_D_FULL + i), 1);
+      mbar_init(bar(B_D_EMPTY + i), FWD_AGG_WARPS);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(B_T_FULL + i), 1);
+      mbar_init(bar(B_T_EMPTY + i), 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const int K = a.K;
+
+  if (warp == 4) {
+    // ------------------------------ producer ------------------------------
+    uint32_t w_it = 0, d_it = 0, h_it = 0;
+    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
+      const int nsub = min(a.st, a.n_sub - s * a.st);
+      const uint32_t H = a.halo_len[s];
+      const uint32_t* hl = a.halo + static_cast<int64_t>(s) * a.hcap;
+      mbar_wait(bar(B_HALO_EMPTY), (h_it & 1) ^ 1);
+      if (lane == 0) mbar_expect_tx(bar(B_HALO_FULL), H * 128u);
+      __syncwarp();
+      for (uint32_t h = lane; h < H; h += 32) {
+        const uint32_t v = hl[h];
+        if (h == 0 || hl[h - 1] != v - 1) {
+          uint32_t n = 1;
+          while (h + n < H && hl[h + n] == v + n) ++n;
+          bulk_g2s(s_halo + h * 128u, a.feat + static_cast<int64_t>(v) * CH, n * 128u,
+                   bar(B_HALO_FULL));
+        }
+      }
+      ++h_it;
+      for (int k = 0; k < K; ++k) {
+        if (lane == 0) {
+          const uint32_t ws = w_it % NSW;
+          mbar_wait(bar(B_W_EMPTY + ws), ((w_it / NSW) & 1) ^ 1);
+          mbar_expect_tx(bar(B_W_FULL + ws), 8192u);
+          bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u,
+                   bar(B_W_FULL + ws));
+        }
+        ++w_it;
+        for (int g = 0; g < nsub; ++g) {
+          if (lane == 0) {
+            const uint32_t ds = d_it % NSD;
+            mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
+            const int64_t bi = static_cast<int64_t>(s * a.st + g) * K + k;
+            const uint32_t o0 = a.blk_off[bi], o1 = a.blk_off[bi + 1];
+            mbar_expect_tx(bar(B_D_FULL + ds), o1 - o0);
+            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(B_D_FULL + ds));
+          }
+          ++d_it;
+        }
+      }
+      __syncwarp();
+    }
+  } else if (warp == 5) {
+    // ------------------------------ MMA issuer -----------------------------
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, 64, false, false);
+      uint32_t w_it = 0, a_it = 0, t_it = 0;
+      for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
+        const int nsub = min(a.st, a.n_sub - s * a.st);
+        const uint32_t ab = t_it & 1;
+        mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
+        tc_fence_after();
+        for (int k = 0; k < K; ++k) {
+          const uint32_t ws = w_it % NSW;
+          mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
+          for (int g = 0; g < nsub; ++g) {
+            const uint32_t as = a_it % NSA;
+            mbar_wait(bar(B_A_FULL + as), (a_it / NSA) & 1);
+            tc_fence_after();
+            const uint32_t d = tmem + ab * FWD_ACC_COLS + g * 64;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks) {
+              const uint64_t ad = sdesc_sw128(s_a + as * 16384u + 32u * ks, 16, 1024);
+              const uint64_t bd = sdesc_sw128(s_w + ws * 8192u + 32u * ks, 16, 1024);
+              umma_bf16(d, ad, bd, idesc, (k > 0 || ks > 0) ? 1u : 0u);
+            }
+            umma_commit(bar(B_A_EMPTY + as));
+            ++a_it;
+          }
+          umma_commit(bar(B_W_EMPTY + ws));
+          ++w_it;
+        }
+        umma_commit(bar(B_T_FULL + ab));
+        ++t_it;
+      }
+    }
+    __syncwarp();
+  } else if (warp >= FWD_AGG_WARP0) {
+    // ------------------------------ aggregation ----------------------------
+    const int aw = warp - FWD_AGG_WARP0;
+    const int sub_l = lane >> 3, l8 = lane & 7;
+    uint32_t a_it = 0, d_it = 0, h_it = 0;
+    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
+      const int nsub = min(a.st, a.n_sub - s * a.st);
+      mbar_wait(bar(B_HALO_FULL), h_it & 1);
+      ++h_it;
+      for (int k = 0; k < K; ++k) {
+        for (int g = 0; g < nsub; ++g) {
+          const uint32_t ds = d_it % NSD, as = a_it % NSA;
+          mbar_wait(bar(B_D_FULL + ds), (d_it / NSD) & 1);
+          mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
+          const uint8_t* blk = g_d + ds * BLOCK_MAX_BYTES;
+          const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
+          const uint16_t* ents = reinterpret_cast<const uint16_t*>(blk + 512);
+          uint8_t* A = g_a + as * 16384;
+#pragma unroll 1
+          for (int q = aw; q < TM / 4; q += FWD_AGG_WARPS) {
+            const uint32_t item = items[q * 4 + sub_l];
+            const uint32_t r = item & 127u, c = (item >> 7) & 31u, eo = item >> 12;
+            uint32_t cmax = c;
+            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 8));
+            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 16));
+            uint4 outv;
+            if (cmax <= 1) {
+              // copy (or zero) path: exact bf16 row copy, no arithmetic
+              outv = make_uint4(0, 0, 0, 0);
+              if (c == 1) {
+                const uint32_t h = ents[eo];
+                outv = *reinterpret_cast<const uint4*>(g_halo + h * 128u + l8 * 16u);
+              }
+            } else {
+              float acc[8];
+#pragma unroll
+              for (int x = 0; x < 8; ++x) acc[x] = 0.f;
+              for (uint32_t it = 0; it < cmax; ++it) {
+                if (it < c) {
+                  const uint32_t h = ents[eo + it];
+                  const uint4 v = *reinterpret_cast<const uint4*>(g_halo + h * 128u + l8 * 16u);
+                  acc_bf16x2(acc[0], acc[1], v.x);
+                  acc_bf16x2(acc[2], acc[3], v.y);
+                  acc_bf16x2(acc[4], acc[5], v.z);
+                  acc_bf16x2(acc[6], acc[7], v.w);
+                }
+              }
+              outv.x = pack_bf16x2(acc[0], acc[1]);
+              outv.y = pack_bf16x2(acc[2], acc[3]);
+              outv.z = pack_bf16x2(acc[4], acc[5]);
+              outv.w = pack_bf16x2(acc[6], acc[7]);
+              if (c == 1) outv = *reinterpret_cast<const uint4*>(g_halo + ents[eo] * 128u + l8 * 16u);
+            }
+            *reinterpret_cast<uint4*>(A + r * 128u + (((l8 ^ (r & 7u)) & 7u) << 4)) = outv;
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(bar(B_A_FULL + as));
+            mbar_arrive(bar(B_D_EMPTY + ds));
+          }
+          ++a_it;
+          ++d_it;
+        }
+      }
+      if (lane == 0) mbar_arrive(bar(B_HALO_EMPTY));
+    }
+  } else {
+    // ------------------------------ epilogue (warps 0-3) -------------------
+    const int e = warp;
+    uint32_t t_it = 0;
+    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
+      const int nsub = min(a.st, a.n_sub - s * a.st);
+      const uint32_t ab = t_it & 1;
+      mbar_wait(bar(B_T_FULL + ab), (t_it >> 1) & 1);
+      tc_fence_after();
+      for (int g = 0; g < nsub; ++g) {
+        uint32_t v[4][16];
+        const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * FWD_ACC_COLS + g * 64;
+        tmem_ld16(t0 + 0, v[0]);
+        tmem_ld16(t0 + 16, v[1]);
+        tmem_ld16(t0 + 32, v[2]);
+        tmem_ld16(t0 + 48, v[3]);
+        tmem_ld_wait();
+        const int64_t row = (static_cast<int64_t>(s) * a.st + g) * TM + 32 * e + lane;
+        if (row < a.n_rows) {
+          float4* o = reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * CH);
+#pragma unroll
+          for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              o[q * 4 + x] = make_float4(__uint_as_float(v[q][4 * x]), __uint_as_float(v[q][4 * x + 1]),
+                                         __uint_as_float(v[q][4 * x + 2]),
+                                         __uint_as_float(v[q][4 * x + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(B_T_EMPTY + ab));
+      ++t_it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_free<512>(tmem);
+}
+
+// ===========================================================================
+// weight-gradient kernel (st = 1: one 128-row tile per super-tile)
+//   D_pair[(2 cells x 64 c_in) x 64 c_out] += A_pair^T (MN-major) x G_tile (MN-major)
+// ===========================================================================
+struct WgArgs {
+  const uint32_t* halo;
+  const uint32_t* halo_len;
+  const uint32_t* blk_off;
+  const uint8_t* blocks;
+  int64_t n_rows;
+  int n_sub, hcap, K;
+  const __nv_bfloat16* feat;   // bf16 F_in (n_cols, 64), permuted
+  const __nv_bfloat16* dense;  // bf16 G_out (n_rows, 64), permuted (row = sub-tile order)
+  float* partial;              // [gridDim.x][K][64 c][64 m]
+};
+
+constexpr int WG_THREADS = 448;
+constexpr int WG_PAIRS = 7;      // cell pairs per CTA (cell group = 14 cells)
+constexpr int WG_NSA = 2;        // A pair stages (32 KB)
+
+struct WgSmem {
+  uint32_t halo, a, gt, d, bar, tmem_slot;
+  size_t total;
+};
+__host__ __device__ inline WgSmem wg_smem_layout(int hcap) {
+  WgSmem L{};
+  uint32_t o = 0;
+  L.halo = o;
+  o += hcap * 128;
+  o = (o + 1023) & ~1023u;
+  L.a = o;
+  o += WG_NSA * 32768;
+  L.gt = o;
+  o += 16384;
+  L.d = o;
+  o += NSD * 2 * BLOCK_MAX_BYTES;
+  o = (o + 7) & ~7u;
+  L.bar = o;
+  o += 32 * 8;
+  L.tmem_slot = o;
+  o += 16;
+  L.total = o + 1024;
+  return L;
+}
+
+enum : int {
+  W_HALO_FULL = 0,
+  W_HALO_EMPTY = 1,
+  W_A_FULL = 2,   // 2
+  W_A_EMPTY = 4,  // 2
+  W_D_FULL = 6,   // 2
+  W_D_EMPTY = 8,  // 2
+  W_G_FULL = 10,
+  W_G_EMPTY = 11,
+  W_DONE = 12,
+  W_COUNT = 13
+};
+
+__global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const WgSmem L = wg_smem_layout(a.hcap);
+  const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_g = base + L.gt, s_d = base + L.d;
+  const uint32_t s_bar = base + L.bar;
+  auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
+  const uint8_t* g_halo = gbase + L.halo;
+  uint8_t* g_a = gbase + L.a;
+  uint8_t* g_gt = gbase + L.gt;
+  const uint8_t* g_d = gbase + L.d;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = a.K;
+  const int cg = blockIdx.y;                 // cell group
+  const int k_begin = cg * 2 * WG_PAIRS;     // first cell of this CTA
+  const int n_pairs = max(0, min(WG_PAIRS, (K - k_begin + 1) / 2));
+  if (threadIdx.x == 0) {
+    mbar_init(bar(W_HALO_FULL), 1);
+    mbar_init(bar(W_HALO_EMPTY), FWD_AGG_WARPS);
+    for (int i = 0; i < WG_NSA; ++i) {
+      mbar_init(bar(W_A_FULL + i), FWD_AGG_WARPS);
+      mbar_init(bar(W_A_EMPTY + i), 1);
+    }
+    for (int i = 0; i < NSD; ++i) {
+      mbar_init(bar(W_D_FULL + i), 1);
+      mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS);
+    }
+    mbar_init(bar(W_G_FULL), 4);
+    mbar_init(bar(W_G_EMPTY), 1);
+    mbar_init(bar(W_DONE), 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // producer: halo + descriptor blocks (two cells per stage)
+    uint32_t d_it = 0, h_it = 0;
+    for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+      const uint32_t H = a.halo_len[s];
+      const uint32_t* hl = a.halo + static_cast<int64_t>(s) * a.hcap;
+      mbar_wait(bar(W_HALO_EMPTY), (h_it & 1) ^ 1);
+      if (lane == 0) mbar_expect_tx(bar(W_HALO_FULL), H * 128u);
+      __syncwarp();
+      for (uint32_t h = lane; h < H; h += 32) {
+        const uint32_t v = hl[h];
+        if (h == 0 || hl[h - 1] != v - 1) {
+          uint32_t n = 1;
+          while (h + n < H && hl[h + n] == v + n) ++n;
+          bulk_g2s(s_halo + h * 128u, a.feat + static_cast<int64_t>(v) * CH, n * 128u,
+                   bar(W_HALO_FULL));
+        }
+      }
+      ++h_it;
+      for (int p = 0; p < n_pairs; ++p) {
+        if (lane == 0) {
+          const uint32_t ds = d_it % NSD;
+          mbar_wait(bar(W_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
+          const int k0 = k_begin + 2 * p;
+          const int64_t bi = static_cast<int64_t>(s) * K + k0;
+          const uint32_t o0 = a.blk_off[bi], o1 = a.blk_off[bi + 1];
+          uint32_t bytes = o1 - o0;
+          uint32_t o2 = o1;
+          if (k0 + 1 < K) {
+            o2 = a.blk_off[bi + 2];
+            bytes += o2 - o1;
+          }
+          mbar_expect_tx(bar(W_D_FULL + ds), bytes);
+          bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(W_D_FULL + ds));
+          if (k0 + 1 < K)
+            bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES + BLOCK_MAX_BYTES, a.blocks + o1, o2 - o1,
+                     bar(W_D_FULL + ds));
+        }
+        ++d_it;
+      }
+      __syncwarp();
+    }
+  } else if (warp == 5) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16(128, 64, true, true);
+      uint32_t a_it = 0, g_it = 0;
+      bool first = true;
+      for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+        mbar_wait(bar(W_G_FULL), g_it & 1);
+        for (int p = 0; p < n_pairs; ++p) {
+          const uint32_t as = a_it % WG_NSA;
+          mbar_wait(bar(W_A_FULL + as), (a_it / WG_NSA) & 1);
+          tc_fence_after();
+          const uint32_t d = tmem + p * 64;
+#pragma unroll
+          for (int ks = 0; ks < 8; ++ks) {
+            // K = points: 16 rows per step (2 x 8-row groups of 1024 B)
+            const uint64_t ad = sdesc_sw128(s_a + as * 32768u + 2048u * ks, 16384, 1024);
+            const uint64_t bd = sdesc_sw128(s_g + 2048u * ks, 16384, 1024);
+            umma_bf16(d, ad, bd, idesc, (first && ks == 0) ? 0u : 1u);
+          }
+          umma_commit(bar(W_A_EMPTY + as));
+          ++a_it;
+        }
+        first = false;
+        umma_commit(bar(W_G_EMPTY));
+        ++g_it;
+      }
+      umma_commit(bar(W_DONE));
+    }
+    __syncwarp();
+  } else if (warp >= FWD_AGG_WARP0) {
+    const int aw = warp - FWD_AGG_WARP0;
+    const int sub_l = lane >> 3, l8 = lane & 7;
+    uint32_t a_it = 0, d_it = 0, h_it = 0;
+    for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+      mbar_wait(bar(W_HALO_FULL), h_it & 1);
+      ++h_it;
+      for (int p = 0; p < n_pairs; ++p) {
+        const uint32_t ds = d_it % NSD, as = a_it % WG_NSA;
+        mbar_wait(bar(W_D_FULL + ds), (d_it / NSD) & 1);
+        mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
+        const int ncell = (k_begin + 2 * p + 1 < K) ? 2 : 1;
+        for (int half = 0; half < 2; ++half) {
+          uint8_t* A = g_a + as * 32768 + half * 16384;
+          const uint8_t* blk = g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES;
+          const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
+          const uint16_t* ents = reinterpret_cast<const uint16_t*>(blk + 512);
+#pragma unroll 1
+          for (int q = aw; q < TM / 4; q += FWD_AGG_WARPS) {
+            uint32_t r, c, eo;
+            if (half < ncell) {
+              const uint32_t item = items[q * 4 + sub_l];
+              r = item & 127u;
+              c = (item >> 7) & 31u;
+              eo = item >> 12;
+            } else {
+              r = q * 4 + sub_l;
+              c = 0;
+              eo = 0;
+            }
+            uint32_t cmax = c;
+            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 8));
+            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 16));
+            uint4 outv = make_uint4(0, 0, 0, 0);
+            if (cmax <= 1) {
+              if (c == 1)
+                outv = *reinterpret_cast<const uint4*>(g_halo + ents[eo] * 128u + l8 * 16u);
+            } else {
+              float acc[8];
+#pragma unroll
+              for (int x = 0; x < 8; ++x) acc[x] = 0.f;
+              for (uint32_t it = 0; it < cmax; ++it) {
+                if (it < c) {
+                  const uint4 v =
+                      *reinterpret_cast<const uint4*>(g_halo + ents[eo + it] * 128u + l8 * 16u);
+                  acc_bf16x2(acc[0], acc[1], v.x);
+                  acc_bf16x2(acc[2], acc[3], v.y);
+                  acc_bf16x2(acc[4], acc[5], v.z);
+                  acc_bf16x2(acc[6], acc[7], v.w);
+                }
+              }
+              outv.x = pack_bf16x2(acc[0], acc[1]);
+              outv.y = pack_bf16x2(acc[2], acc[3]);
+              outv.z = pack_bf16x2(acc[4], acc[5]);
+              outv.w = pack_bf16x2(acc[6], acc[7]);
+              if (c == 1)
+                outv = *reinterpret_cast<const uint4*>(g_halo + ents[eo] * 128u + l8 * 16u);
+            }
+            *reinterpret_cast<uint4*>(A + r * 128u + (((l8 ^ (r & 7u)) & 7u) << 4)) = outv;
+          }
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(bar(W_A_FULL + as));
+          mbar_arrive(bar(W_D_EMPTY + ds));
+        }
+        ++a_it;
+        ++d_it;
+      }
+      if (lane == 0) mbar_arrive(bar(W_HALO_EMPTY));
+    }
+  } else {
+    // warps 0-3: dense G tile loader during the sweep, epilogue at the end
+    uint32_t g_it = 0;
+    for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+      mbar_wait(bar(W_G_EMPTY), (g_it & 1) ^ 1);
+      // 128 rows x 8 chunks of 16 B; warp e copies rows 32e..32e+31
+      for (int x = lane; x < 32 * 8; x += 32) {
+        const int r = 32 * warp + (x >> 3), q = x & 7;
+        const int64_t row = static_cast<int64_t>(s) * TM + r;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (row < a.n_rows) v = reinterpret_cast<const uint4*>(a.dense + row * CH)[q];
+        *reinterpret_cast<uint4*>(g_gt + r * 128 + (((q ^ (r & 7)) & 7) << 4)) = v;
+      }
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(W_G_FULL));
+      ++g_it;
+    }
+    // epilogue: TMEM lanes 32e..32e+31 of each pair accumulator -> partial
+    mbar_wait(bar(W_DONE), 0);
+    if (blockIdx.x >= a.n_sub) goto done;
+    tc_fence_after();
+    const int e = warp;
+    for (int p = 0; p < n_pairs; ++p) {
+      uint32_t v[4][16];
+      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + p * 64;
+      tmem_ld16(t0 + 0, v[0]);
+      tmem_ld16(t0 + 16, v[1]);
+      tmem_ld16(t0 + 32, v[2]);
+      tmem_ld16(t0 + 48, v[3]);
+      tmem_ld_wait();
+      const int k = k_begin + 2 * p + (e >> 1);
+      const int c = 32 * (e & 1) + lane;
+      if (k < K) {
+        float4* o = reinterpret_cast<float4*>(
+            a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * CH + c) * CH);
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+            o[q * 4 + x] = make_float4(__uint_as_float(v[q][4 * x]), __uint_as_float(v[q][4 * x + 1]),
+                                       __uint_as_float(v[q][4 * x + 2]),
+                                       __uint_as_float(v[q][4 * x + 3]));
+      }
+    }
+  }
+done:
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_free<512>(tmem);
+}
+
+// grad_w[k][m][c] = sum over CTAs x (fixed order) of partial[x][k][c][m]
+__global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, int K,
+                               float* __restrict__ grad_w) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (k, m, c)
+  if (idx >= K * CH * CH) return;
+  const int k = idx / (CH * CH), m = (idx / CH) % CH, c = idx % CH;
+  float s = 0.f;
+  for (int x = 0; x < n_part; ++x) s += partial[((static_cast<int64_t>(x) * K + k) * CH + c) * CH + m];
+  grad_w[idx] = s;
+}
+
+// ===========================================================================
+// host drivers
+// ===========================================================================
+constexpr int FWD_ST = 3, FWD_HCAP = 1280;
+constexpr int WG_HCAP = 768;
+
+static TcPlan* get_plan(npcg_context* ctx, npcg_neighbors* nb) {
+  if (!nb->tc) {
+    auto* p = new TcPlan();
+    nb->tc.reset(p);
+    p->inv_perm_out.alloc(ctx, nb->n_out);
+    p->inv_perm_in.alloc(ctx, nb->n_in);
+    if (nb->n_out)
+      launch(ctx, "inverse_perm", k_inverse_perm, dim3(static_cast<unsigned>(ceil_div(nb->n_out, 256))),
+             dim3(256), 0, static_cast<const uint32_t*>(nb->perm_out.get()), nb->n_out,
+             p->inv_perm_out.get());
+    if (nb->n_in)
+      launch(ctx, "inverse_perm", k_inverse_perm, dim3(static_cast<unsigned>(ceil_div(nb->n_in, 256))),
+             dim3(256), 0, static_cast<const uint32_t*>(nb->perm_in.get()), nb->n_in,
+             p->inv_perm_in.get());
+  }
+  return nb->tc.get();
+}
+
+static TcDirPlan* plan_fwd(npcg_context* ctx, npcg_neighbors* nb) {
+  TcPlan* p = get_plan(ctx, nb);
+  if (!p->fwd)
+    p->fwd = build_dir_plan(ctx, nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out,
+                            nb->n_in, nb->perm_out.get(), p->inv_perm_in.get(),
+                            static_cast<int>(nb->n_kernels), FWD_ST, FWD_HCAP);
+  return p->fwd.get();
+}
+static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
+  TcPlan* p = get_plan(ctx, nb);
+  if (!p->bwd) {
+    build_tcsr(ctx, nb);
+    p->bwd = build_dir_plan(ctx, nb->tcsr->row_ptr.get(), nb->tcsr->col.get(), nb->tcsr->k.get(),
+                            nb->n_in, nb->n_out, nb->perm_in.get(), p->inv_perm_out.get(),
+                            static_cast<int>(nb->n_kernels), FWD_ST, FWD_HCAP);
+  }
+  return p->bwd.get();
+}
+static TcDirPlan* plan_wg(npcg_context* ctx, npcg_neighbors* nb) {
+  TcPlan* p = get_plan(ctx, nb);
+  if (!p->wg)
+    p->wg = build_dir_plan(ctx, nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out,
+                           nb->n_in, nb->perm_out.get(), p->inv_perm_in.get(),
+                           static_cast<int>(nb->n_kernels), 1, WG_HCAP);
+  return p->wg.get();
+}
+
+void tc_prepare(npcg_context* ctx, npcg_neighbors* nb) {
+  plan_fwd(ctx, nb);
+  plan_bwd(ctx, nb);
+  plan_wg(ctx, nb);
+}
+
+static void convert(npcg_context* ctx, const float* src, const uint32_t* perm, int64_t n,
+                    DevBuf<__nv_bfloat16>& dst) {
+  if (dst.size() < n * CH) dst.alloc(ctx, n * CH);
+  if (n == 0) return;
+  launch(ctx, "to_bf16_perm", k_to_bf16_perm, dim3(static_cast<unsigned>(ceil_div(n * 8, 256))),
+         dim3(256), 0, src, perm, n, dst.get());
+}
+
+static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose) {
+  if (p->wpack.size() < static_cast<int64_t>(K) * 8192) p->wpack.alloc(ctx, static_cast<int64_t>(K) * 8192);
+  launch(ctx, "pack_w", k_pack_w, dim3(static_cast<unsigned>(ceil_div(K * CH * CH, 256))), dim3(256),
+         0, w, K, transpose, p->wpack.get());
+}
+
+static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16* feat,
+                           const uint8_t* wpack, const uint32_t* perm_rows, float* out,
+                           const char* name) {
+  if (P->n_super == 0) return;
+  FwdArgs a{};
+  a.halo = P->halo.get();
+  a.halo_len = P->halo_len.get();
+  a.blk_off = P->blk_off.get();
+  a.blocks = P->blocks.get();
+  a.perm_rows = perm_rows;
+  a.n_rows = P->n_rows;
+  a.n_sub = P->n_sub;
+  a.n_super = P->n_super;
+  a.st = P->st;
+  a.hcap = P->hcap;
+  a.K = P->K;
+  a.feat = feat;
+  a.wpack = wpack;
+  a.out = out;
+  const FwdSmem L = fwd_smem_layout(P->hcap);
+  NPCG_CUDA(cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(L.total)));
+  const int grid = std::min(P->n_super, ctx->num_sms);
+  launch(ctx, name, k_conv_fwd_tc, dim3(grid), dim3(FWD_THREADS), L.total, a);
+}
+
+static bool plan_ok(const TcDirPlan* P) { return P->n_overflow == 0; }
+
+void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
+                float* fout) {
+  TcDirPlan* P = plan_fwd(ctx, nb);
+  if (!plan_ok(P)) {  // irregular geometry beyond the tile capacities: exact engine
+    const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
+    mvmr_rows<float>(ctx, v, w, fin, 1, CH, CH, fout);
+    return;
+  }
+  TcPlan* p = nb->tc.get();
+  convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+  pack_w(ctx, p, w, P->K, false);
+  run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout, "conv_fwd_tc");
+}
+
+void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
+                 const float* gout, float* grad_in, float* grad_w) {
+  TcPlan* p = get_plan(ctx, nb);
+  const int K = static_cast<int>(nb->n_kernels);
+  if (grad_in) {
+    TcDirPlan* P = plan_bwd(ctx, nb);
+    if (!plan_ok(P)) {
+      DevBuf<float> wt(ctx, static_cast<int64_t>(K) * CH * CH);
+      transpose_w<float>(ctx, w, K, CH, CH, wt.get());
+      mvmr_rows<float>(ctx, nb->tcsr->view(), wt.get(), gout, 1, CH, CH, grad_in);
+    } else {
+      convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
+      pack_w(ctx, p, w, K, true);
+      run_fwd_kernel(ctx, P, p->feat_out.get(), p->wpack.get(), nb->perm_in.get(), grad_in,
+                     "conv_dgrad_tc");
+    }
+  }
+  if (grad_w) {
+    TcDirPlan* P = plan_wg(ctx, nb);
+    if (!plan_ok(P)) {
+      build_cells(ctx, nb);
+      vvor_cells<float>(ctx, *nb->cells, gout, fin, 1, CH, CH, grad_w);
+      return;
+    }
+    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+    if (!grad_in || !plan_ok(plan_bwd(ctx, nb)))
+      convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
+    const int gx = std::max(1, std::min(P->n_sub, ctx->num_sms / 2));
+    const int64_t need = static_cast<int64_t>(gx) * K * CH * CH;
+    if (p->partial.size() < need) p->partial.alloc(ctx, need);
+    NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
+    WgArgs a{};
+    a.halo = P->halo.get();
+    a.halo_len = P->halo_len.get();
+    a.blk_off = P->blk_off.get();
+    a.blocks = P->blocks.get();
+    a.n_rows = P->n_rows;
+    a.n_sub = P->n_sub;
+    a.hcap = P->hcap;
+    a.K = K;
+    a.feat = p->feat_in.get();
+    a.dense = p->feat_out.get();
+    a.partial = p->partial.get();
+    const WgSmem L = wg_smem_layout(P->hcap);
+    NPCG_CUDA(cudaFuncSetAttribute(k_conv_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   static_cast<int>(L.total)));
+    const int groups = (K + 2 * WG_PAIRS - 1) / (2 * WG_PAIRS);
+    launch(ctx, "conv_wgrad_tc", k_conv_wgrad_tc, dim3(gx, groups), dim3(WG_THREADS), L.total, a);
+    launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(K * CH * CH, 256))),
+           dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, grad_w);
+  }
+}
+
+// plan statistics for the bench / tests: [n_super, n_overflow, max_halo, mean_halo*100] x 3 dirs
+void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12) {
+  tc_prepare(ctx, nb);
+  TcPlan* p = nb->tc.get();
+  const TcDirPlan* ds[3] = {p->fwd.get(), p->bwd.get(), p->wg.get()};
+  for (int i = 0; i < 3; ++i) {
+    out12[4 * i + 0] = ds[i]->n_super;
+    out12[4 * i + 1] = ds[i]->n_overflow;
+    out12[4 * i + 2] = ds[i]->max_halo;
+    out12[4 * i + 3] = static_cast<int64_t>(ds[i]->mean_halo * 100);
+  }
+}
+
 }  // namespace npcg

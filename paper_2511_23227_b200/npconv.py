@@ -345,6 +345,15 @@ class Neighbors:
         return TripletList(i, j, k, self.n_out, self.n_in, self.n_kernels, SortAxis(axis),
                            handle=self if axis == SortAxis.none else None)
 
+    def plan_stats(self) -> dict:
+        out = (C.c_int64 * 12)()
+        h = self.ctx.bind()
+        self.ctx.check(L.lib().npcg_neighbors_plan_stats(h, self.h, out), "plan_stats")
+        v = list(out)
+        return {name: {"super_tiles": v[4 * i], "overflow": v[4 * i + 1], "max_halo": v[4 * i + 2],
+                       "mean_halo": v[4 * i + 3] / 100.0}
+                for i, name in enumerate(("fwd", "dgrad", "wgrad"))}
+
     def prepare(self, math: Math = Math.auto):
         h = self.ctx.bind()
         self.ctx.check(L.lib().npcg_neighbors_prepare(h, self.h, int(math)), "prepare")

@@ -126,3 +126,132 @@ def test_c2_fwd_bwd_parity(npc, orc):
     assert rel(out.cpu(), fo) <= 1e-5
     assert rel(res.grad_in.cpu(), gi) <= 1e-5
     assert rel(res.grad_w.cpu(), gw) <= 1e-5
+
+
+# ---------------------------------------------------------------------------
+# bf16 tensor-core path (tcgen05): C = 64, G = 1, t = 3
+# ---------------------------------------------------------------------------
+def _bf16(x):
+    return torch.as_tensor(np.ascontiguousarray(x, dtype=np.float32)).to(torch.bfloat16).float().numpy()
+
+
+def _emulate_tc(ti, tj, tk, n_out, n_in, w, f, g):
+    """The exact arithmetic of the tensor-core engines, in numpy: per (row, cell)
+    aggregation of bf16-rounded neighbor rows with fp32 accumulation in CSR order,
+    rounded to bf16, then GEMMs against bf16-rounded weights (fp64 here; the
+    device accumulates in fp32, so agreement is ~1e-6)."""
+    K = w.shape[0]
+    wb = _bf16(w[:, 0]).astype(np.float64)          # (K, Cin, Cout)
+    fb, gb = _bf16(f[:, 0]), _bf16(g[:, 0])
+    ti, tj, tk = ti.astype(np.int64), tj.astype(np.int64), tk.astype(np.int64)
+    # forward aggregation over (i, k), CSR order = (i, j) order of the build
+    A = np.zeros((n_out, K, 64), np.float32)
+    np.add.at(A, (ti, tk), fb[tj])
+    A = _bf16(A.reshape(-1, 64)).reshape(n_out, K, 64).astype(np.float64)
+    fout = np.einsum("nkc,kcm->nm", A, wb)
+    # dgrad aggregation over (j, k) in (j, i) order
+    o = np.lexsort((ti, tj))
+    B = np.zeros((n_in, K, 64), np.float32)
+    np.add.at(B, (tj[o], tk[o]), gb[ti[o]])
+    B = _bf16(B.reshape(-1, 64)).reshape(n_in, K, 64).astype(np.float64)
+    gin = np.einsum("nkm,kcm->nc", B, wb)
+    gw = np.einsum("nm,nkc->kmc", gb.astype(np.float64), A)
+    return fout, gin, gw
+
+
+def _bf16_case(npc, orc, n, seed=1):
+    xyz = orc.gen_uniform_cube(n, 1.0, seed)
+    r = 1.8 * n ** (-1 / 3)
+    w = orc.make_weights(3, 1, 64, 64, 2)
+    f = orc.gen_features(n, 1, 64, 3)
+    go = orc.gen_features(n, 1, 64, 4)
+    ti, tj, tk = orc.build_triplets(xyz, xyz, r, 3)
+    return xyz, r, w, f, go, (ti, tj, tk)
+
+
+def test_bf16_path_matches_emulation_and_oracle(npc, orc):
+    n = 8192
+    xyz, r, w, f, go, (ti, tj, tk) = _bf16_case(npc, orc, n)
+    cl = npc.make_point_cloud(xyz)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
+    out = op.forward(cl, T(f))
+    res = op.backward(T(go))
+    st = op.neighbors().plan_stats()
+    assert all(v["overflow"] == 0 for v in st.values()), st
+    efo, egi, egw = _emulate_tc(ti, tj, tk, n, n, w, f, go)
+    # precision-isolated: identical bf16 operands, only accumulation order differs
+    assert rel(out.cpu().numpy()[:, 0], efo) <= 2e-5
+    assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= 2e-5
+    assert rel(res.grad_w.cpu().numpy()[:, 0], egw) <= 2e-5
+    # end-to-end bound vs the fp64 oracle on the fp32 inputs (SURVEY.md §8d: <= 1e-2)
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
+                                go.astype(np.float64))
+    assert rel(out.cpu(), fo) <= 1e-2
+    assert rel(res.grad_in.cpu(), gi) <= 1e-2
+    assert rel(res.grad_w.cpu(), gw) <= 1e-2
+
+
+def test_bf16_path_deterministic(npc, orc):
+    n = 20000
+    xyz, r, w, f, go, _ = _bf16_case(npc, orc, n, seed=5)
+    cl = npc.make_point_cloud(xyz)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
+    a = op.forward(cl, T(f))
+    ra = op.backward(T(go))
+    b = op.forward(cl, T(f))
+    rb = op.backward(T(go))
+    assert torch.equal(a, b)
+    assert torch.equal(ra.grad_in, rb.grad_in)
+    assert torch.equal(ra.grad_w, rb.grad_w)
+
+
+def test_bf16_raw_triplets_api(npc, orc):
+    """npcg_mvmr / mvmr_transposed / vvor with math=bf16 on a raw TripletList
+    (identity order, no coordinates)."""
+    n = 3000
+    xyz, r, w, f, go, (ti, tj, tk) = _bf16_case(npc, orc, n, seed=9)
+    si, sj, sk = orc.sort_triplets(ti, tj, tk, 3, n, n, 27)
+    tl = npc.TripletList.from_numpy(si, sj, sk, n, n, 27, 3)
+    c = npc.ExecConfig(math=npc.Math.bf16)
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
+                                go.astype(np.float64))
+    assert rel(npc.mvmr(T(w), T(f), tl, n, c).out.cpu(), fo) <= 1e-2
+    assert rel(npc.mvmr_transposed(T(w), T(go), tl, n, c).out.cpu(), gi) <= 1e-2
+    assert rel(npc.vvor(T(go), T(f), tl, 27, c).grad.cpu(), gw) <= 1e-2
+
+
+def test_bf16_clustered_cloud(npc, orc, ref):
+    """Dense clusters stress the tile capacities; super-tiles beyond them are
+    served by the exact engine, results stay within the bf16 bound."""
+    xyz = ref.gen_gaussian_clusters(30000, 20, 4.0, 0.15, 21)
+    r = 0.08
+    w = orc.make_weights(3, 1, 64, 64, 2)
+    f = orc.gen_features(30000, 1, 64, 3)
+    go = orc.gen_features(30000, 1, 64, 4)
+    ti, tj, tk = orc.build_triplets(xyz, xyz, r, 3)
+    cl = npc.make_point_cloud(xyz)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
+    out = op.forward(cl, T(f))
+    res = op.backward(T(go))
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, 30000,
+                                go.astype(np.float64))
+    assert rel(out.cpu(), fo) <= 1e-2
+    assert rel(res.grad_in.cpu(), gi) <= 1e-2
+    assert rel(res.grad_w.cpu(), gw) <= 1e-2
+
+
+@pytest.mark.slow
+def test_c2_bf16_fwd_bwd(npc, orc):
+    """BASELINE config 2 (100K, C=64) on the tensor-core path, bound 1e-2."""
+    n = 100000
+    xyz, r, w, f, go, (ti, tj, tk) = _bf16_case(npc, orc, n)
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
+                                go.astype(np.float64))
+    cl = npc.make_point_cloud(xyz)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.auto))
+    out = op.forward(cl, T(f))
+    res = op.backward(T(go))
+    st = op.neighbors().plan_stats()
+    assert all(v["overflow"] == 0 for v in st.values()), st
+    e = (rel(out.cpu(), fo), rel(res.grad_in.cpu(), gi), rel(res.grad_w.cpu(), gw))
+    assert max(e) <= 1e-2, e
