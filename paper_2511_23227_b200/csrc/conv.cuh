@@ -9,6 +9,9 @@ namespace npcg {
 template <typename T>
 void mvmr_rows(npcg_context* ctx, const CsrView& csr, const T* w, const T* fin, int G, int cin,
                int cout, T* out);
+void mvmr_rows_subset_f32(npcg_context* ctx, const CsrView& csr, const uint32_t* perm,
+                          const uint32_t* list, int64_t n_list, const float* w, const float* fin,
+                          int cin, int cout, float* out);
 template <typename T>
 void transpose_w(npcg_context* ctx, const T* w, int64_t KG, int cin, int cout, T* wt);
 template <typename T>

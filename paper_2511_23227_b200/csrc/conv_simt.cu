@@ -64,6 +64,55 @@ __global__ void __launch_bounds__(256) k_mvmr_rows(CsrView csr, const T* __restr
   }
 }
 
+// Rows given as a list of positions into `perm` (row = perm[list[x]]): the
+// exact engine for the rows of tensor-core super-tiles beyond tile capacity.
+template <typename T, int R>
+__global__ void __launch_bounds__(256) k_mvmr_rows_subset(CsrView csr, const uint32_t* __restrict__ perm,
+                                                          const uint32_t* __restrict__ list,
+                                                          int64_t n_list, const T* __restrict__ w,
+                                                          const T* __restrict__ fin, int cin,
+                                                          int cout, T* __restrict__ out) {
+  const int64_t x = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (x >= n_list) return;
+  const int64_t row = perm[list[x]];
+  T acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) acc[r] = T(0);
+  for (int64_t e = csr.row_ptr[row]; e < csr.row_ptr[row + 1]; ++e) {
+    const T* f = fin + static_cast<int64_t>(csr.col[e]) * cin;
+    const T* wm = w + static_cast<int64_t>(csr.k[e]) * cin * cout;
+    for (int c0 = 0; c0 < cin; c0 += 32) {
+      const T fv = (c0 + lane < cin) ? f[c0 + lane] : T(0);
+      const int cn = cin - c0 < 32 ? cin - c0 : 32;
+      for (int cc = 0; cc < cn; ++cc) {
+        const T fc = __shfl_sync(0xffffffffu, fv, cc);
+        const T* wr = wm + static_cast<int64_t>(c0 + cc) * cout;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const int m = lane + 32 * r;
+          if (m < cout) acc[r] = fma(wr[m], fc, acc[r]);
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int m = lane + 32 * r;
+    if (m < cout) out[row * cout + m] = acc[r];
+  }
+}
+
+void mvmr_rows_subset_f32(npcg_context* ctx, const CsrView& csr, const uint32_t* perm,
+                          const uint32_t* list, int64_t n_list, const float* w, const float* fin,
+                          int cin, int cout, float* out) {
+  if (n_list == 0) return;
+  const unsigned blocks = static_cast<unsigned>(ceil_div(n_list * 32, 256));
+  if (cout > 64) fail(NPCG_ERR_UNSUPPORTED, "row-subset engine: C_out <= 64");
+  launch(ctx, "mvmr_simt_subset", k_mvmr_rows_subset<float, 2>, dim3(blocks), dim3(256), 0, csr,
+         perm, list, n_list, w, fin, cin, cout, out);
+}
+
 template <typename T>
 void mvmr_rows(npcg_context* ctx, const CsrView& csr, const T* w, const T* fin, int G, int cin,
                int cout, T* out) {

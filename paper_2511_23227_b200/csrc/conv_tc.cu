@@ -38,7 +38,7 @@ constexpr int TM = 128;
 constexpr int CH = 64;
 constexpr int KMAX = 32;
 constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sorts in smem
-constexpr int MAX_BLOCK_ENTRIES = 1024;  // entries per (sub-tile, cell) block
+constexpr int MAX_BLOCK_ENTRIES = 512;   // entries per (sub-tile, cell) block
 constexpr int BLOCK_MAX_BYTES = 512 + 2 * MAX_BLOCK_ENTRIES;
 constexpr uint32_t kOverflow = 0xFFFFFFFFu;
 
@@ -47,13 +47,17 @@ struct TcDirPlan {
   int hcap = 1280;
   int64_t n_rows = 0, n_cols = 0;
   int n_sub = 0, n_super = 0, K = 0;
-  DevBuf<uint32_t> halo;      // n_super * hcap, permuted column index
+  DevBuf<uint32_t> halo;      // n_super * hcap permuted source row of each halo row
+  DevBuf<uint2> runs;         // n_super * hcap copy runs {src row, dst row | len << 16}
+  DevBuf<uint32_t> n_runs;    // n_super
   DevBuf<uint32_t> halo_len;  // n_super (kOverflow marks a super-tile the planner rejected)
   DevBuf<uint32_t> blk_off;   // n_sub*K + 1 byte offsets of the stage-descriptor blocks
   DevBuf<uint8_t> blocks;
   int n_overflow = 0;
   int max_halo = 0;
   double mean_halo = 0.0;
+  DevBuf<uint32_t> spill_rows;  // permuted positions of rows in overflow super-tiles
+  int64_t n_spill = 0;
 };
 
 struct TcPlan {
@@ -127,7 +131,8 @@ __global__ void __launch_bounds__(512) k_plan_super(
     const uint32_t* __restrict__ kk, const uint32_t* __restrict__ perm_rows,
     const uint32_t* __restrict__ inv_perm_cols, int64_t n_rows, int K, int n_sub, int st, int hcap,
     const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ sub_bad,
-    uint32_t* __restrict__ halo_out, uint32_t* __restrict__ halo_len,
+    uint32_t* __restrict__ halo_out, uint2* __restrict__ runs_out, uint32_t* __restrict__ n_runs,
+    uint32_t* __restrict__ halo_len,
     uint8_t* __restrict__ blocks) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* buf = reinterpret_cast<uint32_t*>(sm);                          // MAXE_ST
@@ -264,6 +269,42 @@ __global__ void __launch_bounds__(512) k_plan_super(
     }
   }
   __syncthreads();
+  // 4b. copy runs of consecutive rows: {src row, dst | len << 16}
+  {
+    const int per2 = (H + blockDim.x - 1) / blockDim.x;
+    const int a0 = tid * per2, a1 = min(H, a0 + per2);
+    int nst = 0;
+    for (int x = a0; x < a1; ++x)
+      if (x == 0 || buf[x] != buf[x - 1] + 1) ++nst;
+    int ri = nst;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, ri, o);
+      if (lane >= o) ri += n;
+    }
+    if (lane == 31) wsum[warp] = ri;
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int w = 0; w < 16; ++w) {
+        const int v = wsum[w];
+        wsum[w] = acc;
+        acc += v;
+      }
+      n_runs[s] = acc;
+    }
+    __syncthreads();
+    int r0 = ri - nst + wsum[warp];
+    for (int x = a0; x < a1; ++x) {
+      if (x == 0 || buf[x] != buf[x - 1] + 1) {
+        int e = x + 1;
+        while (e < H && buf[e] == buf[e - 1] + 1) ++e;
+        runs_out[static_cast<int64_t>(s) * hcap + r0++] =
+            make_uint2(buf[x], static_cast<uint32_t>(x) | (static_cast<uint32_t>(e - x) << 16));
+      }
+    }
+  }
+  __syncthreads();
   // 5. items per (sub, cell) block: rows by count descending (stable in r)
   const unsigned lt = (1u << lane) - 1u;
   for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
@@ -338,6 +379,8 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   exclusive_scan_u32(ctx, blk_size.get(), P->blk_off.get(), nblk + 1, &total);
   P->blocks.alloc(ctx, total);
   P->halo.alloc(ctx, static_cast<int64_t>(P->n_super) * hcap);
+  P->runs.alloc(ctx, static_cast<int64_t>(P->n_super) * hcap);
+  P->n_runs.alloc(ctx, P->n_super);
   P->halo_len.alloc(ctx, P->n_super);
   const size_t smem = MAXE_ST * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
   NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -345,7 +388,7 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   launch(ctx, "plan_super", k_plan_super, dim3(P->n_super), dim3(512), smem, row_ptr, col, kk,
          perm_rows, inv_perm_cols, n_rows, K, P->n_sub, st, hcap,
          static_cast<const uint32_t*>(P->blk_off.get()), static_cast<const uint32_t*>(sub_bad.get()),
-         P->halo.get(), P->halo_len.get(), P->blocks.get());
+         P->halo.get(), P->runs.get(), P->n_runs.get(), P->halo_len.get(), P->blocks.get());
   std::vector<uint32_t> hl(P->n_super);
   NPCG_CUDA(cudaMemcpyAsync(hl.data(), P->halo_len.get(), hl.size() * 4, cudaMemcpyDeviceToHost,
                             ctx->stream));
@@ -361,6 +404,19 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   }
   const int ok = P->n_super - P->n_overflow;
   P->mean_halo = ok ? sum / ok : 0.0;
+  if (P->n_overflow) {
+    std::vector<uint32_t> rows;
+    const int64_t per = static_cast<int64_t>(st) * TM;
+    for (int s2 = 0; s2 < P->n_super; ++s2)
+      if (hl[s2] == kOverflow)
+        for (int64_t p = s2 * per; p < std::min(n_rows, (s2 + 1) * per); ++p)
+          rows.push_back(static_cast<uint32_t>(p));
+    P->n_spill = static_cast<int64_t>(rows.size());
+    P->spill_rows.alloc(ctx, P->n_spill);
+    NPCG_CUDA(cudaMemcpyAsync(P->spill_rows.get(), rows.data(), rows.size() * 4,
+                              cudaMemcpyHostToDevice, ctx->stream));
+    NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  }
   return P;
 }
 
@@ -402,6 +458,8 @@ __global__ void k_pack_w(const float* __restrict__ w, int K, bool transpose,
 // ===========================================================================
 struct FwdArgs {
   const uint32_t* halo;
+  const uint2* runs;
+  const uint32_t* n_runs;
   const uint32_t* halo_len;
   const uint32_t* blk_off;
   const uint8_t* blocks;
@@ -413,16 +471,18 @@ struct FwdArgs {
   float* out;                 // (n_rows, 64), original order
 };
 
-constexpr int FWD_THREADS = 448;
 constexpr int FWD_AGG_WARP0 = 6;
-constexpr int FWD_AGG_WARPS = 8;
-constexpr int NSA = 2;  // A stages (16 KB)
-constexpr int NSW = 2;  // W stages (8 KB)
-constexpr int NSD = 2;  // stage-descriptor slots
-constexpr int FWD_ACC_COLS = 192;  // 3 sub-tiles x 64 fp32 columns
+constexpr int FWD_AGG_WARPS = 16;
+constexpr int FWD_W_WARP = FWD_AGG_WARP0 + FWD_AGG_WARPS;
+constexpr int FWD_THREADS = 32 * (FWD_W_WARP + 1);
+constexpr int FWD_ST = 2, FWD_HCAP = 960;  // 256-row super-tiles, halo <= 960 rows (120 KB)
+constexpr int NSA = 4;  // A stages (16 KB)
+constexpr int NSW = 3;  // W stages (8 KB)
+constexpr int NSD = 8;  // stage-descriptor slots
+constexpr int FWD_ACC_COLS = FWD_ST * 64;  // fp32 accumulator columns per TMEM buffer
 
 struct FwdSmem {
-  uint32_t halo, a, w, d, bar, tmem_slot;
+  uint32_t halo, a, w, d, bar, tmem_slot, offs;
   size_t total;
 };
 __host__ __device__ inline FwdSmem fwd_smem_layout(int hcap) {
@@ -439,27 +499,139 @@ __host__ __device__ inline FwdSmem fwd_smem_layout(int hcap) {
   o += NSD * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
   L.bar = o;
-  o += 32 * 8;
+  o += 48 * 8;
   L.tmem_slot = o;
   o += 16;
+  L.offs = o;
+  o += 128 * 4;
   L.total = o + 1024;  // alignment slack
   return L;
+}
+
+// Warm L2 with the next super-tile's halo rows (one prefetch per copy run).
+__device__ __forceinline__ void prefetch_halo_l2(const uint2* runs, uint32_t nr,
+                                                 const __nv_bfloat16* feat, int lane) {
+  for (uint32_t r = lane; r < nr; r += 32) {
+    const uint2 v = runs[r];
+    bulk_prefetch_l2(feat + static_cast<int64_t>(v.x) * CH, (v.y >> 16) * 128u);
+  }
+}
+// Cooperative halo load by the aggregation warps: 16-byte cp.async per lane,
+// 8 lanes per 128-byte row (coalesced within runs of consecutive rows).
+template <int NT>
+__device__ __forceinline__ void coop_load_halo(const uint32_t* rows, uint32_t H,
+                                               const __nv_bfloat16* feat, uint32_t s_halo,
+                                               int t) {
+  const uint32_t q = static_cast<uint32_t>(t & 7);
+  for (uint32_t h = static_cast<uint32_t>(t) >> 3; h < H; h += NT / 8)
+    cp_async16(s_halo + h * 128u + q * 16u,
+               reinterpret_cast<const uint8_t*>(feat + static_cast<int64_t>(rows[h]) * CH) + q * 16u);
+  cp_async_wait_all();
+}
+// Issue the bulk copies of one super-tile halo (runs of consecutive rows).
+__device__ __forceinline__ void load_halo(const uint2* runs, uint32_t nr,
+                                          const __nv_bfloat16* feat, uint32_t s_halo,
+                                          uint32_t bar_full, int lane) {
+  for (uint32_t r = lane; r < nr; r += 32) {
+    const uint2 v = runs[r];
+    bulk_g2s(s_halo + (v.y & 0xFFFFu) * 128u, feat + static_cast<int64_t>(v.x) * CH,
+             (v.y >> 16) * 128u, bar_full);
+  }
 }
 
 // barrier indices
 enum : int {
   B_HALO_FULL = 0,
   B_HALO_EMPTY = 1,
-  B_A_FULL = 2,          // NSA
-  B_A_EMPTY = 4,         // NSA
-  B_W_FULL = 6,          // NSW
-  B_W_EMPTY = 8,         // NSW
-  B_D_FULL = 10,         // NSD
-  B_D_EMPTY = 12,        // NSD
-  B_T_FULL = 14,         // 2
-  B_T_EMPTY = 16,        // 2
-  B_COUNT = 18
+  B_A_FULL = 2,              // NSA
+  B_A_EMPTY = B_A_FULL + NSA,
+  B_W_FULL = B_A_EMPTY + NSA,  // NSW
+  B_W_EMPTY = B_W_FULL + NSW,
+  B_D_FULL = B_W_EMPTY + NSW,  // NSD
+  B_D_EMPTY = B_D_FULL + NSD,
+  B_T_FULL = B_D_EMPTY + NSD,  // 2
+  B_T_EMPTY = B_T_FULL + 2,
+  B_COUNT = B_T_EMPTY + 2
 };
+static_assert(B_COUNT <= 48, "barrier region");
+
+// One pipeline stage of the aggregation: the 128 rows of a sub-tile for one
+// kernel cell.  Warp `aw` of NW handles quads aw, aw+NW, ... (4 rows, a
+// quarter-warp per 128-byte row).  Items are rows sorted by entry count
+// (descending), so quads are mostly count-uniform: count 0 -> zero row,
+// count 1 -> exact bf16 copy of the halo row, count >= 2 -> fp32 sum
+// (FHADD.BF16) rounded once to bf16.  All loads of the warp's quads are issued
+// before their uses (ILP), stores go to the SW128 K-major A tile.
+template <int NW>
+__device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_halo, uint32_t s_A,
+                                                int aw, int lane) {
+  constexpr int NQ = (TM / 4) / NW;
+  const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
+  const uint16_t* ents = reinterpret_cast<const uint16_t*>(blk + 512);
+  const int sub_l = lane >> 3;
+  const uint32_t l8x16 = static_cast<uint32_t>(lane & 7) << 4;
+  uint32_t it[NQ];
+#pragma unroll
+  for (int qi = 0; qi < NQ; ++qi) it[qi] = items[(aw + NW * qi) * 4 + sub_l];
+  uint32_t packed = 0;
+#pragma unroll
+  for (int qi = 0; qi < NQ; ++qi) packed |= ((it[qi] >> 7) & 31u) << (8 * qi);
+  packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 8));
+  packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 16));
+  uint4 v[NQ];
+#pragma unroll
+  for (int qi = 0; qi < NQ; ++qi) {
+    v[qi] = make_uint4(0, 0, 0, 0);
+    if (((it[qi] >> 7) & 31u) == 1u) {
+      const uint32_t h = ents[it[qi] >> 12];
+      v[qi] = lds128(s_halo + h * 128u + l8x16);
+    }
+  }
+  // quads with a row of >= 2 entries: fp32 sums, entries of all such quads interleaved
+  uint32_t cmall = packed;
+#pragma unroll
+  for (int qi = 1; qi < NQ; ++qi) cmall = __vmaxu4(cmall, packed >> (8 * qi));
+  cmall &= 0xFFu;
+  if (cmall >= 2u) {
+    float acc[NQ][8];
+#pragma unroll
+    for (int qi = 0; qi < NQ; ++qi)
+#pragma unroll
+      for (int x = 0; x < 8; ++x) acc[qi][x] = 0.f;
+    for (uint32_t e = 0; e < cmall; ++e) {
+      uint4 w[NQ];
+#pragma unroll
+      for (int qi = 0; qi < NQ; ++qi) {
+        const uint32_t c = (it[qi] >> 7) & 31u;
+        w[qi] = make_uint4(0, 0, 0, 0);
+        if (e < c && ((packed >> (8 * qi)) & 0xFFu) >= 2u)
+          w[qi] = lds128(s_halo + static_cast<uint32_t>(ents[(it[qi] >> 12) + e]) * 128u + l8x16);
+      }
+#pragma unroll
+      for (int qi = 0; qi < NQ; ++qi) {
+        acc_bf16x2(acc[qi][0], acc[qi][1], w[qi].x);
+        acc_bf16x2(acc[qi][2], acc[qi][3], w[qi].y);
+        acc_bf16x2(acc[qi][4], acc[qi][5], w[qi].z);
+        acc_bf16x2(acc[qi][6], acc[qi][7], w[qi].w);
+      }
+    }
+#pragma unroll
+    for (int qi = 0; qi < NQ; ++qi) {
+      const uint32_t c = (it[qi] >> 7) & 31u;
+      if (((packed >> (8 * qi)) & 0xFFu) >= 2u && c != 1u) {
+        v[qi].x = pack_bf16x2(acc[qi][0], acc[qi][1]);
+        v[qi].y = pack_bf16x2(acc[qi][2], acc[qi][3]);
+        v[qi].z = pack_bf16x2(acc[qi][4], acc[qi][5]);
+        v[qi].w = pack_bf16x2(acc[qi][6], acc[qi][7]);
+      }
+    }
+  }
+#pragma unroll
+  for (int qi = 0; qi < NQ; ++qi) {
+    const uint32_t r = it[qi] & 127u;
+    sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), v[qi]);
+  }
+}
 
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -471,8 +643,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   const uint32_t s_bar = base + L.bar;
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
-  const uint8_t* g_halo = gbase + L.halo;
-  uint8_t* g_a = gbase + L.a;
   const uint8_t* g_d = gbase + L.d;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -497,7 +667,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == 5) tmem_alloc<256>(smem_u32(tmem_slot));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -505,40 +675,22 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   const int K = a.K;
 
   if (warp == 4) {
-    // ------------------------------ producer ------------------------------
-    uint32_t w_it = 0, d_it = 0, h_it = 0;
+    // ------------------------ producer: halo + descriptors -----------------
+    uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
+    uint32_t d_it = 0;
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       const int nsub = min(a.st, a.n_sub - s * a.st);
-      const uint32_t H = a.halo_len[s];
-      const uint32_t* hl = a.halo + static_cast<int64_t>(s) * a.hcap;
-      mbar_wait(bar(B_HALO_EMPTY), (h_it & 1) ^ 1);
-      if (lane == 0) mbar_expect_tx(bar(B_HALO_FULL), H * 128u);
+      if (a.halo_len[s] == kOverflow) continue;
+      // stage this super-tile's descriptor offsets in smem
+      const int64_t ob = static_cast<int64_t>(s) * a.st * K;
+      for (int x = lane; x <= nsub * K; x += 32) offs[x] = a.blk_off[ob + x];
       __syncwarp();
-      for (uint32_t h = lane; h < H; h += 32) {
-        const uint32_t v = hl[h];
-        if (h == 0 || hl[h - 1] != v - 1) {
-          uint32_t n = 1;
-          while (h + n < H && hl[h + n] == v + n) ++n;
-          bulk_g2s(s_halo + h * 128u, a.feat + static_cast<int64_t>(v) * CH, n * 128u,
-                   bar(B_HALO_FULL));
-        }
-      }
-      ++h_it;
       for (int k = 0; k < K; ++k) {
-        if (lane == 0) {
-          const uint32_t ws = w_it % NSW;
-          mbar_wait(bar(B_W_EMPTY + ws), ((w_it / NSW) & 1) ^ 1);
-          mbar_expect_tx(bar(B_W_FULL + ws), 8192u);
-          bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u,
-                   bar(B_W_FULL + ws));
-        }
-        ++w_it;
         for (int g = 0; g < nsub; ++g) {
           if (lane == 0) {
             const uint32_t ds = d_it % NSD;
             mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
-            const int64_t bi = static_cast<int64_t>(s * a.st + g) * K + k;
-            const uint32_t o0 = a.blk_off[bi], o1 = a.blk_off[bi + 1];
+            const uint32_t o0 = offs[g * K + k], o1 = offs[g * K + k + 1];
             mbar_expect_tx(bar(B_D_FULL + ds), o1 - o0);
             bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(B_D_FULL + ds));
           }
@@ -546,7 +698,29 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         }
       }
       __syncwarp();
+      // warm L2 with the next super-tile's halo rows (after this tile's descriptors)
+      const int s_next = s + gridDim.x;
+      if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
+        prefetch_halo_l2(a.runs + static_cast<int64_t>(s_next) * a.hcap, a.n_runs[s_next],
+                         a.feat, lane);
     }
+  } else if (warp == FWD_W_WARP) {
+    // ------------------------ producer: W_k per super-tile and cell ---------
+    if (lane == 0) {
+      uint32_t w_it = 0;
+      for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
+        if (a.halo_len[s] == kOverflow) continue;
+        for (int k = 0; k < K; ++k) {
+          const uint32_t ws = w_it % NSW;
+          mbar_wait_sleep(bar(B_W_EMPTY + ws), ((w_it / NSW) & 1) ^ 1);
+          mbar_expect_tx(bar(B_W_FULL + ws), 8192u);
+          bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u,
+                   bar(B_W_FULL + ws));
+          ++w_it;
+        }
+      }
+    }
+    __syncwarp();
   } else if (warp == 5) {
     // ------------------------------ MMA issuer -----------------------------
     if (lane == 0) {
@@ -554,6 +728,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       uint32_t w_it = 0, a_it = 0, t_it = 0;
       for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
         const int nsub = min(a.st, a.n_sub - s * a.st);
+        if (a.halo_len[s] == kOverflow) continue;
         const uint32_t ab = t_it & 1;
         mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -585,58 +760,22 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   } else if (warp >= FWD_AGG_WARP0) {
     // ------------------------------ aggregation ----------------------------
     const int aw = warp - FWD_AGG_WARP0;
-    const int sub_l = lane >> 3, l8 = lane & 7;
-    uint32_t a_it = 0, d_it = 0, h_it = 0;
+    uint32_t a_it = 0, d_it = 0;
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       const int nsub = min(a.st, a.n_sub - s * a.st);
-      mbar_wait(bar(B_HALO_FULL), h_it & 1);
-      ++h_it;
+      const uint32_t H = a.halo_len[s];
+      if (H == kOverflow) continue;
+      named_bar_sync(1, 32 * FWD_AGG_WARPS);  // all aggregation warps done with the previous halo
+      coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat,
+                                         s_halo, 32 * aw + lane);
+      named_bar_sync(1, 32 * FWD_AGG_WARPS);
       for (int k = 0; k < K; ++k) {
         for (int g = 0; g < nsub; ++g) {
           const uint32_t ds = d_it % NSD, as = a_it % NSA;
           mbar_wait(bar(B_D_FULL + ds), (d_it / NSD) & 1);
           mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
-          const uint8_t* blk = g_d + ds * BLOCK_MAX_BYTES;
-          const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
-          const uint16_t* ents = reinterpret_cast<const uint16_t*>(blk + 512);
-          uint8_t* A = g_a + as * 16384;
-#pragma unroll 1
-          for (int q = aw; q < TM / 4; q += FWD_AGG_WARPS) {
-            const uint32_t item = items[q * 4 + sub_l];
-            const uint32_t r = item & 127u, c = (item >> 7) & 31u, eo = item >> 12;
-            uint32_t cmax = c;
-            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 8));
-            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 16));
-            uint4 outv;
-            if (cmax <= 1) {
-              // copy (or zero) path: exact bf16 row copy, no arithmetic
-              outv = make_uint4(0, 0, 0, 0);
-              if (c == 1) {
-                const uint32_t h = ents[eo];
-                outv = *reinterpret_cast<const uint4*>(g_halo + h * 128u + l8 * 16u);
-              }
-            } else {
-              float acc[8];
-#pragma unroll
-              for (int x = 0; x < 8; ++x) acc[x] = 0.f;
-              for (uint32_t it = 0; it < cmax; ++it) {
-                if (it < c) {
-                  const uint32_t h = ents[eo + it];
-                  const uint4 v = *reinterpret_cast<const uint4*>(g_halo + h * 128u + l8 * 16u);
-                  acc_bf16x2(acc[0], acc[1], v.x);
-                  acc_bf16x2(acc[2], acc[3], v.y);
-                  acc_bf16x2(acc[4], acc[5], v.z);
-                  acc_bf16x2(acc[6], acc[7], v.w);
-                }
-              }
-              outv.x = pack_bf16x2(acc[0], acc[1]);
-              outv.y = pack_bf16x2(acc[2], acc[3]);
-              outv.z = pack_bf16x2(acc[4], acc[5]);
-              outv.w = pack_bf16x2(acc[6], acc[7]);
-              if (c == 1) outv = *reinterpret_cast<const uint4*>(g_halo + ents[eo] * 128u + l8 * 16u);
-            }
-            *reinterpret_cast<uint4*>(A + r * 128u + (((l8 ^ (r & 7u)) & 7u) << 4)) = outv;
-          }
+          aggregate_stage<FWD_AGG_WARPS>(g_d + ds * BLOCK_MAX_BYTES, s_halo, s_a + as * 16384u,
+                                         aw, lane);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -647,7 +786,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           ++d_it;
         }
       }
-      if (lane == 0) mbar_arrive(bar(B_HALO_EMPTY));
     }
   } else {
     // ------------------------------ epilogue (warps 0-3) -------------------
@@ -655,27 +793,26 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     uint32_t t_it = 0;
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       const int nsub = min(a.st, a.n_sub - s * a.st);
+      if (a.halo_len[s] == kOverflow) continue;
       const uint32_t ab = t_it & 1;
-      mbar_wait(bar(B_T_FULL + ab), (t_it >> 1) & 1);
+      mbar_wait_sleep(bar(B_T_FULL + ab), (t_it >> 1) & 1);
       tc_fence_after();
       for (int g = 0; g < nsub; ++g) {
-        uint32_t v[4][16];
         const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * FWD_ACC_COLS + g * 64;
-        tmem_ld16(t0 + 0, v[0]);
-        tmem_ld16(t0 + 16, v[1]);
-        tmem_ld16(t0 + 32, v[2]);
-        tmem_ld16(t0 + 48, v[3]);
-        tmem_ld_wait();
         const int64_t row = (static_cast<int64_t>(s) * a.st + g) * TM + 32 * e + lane;
-        if (row < a.n_rows) {
-          float4* o = reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * CH);
+        float4* o = row < a.n_rows
+                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * CH)
+                        : nullptr;
 #pragma unroll
-          for (int q = 0; q < 4; ++q)
+        for (int q = 0; q < 4; ++q) {
+          uint32_t v[16];
+          tmem_ld16(t0 + 16 * q, v);
+          tmem_ld_wait();
+          if (o)
 #pragma unroll
             for (int x = 0; x < 4; ++x)
-              o[q * 4 + x] = make_float4(__uint_as_float(v[q][4 * x]), __uint_as_float(v[q][4 * x + 1]),
-                                         __uint_as_float(v[q][4 * x + 2]),
-                                         __uint_as_float(v[q][4 * x + 3]));
+              o[q * 4 + x] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                         __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
         }
       }
       tc_fence_before();
@@ -687,7 +824,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_free<512>(tmem);
+  if (warp == 5) tmem_free<256>(tmem);
 }
 
 // ===========================================================================
@@ -696,6 +833,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
 // ===========================================================================
 struct WgArgs {
   const uint32_t* halo;
+  const uint2* runs;
+  const uint32_t* n_runs;
   const uint32_t* halo_len;
   const uint32_t* blk_off;
   const uint8_t* blocks;
@@ -706,12 +845,13 @@ struct WgArgs {
   float* partial;              // [gridDim.x][K][64 c][64 m]
 };
 
-constexpr int WG_THREADS = 448;
+constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
 constexpr int WG_PAIRS = 7;      // cell pairs per CTA (cell group = 14 cells)
 constexpr int WG_NSA = 2;        // A pair stages (32 KB)
+constexpr int WG_NSD = 6;        // descriptor slots (2 blocks each)
 
 struct WgSmem {
-  uint32_t halo, a, gt, d, bar, tmem_slot;
+  uint32_t halo, a, gt, d, bar, tmem_slot, offs;
   size_t total;
 };
 __host__ __device__ inline WgSmem wg_smem_layout(int hcap) {
@@ -725,12 +865,14 @@ __host__ __device__ inline WgSmem wg_smem_layout(int hcap) {
   L.gt = o;
   o += 16384;
   L.d = o;
-  o += NSD * 2 * BLOCK_MAX_BYTES;
+  o += WG_NSD * 2 * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
   L.bar = o;
   o += 32 * 8;
   L.tmem_slot = o;
   o += 16;
+  L.offs = o;
+  o += 64 * 4;
   L.total = o + 1024;
   return L;
 }
@@ -740,12 +882,12 @@ enum : int {
   W_HALO_EMPTY = 1,
   W_A_FULL = 2,   // 2
   W_A_EMPTY = 4,  // 2
-  W_D_FULL = 6,   // 2
-  W_D_EMPTY = 8,  // 2
-  W_G_FULL = 10,
-  W_G_EMPTY = 11,
-  W_DONE = 12,
-  W_COUNT = 13
+  W_D_FULL = 6,   // WG_NSD
+  W_D_EMPTY = 12, // WG_NSD
+  W_G_FULL = 18,
+  W_G_EMPTY = 19,
+  W_DONE = 20,
+  W_COUNT = 21
 };
 
 __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
@@ -758,8 +900,6 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   const uint32_t s_bar = base + L.bar;
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
-  const uint8_t* g_halo = gbase + L.halo;
-  uint8_t* g_a = gbase + L.a;
   uint8_t* g_gt = gbase + L.gt;
   const uint8_t* g_d = gbase + L.d;
 
@@ -775,7 +915,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       mbar_init(bar(W_A_FULL + i), FWD_AGG_WARPS);
       mbar_init(bar(W_A_EMPTY + i), 1);
     }
-    for (int i = 0; i < NSD; ++i) {
+    for (int i = 0; i < WG_NSD; ++i) {
       mbar_init(bar(W_D_FULL + i), 1);
       mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS);
     }
@@ -792,45 +932,32 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
 
   if (warp == 4) {
     // producer: halo + descriptor blocks (two cells per stage)
-    uint32_t d_it = 0, h_it = 0;
+    uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
+    uint32_t d_it = 0;
     for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
-      const uint32_t H = a.halo_len[s];
-      const uint32_t* hl = a.halo + static_cast<int64_t>(s) * a.hcap;
-      mbar_wait(bar(W_HALO_EMPTY), (h_it & 1) ^ 1);
-      if (lane == 0) mbar_expect_tx(bar(W_HALO_FULL), H * 128u);
+      if (a.halo_len[s] == kOverflow) continue;
+      for (int x = lane; x <= K; x += 32) offs[x] = a.blk_off[static_cast<int64_t>(s) * K + x];
       __syncwarp();
-      for (uint32_t h = lane; h < H; h += 32) {
-        const uint32_t v = hl[h];
-        if (h == 0 || hl[h - 1] != v - 1) {
-          uint32_t n = 1;
-          while (h + n < H && hl[h + n] == v + n) ++n;
-          bulk_g2s(s_halo + h * 128u, a.feat + static_cast<int64_t>(v) * CH, n * 128u,
-                   bar(W_HALO_FULL));
-        }
-      }
-      ++h_it;
       for (int p = 0; p < n_pairs; ++p) {
         if (lane == 0) {
-          const uint32_t ds = d_it % NSD;
-          mbar_wait(bar(W_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
+          const uint32_t ds = d_it % WG_NSD;
+          mbar_wait(bar(W_D_EMPTY + ds), ((d_it / WG_NSD) & 1) ^ 1);
           const int k0 = k_begin + 2 * p;
-          const int64_t bi = static_cast<int64_t>(s) * K + k0;
-          const uint32_t o0 = a.blk_off[bi], o1 = a.blk_off[bi + 1];
-          uint32_t bytes = o1 - o0;
-          uint32_t o2 = o1;
-          if (k0 + 1 < K) {
-            o2 = a.blk_off[bi + 2];
-            bytes += o2 - o1;
-          }
-          mbar_expect_tx(bar(W_D_FULL + ds), bytes);
+          const uint32_t o0 = offs[k0], o1 = offs[k0 + 1];
+          const uint32_t o2 = (k0 + 1 < K) ? offs[k0 + 2] : o1;
+          mbar_expect_tx(bar(W_D_FULL + ds), o2 - o0);
           bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(W_D_FULL + ds));
-          if (k0 + 1 < K)
+          if (o2 > o1)
             bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES + BLOCK_MAX_BYTES, a.blocks + o1, o2 - o1,
                      bar(W_D_FULL + ds));
         }
         ++d_it;
       }
       __syncwarp();
+      const int s_next = s + gridDim.x;
+      if (s_next < a.n_sub && a.halo_len[s_next] != kOverflow)
+        prefetch_halo_l2(a.runs + static_cast<int64_t>(s_next) * a.hcap, a.n_runs[s_next],
+                         a.feat, lane);
     }
   } else if (warp == 5) {
     if (lane == 0) {
@@ -838,6 +965,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       uint32_t a_it = 0, g_it = 0;
       bool first = true;
       for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+        if (a.halo_len[s] == kOverflow) continue;
         mbar_wait(bar(W_G_FULL), g_it & 1);
         for (int p = 0; p < n_pairs; ++p) {
           const uint32_t as = a_it % WG_NSA;
@@ -863,65 +991,22 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     __syncwarp();
   } else if (warp >= FWD_AGG_WARP0) {
     const int aw = warp - FWD_AGG_WARP0;
-    const int sub_l = lane >> 3, l8 = lane & 7;
-    uint32_t a_it = 0, d_it = 0, h_it = 0;
+    uint32_t a_it = 0, d_it = 0;
     for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
-      mbar_wait(bar(W_HALO_FULL), h_it & 1);
-      ++h_it;
+      const uint32_t H = a.halo_len[s];
+      if (H == kOverflow) continue;
+      named_bar_sync(1, 32 * FWD_AGG_WARPS);
+      coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat,
+                                         s_halo, 32 * aw + lane);
+      named_bar_sync(1, 32 * FWD_AGG_WARPS);
       for (int p = 0; p < n_pairs; ++p) {
-        const uint32_t ds = d_it % NSD, as = a_it % WG_NSA;
-        mbar_wait(bar(W_D_FULL + ds), (d_it / NSD) & 1);
+        const uint32_t ds = d_it % WG_NSD, as = a_it % WG_NSA;
+        mbar_wait(bar(W_D_FULL + ds), (d_it / WG_NSD) & 1);
         mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
         const int ncell = (k_begin + 2 * p + 1 < K) ? 2 : 1;
-        for (int half = 0; half < 2; ++half) {
-          uint8_t* A = g_a + as * 32768 + half * 16384;
-          const uint8_t* blk = g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES;
-          const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
-          const uint16_t* ents = reinterpret_cast<const uint16_t*>(blk + 512);
-#pragma unroll 1
-          for (int q = aw; q < TM / 4; q += FWD_AGG_WARPS) {
-            uint32_t r, c, eo;
-            if (half < ncell) {
-              const uint32_t item = items[q * 4 + sub_l];
-              r = item & 127u;
-              c = (item >> 7) & 31u;
-              eo = item >> 12;
-            } else {
-              r = q * 4 + sub_l;
-              c = 0;
-              eo = 0;
-            }
-            uint32_t cmax = c;
-            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 8));
-            cmax = max(cmax, __shfl_xor_sync(0xffffffffu, cmax, 16));
-            uint4 outv = make_uint4(0, 0, 0, 0);
-            if (cmax <= 1) {
-              if (c == 1)
-                outv = *reinterpret_cast<const uint4*>(g_halo + ents[eo] * 128u + l8 * 16u);
-            } else {
-              float acc[8];
-#pragma unroll
-              for (int x = 0; x < 8; ++x) acc[x] = 0.f;
-              for (uint32_t it = 0; it < cmax; ++it) {
-                if (it < c) {
-                  const uint4 v =
-                      *reinterpret_cast<const uint4*>(g_halo + ents[eo + it] * 128u + l8 * 16u);
-                  acc_bf16x2(acc[0], acc[1], v.x);
-                  acc_bf16x2(acc[2], acc[3], v.y);
-                  acc_bf16x2(acc[4], acc[5], v.z);
-                  acc_bf16x2(acc[6], acc[7], v.w);
-                }
-              }
-              outv.x = pack_bf16x2(acc[0], acc[1]);
-              outv.y = pack_bf16x2(acc[2], acc[3]);
-              outv.z = pack_bf16x2(acc[4], acc[5]);
-              outv.w = pack_bf16x2(acc[6], acc[7]);
-              if (c == 1)
-                outv = *reinterpret_cast<const uint4*>(g_halo + ents[eo] * 128u + l8 * 16u);
-            }
-            *reinterpret_cast<uint4*>(A + r * 128u + (((l8 ^ (r & 7u)) & 7u) << 4)) = outv;
-          }
-        }
+        for (int half = 0; half < ncell; ++half)
+          aggregate_stage<FWD_AGG_WARPS>(g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES,
+                                         s_halo, s_a + as * 32768u + half * 16384u, aw, lane);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
@@ -931,13 +1016,13 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         ++a_it;
         ++d_it;
       }
-      if (lane == 0) mbar_arrive(bar(W_HALO_EMPTY));
     }
   } else {
     // warps 0-3: dense G tile loader during the sweep, epilogue at the end
     uint32_t g_it = 0;
     for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
-      mbar_wait(bar(W_G_EMPTY), (g_it & 1) ^ 1);
+      if (a.halo_len[s] == kOverflow) continue;
+      mbar_wait_sleep(bar(W_G_EMPTY), (g_it & 1) ^ 1);
       // 128 rows x 8 chunks of 16 B; warp e copies rows 32e..32e+31
       for (int x = lane; x < 32 * 8; x += 32) {
         const int r = 32 * warp + (x >> 3), q = x & 7;
@@ -952,30 +1037,31 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       ++g_it;
     }
     // epilogue: TMEM lanes 32e..32e+31 of each pair accumulator -> partial
-    mbar_wait(bar(W_DONE), 0);
-    if (blockIdx.x >= a.n_sub) goto done;
+    mbar_wait_sleep(bar(W_DONE), 0);
+    {
+      bool any = false;
+      for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) any |= a.halo_len[s] != kOverflow;
+      if (!any) goto done;
+    }
     tc_fence_after();
     const int e = warp;
     for (int p = 0; p < n_pairs; ++p) {
-      uint32_t v[4][16];
       const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + p * 64;
-      tmem_ld16(t0 + 0, v[0]);
-      tmem_ld16(t0 + 16, v[1]);
-      tmem_ld16(t0 + 32, v[2]);
-      tmem_ld16(t0 + 48, v[3]);
-      tmem_ld_wait();
       const int k = k_begin + 2 * p + (e >> 1);
       const int c = 32 * (e & 1) + lane;
-      if (k < K) {
-        float4* o = reinterpret_cast<float4*>(
-            a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * CH + c) * CH);
+      float4* o = k < K ? reinterpret_cast<float4*>(
+                              a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * CH + c) * CH)
+                        : nullptr;
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
+      for (int q = 0; q < 4; ++q) {
+        uint32_t v[16];
+        tmem_ld16(t0 + 16 * q, v);
+        tmem_ld_wait();
+        if (o)
 #pragma unroll
           for (int x = 0; x < 4; ++x)
-            o[q * 4 + x] = make_float4(__uint_as_float(v[q][4 * x]), __uint_as_float(v[q][4 * x + 1]),
-                                       __uint_as_float(v[q][4 * x + 2]),
-                                       __uint_as_float(v[q][4 * x + 3]));
+            o[q * 4 + x] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                       __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
       }
     }
   }
@@ -1000,7 +1086,6 @@ __global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, in
 // ===========================================================================
 // host drivers
 // ===========================================================================
-constexpr int FWD_ST = 3, FWD_HCAP = 1280;
 constexpr int WG_HCAP = 768;
 
 static TcPlan* get_plan(npcg_context* ctx, npcg_neighbors* nb) {
@@ -1074,6 +1159,8 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   if (P->n_super == 0) return;
   FwdArgs a{};
   a.halo = P->halo.get();
+  a.runs = P->runs.get();
+  a.n_runs = P->n_runs.get();
   a.halo_len = P->halo_len.get();
   a.blk_off = P->blk_off.get();
   a.blocks = P->blocks.get();
@@ -1094,55 +1181,126 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   launch(ctx, name, k_conv_fwd_tc, dim3(grid), dim3(FWD_THREADS), L.total, a);
 }
 
-static bool plan_ok(const TcDirPlan* P) { return P->n_overflow == 0; }
 
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
                 float* fout) {
   TcDirPlan* P = plan_fwd(ctx, nb);
-  if (!plan_ok(P)) {  // irregular geometry beyond the tile capacities: exact engine
-    const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
-    mvmr_rows<float>(ctx, v, w, fin, 1, CH, CH, fout);
+  TcPlan* p = nb->tc.get();
+  if (P->n_overflow < P->n_super) {
+    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+    pack_w(ctx, p, w, P->K, false);
+    run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
+                   "conv_fwd_tc");
+  }
+  // rows of super-tiles beyond the tile capacities: exact engine on those rows only
+  const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
+  mvmr_rows_subset_f32(ctx, v, nb->perm_out.get(), P->spill_rows.get(), P->n_spill, w, fin, CH,
+                       CH, fout);
+}
+
+__global__ void k_add_inplace(float* __restrict__ a, const float* __restrict__ b, int64_t n) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < n) a[x] += b[x];
+}
+
+// Exact weight gradient of the rows of overflow tiles (vvor over that subset).
+__global__ void k_gather_rows_triplets(const int64_t* __restrict__ row_ptr,
+                                       const uint32_t* __restrict__ col,
+                                       const uint32_t* __restrict__ kk,
+                                       const uint32_t* __restrict__ perm,
+                                       const uint32_t* __restrict__ list, int64_t n_list,
+                                       const int64_t* __restrict__ off, uint32_t* __restrict__ oi,
+                                       uint32_t* __restrict__ oj, uint32_t* __restrict__ ok) {
+  const int64_t x = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (x >= n_list) return;
+  const uint32_t row = perm[list[x]];
+  const int64_t s = row_ptr[row], n = row_ptr[row + 1] - s;
+  for (int64_t q = lane; q < n; q += 32) {
+    oi[off[x] + q] = row;
+    oj[off[x] + q] = col[s + q];
+    ok[off[x] + q] = kk[s + q];
+  }
+}
+__global__ void k_row_lens(const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ perm,
+                           const uint32_t* __restrict__ list, int64_t n_list,
+                           int64_t* __restrict__ len) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < n_list) {
+    const uint32_t row = perm[list[x]];
+    len[x] = row_ptr[row + 1] - row_ptr[row];
+  }
+}
+
+static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, const float* fin,
+                        const float* gout, float* grad_w, bool accumulate) {
+  const int K = static_cast<int>(nb->n_kernels);
+  DevBuf<int64_t> len(ctx, P->n_spill + 1), off(ctx, P->n_spill + 1);
+  NPCG_CUDA(cudaMemsetAsync(len.get(), 0, (P->n_spill + 1) * 8, ctx->stream));
+  launch(ctx, "spill_lens", k_row_lens, dim3(static_cast<unsigned>(ceil_div(P->n_spill, 256))),
+         dim3(256), 0, static_cast<const int64_t*>(nb->row_ptr.get()),
+         static_cast<const uint32_t*>(nb->perm_out.get()),
+         static_cast<const uint32_t*>(P->spill_rows.get()), P->n_spill, len.get());
+  int64_t total = 0;
+  exclusive_scan_i64(ctx, len.get(), off.get(), P->n_spill + 1, &total);
+  DevBuf<uint32_t> ti(ctx, total), tj(ctx, total), tk(ctx, total);
+  launch(ctx, "spill_gather", k_gather_rows_triplets,
+         dim3(static_cast<unsigned>(ceil_div(P->n_spill * 32, 256))), dim3(256), 0,
+         static_cast<const int64_t*>(nb->row_ptr.get()), static_cast<const uint32_t*>(nb->col_j.get()),
+         static_cast<const uint32_t*>(nb->col_k.get()), static_cast<const uint32_t*>(nb->perm_out.get()),
+         static_cast<const uint32_t*>(P->spill_rows.get()), P->n_spill,
+         static_cast<const int64_t*>(off.get()), ti.get(), tj.get(), tk.get());
+  npcg_triplets T{ti.get(), tj.get(), tk.get(), total, nb->n_out, nb->n_in, K, 0};
+  CellPlan cells;
+  cells_from_triplets(ctx, &T, K, &cells);
+  if (!accumulate) {
+    vvor_cells<float>(ctx, cells, gout, fin, 1, CH, CH, grad_w);
     return;
   }
-  TcPlan* p = nb->tc.get();
-  convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
-  pack_w(ctx, p, w, P->K, false);
-  run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout, "conv_fwd_tc");
+  DevBuf<float> tmp(ctx, static_cast<int64_t>(K) * CH * CH);
+  vvor_cells<float>(ctx, cells, gout, fin, 1, CH, CH, tmp.get());
+  launch(ctx, "add_inplace", k_add_inplace, dim3(static_cast<unsigned>(ceil_div(K * CH * CH, 256))),
+         dim3(256), 0, grad_w, static_cast<const float*>(tmp.get()),
+         static_cast<int64_t>(K) * CH * CH);
 }
 
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
                  const float* gout, float* grad_in, float* grad_w) {
   TcPlan* p = get_plan(ctx, nb);
   const int K = static_cast<int>(nb->n_kernels);
+  bool g_converted = false;
   if (grad_in) {
     TcDirPlan* P = plan_bwd(ctx, nb);
-    if (!plan_ok(P)) {
-      DevBuf<float> wt(ctx, static_cast<int64_t>(K) * CH * CH);
-      transpose_w<float>(ctx, w, K, CH, CH, wt.get());
-      mvmr_rows<float>(ctx, nb->tcsr->view(), wt.get(), gout, 1, CH, CH, grad_in);
-    } else {
+    if (P->n_overflow < P->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
+      g_converted = true;
       pack_w(ctx, p, w, K, true);
       run_fwd_kernel(ctx, P, p->feat_out.get(), p->wpack.get(), nb->perm_in.get(), grad_in,
                      "conv_dgrad_tc");
     }
+    if (P->n_spill) {
+      DevBuf<float> wt(ctx, static_cast<int64_t>(K) * CH * CH);
+      transpose_w<float>(ctx, w, K, CH, CH, wt.get());
+      mvmr_rows_subset_f32(ctx, nb->tcsr->view(), nb->perm_in.get(), P->spill_rows.get(),
+                           P->n_spill, wt.get(), gout, CH, CH, grad_in);
+    }
   }
   if (grad_w) {
     TcDirPlan* P = plan_wg(ctx, nb);
-    if (!plan_ok(P)) {
-      build_cells(ctx, nb);
-      vvor_cells<float>(ctx, *nb->cells, gout, fin, 1, CH, CH, grad_w);
+    if (P->n_overflow == P->n_super) {
+      wgrad_spill(ctx, nb, P, fin, gout, grad_w, false);
       return;
     }
     convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
-    if (!grad_in || !plan_ok(plan_bwd(ctx, nb)))
-      convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
+    if (!g_converted) convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
     const int gx = std::max(1, std::min(P->n_sub, ctx->num_sms / 2));
     const int64_t need = static_cast<int64_t>(gx) * K * CH * CH;
     if (p->partial.size() < need) p->partial.alloc(ctx, need);
     NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
     WgArgs a{};
     a.halo = P->halo.get();
+    a.runs = P->runs.get();
+    a.n_runs = P->n_runs.get();
     a.halo_len = P->halo_len.get();
     a.blk_off = P->blk_off.get();
     a.blocks = P->blocks.get();
@@ -1160,6 +1318,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     launch(ctx, "conv_wgrad_tc", k_conv_wgrad_tc, dim3(gx, groups), dim3(WG_THREADS), L.total, a);
     launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(K * CH * CH, 256))),
            dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, grad_w);
+    if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true);
   }
 }
 
