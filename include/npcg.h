@@ -237,6 +237,12 @@ npcg_status npcg_neighbors_prepare(npcg_context* ctx, npcg_neighbors* nb, int32_
  * [super-tiles, super-tiles beyond tile capacity (served by the exact engine),
  *  max halo rows, mean halo rows x 100].  stats: HOST int64[12]. */
 npcg_status npcg_neighbors_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* stats);
+/* Debug instrumentation: runs one tensor-core forward with per-stage pipeline
+ * event clocks recorded for CTA 0; trace: HOST int64[512 x 8] (SM clock64 of
+ * descriptor issue / arrival, A-slot free, aggregation done, MMA start / issue,
+ * W arrival per stage).  Synchronises. */
+npcg_status npcg_debug_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w,
+                                     const float* fin, float* fout, int64_t* trace);
 
 /* ---- strided path ------------------------------- */
 /* spatial.hpp:47-48 voxel_downsample.  kept (n_points) / parent (n_points)

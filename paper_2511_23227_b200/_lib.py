@@ -83,6 +83,7 @@ _SIGS = {
                                      C.POINTER(npcg_exec_config), _P, _P]),
     "npcg_neighbors_prepare": (C.c_int, [_P, _P, _I32]),
     "npcg_neighbors_plan_stats": (C.c_int, [_P, _P, _P]),
+    "npcg_debug_trace_forward": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "npcg_voxel_downsample": (C.c_int, [_P, C.POINTER(npcg_cloud), _D, _P, _P, _P, _PI64]),
 }
 

@@ -688,6 +688,16 @@ npcg_status npcg_neighbors_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int
   });
 }
 
+npcg_status npcg_debug_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w,
+                                     const float* fin, float* fout, int64_t* trace) {
+  if (!ctx || !nb || !trace) return NPCG_ERR_INVALID;
+  return guard(ctx, [&] {
+    if (nb->t == 0 || !tc_supported(1, 64, 64, nb->n_kernels))
+      fail(NPCG_ERR_UNSUPPORTED, "trace: tensor-core plan needs C=64, K<=32");
+    tc_trace_forward(ctx, nb, w, fin, fout, trace);
+  });
+}
+
 npcg_status npcg_voxel_downsample(npcg_context* ctx, const npcg_cloud* cloud, double voxel,
                                   int64_t* kept, int64_t* parent, int64_t* out_offsets,
                                   int64_t* n_kept) {

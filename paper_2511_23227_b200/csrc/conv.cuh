@@ -29,5 +29,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
                  const float* gout, float* grad_in, float* grad_w);
 void tc_prepare(npcg_context* ctx, npcg_neighbors* nb);
 void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12);
+void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
+                      float* fout, int64_t* trace_host);
 
 }  // namespace npcg

@@ -469,10 +469,18 @@ struct FwdArgs {
   const __nv_bfloat16* feat;  // bf16 (n_cols, 64), permuted
   const uint8_t* wpack;       // K x 8 KB
   float* out;                 // (n_rows, 64), original order
+  long long* trace;           // debug: per-stage event clocks of CTA 0 (nullptr = off)
 };
+constexpr int TRACE_STAGES = 512;
+constexpr int TRACE_EV = 8;  // 0 d_issue, 1 d_full, 2 a_empty, 3 agg_done, 4 mma_start, 5 mma_issued, 6 w_full
+__device__ __forceinline__ void trace_ev(long long* tr, uint32_t stage, int ev) {
+  if (tr && blockIdx.x == 0 && stage < TRACE_STAGES) tr[stage * TRACE_EV + ev] = clock64();
+}
 
 constexpr int FWD_AGG_WARP0 = 6;
 constexpr int FWD_AGG_WARPS = 16;
+constexpr int AGG_GROUPS = 4;                           // stage s is aggregated by group s % 4
+constexpr int AGG_GROUP_WARPS = FWD_AGG_WARPS / AGG_GROUPS;
 constexpr int FWD_W_WARP = FWD_AGG_WARP0 + FWD_AGG_WARPS;
 constexpr int FWD_THREADS = 32 * (FWD_W_WARP + 1);
 constexpr int FWD_ST = 2, FWD_HCAP = 960;  // 256-row super-tiles, halo <= 960 rows (120 KB)
@@ -508,12 +516,22 @@ __host__ __device__ inline FwdSmem fwd_smem_layout(int hcap) {
   return L;
 }
 
-// Warm L2 with the next super-tile's halo rows (one prefetch per copy run).
-__device__ __forceinline__ void prefetch_halo_l2(const uint2* runs, uint32_t nr,
-                                                 const __nv_bfloat16* feat, int lane) {
-  for (uint32_t r = lane; r < nr; r += 32) {
-    const uint2 v = runs[r];
-    bulk_prefetch_l2(feat + static_cast<int64_t>(v.x) * CH, (v.y >> 16) * 128u);
+// Warm L2 with a super-tile's halo rows: one prefetch.global.L2 per 128-byte
+// row, row indices loaded in batches of 8 per lane before the prefetches.
+template <int NT>
+__device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t H,
+                                                 const __nv_bfloat16* feat, int t) {
+  for (uint32_t h0 = 0; h0 < H; h0 += 8 * NT) {
+    uint32_t r[8];
+#pragma unroll
+    for (int x = 0; x < 8; ++x) {
+      const uint32_t h = h0 + x * NT + t;
+      r[x] = h < H ? rows[h] : 0xFFFFFFFFu;
+    }
+#pragma unroll
+    for (int x = 0; x < 8; ++x)
+      if (r[x] != 0xFFFFFFFFu)
+        asm volatile("prefetch.global.L2 [%0];" ::"l"(feat + static_cast<int64_t>(r[x]) * CH));
   }
 }
 // Cooperative halo load by the aggregation warps: 16-byte cp.async per lane,
@@ -564,72 +582,69 @@ static_assert(B_COUNT <= 48, "barrier region");
 // before their uses (ILP), stores go to the SW128 K-major A tile.
 template <int NW>
 __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_halo, uint32_t s_A,
-                                                int aw, int lane) {
-  constexpr int NQ = (TM / 4) / NW;
+                                                int wig, int lane) {
+  constexpr int NQ = (TM / 4) / NW;  // quads per warp, round-robin over count-sorted items
   const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
   const uint16_t* ents = reinterpret_cast<const uint16_t*>(blk + 512);
   const int sub_l = lane >> 3;
   const uint32_t l8x16 = static_cast<uint32_t>(lane & 7) << 4;
-  uint32_t it[NQ];
+  uint32_t it[NQ], cm[NQ];
 #pragma unroll
-  for (int qi = 0; qi < NQ; ++qi) it[qi] = items[(aw + NW * qi) * 4 + sub_l];
-  uint32_t packed = 0;
+  for (int qi = 0; qi < NQ; ++qi) it[qi] = items[(wig + NW * qi) * 4 + sub_l];
 #pragma unroll
-  for (int qi = 0; qi < NQ; ++qi) packed |= ((it[qi] >> 7) & 31u) << (8 * qi);
-  packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 8));
-  packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 16));
+  for (int qb = 0; qb < NQ; qb += 4) {
+    uint32_t packed = 0;
+#pragma unroll
+    for (int x = 0; x < 4 && qb + x < NQ; ++x) packed |= ((it[qb + x] >> 7) & 31u) << (8 * x);
+    packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 8));
+    packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 16));
+#pragma unroll
+    for (int x = 0; x < 4 && qb + x < NQ; ++x) cm[qb + x] = (packed >> (8 * x)) & 0xFFu;
+  }
+  // pass 1: quads whose rows have at most one entry: zero rows / exact bf16 copies
   uint4 v[NQ];
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     v[qi] = make_uint4(0, 0, 0, 0);
-    if (((it[qi] >> 7) & 31u) == 1u) {
-      const uint32_t h = ents[it[qi] >> 12];
-      v[qi] = lds128(s_halo + h * 128u + l8x16);
-    }
-  }
-  // quads with a row of >= 2 entries: fp32 sums, entries of all such quads interleaved
-  uint32_t cmall = packed;
-#pragma unroll
-  for (int qi = 1; qi < NQ; ++qi) cmall = __vmaxu4(cmall, packed >> (8 * qi));
-  cmall &= 0xFFu;
-  if (cmall >= 2u) {
-    float acc[NQ][8];
-#pragma unroll
-    for (int qi = 0; qi < NQ; ++qi)
-#pragma unroll
-      for (int x = 0; x < 8; ++x) acc[qi][x] = 0.f;
-    for (uint32_t e = 0; e < cmall; ++e) {
-      uint4 w[NQ];
-#pragma unroll
-      for (int qi = 0; qi < NQ; ++qi) {
-        const uint32_t c = (it[qi] >> 7) & 31u;
-        w[qi] = make_uint4(0, 0, 0, 0);
-        if (e < c && ((packed >> (8 * qi)) & 0xFFu) >= 2u)
-          w[qi] = lds128(s_halo + static_cast<uint32_t>(ents[(it[qi] >> 12) + e]) * 128u + l8x16);
-      }
-#pragma unroll
-      for (int qi = 0; qi < NQ; ++qi) {
-        acc_bf16x2(acc[qi][0], acc[qi][1], w[qi].x);
-        acc_bf16x2(acc[qi][2], acc[qi][3], w[qi].y);
-        acc_bf16x2(acc[qi][4], acc[qi][5], w[qi].z);
-        acc_bf16x2(acc[qi][6], acc[qi][7], w[qi].w);
-      }
-    }
-#pragma unroll
-    for (int qi = 0; qi < NQ; ++qi) {
-      const uint32_t c = (it[qi] >> 7) & 31u;
-      if (((packed >> (8 * qi)) & 0xFFu) >= 2u && c != 1u) {
-        v[qi].x = pack_bf16x2(acc[qi][0], acc[qi][1]);
-        v[qi].y = pack_bf16x2(acc[qi][2], acc[qi][3]);
-        v[qi].z = pack_bf16x2(acc[qi][4], acc[qi][5]);
-        v[qi].w = pack_bf16x2(acc[qi][6], acc[qi][7]);
-      }
-    }
+    if (cm[qi] <= 1u && ((it[qi] >> 7) & 31u) == 1u)
+      v[qi] = lds128(s_halo + static_cast<uint32_t>(ents[it[qi] >> 12]) * 128u + l8x16);
   }
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
-    const uint32_t r = it[qi] & 127u;
-    sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), v[qi]);
+    if (cm[qi] <= 1u) {
+      const uint32_t r = it[qi] & 127u;
+      sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), v[qi]);
+    }
+  }
+  // pass 2: quads with a row of >= 2 entries: fp32 sums rounded once to bf16
+#pragma unroll
+  for (int qi = 0; qi < NQ; ++qi) {
+    if (cm[qi] >= 2u) {
+      const uint32_t c = (it[qi] >> 7) & 31u, eo = it[qi] >> 12;
+      float acc[8];
+#pragma unroll
+      for (int x = 0; x < 8; ++x) acc[x] = 0.f;
+      for (uint32_t e = 0; e < cm[qi]; e += 2) {
+        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
+        if (e < c) w0 = lds128(s_halo + static_cast<uint32_t>(ents[eo + e]) * 128u + l8x16);
+        if (e + 1 < c) w1 = lds128(s_halo + static_cast<uint32_t>(ents[eo + e + 1]) * 128u + l8x16);
+        acc_bf16x2(acc[0], acc[1], w0.x);
+        acc_bf16x2(acc[2], acc[3], w0.y);
+        acc_bf16x2(acc[4], acc[5], w0.z);
+        acc_bf16x2(acc[6], acc[7], w0.w);
+        acc_bf16x2(acc[0], acc[1], w1.x);
+        acc_bf16x2(acc[2], acc[3], w1.y);
+        acc_bf16x2(acc[4], acc[5], w1.z);
+        acc_bf16x2(acc[6], acc[7], w1.w);
+      }
+      uint4 o;
+      o.x = pack_bf16x2(acc[0], acc[1]);
+      o.y = pack_bf16x2(acc[2], acc[3]);
+      o.z = pack_bf16x2(acc[4], acc[5]);
+      o.w = pack_bf16x2(acc[6], acc[7]);
+      const uint32_t r = it[qi] & 127u;
+      sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), o);
+    }
   }
 }
 
@@ -650,7 +665,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     mbar_init(bar(B_HALO_FULL), 1);
     mbar_init(bar(B_HALO_EMPTY), FWD_AGG_WARPS);
     for (int i = 0; i < NSA; ++i) {
-      mbar_init(bar(B_A_FULL + i), FWD_AGG_WARPS);
+      mbar_init(bar(B_A_FULL + i), AGG_GROUP_WARPS);
       mbar_init(bar(B_A_EMPTY + i), 1);
     }
     for (int i = 0; i < NSW; ++i) {
@@ -659,7 +674,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     }
     for (int i = 0; i < NSD; ++i) {
       mbar_init(bar(B_D_FULL + i), 1);
-      mbar_init(bar(B_D_EMPTY + i), FWD_AGG_WARPS);
+      mbar_init(bar(B_D_EMPTY + i), AGG_GROUP_WARPS);
     }
     for (int i = 0; i < 2; ++i) {
       mbar_init(bar(B_T_FULL + i), 1);
@@ -693,16 +708,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             const uint32_t o0 = offs[g * K + k], o1 = offs[g * K + k + 1];
             mbar_expect_tx(bar(B_D_FULL + ds), o1 - o0);
             bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(B_D_FULL + ds));
+            trace_ev(a.trace, d_it, 0);
           }
           ++d_it;
         }
       }
       __syncwarp();
-      // warm L2 with the next super-tile's halo rows (after this tile's descriptors)
-      const int s_next = s + gridDim.x;
-      if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
-        prefetch_halo_l2(a.runs + static_cast<int64_t>(s_next) * a.hcap, a.n_runs[s_next],
-                         a.feat, lane);
     }
   } else if (warp == FWD_W_WARP) {
     // ------------------------ producer: W_k per super-tile and cell ---------
@@ -723,43 +734,52 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     __syncwarp();
   } else if (warp == 5) {
     // ------------------------------ MMA issuer -----------------------------
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, 64, false, false);
-      uint32_t w_it = 0, a_it = 0, t_it = 0;
-      for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
-        const int nsub = min(a.st, a.n_sub - s * a.st);
-        if (a.halo_len[s] == kOverflow) continue;
-        const uint32_t ab = t_it & 1;
-        mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
-        tc_fence_after();
-        for (int k = 0; k < K; ++k) {
-          const uint32_t ws = w_it % NSW;
-          mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
-          for (int g = 0; g < nsub; ++g) {
-            const uint32_t as = a_it % NSA;
-            mbar_wait(bar(B_A_FULL + as), (a_it / NSA) & 1);
-            tc_fence_after();
-            const uint32_t d = tmem + ab * FWD_ACC_COLS + g * 64;
+    // The whole warp runs the loop converged (warp-uniform descriptors); one
+    // elected lane issues tcgen05.mma / commit.
+    constexpr uint32_t idesc = idesc_bf16(128, 64, false, false);
+    const uint64_t a_desc0 = sdesc_sw128(s_a, 16, 1024), b_desc0 = sdesc_sw128(s_w, 16, 1024);
+    uint32_t w_it = 0, a_it = 0, t_it = 0;
+    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
+      const int nsub = min(a.st, a.n_sub - s * a.st);
+      if (a.halo_len[s] == kOverflow) continue;
+      const uint32_t ab = t_it & 1;
+      mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int k = 0; k < K; ++k) {
+        const uint32_t ws = w_it % NSW;
+        mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
+        if (lane == 0) trace_ev(a.trace, a_it, 6);
+        for (int g = 0; g < nsub; ++g) {
+          const uint32_t as = a_it % NSA;
+          mbar_wait(bar(B_A_FULL + as), (a_it / NSA) & 1);
+          if (lane == 0) trace_ev(a.trace, a_it, 4);
+          tc_fence_after();
+          const uint32_t d = tmem + ab * FWD_ACC_COLS + g * 64;
+          // descriptor start-address field is in 16-byte units
+          const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
+          const uint64_t bd = b_desc0 + ((ws * 8192u) >> 4);
+          if (elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks) {
-              const uint64_t ad = sdesc_sw128(s_a + as * 16384u + 32u * ks, 16, 1024);
-              const uint64_t bd = sdesc_sw128(s_w + ws * 8192u + 32u * ks, 16, 1024);
-              umma_bf16(d, ad, bd, idesc, (k > 0 || ks > 0) ? 1u : 0u);
-            }
+            for (int ks = 0; ks < 4; ++ks)
+              umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc, (k > 0 || ks > 0) ? 1u : 0u);
             umma_commit(bar(B_A_EMPTY + as));
-            ++a_it;
           }
-          umma_commit(bar(B_W_EMPTY + ws));
-          ++w_it;
+          __syncwarp();
+          if (lane == 0) trace_ev(a.trace, a_it, 5);
+          ++a_it;
         }
-        umma_commit(bar(B_T_FULL + ab));
-        ++t_it;
+        if (elect_one()) umma_commit(bar(B_W_EMPTY + ws));
+        __syncwarp();
+        ++w_it;
       }
+      if (elect_one()) umma_commit(bar(B_T_FULL + ab));
+      __syncwarp();
+      ++t_it;
     }
-    __syncwarp();
   } else if (warp >= FWD_AGG_WARP0) {
     // ------------------------------ aggregation ----------------------------
     const int aw = warp - FWD_AGG_WARP0;
+    const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
     uint32_t a_it = 0, d_it = 0;
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       const int nsub = min(a.st, a.n_sub - s * a.st);
@@ -771,16 +791,21 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
       for (int k = 0; k < K; ++k) {
         for (int g = 0; g < nsub; ++g) {
-          const uint32_t ds = d_it % NSD, as = a_it % NSA;
-          mbar_wait(bar(B_D_FULL + ds), (d_it / NSD) & 1);
-          mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
-          aggregate_stage<FWD_AGG_WARPS>(g_d + ds * BLOCK_MAX_BYTES, s_halo, s_a + as * 16384u,
-                                         aw, lane);
-          fence_proxy_async_smem();
-          __syncwarp();
-          if (lane == 0) {
-            mbar_arrive(bar(B_A_FULL + as));
-            mbar_arrive(bar(B_D_EMPTY + ds));
+          if (static_cast<int>(a_it % AGG_GROUPS) == grp) {
+            const uint32_t ds = d_it % NSD, as = a_it % NSA;
+            mbar_wait(bar(B_D_FULL + ds), (d_it / NSD) & 1);
+            if (wig == 0 && lane == 0) trace_ev(a.trace, d_it, 1);
+            mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
+            if (wig == 0 && lane == 0) trace_ev(a.trace, a_it, 2);
+            aggregate_stage<AGG_GROUP_WARPS>(g_d + ds * BLOCK_MAX_BYTES, s_halo,
+                                             s_a + as * 16384u, wig, lane);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (wig == 0 && lane == 0) trace_ev(a.trace, a_it, 3);
+            if (lane == 0) {
+              mbar_arrive(bar(B_A_FULL + as));
+              mbar_arrive(bar(B_D_EMPTY + ds));
+            }
           }
           ++a_it;
           ++d_it;
@@ -795,6 +820,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       const int nsub = min(a.st, a.n_sub - s * a.st);
       if (a.halo_len[s] == kOverflow) continue;
       const uint32_t ab = t_it & 1;
+      {  // warm L2 with the next super-tile's halo while this one is aggregated
+        const int s_next = s + gridDim.x;
+        if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
+          prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
+                                a.halo_len[s_next], a.feat, 32 * e + lane);
+      }
       mbar_wait_sleep(bar(B_T_FULL + ab), (t_it >> 1) & 1);
       tc_fence_after();
       for (int g = 0; g < nsub; ++g) {
@@ -849,6 +880,7 @@ constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
 constexpr int WG_PAIRS = 7;      // cell pairs per CTA (cell group = 14 cells)
 constexpr int WG_NSA = 2;        // A pair stages (32 KB)
 constexpr int WG_NSD = 6;        // descriptor slots (2 blocks each)
+constexpr int WG_GROUPS = 2;     // stage (cell pair) s is aggregated by warp group s % 2
 
 struct WgSmem {
   uint32_t halo, a, gt, d, bar, tmem_slot, offs;
@@ -912,12 +944,12 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     mbar_init(bar(W_HALO_FULL), 1);
     mbar_init(bar(W_HALO_EMPTY), FWD_AGG_WARPS);
     for (int i = 0; i < WG_NSA; ++i) {
-      mbar_init(bar(W_A_FULL + i), FWD_AGG_WARPS);
+      mbar_init(bar(W_A_FULL + i), FWD_AGG_WARPS / WG_GROUPS);
       mbar_init(bar(W_A_EMPTY + i), 1);
     }
     for (int i = 0; i < WG_NSD; ++i) {
       mbar_init(bar(W_D_FULL + i), 1);
-      mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS);
+      mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS / WG_GROUPS);
     }
     mbar_init(bar(W_G_FULL), 4);
     mbar_init(bar(W_G_EMPTY), 1);
@@ -954,10 +986,6 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         ++d_it;
       }
       __syncwarp();
-      const int s_next = s + gridDim.x;
-      if (s_next < a.n_sub && a.halo_len[s_next] != kOverflow)
-        prefetch_halo_l2(a.runs + static_cast<int64_t>(s_next) * a.hcap, a.n_runs[s_next],
-                         a.feat, lane);
     }
   } else if (warp == 5) {
     if (lane == 0) {
@@ -991,6 +1019,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     __syncwarp();
   } else if (warp >= FWD_AGG_WARP0) {
     const int aw = warp - FWD_AGG_WARP0;
+    const int grp = aw / (FWD_AGG_WARPS / WG_GROUPS), wig = aw % (FWD_AGG_WARPS / WG_GROUPS);
     uint32_t a_it = 0, d_it = 0;
     for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
       const uint32_t H = a.halo_len[s];
@@ -1000,18 +1029,21 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
                                          s_halo, 32 * aw + lane);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
       for (int p = 0; p < n_pairs; ++p) {
-        const uint32_t ds = d_it % WG_NSD, as = a_it % WG_NSA;
-        mbar_wait(bar(W_D_FULL + ds), (d_it / WG_NSD) & 1);
-        mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
-        const int ncell = (k_begin + 2 * p + 1 < K) ? 2 : 1;
-        for (int half = 0; half < ncell; ++half)
-          aggregate_stage<FWD_AGG_WARPS>(g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES,
-                                         s_halo, s_a + as * 32768u + half * 16384u, aw, lane);
-        fence_proxy_async_smem();
-        __syncwarp();
-        if (lane == 0) {
-          mbar_arrive(bar(W_A_FULL + as));
-          mbar_arrive(bar(W_D_EMPTY + ds));
+        if (static_cast<int>(a_it % WG_GROUPS) == grp) {
+          const uint32_t ds = d_it % WG_NSD, as = a_it % WG_NSA;
+          mbar_wait(bar(W_D_FULL + ds), (d_it / WG_NSD) & 1);
+          mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
+          const int ncell = (k_begin + 2 * p + 1 < K) ? 2 : 1;
+          for (int half = 0; half < ncell; ++half)
+            aggregate_stage<FWD_AGG_WARPS / WG_GROUPS>(
+                g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES, s_halo,
+                s_a + as * 32768u + half * 16384u, wig, lane);
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(bar(W_A_FULL + as));
+            mbar_arrive(bar(W_D_EMPTY + ds));
+          }
         }
         ++a_it;
         ++d_it;
@@ -1022,6 +1054,12 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     uint32_t g_it = 0;
     for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
       if (a.halo_len[s] == kOverflow) continue;
+      {
+        const int s_next = s + gridDim.x;
+        if (s_next < a.n_sub && a.halo_len[s_next] != kOverflow)
+          prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
+                                a.halo_len[s_next], a.feat, 32 * warp + lane);
+      }
       mbar_wait_sleep(bar(W_G_EMPTY), (g_it & 1) ^ 1);
       // 128 rows x 8 chunks of 16 B; warp e copies rows 32e..32e+31
       for (int x = lane; x < 32 * 8; x += 32) {
@@ -1155,7 +1193,7 @@ static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool tra
 
 static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16* feat,
                            const uint8_t* wpack, const uint32_t* perm_rows, float* out,
-                           const char* name) {
+                           const char* name, long long* trace = nullptr) {
   if (P->n_super == 0) return;
   FwdArgs a{};
   a.halo = P->halo.get();
@@ -1174,6 +1212,7 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   a.feat = feat;
   a.wpack = wpack;
   a.out = out;
+  a.trace = trace;
   const FwdSmem L = fwd_smem_layout(P->hcap);
   NPCG_CUDA(cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
@@ -1320,6 +1359,22 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
            dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, grad_w);
     if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true);
   }
+}
+
+// Debug: one traced forward; trace_host receives TRACE_STAGES x TRACE_EV clocks.
+void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
+                      float* fout, int64_t* trace_host) {
+  TcDirPlan* P = plan_fwd(ctx, nb);
+  TcPlan* p = nb->tc.get();
+  convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+  pack_w(ctx, p, w, P->K, false);
+  DevBuf<long long> tr(ctx, TRACE_STAGES * TRACE_EV);
+  NPCG_CUDA(cudaMemsetAsync(tr.get(), 0, TRACE_STAGES * TRACE_EV * 8, ctx->stream));
+  run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
+                 "conv_fwd_tc_traced", tr.get());
+  NPCG_CUDA(cudaMemcpyAsync(trace_host, tr.get(), TRACE_STAGES * TRACE_EV * 8,
+                            cudaMemcpyDeviceToHost, ctx->stream));
+  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 // plan statistics for the bench / tests: [n_super, n_overflow, max_halo, mean_halo*100] x 3 dirs
