@@ -1,0 +1,567 @@
+// npcg/npconv.hpp -- header-only C++ drop-in for the reference `npc::` hot-path
+// API (/root/reference/proj/core/include/npconv/*.hpp), implemented over the
+// C ABI of libnpcg.so (include/npcg.h).
+//
+// A C++ caller of the reference switches by replacing
+//     #include "npconv/{conv_op,engine,spatial,triplets,vvor,tensors}.hpp"
+// with
+//     #include "npcg/npconv.hpp"
+// and linking libnpcg.so + cudart instead of libnpconv.a.  Names, argument
+// meaning, container layouts and error classes are the reference's:
+//
+//   FeatureTensor / WeightTensor / make_weights   tensors.hpp:17-150
+//   PointCloud / make_point_cloud                 point_cloud.hpp:18-50
+//   NeighborList / radius_search                  spatial.hpp:14-40
+//   TripletList / build_triplets_native /         triplets.hpp:20-82
+//     local_voxel_kernel_index / sort_triplets / choose_sort_axis
+//   ExecConfig / mvmr / mvmr_transposed           engine.hpp:22-76
+//   WeightGradient / vvor                         vvor.hpp:17-88
+//   PointConvOp / BackwardResult                  conv_op.hpp:15-203
+//   Error hierarchy                               errors.hpp:10-67
+//
+// Containers are host std::vectors exactly like the reference; each call
+// copies inputs to the device, runs the libnpcg kernels and copies results
+// back (the PointConvOp keeps its neighbor structure and cached inputs on the
+// device between forward and backward).  ExecConfig gains one field, `math`
+// (npcg_math): exact CUDA-core arithmetic or bf16 tensor cores.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <array>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <memory>
+#include <span>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "npcg.h"
+
+namespace npc {
+
+// ---- errors (errors.hpp:10-67) ----------------------------------------------
+class Error : public std::runtime_error {
+ public:
+  explicit Error(const std::string& w) : std::runtime_error(w) {}
+};
+#define NPCG_ERR_CLASS(N) \
+  class N : public Error { \
+   public:                 \
+    using Error::Error;    \
+  };
+NPCG_ERR_CLASS(OffsetError)
+NPCG_ERR_CLASS(NonFiniteError)
+NPCG_ERR_CLASS(ShapeError)
+NPCG_ERR_CLASS(RadiusError)
+NPCG_ERR_CLASS(VoxelError)
+NPCG_ERR_CLASS(IndexError)
+NPCG_ERR_CLASS(DomainError)
+NPCG_ERR_CLASS(StateError)
+NPCG_ERR_CLASS(IOError)
+NPCG_ERR_CLASS(DeviceError)
+#undef NPCG_ERR_CLASS
+
+namespace detail {
+
+[[noreturn]] inline void raise(npcg_status s, const std::string& what) {
+  switch (s) {
+    case NPCG_ERR_OFFSET: throw OffsetError(what);
+    case NPCG_ERR_NONFINITE: throw NonFiniteError(what);
+    case NPCG_ERR_SHAPE: throw ShapeError(what);
+    case NPCG_ERR_RADIUS: throw RadiusError(what);
+    case NPCG_ERR_VOXEL: throw VoxelError(what);
+    case NPCG_ERR_INDEX: throw IndexError(what);
+    case NPCG_ERR_DOMAIN: throw DomainError(what);
+    case NPCG_ERR_STATE: throw StateError(what);
+    case NPCG_ERR_IO: throw IOError(what);
+    default: throw DeviceError(what + " (" + npcg_status_string(s) + ")");
+  }
+}
+
+// One context per process/device (device 0 unless NPCG_DEVICE is set).
+inline npcg_context* ctx() {
+  static std::unique_ptr<npcg_context, npcg_status (*)(npcg_context*)> c = [] {
+    int dev = 0;
+    if (const char* e = std::getenv("NPCG_DEVICE")) dev = std::atoi(e);
+    npcg_context* p = nullptr;
+    const npcg_status s = npcg_context_create(dev, nullptr, &p);
+    if (s != NPCG_OK) raise(s, "npcg_context_create: a B200 (sm_100a) is required");
+    return std::unique_ptr<npcg_context, npcg_status (*)(npcg_context*)>(p, npcg_context_destroy);
+  }();
+  return c.get();
+}
+
+inline void check(npcg_status s, const char* what) {
+  if (s != NPCG_OK) raise(s, std::string(what) + ": " + npcg_last_error(ctx()));
+}
+
+inline void cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Owning device buffer.
+template <typename T>
+class Dev {
+ public:
+  Dev() = default;
+  explicit Dev(size_t n) : n_(n) {
+    if (n) cuda(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+  }
+  Dev(const T* host, size_t n) : Dev(n) {
+    if (n) cuda(cudaMemcpy(p_, host, n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
+  }
+  ~Dev() {
+    if (p_) cudaFree(p_);
+  }
+  Dev(Dev&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
+  Dev& operator=(Dev&& o) noexcept {
+    std::swap(p_, o.p_);
+    std::swap(n_, o.n_);
+    return *this;
+  }
+  Dev(const Dev&) = delete;
+  T* get() const { return p_; }
+  size_t size() const { return n_; }
+  std::vector<T> host() const {
+    std::vector<T> v(n_);
+    if (n_) {
+      check(npcg_context_synchronize(ctx()), "sync");
+      cuda(cudaMemcpy(v.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+    }
+    return v;
+  }
+
+ private:
+  T* p_ = nullptr;
+  size_t n_ = 0;
+};
+
+template <typename T>
+constexpr npcg_dtype dtype_of() {
+  static_assert(std::is_same_v<T, float> || std::is_same_v<T, double>, "float or double");
+  return std::is_same_v<T, float> ? NPCG_F32 : NPCG_F64;
+}
+
+}  // namespace detail
+
+// ---- tensors (tensors.hpp) --------------------------------------------------
+template <typename T>
+class FeatureTensor {
+ public:
+  FeatureTensor() = default;
+  FeatureTensor(int64_t n, int64_t g, int64_t c) : n_(n), g_(g), c_(c) {
+    if (n < 0 || g < 1 || c < 1)
+      throw ShapeError("FeatureTensor: need n >= 0, groups >= 1, channels >= 1");
+    v_.assign(static_cast<size_t>(n * g * c), T(0));
+  }
+  FeatureTensor(int64_t n, int64_t g, int64_t c, std::vector<T> values)
+      : n_(n), g_(g), c_(c), v_(std::move(values)) {
+    if (n < 0 || g < 1 || c < 1)
+      throw ShapeError("FeatureTensor: need n >= 0, groups >= 1, channels >= 1");
+    if (static_cast<int64_t>(v_.size()) != n * g * c)
+      throw ShapeError("FeatureTensor: value count does not match (n, groups, channels)");
+    for (T x : v_)
+      if (!std::isfinite(static_cast<double>(x))) throw NonFiniteError("FeatureTensor: non-finite value");
+  }
+  int64_t n() const { return n_; }
+  int64_t groups() const { return g_; }
+  int64_t channels() const { return c_; }
+  int64_t row_width() const { return g_ * c_; }
+  std::span<const T> values() const { return v_; }
+  std::span<T> values_mut() { return v_; }
+  const T* row(int64_t p) const { return v_.data() + p * row_width(); }
+  T* row_mut(int64_t p) { return v_.data() + p * row_width(); }
+  T at(int64_t p, int64_t g, int64_t c) const { return v_[(p * g_ + g) * c_ + c]; }
+  T& at(int64_t p, int64_t g, int64_t c) { return v_[(p * g_ + g) * c_ + c]; }
+
+ private:
+  int64_t n_ = 0, g_ = 1, c_ = 1;
+  std::vector<T> v_;
+};
+
+template <typename T>
+class WeightTensor {
+ public:
+  WeightTensor() = default;
+  WeightTensor(int64_t t, int64_t g, int64_t ci, int64_t co) : t_(t), g_(g), ci_(ci), co_(co) {
+    validate();
+    v_.assign(static_cast<size_t>(kernels() * g * ci * co), T(0));
+  }
+  WeightTensor(int64_t t, int64_t g, int64_t ci, int64_t co, std::vector<T> values)
+      : t_(t), g_(g), ci_(ci), co_(co), v_(std::move(values)) {
+    validate();
+    if (static_cast<int64_t>(v_.size()) != kernels() * g_ * ci_ * co_)
+      throw ShapeError("WeightTensor: value count does not match (K, G, C_in_g, C_out_g)");
+    for (T x : v_)
+      if (!std::isfinite(static_cast<double>(x))) throw NonFiniteError("WeightTensor: non-finite value");
+  }
+  int64_t t() const { return t_; }
+  int64_t kernels() const { return t_ * t_ * t_; }
+  int64_t groups() const { return g_; }
+  int64_t c_in() const { return ci_; }
+  int64_t c_out() const { return co_; }
+  std::span<const T> values() const { return v_; }
+  std::span<T> values_mut() { return v_; }
+  T at(int64_t k, int64_t g, int64_t c, int64_t m) const { return v_[((k * g_ + g) * ci_ + c) * co_ + m]; }
+  T& at(int64_t k, int64_t g, int64_t c, int64_t m) { return v_[((k * g_ + g) * ci_ + c) * co_ + m]; }
+
+ private:
+  void validate() const {
+    if (t_ < 1 || t_ % 2 == 0) throw ShapeError("WeightTensor: kernel resolution t must be odd and >= 1");
+    if (g_ < 1 || ci_ < 1 || co_ < 1)
+      throw ShapeError("WeightTensor: need groups >= 1, c_in_g >= 1, c_out_g >= 1");
+  }
+  int64_t t_ = 1, g_ = 1, ci_ = 1, co_ = 1;
+  std::vector<T> v_;
+};
+
+// vvor.hpp:17-62: (K, G, C_out, C_in)
+template <typename T>
+class WeightGradient {
+ public:
+  WeightGradient() = default;
+  WeightGradient(int64_t k, int64_t g, int64_t co, int64_t ci) : k_(k), g_(g), co_(co), ci_(ci) {
+    if (k < 1 || g < 1 || co < 1 || ci < 1) throw ShapeError("WeightGradient: all dimensions must be >= 1");
+    v_.assign(static_cast<size_t>(k * g * co * ci), T(0));
+  }
+  int64_t kernels() const { return k_; }
+  int64_t groups() const { return g_; }
+  int64_t c_out() const { return co_; }
+  int64_t c_in() const { return ci_; }
+  std::span<const T> values() const { return v_; }
+  std::span<T> values_mut() { return v_; }
+  T at(int64_t k, int64_t g, int64_t m, int64_t c) const { return v_[((k * g_ + g) * co_ + m) * ci_ + c]; }
+
+ private:
+  int64_t k_ = 0, g_ = 0, co_ = 0, ci_ = 0;
+  std::vector<T> v_;
+};
+
+// ---- point cloud (point_cloud.hpp) --------------------------------------------
+using Vec3 = std::array<double, 3>;
+
+class PointCloud {
+ public:
+  PointCloud() : off_{0} {}
+  PointCloud(std::vector<Vec3> p, std::vector<int64_t> off) : pos_(std::move(p)), off_(std::move(off)) {}
+  int64_t n_points() const { return static_cast<int64_t>(pos_.size()); }
+  int64_t n_batches() const { return static_cast<int64_t>(off_.size()) - 1; }
+  std::span<const Vec3> positions() const { return pos_; }
+  std::span<const int64_t> batch_offsets() const { return off_; }
+  const Vec3& position(int64_t p) const { return pos_[p]; }
+
+  // device copy of the coordinates (uploaded on first use, cached)
+  const double* device_xyz() const {
+    if (!dev_ && !pos_.empty()) dev_ = std::make_shared<detail::Dev<double>>(&pos_[0][0], pos_.size() * 3);
+    return dev_ ? dev_->get() : nullptr;
+  }
+  npcg_cloud c_view() const {
+    return {device_xyz(), off_.data(), n_points(), n_batches()};
+  }
+
+ private:
+  std::vector<Vec3> pos_;
+  std::vector<int64_t> off_;
+  mutable std::shared_ptr<detail::Dev<double>> dev_;
+};
+
+inline PointCloud make_point_cloud(std::vector<Vec3> p, std::vector<int64_t> off) {
+  const auto n = static_cast<int64_t>(p.size());
+  if (off.size() < 2) throw OffsetError("batch_offsets needs at least [0, N]");
+  if (off.front() != 0) throw OffsetError("batch_offsets must start at 0");
+  if (off.back() != n) throw OffsetError("batch_offsets must end at the point count (" + std::to_string(n) + ")");
+  for (size_t b = 1; b < off.size(); ++b)
+    if (off[b] < off[b - 1]) throw OffsetError("batch_offsets must be monotone non-decreasing");
+  for (const Vec3& q : p)
+    for (double c : q)
+      if (!std::isfinite(c)) throw NonFiniteError("point coordinate is NaN or infinite");
+  return PointCloud(std::move(p), std::move(off));
+}
+inline PointCloud make_point_cloud(std::vector<Vec3> p) {
+  const auto n = static_cast<int64_t>(p.size());
+  return make_point_cloud(std::move(p), {0, n});
+}
+
+// ---- neighbor search + triplets (spatial.hpp / triplets.hpp) -------------------
+struct NeighborList {
+  std::vector<int64_t> out_index, in_index;
+  double radius = 0.0;
+  int64_t size() const { return static_cast<int64_t>(out_index.size()); }
+};
+
+enum class SortAxis : uint8_t { none = 0, by_i = 1, by_j = 2, by_k = 3 };
+enum class ConvMode : uint8_t { native = 0, degraded = 1 };
+
+struct ConvGeometry {
+  double radius = 1.0;
+  int64_t t = 3;
+  ConvMode mode = ConvMode::native;
+  double voxel_size = 1.0;
+};
+
+struct TripletList {
+  std::vector<uint32_t> i, j, k;
+  int64_t n_out = 0, n_in = 0, n_kernels = 0;
+  SortAxis sort_axis = SortAxis::none;
+  int64_t size() const { return static_cast<int64_t>(i.size()); }
+};
+
+namespace detail {
+struct Neighbors {
+  npcg_neighbors* h = nullptr;
+  ~Neighbors() {
+    if (h) npcg_neighbors_destroy(h);
+  }
+};
+inline std::shared_ptr<Neighbors> build(const PointCloud& out, const PointCloud& in, double r, int64_t t) {
+  auto nb = std::make_shared<Neighbors>();
+  const npcg_cloud oc = out.c_view(), ic = in.c_view();
+  if (t == 0) check(npcg_radius_search(ctx(), &oc, &ic, r, &nb->h), "radius_search");
+  else check(npcg_build_triplets_native(ctx(), &oc, &ic, r, t, &nb->h), "build_triplets_native");
+  return nb;
+}
+struct DevTriplets {
+  Dev<uint32_t> i, j, k;
+  npcg_triplets view{};
+  explicit DevTriplets(const TripletList& t)
+      : i(t.i.data(), t.i.size()), j(t.j.data(), t.j.size()), k(t.k.data(), t.k.size()) {
+    view = {i.get(), j.get(), k.get(), t.size(), t.n_out, t.n_in, t.n_kernels,
+            static_cast<int32_t>(t.sort_axis)};
+  }
+};
+inline TripletList export_triplets(const Neighbors& nb, SortAxis axis) {
+  int64_t n = 0, no = 0, ni = 0, nk = 0;
+  check(npcg_neighbors_size(nb.h, &n), "size");
+  check(npcg_neighbors_info(nb.h, &no, &ni, &nk, nullptr), "info");
+  Dev<uint32_t> di(n), dj(n), dk(n);
+  check(npcg_neighbors_export_triplets(ctx(), nb.h, static_cast<int32_t>(axis), di.get(), dj.get(), dk.get()),
+        "export_triplets");
+  TripletList t{di.host(), dj.host(), dk.host(), no, ni, nk, axis};
+  return t;
+}
+}  // namespace detail
+
+// spatial.hpp:39-40
+inline NeighborList radius_search(const PointCloud& queries, const PointCloud& targets, double radius) {
+  auto nb = detail::build(queries, targets, radius, 0);
+  int64_t n = 0;
+  detail::check(npcg_neighbors_size(nb->h, &n), "size");
+  detail::Dev<int64_t> oi(n), ii(n);
+  detail::check(npcg_neighbors_export_pairs(detail::ctx(), nb->h, oi.get(), ii.get()), "export_pairs");
+  return {oi.host(), ii.host(), radius};
+}
+
+// triplets.hpp:48-49
+inline int64_t local_voxel_kernel_index(const Vec3& center, const Vec3& neighbor, double radius, int64_t t) {
+  detail::Dev<double> c(center.data(), 3), n(neighbor.data(), 3);
+  detail::Dev<int64_t> k(1);
+  detail::check(npcg_kernel_index(detail::ctx(), c.get(), n.get(), 1, radius, t, k.get()), "local_voxel_kernel_index");
+  return k.host()[0];
+}
+
+// triplets.hpp:56-57
+inline TripletList build_triplets_native(const PointCloud& out_cloud, const PointCloud& in_cloud,
+                                         const ConvGeometry& geom) {
+  if (geom.t < 1 || geom.t % 2 == 0) throw ShapeError("conv geometry: kernel resolution t must be odd and >= 1");
+  auto nb = detail::build(out_cloud, in_cloud, geom.radius, geom.t);
+  return detail::export_triplets(*nb, SortAxis::none);
+}
+
+// triplets.hpp:78 / 82
+inline TripletList sort_triplets(TripletList t, SortAxis axis) {
+  if (axis == SortAxis::none || t.size() <= 1) {
+    t.sort_axis = axis;
+    return t;
+  }
+  detail::DevTriplets d(t);
+  detail::Dev<uint32_t> oi(t.size()), oj(t.size()), ok(t.size());
+  detail::check(npcg_sort_triplets(detail::ctx(), &d.view, static_cast<int32_t>(axis), oi.get(), oj.get(), ok.get()),
+                "sort_triplets");
+  return {oi.host(), oj.host(), ok.host(), t.n_out, t.n_in, t.n_kernels, axis};
+}
+inline SortAxis choose_sort_axis(const TripletList& t) {
+  return static_cast<SortAxis>(npcg_choose_sort_axis(t.n_out, t.n_in, t.n_kernels));
+}
+
+// ---- engines (engine.hpp / vvor.hpp) ---------------------------------------------
+enum class Executor : uint8_t { naive = 0, grouped = 1 };
+
+struct ExecConfig {
+  int64_t L = 128;
+  int64_t b_out = 32;
+  int64_t b_in = 32;
+  Executor executor = Executor::grouped;
+  bool deterministic = false;
+  int workers = 0;
+  npcg_math math = NPCG_MATH_AUTO;
+  npcg_exec_config c() const {
+    return {L, b_out, b_in, static_cast<int32_t>(executor), deterministic ? 1 : 0, workers,
+            static_cast<int32_t>(math)};
+  }
+};
+
+struct AccessCounters {  // engine.hpp:38-50 (GPU engines do not model CPU reloads)
+  uint64_t w_reads = 0, fin_reads = 0, fout_atomic_writes = 0;
+};
+template <typename T>
+struct MvmrResult {
+  FeatureTensor<T> out;
+  AccessCounters counters;
+  uint64_t aux_bytes = 0;
+};
+template <typename T>
+struct VvorResult {
+  WeightGradient<T> grad;
+  AccessCounters counters;
+  uint64_t aux_bytes = 0;
+};
+
+template <typename T>
+MvmrResult<T> mvmr(const WeightTensor<T>& w, const FeatureTensor<T>& fin, const TripletList& tl, int64_t n_out,
+                   const ExecConfig& cfg = {}) {
+  if (w.groups() != fin.groups()) throw ShapeError("mvmr: weight and feature group counts differ");
+  if (w.c_in() != fin.channels()) throw ShapeError("mvmr: weight C_in_g does not match feature channels");
+  detail::DevTriplets d(tl);
+  detail::Dev<T> dw(w.values().data(), w.values().size()), df(fin.values().data(), fin.values().size());
+  detail::Dev<T> out(static_cast<size_t>(std::max<int64_t>(n_out, 0) * w.groups() * w.c_out()));
+  const npcg_exec_config c = cfg.c();
+  detail::check(npcg_mvmr(detail::ctx(), detail::dtype_of<T>(), dw.get(), w.t(), w.groups(), w.c_in(), w.c_out(),
+                          df.get(), fin.n(), &d.view, n_out, &c, out.get()),
+                "mvmr");
+  return {FeatureTensor<T>(n_out, w.groups(), w.c_out(), out.host()), {}, 0};
+}
+
+template <typename T>
+MvmrResult<T> mvmr_transposed(const WeightTensor<T>& w, const FeatureTensor<T>& gout, const TripletList& tl,
+                              int64_t n_in, const ExecConfig& cfg = {}) {
+  if (w.c_out() != gout.channels()) throw ShapeError("mvmr_transposed: weight C_out_g does not match gradient channels");
+  if (w.groups() != gout.groups()) throw ShapeError("mvmr: weight and feature group counts differ");
+  detail::DevTriplets d(tl);
+  detail::Dev<T> dw(w.values().data(), w.values().size()), dg(gout.values().data(), gout.values().size());
+  detail::Dev<T> out(static_cast<size_t>(std::max<int64_t>(n_in, 0) * w.groups() * w.c_in()));
+  const npcg_exec_config c = cfg.c();
+  detail::check(npcg_mvmr_transposed(detail::ctx(), detail::dtype_of<T>(), dw.get(), w.t(), w.groups(), w.c_in(),
+                                     w.c_out(), dg.get(), gout.n(), &d.view, n_in, &c, out.get()),
+                "mvmr_transposed");
+  return {FeatureTensor<T>(n_in, w.groups(), w.c_in(), out.host()), {}, 0};
+}
+
+template <typename T>
+VvorResult<T> vvor(const FeatureTensor<T>& gout, const FeatureTensor<T>& fin, const TripletList& tl,
+                   int64_t n_kernels, const ExecConfig& cfg = {}) {
+  if (gout.groups() != fin.groups()) throw ShapeError("vvor: gradient and feature group counts differ");
+  if (n_kernels < 1) throw ShapeError("vvor: n_kernels must be >= 1");
+  detail::DevTriplets d(tl);
+  detail::Dev<T> dg(gout.values().data(), gout.values().size()), df(fin.values().data(), fin.values().size());
+  detail::Dev<T> grad(static_cast<size_t>(n_kernels * gout.groups() * gout.channels() * fin.channels()));
+  const npcg_exec_config c = cfg.c();
+  detail::check(npcg_vvor(detail::ctx(), detail::dtype_of<T>(), dg.get(), gout.n(), df.get(), fin.n(), gout.groups(),
+                          fin.channels(), gout.channels(), &d.view, n_kernels, &c, grad.get()),
+                "vvor");
+  VvorResult<T> r{WeightGradient<T>(n_kernels, gout.groups(), gout.channels(), fin.channels()), {}, 0};
+  const auto h = grad.host();
+  std::copy(h.begin(), h.end(), r.grad.values_mut().begin());
+  return r;
+}
+
+// ---- operator (conv_op.hpp) --------------------------------------------------------
+template <typename T>
+struct BackwardResult {
+  FeatureTensor<T> grad_in;
+  WeightGradient<T> grad_w;
+};
+
+template <typename T>
+class PointConvOp {
+ public:
+  PointConvOp(WeightTensor<T> weights, ConvGeometry geometry, ExecConfig config = {})
+      : w_(std::move(weights)), geom_(geometry), cfg_(config) {
+    if (w_.t() != geom_.t) throw ShapeError("PointConvOp: weight kernel resolution != geometry t");
+    dw_ = detail::Dev<T>(w_.values().data(), w_.values().size());
+  }
+  const WeightTensor<T>& weights() const { return w_; }
+  const ConvGeometry& geometry() const { return geom_; }
+  const ExecConfig& config() const { return cfg_; }
+
+  const TripletList& cached_triplets() const {
+    if (!nb_) throw StateError("PointConvOp: no triplet cache yet, run forward first");
+    if (!sorted_) {
+      int64_t no = 0, ni = 0, nk = 0;
+      detail::check(npcg_neighbors_info(nb_->h, &no, &ni, &nk, nullptr), "info");
+      sorted_ = std::make_unique<TripletList>(detail::export_triplets(
+          *nb_, static_cast<SortAxis>(npcg_choose_sort_axis(no, ni, nk))));
+    }
+    return *sorted_;
+  }
+
+  FeatureTensor<T> forward(const PointCloud& in_cloud, const FeatureTensor<T>& fin) {
+    return forward(in_cloud, in_cloud, fin);
+  }
+  FeatureTensor<T> forward(const PointCloud& in_cloud, const PointCloud& out_cloud, const FeatureTensor<T>& fin) {
+    if (geom_.mode != ConvMode::native) throw StateError("PointConvOp: degraded mode is not provided by libnpcg");
+    if (fin.n() != in_cloud.n_points()) throw ShapeError("PointConvOp::forward: feature rows != cloud points");
+    if (fin.groups() != w_.groups() || fin.channels() != w_.c_in())
+      throw ShapeError("mvmr: weight and feature shapes differ");
+    build_cache(in_cloud, out_cloud);
+    dfin_ = detail::Dev<T>(fin.values().data(), fin.values().size());  // conv_op.hpp:138 copy
+    detail::Dev<T> out(static_cast<size_t>(n_out_ * w_.groups() * w_.c_out()));
+    const npcg_exec_config c = cfg_.c();
+    detail::check(npcg_conv_forward(detail::ctx(), nb_->h, detail::dtype_of<T>(), dw_.get(), w_.groups(), w_.c_in(),
+                                    w_.c_out(), dfin_.get(), &c, out.get()),
+                  "PointConvOp::forward");
+    n_in_ = fin.n();
+    has_forward_ = true;
+    return FeatureTensor<T>(n_out_, w_.groups(), w_.c_out(), out.host());
+  }
+
+  BackwardResult<T> backward(const FeatureTensor<T>& gout) {
+    if (!has_forward_) throw StateError("PointConvOp::backward: no cached forward inputs");
+    if (gout.n() != n_out_ || gout.groups() != w_.groups() || gout.channels() != w_.c_out())
+      throw ShapeError("PointConvOp::backward: gout shape mismatch");
+    detail::Dev<T> dg(gout.values().data(), gout.values().size());
+    detail::Dev<T> gi(static_cast<size_t>(n_in_ * w_.groups() * w_.c_in()));
+    detail::Dev<T> gw(static_cast<size_t>(w_.kernels() * w_.groups() * w_.c_out() * w_.c_in()));
+    const npcg_exec_config c = cfg_.c();
+    detail::check(npcg_conv_backward(detail::ctx(), nb_->h, detail::dtype_of<T>(), dw_.get(), w_.groups(), w_.c_in(),
+                                     w_.c_out(), dfin_.get(), dg.get(), &c, gi.get(), gw.get()),
+                  "PointConvOp::backward");
+    BackwardResult<T> r{FeatureTensor<T>(n_in_, w_.groups(), w_.c_in(), gi.host()),
+                        WeightGradient<T>(w_.kernels(), w_.groups(), w_.c_out(), w_.c_in())};
+    const auto h = gw.host();
+    std::copy(h.begin(), h.end(), r.grad_w.values_mut().begin());
+    return r;
+  }
+
+ private:
+  void build_cache(const PointCloud& in_cloud, const PointCloud& out_cloud) {
+    const Key key{in_cloud.positions().data(), out_cloud.positions().data(), in_cloud.n_points(),
+                  out_cloud.n_points()};
+    if (nb_ && key == key_) return;  // conv_op.hpp:109-111 identity cache
+    nb_ = detail::build(out_cloud, in_cloud, geom_.radius, geom_.t);
+    key_ = key;
+    n_out_ = out_cloud.n_points();
+    sorted_.reset();
+    has_forward_ = false;
+  }
+  struct Key {
+    const void* in = nullptr;
+    const void* out = nullptr;
+    int64_t n_in = 0, n_out = 0;
+    bool operator==(const Key&) const = default;
+  };
+  WeightTensor<T> w_;
+  ConvGeometry geom_;
+  ExecConfig cfg_;
+  detail::Dev<T> dw_, dfin_;
+  std::shared_ptr<detail::Neighbors> nb_;
+  mutable std::unique_ptr<TripletList> sorted_;
+  Key key_;
+  int64_t n_out_ = 0, n_in_ = 0;
+  bool has_forward_ = false;
+};
+
+}  // namespace npc

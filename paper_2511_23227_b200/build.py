@@ -66,5 +66,26 @@ def build(force: bool = False, verbose: bool = True) -> str:
     return LIB
 
 
+def build_cpp_tests(verbose: bool = True) -> str:
+    """Builds tests/cpp/test_dropin (the C++ drop-in header against libnpcg.so
+    and the C oracle).  Requires oracle/liboracle.so."""
+    src = os.path.join(ROOT, "tests", "cpp", "test_dropin.cpp")
+    out = os.path.join(ROOT, "tests", "cpp", "test_dropin")
+    deps = [src, LIB, os.path.join(ROOT, "include", "npcg", "npconv.hpp"),
+            os.path.join(ROOT, "oracle", "liboracle.so")]
+    if os.path.exists(out) and os.path.getmtime(out) > max(os.path.getmtime(d) for d in deps):
+        return out
+    cmd = [NVCC, "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", out,
+           "-L" + HERE, "-lnpcg", "-L" + os.path.join(ROOT, "oracle"), "-loracle",
+           "-Xlinker", "-rpath", "-Xlinker", "$ORIGIN/../../paper_2511_23227_b200",
+           "-Xlinker", "-rpath", "-Xlinker", "$ORIGIN/../../oracle"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ drop-in test build failed:\n{r.stderr}")
+    if verbose:
+        print(f"built {out}")
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv)

@@ -255,3 +255,15 @@ def test_c2_bf16_fwd_bwd(npc, orc):
     assert all(v["overflow"] == 0 for v in st.values()), st
     e = (rel(out.cpu(), fo), rel(res.grad_in.cpu(), gi), rel(res.grad_w.cpu(), gw))
     assert max(e) <= 1e-2, e
+
+
+def test_cpp_dropin_header(npc):
+    """The C++ drop-in (include/npcg/npconv.hpp) passes reference-style cases."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "test_dropin")
+    assert os.path.exists(exe), "run __graft_entry__.build() first"
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    print(r.stdout)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert "0 failures" in r.stdout
