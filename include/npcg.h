@@ -224,7 +224,10 @@ npcg_status npcg_conv_forward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype 
                               const void* w, int64_t groups, int64_t c_in, int64_t c_out,
                               const void* fin, const npcg_exec_config* cfg, void* fout);
 /* conv_op.hpp:177-203 backward: grad_in = mvmr_transposed, grad_w = vvor.
- * Either output may be NULL to skip it. */
+ * Either output may be NULL to skip it.  `fin` is the operator's saved input
+ * (PointConvOp copies it at forward, conv_op.hpp:138): on the tensor-core path
+ * the bf16 image the last npcg_conv_forward on this handle made of the same
+ * `fin` pointer is reused, so pass the forward's input unchanged. */
 npcg_status npcg_conv_backward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype,
                                const void* w, int64_t groups, int64_t c_in, int64_t c_out,
                                const void* fin, const void* gout, const npcg_exec_config* cfg,

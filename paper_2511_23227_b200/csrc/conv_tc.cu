@@ -64,6 +64,7 @@ struct TcPlan {
   std::unique_ptr<TcDirPlan> fwd, bwd, wg;
   DevBuf<uint32_t> inv_perm_out, inv_perm_in;
   DevBuf<__nv_bfloat16> feat_in;   // bf16 F_in in perm_in order
+  const void* saved_fin = nullptr;  // fin whose image feat_in holds (set by the forward)
   DevBuf<__nv_bfloat16> feat_out;  // bf16 G_out in perm_out order
   DevBuf<uint8_t> wpack;           // K x 8 KB, SW128 K-major B operand
   DevBuf<float> partial;           // wgrad per-CTA partials
@@ -1227,6 +1228,7 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const flo
   TcPlan* p = nb->tc.get();
   if (P->n_overflow < P->n_super) {
     convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+    p->saved_fin = fin;  // PointConvOp saves its input at forward (conv_op.hpp:138)
     pack_w(ctx, p, w, P->K, false);
     run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
                    "conv_fwd_tc");
@@ -1330,7 +1332,12 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
       wgrad_spill(ctx, nb, P, fin, gout, grad_w, false);
       return;
     }
-    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+    // the bf16 input image saved by the forward on this handle is reused when
+    // the backward is handed the same input (the operator's saved copy)
+    if (fin != p->saved_fin) {
+      convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+      p->saved_fin = fin;
+    }
     if (!g_converted) convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
     const int gx = std::max(1, std::min(P->n_sub, ctx->num_sms / 2));
     const int64_t need = static_cast<int64_t>(gx) * K * CH * CH;
@@ -1367,6 +1374,7 @@ void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, con
   TcDirPlan* P = plan_fwd(ctx, nb);
   TcPlan* p = nb->tc.get();
   convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+  p->saved_fin = fin;
   pack_w(ctx, p, w, P->K, false);
   DevBuf<long long> tr(ctx, TRACE_STAGES * TRACE_EV);
   NPCG_CUDA(cudaMemsetAsync(tr.get(), 0, TRACE_STAGES * TRACE_EV * 8, ctx->stream));
