@@ -19,6 +19,8 @@
  *   npcg_conv_forward             conv_op.hpp:129-175 PointConvOp::forward (cache hit)
  *   npcg_conv_backward            conv_op.hpp:177-203 PointConvOp::backward
  *   npcg_voxel_downsample         spatial.hpp:47-48   voxel_downsample
+ *   npcg_build_triplets_degraded  triplets.hpp:63-76  build_triplets_degraded
+ *   npcg_neighbors_export_sites   conv_op.hpp:56-57   snapped_cloud / site_map
  *
  * Conventions
  *  - All tensor / index arrays are DEVICE pointers on the context's device.
@@ -167,6 +169,25 @@ npcg_status npcg_radius_search(npcg_context* ctx, const npcg_cloud* queries,
 npcg_status npcg_build_triplets_native(npcg_context* ctx, const npcg_cloud* out_cloud,
                                        const npcg_cloud* in_cloud, double radius, int64_t t,
                                        npcg_neighbors** out);
+
+/* triplets.hpp:63-76 build_triplets_degraded (ConvMode::degraded).  Sites =
+ * voxel_downsample(in_cloud, voxel_size) snapped to voxel centres; triplets
+ * (site, neighbor site, k) for the occupied voxels within (t-1)/2 voxels, in
+ * the reference's build order (export with NPCG_SORT_NONE).  The handle's
+ * clouds are the sites (n_out = n_in = sites); npcg_conv_forward / backward
+ * on it gather the in_cloud rows through kept_index and scatter the input
+ * gradient back (conv_op.hpp:133-158, 193-202).  Errors: SHAPE (t), VOXEL. */
+npcg_status npcg_build_triplets_degraded(npcg_context* ctx, const npcg_cloud* in_cloud,
+                                         double voxel_size, int64_t t, npcg_neighbors** out);
+/* Degraded handles only (else STATE): site count, original point count, batches. */
+npcg_status npcg_neighbors_sites(const npcg_neighbors* nb, int64_t* n_sites, int64_t* n_fine,
+                                 int64_t* n_batches);
+/* conv_op.hpp:56-57 snapped_cloud() / site_map(): snapped_xyz (n_sites, 3)
+ * float64, kept (n_sites) and parent (n_fine) int64 DEVICE; site_offsets HOST
+ * int64[n_batches + 1].  Any output may be NULL.  STATE on a native handle. */
+npcg_status npcg_neighbors_export_sites(npcg_context* ctx, const npcg_neighbors* nb,
+                                        double* snapped_xyz, int64_t* kept, int64_t* parent,
+                                        int64_t* site_offsets);
 
 npcg_status npcg_neighbors_destroy(npcg_neighbors* nb);
 npcg_status npcg_neighbors_size(const npcg_neighbors* nb, int64_t* n_pairs);

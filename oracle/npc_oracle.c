@@ -491,3 +491,71 @@ int64_t orc_voxel_downsample(const double* xyz, const int64_t* off, int64_t nb, 
   free(keyed);
   return m;
 }
+
+/* ------------------------------------------------------------------ */
+/* Degraded (voxel) build, triplets.cpp:78-133.                         */
+/* Sites = voxel_downsample(in, v) (representative per occupied voxel,  */
+/* (batch, key) order); site key = floor(p_rep / v) per axis; snapped   */
+/* position = (key + 0.5) * v; for each site s and integer offsets      */
+/* (dx, dy, dz) in [-h, h]^3 (dx outer, dz inner, h = (t-1)/2) whose    */
+/* voxel of the same batch is occupied: triplet (s, site of that voxel, */
+/* k = ((dx+h) t + (dy+h)) t + (dz+h)).  Returns the number of sites,   */
+/* or -3 (ShapeError: t) / -5 (VoxelError), validated in that order     */
+/* (triplets.cpp:79-81).  snapped: n*3, kept: n, parent: n, site_off:   */
+/* nb+1 (all caller-allocated at the input size).                       */
+/* ------------------------------------------------------------------ */
+int64_t orc_build_triplets_degraded(const double* xyz, const int64_t* off, int64_t nb,
+                                    double voxel, int64_t t, double* snapped, int64_t* kept,
+                                    int64_t* parent, int64_t* site_off, orc_triplets** res) {
+  *res = NULL;
+  if (t < 1 || t % 2 == 0) return -3;
+  if (!(voxel > 0.0)) return -5;
+  const int64_t ns = orc_voxel_downsample(xyz, off, nb, voxel, kept, parent, site_off);
+  if (ns < 0) return ns;
+  orc_keyed* keys = (orc_keyed*)malloc((size_t)(ns > 0 ? ns : 1) * sizeof(orc_keyed));
+  for (int64_t b = 0; b < nb; ++b)
+    for (int64_t s = site_off[b]; s < site_off[b + 1]; ++s) {
+      const double* p = xyz + 3 * kept[s];
+      keys[s].b = b;
+      keys[s].x = cell_of(p[0], voxel);
+      keys[s].y = cell_of(p[1], voxel);
+      keys[s].z = cell_of(p[2], voxel);
+      keys[s].index = s;
+      snapped[3 * s + 0] = ((double)keys[s].x + 0.5) * voxel;
+      snapped[3 * s + 1] = ((double)keys[s].y + 0.5) * voxel;
+      snapped[3 * s + 2] = ((double)keys[s].z + 0.5) * voxel;
+    }
+  /* sites are in (batch, key) order already (voxel_downsample output order) */
+  const int64_t h = (t - 1) / 2;
+  orc_triplets* tl = (orc_triplets*)calloc(1, sizeof(orc_triplets));
+  int64_t cap = 16;
+  tl->i = (uint32_t*)malloc((size_t)cap * 4);
+  tl->j = (uint32_t*)malloc((size_t)cap * 4);
+  tl->k = (uint32_t*)malloc((size_t)cap * 4);
+  for (int64_t s = 0; s < ns; ++s)
+    for (int64_t dx = -h; dx <= h; ++dx)
+      for (int64_t dy = -h; dy <= h; ++dy)
+        for (int64_t dz = -h; dz <= h; ++dz) {
+          orc_keyed q = {keys[s].b, keys[s].x + dx, keys[s].y + dy, keys[s].z + dz, 0};
+          int64_t lo = 0, hi = ns;
+          while (lo < hi) {
+            const int64_t mid = (lo + hi) / 2;
+            if (key_cmp4(&keys[mid], &q) < 0) lo = mid + 1;
+            else hi = mid;
+          }
+          if (lo >= ns || key_cmp4(&keys[lo], &q) != 0) continue;
+          if (tl->n == cap) {
+            cap *= 2;
+            tl->i = (uint32_t*)realloc(tl->i, (size_t)cap * 4);
+            tl->j = (uint32_t*)realloc(tl->j, (size_t)cap * 4);
+            tl->k = (uint32_t*)realloc(tl->k, (size_t)cap * 4);
+          }
+          tl->i[tl->n] = (uint32_t)s;
+          tl->j[tl->n] = (uint32_t)lo;
+          tl->k[tl->n] = (uint32_t)(((dx + h) * t + (dy + h)) * t + (dz + h));
+          tl->n++;
+        }
+  free(keys);
+  *res = tl;
+  return ns;
+}

@@ -91,6 +91,9 @@ class Oracle:
         lib.orc_rel_error_f64.argtypes = [_P, _P, _I64, _D]
         lib.orc_rel_error_f32.argtypes = [_P, _P, _I64, _D]
         lib.orc_voxel_downsample.argtypes = [_P, _P, _I64, _D, _P, _P, _P]
+        lib.orc_build_triplets_degraded.restype = _I64
+        lib.orc_build_triplets_degraded.argtypes = [_P, _P, _I64, _D, _I64, _P, _P, _P, _P,
+                                                    C.POINTER(_P)]
 
     # -- generators (random.hpp / synthetic.cpp / tensors.hpp) --------------
     def mt_draws(self, seed: int, n: int) -> np.ndarray:
@@ -209,6 +212,30 @@ class Oracle:
             raise OracleError(-m, "voxel_downsample")
         return kept[:m].copy(), parent, out_off
 
+    def build_triplets_degraded(self, xyz, voxel, t, offsets=None):
+        """triplets.cpp:78-133: ((i, j, k) in build order, snapped xyz, kept, parent, site offsets)."""
+        return _degraded(self.lib, "orc_build_triplets_degraded", "orc", xyz, voxel, t, offsets)
+
+
+def _degraded(lib, fn, pfx, xyz, voxel, t, offsets):
+    xyz = _f64(xyz).reshape(-1, 3)
+    off = _offsets(len(xyz), offsets)
+    n = len(xyz)
+    snapped = np.empty((max(n, 1), 3), dtype=np.float64)
+    kept = np.empty(max(n, 1), dtype=np.int64)
+    parent = np.empty(max(n, 1), dtype=np.int64)
+    site_off = np.empty(len(off), dtype=np.int64)
+    h = _P()
+    m = getattr(lib, fn)(_ptr(xyz), _ptr(off), len(off) - 1, voxel, t, _ptr(snapped), _ptr(kept),
+                         _ptr(parent), _ptr(site_off), C.byref(h))
+    if m < 0:
+        raise OracleError(-m, "build_triplets_degraded")
+    size = getattr(lib, pfx + "_triplets_size")(h)
+    ti, tj, tk = (np.empty(size, dtype=np.uint32) for _ in range(3))
+    getattr(lib, pfx + "_triplets_copy")(h, _ptr(ti), _ptr(tj), _ptr(tk))
+    getattr(lib, pfx + "_triplets_free")(h)
+    return (ti, tj, tk), snapped[:m].copy(), kept[:m].copy(), parent[:n].copy(), site_off
+
 
 def reference_available(path: str | None = None) -> bool:
     return os.path.exists(path or os.path.join(_HERE, "_ref", "libnpref.so"))
@@ -256,6 +283,9 @@ class Reference:
                                          _I64, _I64, _I64, _P, _P, _P, _P]
         lib.ref_voxel_downsample.argtypes = [_P, _P, _I64, _D, _P, _P, _P]
         lib.ref_voxel_downsample.restype = _I64
+        lib.ref_build_triplets_degraded.argtypes = [_P, _P, _I64, _D, _I64, _P, _P, _P, _P,
+                                                    C.POINTER(_P)]
+        lib.ref_build_triplets_degraded.restype = _I64
         lib.ref_conv_layer_f32.argtypes = [_P, _I64, _D, _I64, _I64, _I64, _P, _P, _P, _INT, _INT,
                                            _P, _P, _P, _P, C.POINTER(_P)]
         lib.ref_conv_cache_free.argtypes = [_P]
@@ -434,6 +464,10 @@ class Reference:
         if m < 0:
             raise OracleError(-m, "voxel_downsample")
         return kept[:m].copy(), parent, out_off
+
+    def build_triplets_degraded(self, xyz, voxel, t, offsets=None):
+        """The reference's build_triplets_degraded (triplets.hpp:63-76)."""
+        return _degraded(self.lib, "ref_build_triplets_degraded", "ref", xyz, voxel, t, offsets)
 
     def conv_layer_f32(self, xyz, radius, t, w, fin, gout, workers=0, build=True, cache=None,
                        outputs=False):

@@ -299,6 +299,28 @@ int64_t ref_voxel_downsample(const double* xyz, const int64_t* off, int64_t nb, 
   } catch (const std::exception& e) { return -status_of(e); }
 }
 
+// triplets.hpp:63-76 build_triplets_degraded (ConvMode::degraded geometry)
+int64_t ref_build_triplets_degraded(const double* xyz, const int64_t* off, int64_t nb, double v,
+                                    int64_t t, double* snapped, int64_t* kept, int64_t* parent,
+                                    int64_t* site_off, void** out) {
+  try {
+    ConvGeometry g;
+    g.mode = ConvMode::degraded;
+    g.voxel_size = v;
+    g.t = t;
+    DegradedBuild b = build_triplets_degraded(cloud_of(xyz, off, nb), g);
+    const int64_t ns = b.snapped.n_points();
+    for (int64_t s = 0; s < ns; ++s)
+      for (int a = 0; a < 3; ++a) snapped[3 * s + a] = b.snapped.position(s)[a];
+    std::memcpy(kept, b.sites.kept_index.data(), b.sites.kept_index.size() * 8);
+    std::memcpy(parent, b.sites.parent_of.data(), b.sites.parent_of.size() * 8);
+    auto o = b.snapped.batch_offsets();
+    std::memcpy(site_off, o.data(), o.size() * 8);
+    *out = new RefTriplets{std::move(b.triplets)};
+    return ns;
+  } catch (const std::exception& e) { return -status_of(e); }
+}
+
 // The reference's own conv-layer chain, timed with steady_clock exactly as
 // SURVEY.md §8d prescribes: build_triplets_native -> sort_triplets(by_k) ->
 // mvmr -> mvmr_transposed -> vvor (ExecConfig{grouped, L=128,

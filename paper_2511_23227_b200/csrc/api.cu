@@ -110,6 +110,31 @@ std::unique_ptr<npcg_neighbors> handle_from_triplets(npcg_context* ctx, const np
   return nb;
 }
 
+// dst[m] = src[idx[m]] / dst[idx[m]] = src[m], rows of `width` bytes (width % 4 == 0)
+template <bool SCATTER>
+__global__ void k_move_rows(const uint32_t* __restrict__ src, const int64_t* __restrict__ idx,
+                            int64_t n, int64_t words, uint32_t* __restrict__ dst) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= n * words) return;
+  const int64_t m = x / words, w = x % words;
+  if (SCATTER) dst[idx[m] * words + w] = src[m * words + w];
+  else dst[m * words + w] = src[idx[m] * words + w];
+}
+void gather_rows(npcg_context* ctx, const void* src, const int64_t* idx, int64_t n, int64_t width,
+                 void* dst) {
+  if (n == 0) return;
+  const int64_t words = width / 4;
+  launch(ctx, "gather_rows", k_move_rows<false>, dim3(static_cast<unsigned>(ceil_div(n * words, 256))),
+         dim3(256), 0, static_cast<const uint32_t*>(src), idx, n, words, static_cast<uint32_t*>(dst));
+}
+void scatter_rows(npcg_context* ctx, const void* src, const int64_t* idx, int64_t n, int64_t width,
+                  void* dst) {
+  if (n == 0) return;
+  const int64_t words = width / 4;
+  launch(ctx, "scatter_rows", k_move_rows<true>, dim3(static_cast<unsigned>(ceil_div(n * words, 256))),
+         dim3(256), 0, static_cast<const uint32_t*>(src), idx, n, words, static_cast<uint32_t*>(dst));
+}
+
 void forward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, const void* w,
                   int64_t G, int64_t cin, int64_t cout, const void* fin,
                   const npcg_exec_config* cfg, void* fout) {
@@ -393,6 +418,54 @@ npcg_status npcg_build_triplets_native(npcg_context* ctx, const npcg_cloud* out_
   return build_common(ctx, out_cloud, in_cloud, radius, t, out);
 }
 
+npcg_status npcg_build_triplets_degraded(npcg_context* ctx, const npcg_cloud* in_cloud,
+                                         double voxel_size, int64_t t, npcg_neighbors** out) {
+  if (!ctx || !out) return NPCG_ERR_INVALID;
+  *out = nullptr;
+  return guard(ctx, [&] {
+    // triplets.cpp:79-81: validate_t, then the voxel size
+    if (t < 1 || t % 2 == 0)
+      fail(NPCG_ERR_SHAPE, "conv geometry: kernel resolution t must be odd and >= 1");
+    if (!(voxel_size > 0.0)) fail(NPCG_ERR_VOXEL, "build_triplets_degraded: voxel_size must be > 0");
+    validate_cloud(ctx, in_cloud, "in_cloud");
+    auto nb = std::make_unique<npcg_neighbors>();
+    build_degraded(ctx, in_cloud, voxel_size, t, nb.get());
+    NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    *out = nb.release();
+  });
+}
+
+npcg_status npcg_neighbors_sites(const npcg_neighbors* nb, int64_t* n_sites, int64_t* n_fine,
+                                 int64_t* n_batches) {
+  if (!nb) return NPCG_ERR_INVALID;
+  if (!nb->degraded) return NPCG_ERR_STATE;
+  if (n_sites) *n_sites = nb->n_out;
+  if (n_fine) *n_fine = nb->n_fine;
+  if (n_batches) *n_batches = static_cast<int64_t>(nb->site_offsets.size()) - 1;
+  return NPCG_OK;
+}
+
+npcg_status npcg_neighbors_export_sites(npcg_context* ctx, const npcg_neighbors* nb,
+                                        double* snapped_xyz, int64_t* kept, int64_t* parent,
+                                        int64_t* site_offsets) {
+  if (!ctx || !nb) return NPCG_ERR_INVALID;
+  return guard(ctx, [&] {
+    if (!nb->degraded) fail(NPCG_ERR_STATE, "PointConvOp: no degraded cache");
+    const int64_t ns = nb->n_out;
+    if (snapped_xyz && ns)
+      NPCG_CUDA(cudaMemcpyAsync(snapped_xyz, nb->site_xyz.get(), 3 * ns * sizeof(double),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    if (kept && ns)
+      NPCG_CUDA(cudaMemcpyAsync(kept, nb->kept.get(), ns * sizeof(int64_t),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    if (parent && nb->n_fine)
+      NPCG_CUDA(cudaMemcpyAsync(parent, nb->parent.get(), nb->n_fine * sizeof(int64_t),
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    if (site_offsets)
+      std::copy(nb->site_offsets.begin(), nb->site_offsets.end(), site_offsets);
+  });
+}
+
 npcg_status npcg_neighbors_destroy(npcg_neighbors* nb) {
   if (!nb) return NPCG_ERR_INVALID;
   delete nb;
@@ -647,6 +720,17 @@ npcg_status npcg_conv_forward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype 
     need(fout, "fout");
     need(w, "w");
     if (nb->n_in > 0) need(fin, "fin");
+    if (nb->degraded) {
+      // conv_op.hpp:133-158: the engines see one row per site, gathered from
+      // each site's representative point; the gathered rows are the
+      // operator's saved input for the backward
+      const int64_t width = groups * c_in * static_cast<int64_t>(dsize(dtype));
+      if (nb->site_fin.size() < nb->n_in * width) nb->site_fin.alloc(ctx, nb->n_in * width);
+      gather_rows(ctx, fin, nb->kept.get(), nb->n_in, width, nb->site_fin.get());
+      nb->site_fin_dtype = dtype;
+      forward_impl(ctx, nb, dtype, w, groups, c_in, c_out, nb->site_fin.get(), cfg, fout);
+      return;
+    }
     forward_impl(ctx, nb, dtype, w, groups, c_in, c_out, fin, cfg, fout);
   });
 }
@@ -660,6 +744,22 @@ npcg_status npcg_conv_backward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype
     check_op(nb, dtype, groups, c_in, c_out, cfg);
     need(w, "w");
     if (nb->n_out > 0) need(gout, "gout");
+    if (nb->degraded) {
+      // conv_op.hpp:177-202: gradients w.r.t. the rows saved by the forward;
+      // site input gradients scatter back to the representative points,
+      // merged-away points keep zero rows
+      if (nb->site_fin_dtype != dtype)
+        fail(NPCG_ERR_STATE, "PointConvOp::backward: no cached forward inputs");
+      const int64_t width = groups * c_in * static_cast<int64_t>(dsize(dtype));
+      DevBuf<uint8_t> gi_sites(ctx, grad_in ? std::max<int64_t>(nb->n_in * width, 1) : 0);
+      backward_impl(ctx, nb, dtype, w, groups, c_in, c_out, nb->site_fin.get(), gout, cfg,
+                    grad_in ? gi_sites.get() : nullptr, grad_w);
+      if (grad_in && nb->n_fine) {
+        NPCG_CUDA(cudaMemsetAsync(grad_in, 0, nb->n_fine * width, ctx->stream));
+        scatter_rows(ctx, gi_sites.get(), nb->kept.get(), nb->n_in, width, grad_in);
+      }
+      return;
+    }
     if (grad_w && nb->n_in > 0) need(fin, "fin");
     backward_impl(ctx, nb, dtype, w, groups, c_in, c_out, fin, gout, cfg, grad_in, grad_w);
   });

@@ -288,7 +288,7 @@ __global__ void k_morton_keys(const double* __restrict__ xyz, const uint32_t* __
   keys[p] = (static_cast<uint64_t>(bid[p]) << (3 * axis_bits)) | m;
 }
 
-static void spatial_order(npcg_context* ctx, const double* xyz, const uint32_t* bid, int64_t n,
+void spatial_order(npcg_context* ctx, const double* xyz, const uint32_t* bid, int64_t n,
                           int64_t n_batches, double edge, DevBuf<uint32_t>& perm) {
   perm.alloc(ctx, n);
   if (n == 0) return;

@@ -71,6 +71,15 @@ struct npcg_neighbors {
   npcg::DevBuf<uint32_t> col_k;
   npcg::DevBuf<uint32_t> perm_out, perm_in;  // spatial order of each cloud (may alias: same cloud)
   bool same_cloud = false;
+  // degraded mode (triplets.cpp:78-133): the handle's clouds are the snapped
+  // sites; conv calls gather / scatter the n_fine original rows through kept
+  bool degraded = false;
+  int64_t n_fine = 0;
+  npcg::DevBuf<double> site_xyz;       // (n_sites, 3) voxel centres
+  npcg::DevBuf<int64_t> kept, parent;  // DownsampleMap: kept_index (n_sites), parent_of (n_fine)
+  std::vector<int64_t> site_offsets;   // host, n_batches + 1
+  npcg::DevBuf<uint8_t> site_fin;      // engine-facing rows saved by the last forward
+  int32_t site_fin_dtype = -1;
   // cached plans
   std::unique_ptr<npcg::CsrPlan> tcsr;   // transposed CSR (rows = input points)
   std::unique_ptr<npcg::CellPlan> cells; // (k, i, j)
@@ -80,6 +89,13 @@ struct npcg_neighbors {
 namespace npcg {
 
 void validate_cloud(npcg_context* ctx, const npcg_cloud* c, const char* what);
+// (batch, Morton code of the `edge` cell) order of a cloud -> perm
+void spatial_order(npcg_context* ctx, const double* xyz, const uint32_t* bid, int64_t n,
+                   int64_t n_batches, double edge, DevBuf<uint32_t>& perm);
+void batch_ids_of(npcg_context* ctx, const npcg_cloud* c, DevBuf<uint32_t>& bid);
+// Degraded build (triplets.cpp:78-133) into nb; t and voxel validated by the caller.
+void build_degraded(npcg_context* ctx, const npcg_cloud* in_cloud, double voxel, int64_t t,
+                    npcg_neighbors* nb);
 void build_neighbors(npcg_context* ctx, const npcg_cloud* out_cloud, const npcg_cloud* in_cloud,
                      double radius, int64_t t, npcg_neighbors* nb);
 // Expand CSR rows into an explicit row-index array (u32 or i64).

@@ -326,6 +326,32 @@ class Neighbors:
         L.lib().npcg_neighbors_info(handle, C.byref(no), C.byref(ni), C.byref(nk), C.byref(r))
         self.size, self.n_out, self.n_in, self.n_kernels, self.radius = (
             n.value, no.value, ni.value, nk.value, r.value)
+        ns, nf, nbat = C.c_int64(), C.c_int64(), C.c_int64()
+        self.degraded = L.lib().npcg_neighbors_sites(handle, C.byref(ns), C.byref(nf),
+                                                     C.byref(nbat)) == 0
+        # rows of the caller's input features (degraded: the original points)
+        self.n_fine = nf.value if self.degraded else self.n_in
+        self._sites = None
+
+    def sites(self):
+        """Degraded handles (conv_op.hpp:56-57): (snapped_cloud, DownsampleMap)."""
+        if not self.degraded:
+            raise StateError("PointConvOp: no degraded cache")
+        if self._sites is None:
+            dev = torch.device("cuda", self.ctx.device)
+            nbat = C.c_int64()
+            L.lib().npcg_neighbors_sites(self.h, None, None, C.byref(nbat))
+            xyz = torch.empty((self.n_out, 3), dtype=torch.float64, device=dev)
+            kept = torch.empty(max(self.n_out, 1), dtype=torch.int64, device=dev)
+            parent = torch.empty(max(self.n_fine, 1), dtype=torch.int64, device=dev)
+            off = np.zeros(nbat.value + 1, dtype=np.int64)
+            h = self.ctx.bind()
+            self.ctx.check(L.lib().npcg_neighbors_export_sites(
+                h, self.h, _ptr(xyz), _ptr(kept), _ptr(parent),
+                off.ctypes.data_as(C.c_void_p)), "export_sites")
+            self._sites = (PointCloud(xyz, off),
+                           DownsampleMap(kept[:self.n_out], parent[:self.n_fine]))
+        return self._sites
 
     def __del__(self):
         try:
@@ -425,9 +451,37 @@ def radius_search(queries: PointCloud, targets: PointCloud, radius: float) -> Ne
 
 
 def build_neighbors(out_cloud: PointCloud, in_cloud: PointCloud, geom: ConvGeometry) -> Neighbors:
+    """Native mode: radius neighbors of out_cloud in in_cloud with kernel cells.
+    Degraded mode: the voxel-site build of in_cloud (out_cloud ignored, as the
+    reference's single-cloud degraded forward, conv_op.hpp:116-120)."""
     if geom.mode != ConvMode.native:
-        raise Unsupported("degraded (voxel) mode is not built on the GPU yet (SURVEY §8f next #3)")
+        return _build_degraded(in_cloud, geom.voxel_size, geom.t)
     return _build(out_cloud, in_cloud, geom.radius, geom.t)
+
+
+def _build_degraded(in_cloud: PointCloud, voxel_size: float, t: int) -> Neighbors:
+    ctx = context(in_cloud.xyz.device)
+    h = ctx.bind()
+    ic = in_cloud._c()
+    nb = C.c_void_p()
+    ctx.check(L.lib().npcg_build_triplets_degraded(h, C.byref(ic), float(voxel_size), int(t),
+                                                   C.byref(nb)), "build_triplets_degraded")
+    return Neighbors(ctx, nb, (in_cloud,))
+
+
+@dataclass
+class DegradedBuild:  # triplets.hpp:63-67
+    triplets: "TripletList"
+    snapped: PointCloud
+    sites: "DownsampleMap"
+
+
+def build_triplets_degraded(in_cloud: PointCloud, geom: ConvGeometry) -> DegradedBuild:
+    """triplets.hpp:69-76: site triplets in build order (sort_axis none), the
+    snapped site cloud and the site map."""
+    nb = _build_degraded(in_cloud, geom.voxel_size, geom.t)
+    snapped, sites = nb.sites()
+    return DegradedBuild(nb.export_triplets(SortAxis.none), snapped, sites)
 
 
 def build_triplets_native(out_cloud: PointCloud, in_cloud: PointCloud,
@@ -602,7 +656,7 @@ def conv_backward(nb: Neighbors, weights: torch.Tensor, fin: torch.Tensor, gout:
                   need_w=True):
     K, G, cin, cout = weights.shape
     if need_in and grad_in is None:
-        grad_in = torch.empty((nb.n_in, G, cin), dtype=gout.dtype, device=gout.device)
+        grad_in = torch.empty((nb.n_fine, G, cin), dtype=gout.dtype, device=gout.device)
     if need_w and grad_w is None:
         grad_w = torch.empty((K, G, cout, cin), dtype=gout.dtype, device=gout.device)
     cfg = config._c()
@@ -653,6 +707,18 @@ class PointConvOp:
             axis = SortAxis(L.lib().npcg_choose_sort_axis(nb.n_out, nb.n_in, nb.n_kernels))
             self._sorted = nb.export_triplets(axis)
         return self._sorted
+
+    def snapped_cloud(self) -> PointCloud:
+        """conv_op.hpp:56: sites of the last degraded forward."""
+        if self._nb is None or not self._nb.degraded:
+            raise StateError("PointConvOp: no degraded cache")
+        return self._nb.sites()[0]
+
+    def site_map(self) -> "DownsampleMap":
+        """conv_op.hpp:57."""
+        if self._nb is None or not self._nb.degraded:
+            raise StateError("PointConvOp: no degraded cache")
+        return self._nb.sites()[1]
 
     def _build_cache(self, in_cloud: PointCloud, out_cloud: PointCloud):
         key = (in_cloud.xyz.data_ptr(), out_cloud.xyz.data_ptr(), in_cloud.n_points(),

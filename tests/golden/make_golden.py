@@ -85,6 +85,18 @@ def main():
                         voxel=0.45, kept=kept, parent=parent, kept_offsets=koff)
     out["voxel_clusters"] = int(len(kept))
 
+    # 5b. degraded (voxel) build (triplets.cpp:78-133): clustered 3-batch cloud
+    #     (middle batch empty), t = 3 and t = 5, build order + sites
+    xyz6 = r.gen_gaussian_clusters(900, 8, 4.0, 0.35, 104)
+    off6 = np.array([0, 400, 400, 900], dtype=np.int64)
+    deg = {"xyz": xyz6, "offsets": off6, "voxel": 0.3}
+    for t in (3, 5):
+        (ti, tj, tk), snapped, kept, parent, soff = r.build_triplets_degraded(xyz6, 0.3, t, off6)
+        deg.update({f"t{t}_i": ti, f"t{t}_j": tj, f"t{t}_k": tk, f"t{t}_snapped": snapped,
+                    f"t{t}_kept": kept, f"t{t}_parent": parent, f"t{t}_site_offsets": soff})
+        out[f"degraded_t{t}"] = int(len(ti))
+    np.savez_compressed(os.path.join(HERE, "degraded_clusters.npz"), **deg)
+
     # 6. mt19937_64 draws + generators (random.hpp / synthetic.cpp)
     np.savez_compressed(os.path.join(HERE, "rng.npz"), draws=r.mt_draws(5489, 64),
                         cube=r.gen_uniform_cube(8, 2.0, 7),
@@ -121,6 +133,13 @@ def main():
         "mvmr_identity": {"ref": "test_engine.cpp:75-87", "out": [3.0, 4.0]},
         "mvmr_reduce": {"ref": "test_engine.cpp:89-101", "out": [4.0, 6.0]},
         "dgrad": {"ref": "test_engine.cpp:103-115", "w": [1.0, 3.0, 2.0, 4.0], "out": [4.0, 6.0]},
+        "degraded": {"ref": "test_triplets.cpp:154-215", "voxel": 1.0, "cases": [
+            {"xyz": [[0.25, 0.25, 0.25]], "t": 3, "i": [0], "j": [0], "k": [13],
+             "snapped": [[0.5, 0.5, 0.5]]},
+            {"xyz": [[0.5, 0.5, 0.5], [1.5, 0.5, 0.5]], "t": 3, "k_multiset": [4, 13, 13, 22]},
+            {"xyz": [[0.2, 0.2, 0.2], [0.8, 0.8, 0.8], [5, 5, 5]], "t": 3, "n_sites": 2},
+            {"xyz": [[0.5, 0.5, 0.5], [2.5, 0.5, 0.5]], "t": 5, "k_multiset": [12, 62, 62, 112],
+             "n_kernels": 125}]},
         "counts": out,
     }
     with open(os.path.join(HERE, "golden_hand.json"), "w") as f:

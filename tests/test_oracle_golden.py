@@ -119,3 +119,52 @@ def test_oracle_boundary_exactness(orc, ref):
         a = orc.build_triplets(g, g, r, 3)
         b = ref.build_triplets(g, g, r, 3, axis=0)
         assert all(np.array_equal(p, q) for p, q in zip(a, b)), r
+
+
+def test_degraded_known_answers(orc, golden):
+    """test_triplets.cpp:154-215 through the C oracle."""
+    h = golden("golden_hand.json")["degraded"]
+    v = h["voxel"]
+    c0, c1, c2, c3 = h["cases"]
+    (ti, tj, tk), sn, kept, parent, so = orc.build_triplets_degraded(c0["xyz"], v, c0["t"])
+    assert list(ti) == c0["i"] and list(tj) == c0["j"] and list(tk) == c0["k"]
+    assert sn.tolist() == c0["snapped"]
+    (ti, tj, tk), *_ = orc.build_triplets_degraded(c1["xyz"], v, c1["t"])
+    assert sorted(tk.tolist()) == c1["k_multiset"]
+    assert all(tk[n] > tk[n - 1] for n in range(1, len(ti)) if ti[n] == ti[n - 1])
+    (ti, tj, tk), sn, kept, parent, so = orc.build_triplets_degraded(c2["xyz"], v, c2["t"])
+    assert len(sn) == c2["n_sites"] and parent[0] == parent[1] != parent[2]
+    (ti, tj, tk), *_ = orc.build_triplets_degraded(c3["xyz"], v, c3["t"])
+    assert sorted(tk.tolist()) == c3["k_multiset"]
+    with pytest.raises(Exception):
+        orc.build_triplets_degraded([[0, 0, 0]], 0.0, 3)
+    with pytest.raises(Exception):
+        orc.build_triplets_degraded([[0, 0, 0]], 1.0, 4)
+
+
+def test_degraded_matches_golden(orc, golden):
+    g = golden("degraded_clusters.npz")
+    for t in (3, 5):
+        (ti, tj, tk), sn, kept, parent, so = orc.build_triplets_degraded(
+            g["xyz"], float(g["voxel"]), t, g["offsets"])
+        for got, key in ((ti, "i"), (tj, "j"), (tk, "k"), (sn, "snapped"), (kept, "kept"),
+                         (parent, "parent"), (so, "site_offsets")):
+            assert np.array_equal(got, g[f"t{t}_{key}"]), (t, key)
+
+
+@pytest.mark.parametrize("seed", [1, 2, 3])
+def test_degraded_oracle_vs_reference(orc, ref, seed):
+    """The C restatement against the reference's build_triplets_degraded on
+    fresh seeded clouds (uniform multi-batch with an empty batch, clusters)."""
+    xyz = orc.gen_uniform_cube(2500, 1.0, seed)
+    off = [0, 900, 900, 2500]
+    for v, t in ((0.06, 3), (0.11, 1), (0.09, 5)):
+        a = orc.build_triplets_degraded(xyz, v, t, off)
+        b = ref.build_triplets_degraded(xyz, v, t, off)
+        assert all(np.array_equal(x, y) for x, y in zip(a[0], b[0]))
+        assert all(np.array_equal(x, y) for x, y in zip(a[1:], b[1:]))
+    xyz = ref.gen_gaussian_clusters(3000, 10, 3.0, 0.2, seed + 10)
+    a = orc.build_triplets_degraded(xyz, 0.05, 3)
+    b = ref.build_triplets_degraded(xyz, 0.05, 3)
+    assert all(np.array_equal(x, y) for x, y in zip(a[0], b[0]))
+    assert all(np.array_equal(x, y) for x, y in zip(a[1:], b[1:]))
