@@ -286,6 +286,14 @@ class Reference:
         lib.ref_build_triplets_degraded.argtypes = [_P, _P, _I64, _D, _I64, _P, _P, _P, _P,
                                                     C.POINTER(_P)]
         lib.ref_build_triplets_degraded.restype = _I64
+        lib.ref_write_cloud.argtypes = [C.c_char_p, _P, _P, _I64]
+        lib.ref_write_cloud.restype = _INT
+        lib.ref_read_cloud.argtypes = [C.c_char_p, _P, _P, C.POINTER(_I64)]
+        lib.ref_read_cloud.restype = _I64
+        lib.ref_write_triplets.argtypes = [C.c_char_p, _P, _P, _P, _I64, _I64, _I64, _I64, _INT]
+        lib.ref_write_triplets.restype = _INT
+        lib.ref_read_triplets.argtypes = [C.c_char_p, _P, _P, _P, _P]
+        lib.ref_read_triplets.restype = _INT
         lib.ref_conv_layer_f32.argtypes = [_P, _I64, _D, _I64, _I64, _I64, _P, _P, _P, _INT, _INT,
                                            _P, _P, _P, _P, C.POINTER(_P)]
         lib.ref_conv_cache_free.argtypes = [_P]
@@ -468,6 +476,40 @@ class Reference:
     def build_triplets_degraded(self, xyz, voxel, t, offsets=None):
         """The reference's build_triplets_degraded (triplets.hpp:63-76)."""
         return _degraded(self.lib, "ref_build_triplets_degraded", "ref", xyz, voxel, t, offsets)
+
+    # -- io.hpp / triplets.hpp:84-93 through the reference's writers / readers --
+    def write_cloud(self, path, xyz, offsets=None):
+        xyz = _f64(xyz).reshape(-1, 3)
+        off = _offsets(len(xyz), offsets)
+        rc = self.lib.ref_write_cloud(path.encode(), _ptr(xyz), _ptr(off), len(off) - 1)
+        if rc:
+            raise OracleError(rc, "write_cloud")
+
+    def read_cloud(self, path):
+        nb = _I64()
+        n = self.lib.ref_read_cloud(path.encode(), None, None, C.byref(nb))
+        if n < 0:
+            raise OracleError(-n, "read_cloud")
+        xyz = np.empty((n, 3), dtype=np.float64)
+        off = np.empty(nb.value + 1, dtype=np.int64)
+        self.lib.ref_read_cloud(path.encode(), _ptr(xyz), _ptr(off), C.byref(nb))
+        return xyz, off
+
+    def write_triplets(self, path, ti, tj, tk, n_out, n_in, n_kernels, axis=0):
+        ti, tj, tk = _u32(ti), _u32(tj), _u32(tk)
+        rc = self.lib.ref_write_triplets(path.encode(), _ptr(ti), _ptr(tj), _ptr(tk), len(ti),
+                                         n_out, n_in, n_kernels, axis)
+        if rc:
+            raise OracleError(rc, "write_triplets")
+
+    def read_triplets(self, path):
+        meta = np.zeros(5, dtype=np.int64)
+        rc = self.lib.ref_read_triplets(path.encode(), None, None, None, _ptr(meta))
+        if rc:
+            raise OracleError(rc, "read_triplets")
+        ti, tj, tk = (np.empty(int(meta[0]), dtype=np.uint32) for _ in range(3))
+        self.lib.ref_read_triplets(path.encode(), _ptr(ti), _ptr(tj), _ptr(tk), _ptr(meta))
+        return ti, tj, tk, int(meta[1]), int(meta[2]), int(meta[3]), int(meta[4])
 
     def conv_layer_f32(self, xyz, radius, t, w, fin, gout, workers=0, build=True, cache=None,
                        outputs=False):

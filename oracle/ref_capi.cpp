@@ -24,6 +24,7 @@
 #include "npconv/spatial.hpp"
 #include "npconv/synthetic.hpp"
 #include "npconv/tensors.hpp"
+#include "npconv/io.hpp"
 #include "npconv/triplets.hpp"
 #include "npconv/vvor.hpp"
 
@@ -319,6 +320,62 @@ int64_t ref_build_triplets_degraded(const double* xyz, const int64_t* off, int64
     *out = new RefTriplets{std::move(b.triplets)};
     return ns;
   } catch (const std::exception& e) { return -status_of(e); }
+}
+
+// io.hpp / triplets.hpp:84-93 file formats (NPC1, XYZ, TPL1), through the
+// reference's own writers / readers
+int ref_write_cloud(const char* path, const double* xyz, const int64_t* off, int64_t nb) {
+  try {
+    write_cloud(path, cloud_of(xyz, off, nb));
+    return 0;
+  } catch (const std::exception& e) { return status_of(e); }
+}
+// Returns the point count (xyz / off sized by the caller: query with xyz == NULL
+// first, which also returns the batch count through *nb).
+int64_t ref_read_cloud(const char* path, double* xyz, int64_t* off, int64_t* nb) {
+  try {
+    PointCloud c = read_cloud(path);
+    *nb = c.n_batches();
+    if (xyz) {
+      for (int64_t p = 0; p < c.n_points(); ++p)
+        for (int a = 0; a < 3; ++a) xyz[3 * p + a] = c.position(p)[a];
+      auto o = c.batch_offsets();
+      std::memcpy(off, o.data(), o.size() * 8);
+    }
+    return c.n_points();
+  } catch (const std::exception& e) { return -status_of(e); }
+}
+int ref_write_triplets(const char* path, const uint32_t* i, const uint32_t* j, const uint32_t* k,
+                       int64_t n, int64_t n_out, int64_t n_in, int64_t nk, int axis) {
+  try {
+    TripletList t;
+    t.i.assign(i, i + n);
+    t.j.assign(j, j + n);
+    t.k.assign(k, k + n);
+    t.n_out = n_out;
+    t.n_in = n_in;
+    t.n_kernels = nk;
+    t.sort_axis = static_cast<SortAxis>(axis);
+    write_triplets(path, t);
+    return 0;
+  } catch (const std::exception& e) { return status_of(e); }
+}
+// meta[0..4] = size, n_out, n_in, n_kernels, axis; arrays filled when i != NULL
+int ref_read_triplets(const char* path, uint32_t* i, uint32_t* j, uint32_t* k, int64_t* meta) {
+  try {
+    TripletList t = read_triplets(path);
+    meta[0] = t.size();
+    meta[1] = t.n_out;
+    meta[2] = t.n_in;
+    meta[3] = t.n_kernels;
+    meta[4] = static_cast<int64_t>(t.sort_axis);
+    if (i) {
+      std::memcpy(i, t.i.data(), t.i.size() * 4);
+      std::memcpy(j, t.j.data(), t.j.size() * 4);
+      std::memcpy(k, t.k.data(), t.k.size() * 4);
+    }
+    return 0;
+  } catch (const std::exception& e) { return status_of(e); }
 }
 
 // The reference's own conv-layer chain, timed with steady_clock exactly as

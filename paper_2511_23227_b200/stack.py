@@ -1,0 +1,106 @@
+"""Layer stacks over one cached neighbor structure.
+
+The reference composes layers by calling PointConvOp::forward layer after
+layer (test_conv_op.cpp:291-309); each op keeps its own triplet cache keyed by
+the cloud's identity (conv_op.hpp:106-127), so a stack of L layers on one
+cloud builds L identical caches.  ConvStack keeps the operator semantics
+(no bias, no activation, the saved forward inputs feed the backward) but
+shares ONE device-resident neighbor handle across the layers of a geometry,
+keeps every activation on the device, and can capture a whole
+forward + backward step into a CUDA graph: after the first (plan-building)
+step, a step is a fixed sequence of the library's kernel launches with no
+host synchronisation, which a graph replays without per-launch CPU cost.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import npconv as npc
+
+
+@dataclass
+class StackGrads:
+    grad_in: torch.Tensor          # w.r.t. the stack's input features
+    grad_w: list[torch.Tensor]     # per layer, (K, G, C_out, C_in) (vvor.hpp:12-16)
+
+
+class ConvStack:
+    """Layers l = 0..L-1 with weights (K, G, C_l, C_{l+1}) sharing one geometry."""
+
+    def __init__(self, weights: list[torch.Tensor], geometry: npc.ConvGeometry,
+                 config: npc.ExecConfig = npc.ExecConfig()):
+        if not weights:
+            raise npc.ShapeError("ConvStack: no layers")
+        for a, b in zip(weights, weights[1:]):
+            if a.shape[3] != b.shape[2] or a.shape[0] != b.shape[0] or a.shape[1] != b.shape[1]:
+                raise npc.ShapeError("ConvStack: consecutive layer shapes do not chain")
+        self.ops = [npc.PointConvOp(w, geometry, config, copy_fin=False) for w in weights]
+        self.geometry = geometry
+        self.config = config
+        self._nb: npc.Neighbors | None = None
+        self._key = None
+        self._acts: list[torch.Tensor] = []
+        self._graph = None
+
+    # -- shared cache (conv_op.hpp:106-127, one build for all layers) ----------
+    def neighbors(self, cloud: npc.PointCloud) -> npc.Neighbors:
+        key = (cloud.xyz.data_ptr(), cloud.n_points())
+        if self._nb is None or key != self._key:
+            self._nb = npc.build_neighbors(cloud, cloud, self.geometry)
+            self._key = key
+            self._graph = None
+            for op in self.ops:  # every layer sees the same handle
+                op._nb, op._key, op._sorted = self._nb, (key[0], key[0], key[1], key[1]), None
+        return self._nb
+
+    def forward(self, cloud: npc.PointCloud, fin: torch.Tensor) -> torch.Tensor:
+        nb = self.neighbors(cloud)
+        self._acts = [fin.contiguous()]
+        h = self._acts[0]
+        for op in self.ops:
+            h = npc.conv_forward(nb, op.weights(), h, self.config)
+            self._acts.append(h)
+        return h
+
+    def backward(self, gout: torch.Tensor) -> StackGrads:
+        if len(self._acts) != len(self.ops) + 1:
+            raise npc.StateError("ConvStack::backward: no cached forward inputs")
+        g = gout.contiguous()
+        gws = [None] * len(self.ops)
+        for l in range(len(self.ops) - 1, -1, -1):
+            g, gws[l] = npc.conv_backward(self._nb, self.ops[l].weights(), self._acts[l], g,
+                                          self.config, need_in=True, need_w=True)
+        return StackGrads(g, gws)
+
+    # -- CUDA graph of one forward + backward step ------------------------------
+    def capture(self, cloud: npc.PointCloud, fin: torch.Tensor, gout: torch.Tensor):
+        """Warms the plans up eagerly, then records forward + backward into a
+        CUDA graph over static input buffers (copy new inputs into
+        `static_fin` / `static_gout`, call replay(), read `static_out` and
+        `static_grads`).  Needs a plan without capacity spills (the spill
+        path sizes its work on the host)."""
+        self.forward(cloud, fin)
+        self.backward(gout)
+        torch.cuda.synchronize()
+        self.static_fin = fin.clone()
+        self.static_gout = gout.clone()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):  # one more eager step on the capture stream
+            self.forward(cloud, self.static_fin)
+            self.backward(self.static_gout)
+        torch.cuda.current_stream().wait_stream(side)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            self.static_out = self.forward(cloud, self.static_fin)
+            self.static_grads = self.backward(self.static_gout)
+        self._graph = g
+        return g
+
+    def replay(self):
+        if self._graph is None:
+            raise npc.StateError("ConvStack::replay: no captured graph")
+        self._graph.replay()
+        return self.static_out, self.static_grads
