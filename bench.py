@@ -324,19 +324,46 @@ def run_ours(args):
         hi = [torch.empty_like(d[5], device="cpu").pin_memory() for d in data]
         hw = torch.empty_like(gw_sum, device="cpu").pin_memory()
 
+        # host->device and device->host copies run on their own streams (one copy
+        # engine per direction) and overlap the kernels: the forward starts once
+        # its input landed while the upstream gradient is still being copied, and
+        # the forward output drains to the host while the backward runs.
+        s_h2d, s_d2h = torch.cuda.Stream(dev), torch.cuda.Stream(dev)
+        comp = torch.cuda.current_stream(dev)
+
         def step_e2e():
             gw_sum.zero_()
             for s_, (cl, nb, f, g, fo, gi, gw) in enumerate(data):
-                f.copy_(hf[s_], non_blocking=True)
-                g.copy_(hg[s_], non_blocking=True)
+                ev_f, ev_g = torch.cuda.Event(), torch.cuda.Event()
+                with torch.cuda.stream(s_h2d):
+                    s_h2d.wait_stream(comp)  # previous users of f / g are done
+                    f.copy_(hf[s_], non_blocking=True)
+                    ev_f.record(s_h2d)
+                    g.copy_(hg[s_], non_blocking=True)
+                    ev_g.record(s_h2d)
+                comp.wait_event(ev_f)
                 npc.conv_forward(nb, w, f, cfg, out=fo)
+                ev_fo = torch.cuda.Event()
+                ev_fo.record(comp)
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_fo)
+                    ho[s_].copy_(fo, non_blocking=True)
+                comp.wait_event(ev_g)
                 npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw)
                 gw_sum.add_(gw)
-                ho[s_].copy_(fo, non_blocking=True)
-                hi[s_].copy_(gi, non_blocking=True)
+                ev_b = torch.cuda.Event()
+                ev_b.record(comp)
+                with torch.cuda.stream(s_d2h):
+                    s_d2h.wait_event(ev_b)
+                    hi[s_].copy_(gi, non_blocking=True)
             if world > 1:
                 shard.allreduce_weight_grad(gw_sum)
-            hw.copy_(gw_sum, non_blocking=True)
+            ev_w = torch.cuda.Event()
+            ev_w.record(comp)
+            with torch.cuda.stream(s_d2h):
+                s_d2h.wait_event(ev_w)
+                hw.copy_(gw_sum, non_blocking=True)
+            comp.wait_stream(s_d2h)  # the step ends when every result is on the host
 
         for _ in range(max(1, args.warmup)):
             step_e2e()

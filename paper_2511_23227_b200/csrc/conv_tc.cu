@@ -740,6 +740,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     constexpr uint32_t idesc = idesc_bf16(128, 64, false, false);
     const uint64_t a_desc0 = sdesc_sw128(s_a, 16, 1024), b_desc0 = sdesc_sw128(s_w, 16, 1024);
     uint32_t w_it = 0, a_it = 0, t_it = 0;
+    // The epilogue warps block on named barrier 2 + (tile & 1) (no polling);
+    // the tile's accumulator is handed over once its T_FULL commit landed,
+    // checked after the first cell of the next tile has been issued.
+    bool pending = false;
+    uint32_t pend_t = 0;
+    auto release_epilogue = [&]() {
+      mbar_wait(bar(B_T_FULL + (pend_t & 1)), (pend_t >> 1) & 1);
+      named_bar_arrive(2 + (pend_t & 1), 32 * 5);
+      pending = false;
+    };
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       const int nsub = min(a.st, a.n_sub - s * a.st);
       if (a.halo_len[s] == kOverflow) continue;
@@ -747,6 +757,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
       tc_fence_after();
       for (int k = 0; k < K; ++k) {
+        if (pending && k == 1) release_epilogue();
         const uint32_t ws = w_it % NSW;
         mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
         if (lane == 0) trace_ev(a.trace, a_it, 6);
@@ -775,8 +786,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       }
       if (elect_one()) umma_commit(bar(B_T_FULL + ab));
       __syncwarp();
+      if (pending) release_epilogue();  // K == 1
+      pending = true;
+      pend_t = t_it;
       ++t_it;
     }
+    if (pending) release_epilogue();
   } else if (warp >= FWD_AGG_WARP0) {
     // ------------------------------ aggregation ----------------------------
     const int aw = warp - FWD_AGG_WARP0;
@@ -827,7 +842,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
                                 a.halo_len[s_next], a.feat, 32 * e + lane);
       }
-      mbar_wait_sleep(bar(B_T_FULL + ab), (t_it >> 1) & 1);
+      named_bar_sync(2 + ab, 32 * 5);  // released by the MMA warp once T_FULL(tile) landed
       tc_fence_after();
       for (int g = 0; g < nsub; ++g) {
         const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * FWD_ACC_COLS + g * 64;
