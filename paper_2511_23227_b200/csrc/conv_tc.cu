@@ -61,7 +61,7 @@ struct TcDirPlan {
 };
 
 struct TcPlan {
-  std::unique_ptr<TcDirPlan> fwd, bwd, wg;
+  std::unique_ptr<TcDirPlan> fwd, bwd;  // wgrad reuses the forward plan
   DevBuf<uint32_t> inv_perm_out, inv_perm_in;
   DevBuf<__nv_bfloat16> feat_in;   // bf16 F_in in perm_in order
   const void* saved_fin = nullptr;  // fin whose image feat_in holds (set by the forward)
@@ -886,7 +886,7 @@ struct WgArgs {
   const uint32_t* blk_off;
   const uint8_t* blocks;
   int64_t n_rows;
-  int n_sub, hcap, K;
+  int n_sub, n_super, st, hcap, K;  // the forward plan's super-tiles (st sub-tiles share a halo)
   const __nv_bfloat16* feat;   // bf16 F_in (n_cols, 64), permuted
   const __nv_bfloat16* dense;  // bf16 G_out (n_rows, 64), permuted (row = sub-tile order)
   float* partial;              // [gridDim.x][K][64 c][64 m]
@@ -895,7 +895,8 @@ struct WgArgs {
 constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
 constexpr int WG_PAIRS = 7;      // cell pairs per CTA (cell group = 14 cells)
 constexpr int WG_NSA = 2;        // A pair stages (32 KB)
-constexpr int WG_NSD = 6;        // descriptor slots (2 blocks each)
+constexpr int WG_NSD = 3;        // descriptor slots (2 blocks each)
+constexpr int WG_NSG = 2;        // dense G sub-tile slots (16 KB)
 constexpr int WG_GROUPS = 2;     // stage (cell pair) s is aggregated by warp group s % 2
 
 struct WgSmem {
@@ -911,16 +912,16 @@ __host__ __device__ inline WgSmem wg_smem_layout(int hcap) {
   L.a = o;
   o += WG_NSA * 32768;
   L.gt = o;
-  o += 16384;
+  o += WG_NSG * 16384;
   L.d = o;
   o += WG_NSD * 2 * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
   L.bar = o;
-  o += 32 * 8;
+  o += 24 * 8;
   L.tmem_slot = o;
   o += 16;
   L.offs = o;
-  o += 64 * 4;
+  o += (2 * KMAX + 1) * 4;
   L.total = o + 1024;
   return L;
 }
@@ -928,15 +929,16 @@ __host__ __device__ inline WgSmem wg_smem_layout(int hcap) {
 enum : int {
   W_HALO_FULL = 0,
   W_HALO_EMPTY = 1,
-  W_A_FULL = 2,   // 2
-  W_A_EMPTY = 4,  // 2
-  W_D_FULL = 6,   // WG_NSD
-  W_D_EMPTY = 12, // WG_NSD
-  W_G_FULL = 18,
-  W_G_EMPTY = 19,
-  W_DONE = 20,
-  W_COUNT = 21
+  W_A_FULL = 2,                    // WG_NSA
+  W_A_EMPTY = W_A_FULL + WG_NSA,   // WG_NSA
+  W_D_FULL = W_A_EMPTY + WG_NSA,   // WG_NSD
+  W_D_EMPTY = W_D_FULL + WG_NSD,   // WG_NSD
+  W_G_FULL = W_D_EMPTY + WG_NSD,   // WG_NSG
+  W_G_EMPTY = W_G_FULL + WG_NSG,   // WG_NSG
+  W_DONE = W_G_EMPTY + WG_NSG,
+  W_COUNT = W_DONE + 1
 };
+static_assert(W_COUNT <= 24, "wgrad barrier region");
 
 __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   extern __shared__ uint8_t smem_raw[];
@@ -967,8 +969,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       mbar_init(bar(W_D_FULL + i), 1);
       mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS / WG_GROUPS);
     }
-    mbar_init(bar(W_G_FULL), 4);
-    mbar_init(bar(W_G_EMPTY), 1);
+    for (int i = 0; i < WG_NSG; ++i) {
+      mbar_init(bar(W_G_FULL + i), 4);
+      mbar_init(bar(W_G_EMPTY + i), 1);
+    }
     mbar_init(bar(W_DONE), 1);
     fence_barrier_init();
   }
@@ -982,17 +986,20 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     // producer: halo + descriptor blocks (two cells per stage)
     uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
     uint32_t d_it = 0;
-    for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       if (a.halo_len[s] == kOverflow) continue;
-      for (int x = lane; x <= K; x += 32) offs[x] = a.blk_off[static_cast<int64_t>(s) * K + x];
+      const int nsub = min(a.st, a.n_sub - s * a.st);
+      for (int x = lane; x <= nsub * K; x += 32)
+        offs[x] = a.blk_off[static_cast<int64_t>(s) * a.st * K + x];
       __syncwarp();
+      for (int g = 0; g < nsub; ++g)
       for (int p = 0; p < n_pairs; ++p) {
         if (lane == 0) {
           const uint32_t ds = d_it % WG_NSD;
           mbar_wait(bar(W_D_EMPTY + ds), ((d_it / WG_NSD) & 1) ^ 1);
-          const int k0 = k_begin + 2 * p;
+          const int k0 = g * K + k_begin + 2 * p;
           const uint32_t o0 = offs[k0], o1 = offs[k0 + 1];
-          const uint32_t o2 = (k0 + 1 < K) ? offs[k0 + 2] : o1;
+          const uint32_t o2 = (k_begin + 2 * p + 1 < K) ? offs[k0 + 2] : o1;
           mbar_expect_tx(bar(W_D_FULL + ds), o2 - o0);
           bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(W_D_FULL + ds));
           if (o2 > o1)
@@ -1008,9 +1015,12 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       constexpr uint32_t idesc = idesc_bf16(128, 64, true, true);
       uint32_t a_it = 0, g_it = 0;
       bool first = true;
-      for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+      for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
         if (a.halo_len[s] == kOverflow) continue;
-        mbar_wait(bar(W_G_FULL), g_it & 1);
+        const int nsub = min(a.st, a.n_sub - s * a.st);
+        for (int g = 0; g < nsub; ++g) {
+        const uint32_t gs = g_it % WG_NSG;
+        mbar_wait(bar(W_G_FULL + gs), (g_it / WG_NSG) & 1);
         for (int p = 0; p < n_pairs; ++p) {
           const uint32_t as = a_it % WG_NSA;
           mbar_wait(bar(W_A_FULL + as), (a_it / WG_NSA) & 1);
@@ -1020,15 +1030,16 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
           for (int ks = 0; ks < 8; ++ks) {
             // K = points: 16 rows per step (2 x 8-row groups of 1024 B)
             const uint64_t ad = sdesc_sw128(s_a + as * 32768u + 2048u * ks, 16384, 1024);
-            const uint64_t bd = sdesc_sw128(s_g + 2048u * ks, 16384, 1024);
+            const uint64_t bd = sdesc_sw128(s_g + gs * 16384u + 2048u * ks, 16384, 1024);
             umma_bf16(d, ad, bd, idesc, (first && ks == 0) ? 0u : 1u);
           }
           umma_commit(bar(W_A_EMPTY + as));
           ++a_it;
         }
         first = false;
-        umma_commit(bar(W_G_EMPTY));
+        umma_commit(bar(W_G_EMPTY + gs));
         ++g_it;
+        }
       }
       umma_commit(bar(W_DONE));
     }
@@ -1037,13 +1048,15 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     const int aw = warp - FWD_AGG_WARP0;
     const int grp = aw / (FWD_AGG_WARPS / WG_GROUPS), wig = aw % (FWD_AGG_WARPS / WG_GROUPS);
     uint32_t a_it = 0, d_it = 0;
-    for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       const uint32_t H = a.halo_len[s];
       if (H == kOverflow) continue;
+      const int nsub = min(a.st, a.n_sub - s * a.st);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
       coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat,
                                          s_halo, 32 * aw + lane);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
+      for (int g = 0; g < nsub; ++g)
       for (int p = 0; p < n_pairs; ++p) {
         if (static_cast<int>(a_it % WG_GROUPS) == grp) {
           const uint32_t ds = d_it % WG_NSD, as = a_it % WG_NSA;
@@ -1068,33 +1081,38 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   } else {
     // warps 0-3: dense G tile loader during the sweep, epilogue at the end
     uint32_t g_it = 0;
-    for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) {
+    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       if (a.halo_len[s] == kOverflow) continue;
+      const int nsub = min(a.st, a.n_sub - s * a.st);
       {
         const int s_next = s + gridDim.x;
-        if (s_next < a.n_sub && a.halo_len[s_next] != kOverflow)
+        if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
           prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
                                 a.halo_len[s_next], a.feat, 32 * warp + lane);
       }
-      mbar_wait_sleep(bar(W_G_EMPTY), (g_it & 1) ^ 1);
-      // 128 rows x 8 chunks of 16 B; warp e copies rows 32e..32e+31
-      for (int x = lane; x < 32 * 8; x += 32) {
-        const int r = 32 * warp + (x >> 3), q = x & 7;
-        const int64_t row = static_cast<int64_t>(s) * TM + r;
-        uint4 v = make_uint4(0, 0, 0, 0);
-        if (row < a.n_rows) v = reinterpret_cast<const uint4*>(a.dense + row * CH)[q];
-        *reinterpret_cast<uint4*>(g_gt + r * 128 + (((q ^ (r & 7)) & 7) << 4)) = v;
+      for (int g = 0; g < nsub; ++g) {
+        const uint32_t gs = g_it % WG_NSG;
+        mbar_wait_sleep(bar(W_G_EMPTY + gs), ((g_it / WG_NSG) & 1) ^ 1);
+        // 128 rows x 8 chunks of 16 B; warp e copies rows 32e..32e+31
+        uint8_t* gt = g_gt + gs * 16384u;
+        for (int x = lane; x < 32 * 8; x += 32) {
+          const int r = 32 * warp + (x >> 3), q = x & 7;
+          const int64_t row = (static_cast<int64_t>(s) * a.st + g) * TM + r;
+          uint4 v = make_uint4(0, 0, 0, 0);
+          if (row < a.n_rows) v = reinterpret_cast<const uint4*>(a.dense + row * CH)[q];
+          *reinterpret_cast<uint4*>(gt + r * 128 + (((q ^ (r & 7)) & 7) << 4)) = v;
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(W_G_FULL + gs));
+        ++g_it;
       }
-      fence_proxy_async_smem();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(bar(W_G_FULL));
-      ++g_it;
     }
     // epilogue: TMEM lanes 32e..32e+31 of each pair accumulator -> partial
     mbar_wait_sleep(bar(W_DONE), 0);
     {
       bool any = false;
-      for (int s = blockIdx.x; s < a.n_sub; s += gridDim.x) any |= a.halo_len[s] != kOverflow;
+      for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) any |= a.halo_len[s] != kOverflow;
       if (!any) goto done;
     }
     tc_fence_after();
@@ -1140,7 +1158,6 @@ __global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, in
 // ===========================================================================
 // host drivers
 // ===========================================================================
-constexpr int WG_HCAP = 768;
 
 static TcPlan* get_plan(npcg_context* ctx, npcg_neighbors* nb) {
   if (!nb->tc) {
@@ -1178,19 +1195,10 @@ static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
   }
   return p->bwd.get();
 }
-static TcDirPlan* plan_wg(npcg_context* ctx, npcg_neighbors* nb) {
-  TcPlan* p = get_plan(ctx, nb);
-  if (!p->wg)
-    p->wg = build_dir_plan(ctx, nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out,
-                           nb->n_in, nb->perm_out.get(), p->inv_perm_in.get(),
-                           static_cast<int>(nb->n_kernels), 1, WG_HCAP);
-  return p->wg.get();
-}
 
 void tc_prepare(npcg_context* ctx, npcg_neighbors* nb) {
   plan_fwd(ctx, nb);
   plan_bwd(ctx, nb);
-  plan_wg(ctx, nb);
 }
 
 static void convert(npcg_context* ctx, const float* src, const uint32_t* perm, int64_t n,
@@ -1342,7 +1350,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     }
   }
   if (grad_w) {
-    TcDirPlan* P = plan_wg(ctx, nb);
+    TcDirPlan* P = plan_fwd(ctx, nb);  // same rows and gathers as the forward
     if (P->n_overflow == P->n_super) {
       wgrad_spill(ctx, nb, P, fin, gout, grad_w, false);
       return;
@@ -1354,7 +1362,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
       p->saved_fin = fin;
     }
     if (!g_converted) convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
-    const int gx = std::max(1, std::min(P->n_sub, ctx->num_sms / 2));
+    const int gx = std::max(1, std::min(P->n_super, ctx->num_sms / 2));
     const int64_t need = static_cast<int64_t>(gx) * K * CH * CH;
     if (p->partial.size() < need) p->partial.alloc(ctx, need);
     NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
@@ -1367,6 +1375,8 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     a.blocks = P->blocks.get();
     a.n_rows = P->n_rows;
     a.n_sub = P->n_sub;
+    a.n_super = P->n_super;
+    a.st = P->st;
     a.hcap = P->hcap;
     a.K = K;
     a.feat = p->feat_in.get();
@@ -1404,7 +1414,7 @@ void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, con
 void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12) {
   tc_prepare(ctx, nb);
   TcPlan* p = nb->tc.get();
-  const TcDirPlan* ds[3] = {p->fwd.get(), p->bwd.get(), p->wg.get()};
+  const TcDirPlan* ds[3] = {p->fwd.get(), p->bwd.get(), p->fwd.get()};  // wgrad runs on the forward plan
   for (int i = 0; i < 3; ++i) {
     out12[4 * i + 0] = ds[i]->n_super;
     out12[4 * i + 1] = ds[i]->n_overflow;
