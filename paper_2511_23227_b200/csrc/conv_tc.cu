@@ -23,10 +23,14 @@
 //   warp 4     producer: halo / W_k / stage-descriptor bulk copies
 //   warp 5     MMA issuer (one elected lane) + TMEM allocator
 //   warps 6-13 aggregation (quarter-warp per row, 4 rows per step)
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
 
 #include "conv.cuh"
 #include "tc_common.cuh"
@@ -60,8 +64,13 @@ struct TcDirPlan {
   int64_t n_spill = 0;
 };
 
+struct GatherPlan;
+struct GatherPlanDeleter {
+  void operator()(GatherPlan* p) const;
+};
 struct TcPlan {
   std::unique_ptr<TcDirPlan> fwd, bwd;  // wgrad reuses the forward plan
+  std::unique_ptr<GatherPlan, GatherPlanDeleter> gfwd, gbwd;  // gather-engine plans
   DevBuf<uint32_t> inv_perm_out, inv_perm_in;
   DevBuf<__nv_bfloat16> feat_in;   // bf16 F_in in perm_in order
   const void* saved_fin = nullptr;  // fin whose image feat_in holds (set by the forward)
@@ -70,7 +79,7 @@ struct TcPlan {
   DevBuf<float> partial;           // wgrad per-CTA partials
 };
 
-void destroy_tc_plan(TcPlan* p) { delete p; }
+void destroy_tc_plan(TcPlan* p);
 
 bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K) {
   return G == 1 && cin == CH && cout == CH && K >= 1 && K <= KMAX;
@@ -1156,6 +1165,593 @@ __global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, in
 }
 
 // ===========================================================================
+// gather engine (forward / dgrad): A tiles assembled by TMA tile::gather4
+// ===========================================================================
+// A stage (128-row sub-tile t, cell k) needs A_k[r] = sum of the bf16 feature
+// rows of row r's neighbors in cell k.  Instead of staging a halo and summing
+// on the SM, one producer lane issues 32 cp.async.bulk.tensor.tile::gather4
+// per stage: 4 arbitrary 128-byte rows each, written straight into the
+// SWIZZLE_128B K-major A tile (the swizzle comes from the tensor map).  Row r
+// receives its FIRST neighbor (or an out-of-bounds coordinate -> a zero row);
+// the remaining neighbors of rows with >= 2 entries ("extras", ~40 rows per
+// stage) are gathered the same way into an extras tile, and fixup warps add
+// them to their rows in fp32, in CSR order, rounding once (the numerics of
+// the halo engine's emulation, exactly).  No halo: shared memory holds 5 A +
+// 5 extras stages instead, so the gathers of several stages are in flight.
+//
+// Stage descriptor (per (sub-tile, cell), 16-byte aligned):
+//   u32 hdr[4] = {nfix, E, 0, 0} | u32 src[128] | u32 ext[E] | u32 fix[nfix]
+//   src[r] = bf16 feature row of row r's first entry or 0xFFFFFFFF (zero row)
+//   fix    = r | (count - 1) << 7 | ext_offset << 12
+constexpr uint32_t kOOB = 0xFFFFFFFFu;
+constexpr int G_XCAP = 128;   // extras rows gathered per stage (more -> read from L2)
+constexpr int G_NSA = 5;      // A + extras stages
+constexpr int G_NSW = 3;      // W stages
+constexpr int G_NSD = 8;      // descriptor stages
+constexpr int G_DWORDS = 512;           // E + nfix per stage (more -> exact engine)
+constexpr int G_DCAP = 528 + 4 * G_DWORDS;
+constexpr int G_ST = 2;       // sub-tiles per super-tile (W_k loaded once per super-tile)
+constexpr int G_LOAD_WARPS = 8;   // cp.async gather warps (warps 7 ..)
+constexpr int G_FIX_WARP0 = 7 + G_LOAD_WARPS;
+constexpr int G_FIX_GROUPS = 2;   // fixup groups alternate stages
+constexpr int G_FIX_GW = 4;       // warps per fixup group
+constexpr int G_FIX_WARPS = G_FIX_GROUPS * G_FIX_GW;
+constexpr int G_THREADS = 32 * (G_FIX_WARP0 + G_FIX_WARPS);
+
+struct GatherPlan {
+  int64_t n_rows = 0;
+  int n_sub = 0, n_super = 0, K = 0;
+  DevBuf<uint32_t> blk_off;    // n_sub * K + 1
+  DevBuf<uint8_t> blocks;
+  DevBuf<uint32_t> super_bad;  // per super-tile: rows served by the exact engine
+  DevBuf<uint32_t> spill_rows;
+  int64_t n_spill = 0;
+  int n_overflow = 0;
+};
+
+// Per 128-row sub-tile (one thread per row): block sizes (COUNT) or contents (FILL).
+template <bool FILL>
+__global__ void __launch_bounds__(TM) k_gplan(const int64_t* __restrict__ row_ptr,
+                                              const uint32_t* __restrict__ col,
+                                              const uint32_t* __restrict__ kk,
+                                              const uint32_t* __restrict__ perm_rows,
+                                              const uint32_t* __restrict__ inv_perm_cols,
+                                              int64_t n_rows, int K,
+                                              const uint32_t* __restrict__ blk_off,
+                                              uint32_t* __restrict__ blk_size,
+                                              uint32_t* __restrict__ sub_bad,
+                                              uint8_t* __restrict__ blocks) {
+  __shared__ uint8_t cnt[KMAX][TM], run[KMAX][TM];
+  __shared__ uint16_t fpos[KMAX][TM], xpos[KMAX][TM];
+  __shared__ int nfix_k[KMAX], next_k[KMAX], wsum[2][4], bad;
+  const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
+  const int sub = blockIdx.x;
+  for (int k = 0; k < KMAX; ++k) {
+    cnt[k][r] = 0;
+    run[k][r] = 0;
+  }
+  if (r == 0) bad = 0;
+  __syncthreads();
+  const int64_t p = static_cast<int64_t>(sub) * TM + r;
+  uint32_t row_i = 0;
+  int64_t e0 = 0, e1 = 0;
+  if (p < n_rows) {
+    row_i = perm_rows[p];
+    e0 = row_ptr[row_i];
+    e1 = row_ptr[row_i + 1];
+    for (int64_t e = e0; e < e1; ++e) {
+      const uint32_t k = kk[e];
+      if (cnt[k][r] < 255) cnt[k][r]++;
+    }
+  }
+  for (int k = 0; k < K; ++k) {
+    const int c = cnt[k][r];
+    if (c > 32) bad = 1;
+    const int nf = c >= 2, ne = c > 1 ? c - 1 : 0;
+    int inf = nf, ine = ne;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int a = __shfl_up_sync(0xffffffffu, inf, o), b = __shfl_up_sync(0xffffffffu, ine, o);
+      if (lane >= o) {
+        inf += a;
+        ine += b;
+      }
+    }
+    if (lane == 31) {
+      wsum[0][warp] = inf;
+      wsum[1][warp] = ine;
+    }
+    __syncthreads();
+    int bf = 0, be = 0, tf = 0, te = 0;
+    for (int w = 0; w < 4; ++w) {
+      if (w < warp) {
+        bf += wsum[0][w];
+        be += wsum[1][w];
+      }
+      tf += wsum[0][w];
+      te += wsum[1][w];
+    }
+    fpos[k][r] = static_cast<uint16_t>(bf + inf - nf);
+    xpos[k][r] = static_cast<uint16_t>(be + ine - ne);
+    if (r == 0) {
+      nfix_k[k] = tf;
+      next_k[k] = te;
+    }
+    __syncthreads();
+  }
+  if (!FILL) {
+    if (r < K) {
+      if (nfix_k[r] + next_k[r] > G_DWORDS) bad = 1;
+      blk_size[static_cast<int64_t>(sub) * K + r] =
+          (528u + 4u * static_cast<uint32_t>(nfix_k[r] + next_k[r]) + 15u) & ~15u;
+    }
+    __syncthreads();
+    if (r == 0) sub_bad[sub] = bad;
+    return;
+  }
+  // FILL: header, zero rows, entries in CSR order, fixup items
+  for (int k = 0; k < K; ++k) {
+    uint8_t* b = blocks + blk_off[static_cast<int64_t>(sub) * K + k];
+    if (r == 0) {
+      reinterpret_cast<uint32_t*>(b)[0] = static_cast<uint32_t>(nfix_k[k]);
+      reinterpret_cast<uint32_t*>(b)[1] = static_cast<uint32_t>(next_k[k]);
+      reinterpret_cast<uint32_t*>(b)[2] = 0;
+      reinterpret_cast<uint32_t*>(b)[3] = 0;
+    }
+    const int c = cnt[k][r];
+    if (c == 0) reinterpret_cast<uint32_t*>(b + 16)[r] = kOOB;
+    if (c >= 2)
+      reinterpret_cast<uint32_t*>(b + 528 + 4 * next_k[k])[fpos[k][r]] =
+          static_cast<uint32_t>(r) | (static_cast<uint32_t>(c - 1) << 7) |
+          (static_cast<uint32_t>(xpos[k][r]) << 12);
+  }
+  for (int64_t e = e0; e < e1; ++e) {
+    const int k = static_cast<int>(kk[e]);
+    const uint32_t v = inv_perm_cols[col[e]];
+    uint8_t* b = blocks + blk_off[static_cast<int64_t>(sub) * K + k];
+    const int n = run[k][r]++;
+    if (n == 0) reinterpret_cast<uint32_t*>(b + 16)[r] = v;
+    else reinterpret_cast<uint32_t*>(b + 528)[xpos[k][r] + n - 1] = v;
+  }
+}
+
+static std::unique_ptr<GatherPlan> build_gather_plan(npcg_context* ctx, const int64_t* row_ptr,
+                                                     const uint32_t* col, const uint32_t* kk,
+                                                     int64_t n_rows, const uint32_t* perm_rows,
+                                                     const uint32_t* inv_perm_cols, int K) {
+  auto P = std::make_unique<GatherPlan>();
+  P->n_rows = n_rows;
+  P->K = K;
+  P->n_sub = static_cast<int>(ceil_div(n_rows, TM));
+  P->n_super = static_cast<int>(ceil_div(P->n_sub, G_ST));
+  if (P->n_sub == 0) return P;
+  const int64_t nblk = static_cast<int64_t>(P->n_sub) * K;
+  DevBuf<uint32_t> blk_size(ctx, nblk + 1), sub_bad(ctx, P->n_sub);
+  NPCG_CUDA(cudaMemsetAsync(blk_size.get() + nblk, 0, 4, ctx->stream));
+  launch(ctx, "gplan_count", k_gplan<false>, dim3(P->n_sub), dim3(TM), 0, row_ptr, col, kk,
+         perm_rows, inv_perm_cols, n_rows, K, static_cast<const uint32_t*>(nullptr),
+         blk_size.get(), sub_bad.get(), static_cast<uint8_t*>(nullptr));
+  P->blk_off.alloc(ctx, nblk + 1);
+  uint32_t total = 0;
+  exclusive_scan_u32(ctx, blk_size.get(), P->blk_off.get(), nblk + 1, &total);
+  P->blocks.alloc(ctx, total);
+  launch(ctx, "gplan_fill", k_gplan<true>, dim3(P->n_sub), dim3(TM), 0, row_ptr, col, kk,
+         perm_rows, inv_perm_cols, n_rows, K, static_cast<const uint32_t*>(P->blk_off.get()),
+         static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), P->blocks.get());
+  std::vector<uint32_t> sb(P->n_sub);
+  NPCG_CUDA(cudaMemcpyAsync(sb.data(), sub_bad.get(), sb.size() * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  std::vector<uint32_t> bad(P->n_super, 0);
+  for (int s = 0; s < P->n_sub; ++s) bad[s / G_ST] |= sb[s];
+  std::vector<uint32_t> rows;
+  for (int S = 0; S < P->n_super; ++S)
+    if (bad[S]) {
+      P->n_overflow++;
+      for (int64_t q = static_cast<int64_t>(S) * G_ST * TM;
+           q < std::min<int64_t>(n_rows, static_cast<int64_t>(S + 1) * G_ST * TM); ++q)
+        rows.push_back(static_cast<uint32_t>(q));
+    }
+  P->super_bad.alloc(ctx, P->n_super);
+  NPCG_CUDA(cudaMemcpyAsync(P->super_bad.get(), bad.data(), bad.size() * 4, cudaMemcpyHostToDevice,
+                            ctx->stream));
+  P->n_spill = static_cast<int64_t>(rows.size());
+  if (P->n_spill) {
+    P->spill_rows.alloc(ctx, P->n_spill);
+    NPCG_CUDA(cudaMemcpyAsync(P->spill_rows.get(), rows.data(), rows.size() * 4,
+                              cudaMemcpyHostToDevice, ctx->stream));
+  }
+  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  return P;
+}
+
+struct GArgs {
+  const uint32_t* blk_off;
+  const uint8_t* blocks;
+  const uint32_t* super_bad;
+  const uint32_t* perm_rows;
+  int64_t n_rows;
+  int n_sub, n_super, K;
+  const __nv_bfloat16* feat;  // bf16 (n_cols, 64), permuted
+  const uint8_t* wpack;       // K x 8 KB
+  float* out;
+  long long* trace;
+};
+
+struct GSmem {
+  uint32_t a, x, w, d, bar, tmem_slot, offs;
+  size_t total;
+};
+__host__ __device__ inline GSmem g_smem_layout() {
+  GSmem L{};
+  uint32_t o = 0;
+  L.a = o;
+  o += G_NSA * 16384;
+  L.x = o;
+  o += G_NSA * G_XCAP * 128;
+  L.w = o;
+  o += G_NSW * 8192;
+  L.d = o;
+  o += G_NSD * G_DCAP;
+  o = (o + 7) & ~7u;
+  L.bar = o;
+  o += 48 * 8;
+  L.tmem_slot = o;
+  o += 16;
+  L.offs = o;
+  o += (G_ST * KMAX + 1) * 4;
+  L.total = o + 1024;
+  return L;
+}
+enum : int {
+  G_A_FULL = 0,                   // G_NSA: gathers landed (tx)
+  G_A_READY = G_A_FULL + G_NSA,   // G_NSA: fixups done
+  G_A_EMPTY = G_A_READY + G_NSA,  // G_NSA: MMA done reading
+  G_W_FULL = G_A_EMPTY + G_NSA,   // G_NSW
+  G_W_EMPTY = G_W_FULL + G_NSW,
+  G_D_FULL = G_W_EMPTY + G_NSW,   // G_NSD
+  G_D_EMPTY = G_D_FULL + G_NSD,
+  G_T_FULL = G_D_EMPTY + G_NSD,   // 2
+  G_T_EMPTY = G_T_FULL + 2,
+  G_COUNT = G_T_EMPTY + 2
+};
+static_assert(G_COUNT <= 48, "gather barrier region");
+
+__device__ __forceinline__ void tma_gather4(uint32_t dst, const CUtensorMap* map, uint4 rows,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile::gather4.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(0), "r"(rows.x), "r"(rows.y), "r"(rows.z),
+      "r"(rows.w), "r"(bar)
+      : "memory");
+}
+
+__global__ void __launch_bounds__(G_THREADS, 1)
+    k_conv_gather(const __grid_constant__ CUtensorMap tmap, GArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const GSmem L = g_smem_layout();
+  const uint32_t s_a = base + L.a, s_x = base + L.x, s_w = base + L.w, s_d = base + L.d;
+  const uint32_t s_bar = base + L.bar;
+  auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
+  const uint8_t* g_d = gbase + L.d;
+  const uint8_t* g_x = gbase + L.x;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int K = a.K;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < G_NSA; ++i) {
+      mbar_init(bar(G_A_FULL + i), 32 * G_LOAD_WARPS);  // one cp.async arrive per loader thread
+      mbar_init(bar(G_A_READY + i), G_FIX_GW);
+      mbar_init(bar(G_A_EMPTY + i), 1);
+    }
+    for (int i = 0; i < G_NSW; ++i) {
+      mbar_init(bar(G_W_FULL + i), 1);
+      mbar_init(bar(G_W_EMPTY + i), 1);
+    }
+    for (int i = 0; i < G_NSD; ++i) {
+      mbar_init(bar(G_D_FULL + i), 1);
+      mbar_init(bar(G_D_EMPTY + i), G_LOAD_WARPS + G_FIX_GW);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(G_T_FULL + i), 1);
+      mbar_init(bar(G_T_EMPTY + i), 4);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<256>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  auto nsub_of = [&](int S) { return min(G_ST, a.n_sub - S * G_ST); };
+
+  if (warp == 4) {
+    // ---- descriptor producer: bulk copies into the D ring --------------------
+    uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
+    uint32_t d_it = 0;
+    for (int S = blockIdx.x; S < a.n_super; S += gridDim.x) {
+      if (a.super_bad[S]) continue;
+      const int nsub = nsub_of(S);
+      for (int x = lane; x <= nsub * K; x += 32)
+        offs[x] = a.blk_off[static_cast<int64_t>(S) * G_ST * K + x];
+      __syncwarp();
+      for (int k = 0; k < K; ++k)
+        for (int g = 0; g < nsub; ++g) {
+          if (lane == 0) {
+            const uint32_t ds = d_it % G_NSD;
+            mbar_wait(bar(G_D_EMPTY + ds), ((d_it / G_NSD) & 1) ^ 1);
+            const uint32_t o0 = offs[g * K + k], o1 = offs[g * K + k + 1];
+            mbar_expect_tx(bar(G_D_FULL + ds), o1 - o0);
+            bulk_g2s(s_d + ds * G_DCAP, a.blocks + o0, o1 - o0, bar(G_D_FULL + ds));
+          }
+          ++d_it;
+        }
+      __syncwarp();
+    }
+  } else if (warp >= 7 && warp < G_FIX_WARP0) {
+    // ---- loaders: cp.async (16 B per lane, 4 rows per warp instruction) of
+    // every row's first neighbor into the swizzled A tile (zero-fill for
+    // rows without neighbors) and of up to G_XCAP extras into the X tile;
+    // the A_FULL mbarrier tracks their completion (arrive.noinc) -----------
+    const int lw = warp - 7;
+    const uint32_t q = static_cast<uint32_t>(lane & 7), rq = static_cast<uint32_t>(lane >> 3);
+    constexpr int RI = TM / (4 * G_LOAD_WARPS);  // row iterations per loader warp
+    uint32_t dsto[RI];                           // swizzled destination of this lane's chunks
+#pragma unroll
+    for (int i = 0; i < RI; ++i) {
+      const uint32_t r = static_cast<uint32_t>(lw * 4 * RI + i * 4) + rq;
+      dsto[i] = r * 128u + ((q ^ (r & 7u)) << 4);
+    }
+    const uint8_t* fbase = reinterpret_cast<const uint8_t*>(a.feat) + q * 16u;
+    uint32_t it = 0;
+    for (int S = blockIdx.x; S < a.n_super; S += gridDim.x) {
+      if (a.super_bad[S]) continue;
+      const int nsub = nsub_of(S);
+      for (int k = 0; k < K; ++k)
+        for (int g = 0; g < nsub; ++g, ++it) {
+          const uint32_t ds = it % G_NSD, as = it % G_NSA;
+          mbar_wait(bar(G_D_FULL + ds), (it / G_NSD) & 1);
+          mbar_wait(bar(G_A_EMPTY + as), ((it / G_NSA) & 1) ^ 1);
+          if (lw == 0 && lane == 0) trace_ev(a.trace, it, 0);
+          const uint8_t* blk = g_d + ds * G_DCAP;
+          const uint32_t E = reinterpret_cast<const uint32_t*>(blk)[1];
+          const uint32_t ex = min(E, static_cast<uint32_t>(G_XCAP));
+          const uint32_t* src = reinterpret_cast<const uint32_t*>(blk + 16) + lw * 4 * RI + rq;
+          const uint32_t* ext = reinterpret_cast<const uint32_t*>(blk + 528);
+          const uint32_t sa = s_a + as * 16384u, sx = s_x + as * (G_XCAP * 128u);
+          uint32_t v[RI];
+#pragma unroll
+          for (int i = 0; i < RI; ++i) v[i] = src[i * 4];
+#pragma unroll
+          for (int i = 0; i < RI; ++i)
+            cp_async16_zfill(sa + dsto[i], fbase + static_cast<uint64_t>(v[i] == kOOB ? 0u : v[i]) * 128u,
+                             v[i] == kOOB ? 0u : 16u);
+          for (uint32_t x = static_cast<uint32_t>(lw * 4) + rq; x < ex; x += 4 * G_LOAD_WARPS)
+            cp_async16_zfill(sx + x * 128u + ((q ^ (x & 7u)) << 4),
+                             fbase + static_cast<uint64_t>(ext[x]) * 128u, 16u);
+          cp_async_mbar_arrive_noinc(bar(G_A_FULL + as));
+          __syncwarp();
+          if (lw == 0 && lane == 0) trace_ev(a.trace, it, 1);
+          if (lane == 0) mbar_arrive(bar(G_D_EMPTY + ds));
+        }
+    }
+  } else if (warp == 6) {
+    // ---- W_k producer ------------------------------------------------------------
+    if (lane == 0) {
+      uint32_t w_it = 0;
+      for (int S = blockIdx.x; S < a.n_super; S += gridDim.x) {
+        if (a.super_bad[S]) continue;
+        for (int k = 0; k < K; ++k, ++w_it) {
+          const uint32_t ws = w_it % G_NSW;
+          mbar_wait_sleep(bar(G_W_EMPTY + ws), ((w_it / G_NSW) & 1) ^ 1);
+          mbar_expect_tx(bar(G_W_FULL + ws), 8192u);
+          bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u,
+                   bar(G_W_FULL + ws));
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ---- MMA issuer (as the halo engine) -------------------------------------------
+    constexpr uint32_t idesc = idesc_bf16(128, 64, false, false);
+    const uint64_t a_desc0 = sdesc_sw128(s_a, 16, 1024), b_desc0 = sdesc_sw128(s_w, 16, 1024);
+    uint32_t w_it = 0, it = 0, t_it = 0;
+    bool pending = false;
+    uint32_t pend_t = 0;
+    auto release_epilogue = [&]() {
+      mbar_wait(bar(G_T_FULL + (pend_t & 1)), (pend_t >> 1) & 1);
+      named_bar_arrive(2 + (pend_t & 1), 32 * 5);
+      pending = false;
+    };
+    for (int S = blockIdx.x; S < a.n_super; S += gridDim.x) {
+      if (a.super_bad[S]) continue;
+      const int nsub = nsub_of(S);
+      const uint32_t ab = t_it & 1;
+      mbar_wait(bar(G_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
+      tc_fence_after();
+      for (int k = 0; k < K; ++k) {
+        if (pending && k == 1) release_epilogue();
+        const uint32_t ws = w_it % G_NSW;
+        mbar_wait(bar(G_W_FULL + ws), (w_it / G_NSW) & 1);
+        for (int g = 0; g < nsub; ++g, ++it) {
+          const uint32_t as = it % G_NSA;
+          mbar_wait(bar(G_A_READY + as), (it / G_NSA) & 1);
+          if (lane == 0) trace_ev(a.trace, it, 4);
+          tc_fence_after();
+          const uint32_t d = tmem + ab * (G_ST * 64) + g * 64;
+          const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
+          const uint64_t bd = b_desc0 + ((ws * 8192u) >> 4);
+          if (elect_one()) {
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc, (k > 0 || ks > 0) ? 1u : 0u);
+            umma_commit(bar(G_A_EMPTY + as));
+          }
+          __syncwarp();
+          if (lane == 0) trace_ev(a.trace, it, 5);
+        }
+        if (elect_one()) umma_commit(bar(G_W_EMPTY + ws));
+        __syncwarp();
+        ++w_it;
+      }
+      if (elect_one()) umma_commit(bar(G_T_FULL + ab));
+      __syncwarp();
+      if (pending) release_epilogue();
+      pending = true;
+      pend_t = t_it;
+      ++t_it;
+    }
+    if (pending) release_epilogue();
+  } else if (warp >= G_FIX_WARP0) {
+    // ---- fixups: rows of >= 2 entries, fp32 sum (CSR order) rounded once ---------
+    // quarter-warp per row: lane group q8 = lane / 8 of warp fw handles rows
+    // fw * 4 + q8, + 32, ...; each lane one 16-byte chunk (8 channels)
+    const int fw = (warp - G_FIX_WARP0) % G_FIX_GW, fg = (warp - G_FIX_WARP0) / G_FIX_GW;
+    const uint32_t q = static_cast<uint32_t>(lane & 7);
+    uint32_t it = 0;
+    for (int S = blockIdx.x; S < a.n_super; S += gridDim.x) {
+      if (a.super_bad[S]) continue;
+      const int nsub = nsub_of(S);
+      for (int k = 0; k < K; ++k)
+        for (int g = 0; g < nsub; ++g, ++it) {
+          if (static_cast<int>(it % G_FIX_GROUPS) != fg) continue;
+          const uint32_t ds = it % G_NSD, as = it % G_NSA;
+          mbar_wait(bar(G_D_FULL + ds), (it / G_NSD) & 1);
+          const uint8_t* blk = g_d + ds * G_DCAP;
+          const uint32_t nfix = reinterpret_cast<const uint32_t*>(blk)[0];
+          const uint32_t E = reinterpret_cast<const uint32_t*>(blk)[1];
+          const uint32_t* ext = reinterpret_cast<const uint32_t*>(blk + 528);
+          const uint32_t* fix = ext + E;
+          mbar_wait(bar(G_A_FULL + as), (it / G_NSA) & 1);
+          if (fw == 0 && lane == 0) trace_ev(a.trace, it, 2);
+          const uint32_t sa = s_a + as * 16384u;
+          const uint8_t* gx = g_x + as * (G_XCAP * 128u);
+          for (uint32_t f = static_cast<uint32_t>(fw * 4 + (lane >> 3)); f < nfix; f += G_FIX_GW * 4) {
+            const uint32_t item = fix[f];
+            const uint32_t r = item & 127u, c1 = (item >> 7) & 31u, xo = item >> 12;
+            const uint32_t ra = sa + r * 128u + ((q ^ (r & 7u)) << 4);
+            float acc[8];
+            const uint4 v0 = lds128(ra);
+#pragma unroll
+            for (int x = 0; x < 8; ++x) acc[x] = 0.f;
+            acc_bf16x2(acc[0], acc[1], v0.x);
+            acc_bf16x2(acc[2], acc[3], v0.y);
+            acc_bf16x2(acc[4], acc[5], v0.z);
+            acc_bf16x2(acc[6], acc[7], v0.w);
+            for (uint32_t e = 0; e < c1; ++e) {
+              const uint32_t xr = xo + e;
+              uint4 w;
+              if (xr < static_cast<uint32_t>(G_XCAP))
+                w = *reinterpret_cast<const uint4*>(gx + xr * 128u + ((q ^ (xr & 7u)) << 4));
+              else
+                w = __ldg(reinterpret_cast<const uint4*>(a.feat + static_cast<int64_t>(ext[xr]) * CH) + q);
+              acc_bf16x2(acc[0], acc[1], w.x);
+              acc_bf16x2(acc[2], acc[3], w.y);
+              acc_bf16x2(acc[4], acc[5], w.z);
+              acc_bf16x2(acc[6], acc[7], w.w);
+            }
+            uint4 o;
+            o.x = pack_bf16x2(acc[0], acc[1]);
+            o.y = pack_bf16x2(acc[2], acc[3]);
+            o.z = pack_bf16x2(acc[4], acc[5]);
+            o.w = pack_bf16x2(acc[6], acc[7]);
+            sts128(ra, o);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (fw == 0 && lane == 0) trace_ev(a.trace, it, 3);
+          if (lane == 0) {
+            mbar_arrive(bar(G_A_READY + as));
+            mbar_arrive(bar(G_D_EMPTY + ds));
+          }
+        }
+    }
+  } else {
+    // ---- epilogue (warps 0-3): TMEM -> output rows --------------------------------
+    const int e = warp;
+    uint32_t t_it = 0;
+    for (int S = blockIdx.x; S < a.n_super; S += gridDim.x) {
+      if (a.super_bad[S]) continue;
+      const int nsub = nsub_of(S);
+      const uint32_t ab = t_it & 1;
+      named_bar_sync(2 + ab, 32 * 5);
+      tc_fence_after();
+      for (int g = 0; g < nsub; ++g) {
+        const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * (G_ST * 64) + g * 64;
+        const int64_t row = (static_cast<int64_t>(S) * G_ST + g) * TM + 32 * e + lane;
+        float4* o = row < a.n_rows
+                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * CH)
+                        : nullptr;
+#pragma unroll
+        for (int qq = 0; qq < 4; ++qq) {
+          uint32_t v[16];
+          tmem_ld16(t0 + 16 * qq, v);
+          tmem_ld_wait();
+          if (o)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              o[qq * 4 + x] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                          __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
+        }
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(G_T_EMPTY + ab));
+      ++t_it;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_free<256>(tmem);
+}
+
+// Tensor map of a bf16 (rows, 64) feature matrix for tile::gather4: box 64 x 1,
+// SWIZZLE_128B (matches the A tile layout), out-of-bounds rows read as zeros.
+static CUtensorMap feature_tmap(const __nv_bfloat16* feat, int64_t rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {static_cast<cuuint64_t>(CH), static_cast<cuuint64_t>(std::max<int64_t>(rows, 1))};
+  const cuuint64_t strides[1] = {static_cast<cuuint64_t>(CH) * 2};
+  const cuuint32_t box[2] = {static_cast<cuuint32_t>(CH), 1};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = cuTensorMapEncodeTiled(
+      &m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<__nv_bfloat16*>(feat), dims, strides, box,
+      estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+      CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) fail(NPCG_ERR_CUDA, "cuTensorMapEncodeTiled failed for the feature map");
+  return m;
+}
+
+static void run_gather_kernel(npcg_context* ctx, GatherPlan* P, const __nv_bfloat16* feat,
+                              int64_t n_cols, const uint8_t* wpack, const uint32_t* perm_rows,
+                              float* out, const char* name, long long* trace = nullptr) {
+  if (P->n_super == 0 || P->n_overflow == P->n_super) return;
+  GArgs a{};
+  a.blk_off = P->blk_off.get();
+  a.blocks = P->blocks.get();
+  a.super_bad = P->super_bad.get();
+  a.perm_rows = perm_rows;
+  a.n_rows = P->n_rows;
+  a.n_sub = P->n_sub;
+  a.n_super = P->n_super;
+  a.K = P->K;
+  a.feat = feat;
+  a.wpack = wpack;
+  a.out = out;
+  a.trace = trace;
+  const CUtensorMap tmap = feature_tmap(feat, n_cols);
+  const GSmem L = g_smem_layout();
+  NPCG_CUDA(cudaFuncSetAttribute(k_conv_gather, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(L.total)));
+  const int grid = std::min(P->n_super, ctx->num_sms);
+  launch(ctx, name, k_conv_gather, dim3(grid), dim3(G_THREADS), L.total, tmap, a);
+}
+
+// ===========================================================================
 // host drivers
 // ===========================================================================
 
@@ -1196,7 +1792,15 @@ static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
   return p->bwd.get();
 }
 
+static bool use_gather_engine();
+static GatherPlan* gplan_fwd(npcg_context* ctx, npcg_neighbors* nb);
+static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb);
+
 void tc_prepare(npcg_context* ctx, npcg_neighbors* nb) {
+  if (use_gather_engine()) {
+    gplan_fwd(ctx, nb);
+    gplan_bwd(ctx, nb);
+  }
   plan_fwd(ctx, nb);
   plan_bwd(ctx, nb);
 }
@@ -1245,8 +1849,58 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
 }
 
 
+void GatherPlanDeleter::operator()(GatherPlan* p) const { delete p; }
+void destroy_tc_plan(TcPlan* p) { delete p; }
+
+// Forward / dgrad engine: "halo" (shared-memory halo + SM aggregation, the
+// default: 0.85 ms per 1M-point pass) or "gather" (A tiles gathered from L2
+// by cp.async, fixups on the SM: 0.99 ms; profiles/r1_pipeline_experiments.md).
+// NPCG_TC_ENGINE=gather selects the latter (read once per process).
+static bool use_gather_engine() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("NPCG_TC_ENGINE");
+    v = (e && std::strcmp(e, "gather") == 0) ? 1 : 0;
+  }
+  return v == 1;
+}
+static GatherPlan* gplan_fwd(npcg_context* ctx, npcg_neighbors* nb) {
+  TcPlan* p = get_plan(ctx, nb);
+  if (!p->gfwd)
+    p->gfwd.reset(build_gather_plan(ctx, nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(),
+                                    nb->n_out, nb->perm_out.get(), p->inv_perm_in.get(),
+                                    static_cast<int>(nb->n_kernels)).release());
+  return p->gfwd.get();
+}
+static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
+  TcPlan* p = get_plan(ctx, nb);
+  if (!p->gbwd) {
+    build_tcsr(ctx, nb);
+    p->gbwd.reset(build_gather_plan(ctx, nb->tcsr->row_ptr.get(), nb->tcsr->col.get(),
+                                    nb->tcsr->k.get(), nb->n_in, nb->perm_in.get(),
+                                    p->inv_perm_out.get(), static_cast<int>(nb->n_kernels))
+                      .release());
+  }
+  return p->gbwd.get();
+}
+
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
                 float* fout) {
+  if (use_gather_engine()) {
+    GatherPlan* G = gplan_fwd(ctx, nb);
+    TcPlan* p = nb->tc.get();
+    if (G->n_overflow < G->n_super) {
+      convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+      p->saved_fin = fin;  // PointConvOp saves its input at forward (conv_op.hpp:138)
+      pack_w(ctx, p, w, G->K, false);
+      run_gather_kernel(ctx, G, p->feat_in.get(), nb->n_in, p->wpack.get(), nb->perm_out.get(),
+                        fout, "conv_fwd_tc");
+    }
+    const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
+    mvmr_rows_subset_f32(ctx, v, nb->perm_out.get(), G->spill_rows.get(), G->n_spill, w, fin, CH,
+                         CH, fout);
+    return;
+  }
   TcDirPlan* P = plan_fwd(ctx, nb);
   TcPlan* p = nb->tc.get();
   if (P->n_overflow < P->n_super) {
@@ -1333,7 +1987,22 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
   TcPlan* p = get_plan(ctx, nb);
   const int K = static_cast<int>(nb->n_kernels);
   bool g_converted = false;
-  if (grad_in) {
+  if (grad_in && use_gather_engine()) {
+    GatherPlan* G = gplan_bwd(ctx, nb);
+    if (G->n_overflow < G->n_super) {
+      convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
+      g_converted = true;
+      pack_w(ctx, p, w, K, true);
+      run_gather_kernel(ctx, G, p->feat_out.get(), nb->n_out, p->wpack.get(), nb->perm_in.get(),
+                        grad_in, "conv_dgrad_tc");
+    }
+    if (G->n_spill) {
+      DevBuf<float> wt(ctx, static_cast<int64_t>(K) * CH * CH);
+      transpose_w<float>(ctx, w, K, CH, CH, wt.get());
+      mvmr_rows_subset_f32(ctx, nb->tcsr->view(), nb->perm_in.get(), G->spill_rows.get(),
+                           G->n_spill, wt.get(), gout, CH, CH, grad_in);
+    }
+  } else if (grad_in) {
     TcDirPlan* P = plan_bwd(ctx, nb);
     if (P->n_overflow < P->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
@@ -1396,15 +2065,24 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
 // Debug: one traced forward; trace_host receives TRACE_STAGES x TRACE_EV clocks.
 void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
                       float* fout, int64_t* trace_host) {
-  TcDirPlan* P = plan_fwd(ctx, nb);
-  TcPlan* p = nb->tc.get();
-  convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
-  p->saved_fin = fin;
-  pack_w(ctx, p, w, P->K, false);
+  TcPlan* p = get_plan(ctx, nb);
   DevBuf<long long> tr(ctx, TRACE_STAGES * TRACE_EV);
   NPCG_CUDA(cudaMemsetAsync(tr.get(), 0, TRACE_STAGES * TRACE_EV * 8, ctx->stream));
-  run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
-                 "conv_fwd_tc_traced", tr.get());
+  if (use_gather_engine()) {
+    GatherPlan* G = gplan_fwd(ctx, nb);
+    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+    p->saved_fin = fin;
+    pack_w(ctx, p, w, G->K, false);
+    run_gather_kernel(ctx, G, p->feat_in.get(), nb->n_in, p->wpack.get(), nb->perm_out.get(), fout,
+                      "conv_fwd_tc_traced", tr.get());
+  } else {
+    TcDirPlan* P = plan_fwd(ctx, nb);
+    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
+    p->saved_fin = fin;
+    pack_w(ctx, p, w, P->K, false);
+    run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
+                   "conv_fwd_tc_traced", tr.get());
+  }
   NPCG_CUDA(cudaMemcpyAsync(trace_host, tr.get(), TRACE_STAGES * TRACE_EV * 8,
                             cudaMemcpyDeviceToHost, ctx->stream));
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));

@@ -267,3 +267,20 @@ def test_cpp_dropin_header(npc):
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
+
+
+def test_gather_engine_parity():
+    """The alternative forward / dgrad engine (A tiles gathered from L2 by
+    cp.async, NPCG_TC_ENGINE=gather; the engine is chosen once per process)
+    passes the bf16 emulation / oracle bounds and determinism checks."""
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, NPCG_TC_ENGINE="gather")
+    here = os.path.dirname(os.path.abspath(__file__))
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu",
+                        os.path.join(here, "test_gpu_operator.py"),
+                        "-k", "bf16 and not gather"], env=env, capture_output=True, text=True,
+                       timeout=900)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
+    assert " passed" in r.stdout
