@@ -52,6 +52,16 @@ def parse():
     return p.parse_args()
 
 
+def ncu_traffic(kernel):
+    """DRAM bytes per launch of `kernel` (dram__bytes_read.sum + write) from the
+    committed ncu --set full capture summary, or None."""
+    path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if not os.path.exists(path):
+        return None
+    v = json.load(open(path)).get(kernel)
+    return v.get("dram_bytes_per_launch") if v else None
+
+
 def peaks():
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(path):
@@ -408,14 +418,14 @@ def run_ours(args):
     if "tc" in name or "umma" in name:
         achieved = passes * f_pass / (per_launch_ms / 1e3) / 1e12
         roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": bf16_sus,
-                "unit": "TFLOP/s", "frac": round(achieved / bf16_sus, 4), "traffic": None,
+                "unit": "TFLOP/s", "frac": round(achieved / bf16_sus, 4), "traffic": ncu_traffic(name),
                 "kernel": name, "peak_kind": f"{peak_kind} bf16 sustained",
                 "algorithmic_flop_per_launch": passes * f_pass,
                 "launch_ms": round(per_launch_ms, 4), "share_of_step": round(share, 3)}
     else:
         achieved = passes * b_pass / (per_launch_ms / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                "frac": round(achieved / hbm, 4), "traffic": None, "kernel": name,
+                "frac": round(achieved / hbm, 4), "traffic": ncu_traffic(name), "kernel": name,
                 "peak_kind": f"{peak_kind} copy bandwidth",
                 "algorithmic_bytes_per_launch": passes * b_pass,
                 "launch_ms": round(per_launch_ms, 4), "share_of_step": round(share, 3)}
