@@ -252,13 +252,20 @@ __global__ void k_sort_rows(const int64_t* __restrict__ row_ptr, int64_t n_rows,
 // ---------------------------------------------------------------------------
 // spatial order: (batch, Morton code of the r/2 cell) -> perm
 // ---------------------------------------------------------------------------
+// per-axis minimum cell; warp-reduced, one atomic per warp and axis
 __global__ void k_minmax_cells(const double* __restrict__ xyz, int64_t n, double inv_edge,
                                long long* __restrict__ mn) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= n) return;
 #pragma unroll
-  for (int a = 0; a < 3; ++a)
-    atomicMin(&mn[a], static_cast<long long>(floor(xyz[3 * p + a] * inv_edge)));
+  for (int a = 0; a < 3; ++a) {
+    long long v = p < n ? static_cast<long long>(floor(xyz[3 * p + a] * inv_edge)) : LLONG_MAX;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const long long u = __shfl_xor_sync(0xffffffffu, v, o);
+      v = u < v ? u : v;
+    }
+    if ((threadIdx.x & 31) == 0 && v != LLONG_MAX) atomicMin(&mn[a], v);
+  }
 }
 
 __device__ __forceinline__ uint64_t spread3(uint64_t v) {  // 21 bits -> every third bit
@@ -466,10 +473,15 @@ void sort_triplets_by(npcg_context* ctx, const uint32_t* i, const uint32_t* j, c
          dim3(256), 0, static_cast<const uint32_t*>(perm.get()), n, i, j, k, oi, oj, ok);
 }
 
-__global__ void k_count_keys(const uint32_t* __restrict__ key, int64_t n,
-                             int64_t* __restrict__ cnt) {
+// Sorted keys -> CSR row pointers: position p (0 < p < n) starts rows
+// key[p-1]+1 .. key[p]; p = 0 starts rows 0 .. key[0], p = n closes the rest.
+__global__ void k_row_bounds(const uint32_t* __restrict__ key, int64_t n, int64_t n_rows,
+                             int64_t* __restrict__ row_ptr) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p < n) atomicAdd(reinterpret_cast<unsigned long long*>(&cnt[key[p]]), 1ull);
+  if (p > n) return;
+  const int64_t lo = p == 0 ? 0 : static_cast<int64_t>(key[p - 1]) + 1;
+  const int64_t hi = p == n ? n_rows : min(static_cast<int64_t>(key[p]), n_rows);
+  for (int64_t r = lo; r <= hi; ++r) row_ptr[r] = p;
 }
 
 __global__ void k_oob(const uint32_t* __restrict__ v, int64_t n, int64_t bound, int* flag) {
@@ -498,18 +510,18 @@ static void csr_build(npcg_context* ctx, const uint32_t* rowkey, const uint32_t*
   out->row_ptr.alloc(ctx, n_rows + 1);
   out->col.alloc(ctx, n);
   out->k.alloc(ctx, n);
-  DevBuf<int64_t> cnt(ctx, n_rows + 1);
-  NPCG_CUDA(cudaMemsetAsync(cnt.get(), 0, (n_rows + 1) * 8, ctx->stream));
-  if (n > 0)
-    launch(ctx, "count_keys", k_count_keys, dim3(static_cast<unsigned>(ceil_div(n, 256))),
-           dim3(256), 0, rowkey, n, cnt.get());
-  exclusive_scan_i64(ctx, cnt.get(), out->row_ptr.get(), n_rows + 1, nullptr);
-  if (n == 0) return;
+  if (n == 0) {
+    NPCG_CUDA(cudaMemsetAsync(out->row_ptr.get(), 0, (n_rows + 1) * 8, ctx->stream));
+    return;
+  }
   DevBuf<uint32_t> keys(ctx, n), perm(ctx, n);
   NPCG_CUDA(cudaMemcpyAsync(keys.get(), rowkey, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   iota_u32(ctx, perm.get(), n);
   radix_sort_u32(ctx, keys.get(), perm.get(), n,
                  std::max(1, bits_for(static_cast<uint64_t>(n_rows > 0 ? n_rows - 1 : 0))));
+  // row_ptr[r] = first position of key >= r in the sorted keys (no atomics)
+  launch(ctx, "row_bounds", k_row_bounds, dim3(static_cast<unsigned>(ceil_div(n + 1, 256))),
+         dim3(256), 0, static_cast<const uint32_t*>(keys.get()), n, n_rows, out->row_ptr.get());
   launch(ctx, "gather_csr", k_gather3, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256),
          0, static_cast<const uint32_t*>(perm.get()), n, col, k, static_cast<const uint32_t*>(nullptr),
          out->col.get(), out->k.get(), static_cast<uint32_t*>(nullptr));
@@ -537,26 +549,26 @@ static void cells_build(npcg_context* ctx, const uint32_t* i, const uint32_t* j,
   out->k_ptr.alloc(ctx, n_kernels + 1);
   out->i.alloc(ctx, n);
   out->j.alloc(ctx, n);
-  DevBuf<int64_t> cnt(ctx, n_kernels + 1);
-  NPCG_CUDA(cudaMemsetAsync(cnt.get(), 0, (n_kernels + 1) * 8, ctx->stream));
-  if (n > 0)
-    launch(ctx, "count_keys", k_count_keys, dim3(static_cast<unsigned>(ceil_div(n, 256))),
-           dim3(256), 0, k, n, cnt.get());
-  exclusive_scan_i64(ctx, cnt.get(), out->k_ptr.get(), n_kernels + 1, nullptr);
-  out->k_ptr_host.resize(n_kernels + 1);
-  NPCG_CUDA(cudaMemcpyAsync(out->k_ptr_host.data(), out->k_ptr.get(), (n_kernels + 1) * 8,
-                            cudaMemcpyDeviceToHost, ctx->stream));
-  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
-  if (n == 0) return;
+  out->k_ptr_host.assign(n_kernels + 1, 0);
+  if (n == 0) {
+    NPCG_CUDA(cudaMemsetAsync(out->k_ptr.get(), 0, (n_kernels + 1) * 8, ctx->stream));
+    return;
+  }
   DevBuf<uint32_t> keys(ctx, n), perm(ctx, n);
   NPCG_CUDA(cudaMemcpyAsync(keys.get(), k, n * 4, cudaMemcpyDeviceToDevice, ctx->stream));
   iota_u32(ctx, perm.get(), n);
   radix_sort_u32(ctx, keys.get(), perm.get(), n,
                  std::max(1, bits_for(static_cast<uint64_t>(n_kernels - 1))));
+  // k_ptr from the sorted cells (no atomics on the K counters)
+  launch(ctx, "row_bounds", k_row_bounds, dim3(static_cast<unsigned>(ceil_div(n + 1, 256))),
+         dim3(256), 0, static_cast<const uint32_t*>(keys.get()), n, n_kernels, out->k_ptr.get());
+  NPCG_CUDA(cudaMemcpyAsync(out->k_ptr_host.data(), out->k_ptr.get(), (n_kernels + 1) * 8,
+                            cudaMemcpyDeviceToHost, ctx->stream));
   launch(ctx, "gather_cells", k_gather3, dim3(static_cast<unsigned>(ceil_div(n, 256))),
          dim3(256), 0, static_cast<const uint32_t*>(perm.get()), n, i, j,
          static_cast<const uint32_t*>(nullptr), out->i.get(), out->j.get(),
          static_cast<uint32_t*>(nullptr));
+  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 void build_cells(npcg_context* ctx, npcg_neighbors* nb) {

@@ -31,12 +31,20 @@ __global__ void k_vox_field(const double* __restrict__ xyz, const uint32_t* __re
 __global__ void k_vox_minmax(const double* __restrict__ xyz, int64_t n, double voxel,
                              long long* __restrict__ mn, long long* __restrict__ mx) {
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (p >= n) return;
 #pragma unroll
-  for (int a = 0; a < 3; ++a) {
-    const long long c = static_cast<long long>(floor(__ddiv_rn(xyz[3 * p + a], voxel)));
-    atomicMin(&mn[a], c);
-    atomicMax(&mx[a], c);
+  for (int a = 0; a < 3; ++a) {  // warp-reduced: one atomic per warp and axis
+    long long lo = LLONG_MAX, hi = LLONG_MIN;
+    if (p < n) lo = hi = static_cast<long long>(floor(__ddiv_rn(xyz[3 * p + a], voxel)));
+#pragma unroll
+    for (int o = 16; o; o >>= 1) {
+      const long long u = __shfl_xor_sync(0xffffffffu, lo, o), w = __shfl_xor_sync(0xffffffffu, hi, o);
+      lo = u < lo ? u : lo;
+      hi = w > hi ? w : hi;
+    }
+    if ((threadIdx.x & 31) == 0 && lo != LLONG_MAX) {
+      atomicMin(&mn[a], lo);
+      atomicMax(&mx[a], hi);
+    }
   }
 }
 
