@@ -28,11 +28,15 @@
 
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <array>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstring>
+#include <fstream>
 #include <memory>
+#include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
@@ -388,6 +392,72 @@ inline SortAxis choose_sort_axis(const TripletList& t) {
 }
 
 // ---- engines (engine.hpp / vvor.hpp) ---------------------------------------------
+// ---- voxel downsample + degraded build (spatial.hpp:25-54, triplets.hpp:63-76) --------
+struct DownsampleMap {
+  std::vector<int64_t> kept_index;
+  std::vector<int64_t> parent_of;
+};
+
+// spatial.hpp:47-48
+inline std::pair<PointCloud, DownsampleMap> voxel_downsample(const PointCloud& cloud, double voxel_size) {
+  const int64_t n = cloud.n_points();
+  detail::Dev<int64_t> kept(static_cast<size_t>(std::max<int64_t>(n, 1))),
+      parent(static_cast<size_t>(std::max<int64_t>(n, 1)));
+  std::vector<int64_t> off(static_cast<size_t>(cloud.n_batches() + 1));
+  int64_t nk = 0;
+  const npcg_cloud c = cloud.c_view();
+  detail::check(npcg_voxel_downsample(detail::ctx(), &c, voxel_size, kept.get(), parent.get(), off.data(), &nk),
+                "voxel_downsample");
+  DownsampleMap m;
+  m.kept_index = kept.host();
+  m.kept_index.resize(static_cast<size_t>(nk));
+  m.parent_of = parent.host();
+  m.parent_of.resize(static_cast<size_t>(n));
+  std::vector<Vec3> pts(static_cast<size_t>(nk));
+  for (int64_t s = 0; s < nk; ++s) pts[static_cast<size_t>(s)] = cloud.position(m.kept_index[static_cast<size_t>(s)]);
+  return {PointCloud(std::move(pts), std::move(off)), std::move(m)};
+}
+
+struct DegradedBuild {  // triplets.hpp:63-67
+  TripletList triplets;
+  PointCloud snapped;
+  DownsampleMap sites;
+};
+
+namespace detail {
+inline std::shared_ptr<Neighbors> build_degraded(const PointCloud& in, double voxel, int64_t t) {
+  auto nb = std::make_shared<Neighbors>();
+  const npcg_cloud ic = in.c_view();
+  check(npcg_build_triplets_degraded(ctx(), &ic, voxel, t, &nb->h), "build_triplets_degraded");
+  return nb;
+}
+inline std::pair<PointCloud, DownsampleMap> sites_of(const Neighbors& nb) {
+  int64_t ns = 0, nf = 0, nbat = 0;
+  check(npcg_neighbors_sites(nb.h, &ns, &nf, &nbat), "sites");
+  Dev<double> xyz(static_cast<size_t>(std::max<int64_t>(3 * ns, 1)));
+  Dev<int64_t> kept(static_cast<size_t>(std::max<int64_t>(ns, 1))), parent(static_cast<size_t>(std::max<int64_t>(nf, 1)));
+  std::vector<int64_t> off(static_cast<size_t>(nbat + 1));
+  check(npcg_neighbors_export_sites(ctx(), nb.h, xyz.get(), kept.get(), parent.get(), off.data()), "export_sites");
+  const auto hx = xyz.host();
+  std::vector<Vec3> pts(static_cast<size_t>(ns));
+  for (int64_t s = 0; s < ns; ++s)
+    pts[static_cast<size_t>(s)] = {hx[3 * s], hx[3 * s + 1], hx[3 * s + 2]};
+  DownsampleMap m;
+  m.kept_index = kept.host();
+  m.kept_index.resize(static_cast<size_t>(ns));
+  m.parent_of = parent.host();
+  m.parent_of.resize(static_cast<size_t>(nf));
+  return {PointCloud(std::move(pts), std::move(off)), std::move(m)};
+}
+}  // namespace detail
+
+// triplets.hpp:69-76: site triplets in build order (sort_axis none)
+inline DegradedBuild build_triplets_degraded(const PointCloud& in_cloud, const ConvGeometry& geom) {
+  auto nb = detail::build_degraded(in_cloud, geom.voxel_size, geom.t);
+  auto [snapped, sites] = detail::sites_of(*nb);
+  return {detail::export_triplets(*nb, SortAxis::none), std::move(snapped), std::move(sites)};
+}
+
 enum class Executor : uint8_t { naive = 0, grouped = 1 };
 
 struct ExecConfig {
@@ -499,15 +569,30 @@ class PointConvOp {
   }
 
   FeatureTensor<T> forward(const PointCloud& in_cloud, const FeatureTensor<T>& fin) {
-    return forward(in_cloud, in_cloud, fin);
+    return forward_impl(in_cloud, in_cloud, fin);
   }
   FeatureTensor<T> forward(const PointCloud& in_cloud, const PointCloud& out_cloud, const FeatureTensor<T>& fin) {
-    if (geom_.mode != ConvMode::native) throw StateError("PointConvOp: degraded mode is not provided by libnpcg");
+    if (geom_.mode != ConvMode::native)
+      throw StateError("PointConvOp::forward: two-cloud forward requires native mode");
+    return forward_impl(in_cloud, out_cloud, fin);
+  }
+  // conv_op.hpp:56-57 degraded-mode introspection
+  const PointCloud& snapped_cloud() const {
+    if (!nb_ || geom_.mode != ConvMode::degraded) throw StateError("PointConvOp: no degraded cache");
+    return sites_->first;
+  }
+  const DownsampleMap& site_map() const {
+    if (!nb_ || geom_.mode != ConvMode::degraded) throw StateError("PointConvOp: no degraded cache");
+    return sites_->second;
+  }
+
+  FeatureTensor<T> forward_impl(const PointCloud& in_cloud, const PointCloud& out_cloud, const FeatureTensor<T>& fin) {
     if (fin.n() != in_cloud.n_points()) throw ShapeError("PointConvOp::forward: feature rows != cloud points");
     if (fin.groups() != w_.groups() || fin.channels() != w_.c_in())
       throw ShapeError("mvmr: weight and feature shapes differ");
     build_cache(in_cloud, out_cloud);
-    dfin_ = detail::Dev<T>(fin.values().data(), fin.values().size());  // conv_op.hpp:138 copy
+    // conv_op.hpp:138 copy (degraded: the library gathers the site rows from it)
+    dfin_ = detail::Dev<T>(fin.values().data(), fin.values().size());
     detail::Dev<T> out(static_cast<size_t>(n_out_ * w_.groups() * w_.c_out()));
     const npcg_exec_config c = cfg_.c();
     detail::check(npcg_conv_forward(detail::ctx(), nb_->h, detail::dtype_of<T>(), dw_.get(), w_.groups(), w_.c_in(),
@@ -523,6 +608,7 @@ class PointConvOp {
     if (gout.n() != n_out_ || gout.groups() != w_.groups() || gout.channels() != w_.c_out())
       throw ShapeError("PointConvOp::backward: gout shape mismatch");
     detail::Dev<T> dg(gout.values().data(), gout.values().size());
+    // degraded: gradients of the original rows, zero for merged-away points (conv_op.hpp:193-202)
     detail::Dev<T> gi(static_cast<size_t>(n_in_ * w_.groups() * w_.c_in()));
     detail::Dev<T> gw(static_cast<size_t>(w_.kernels() * w_.groups() * w_.c_out() * w_.c_in()));
     const npcg_exec_config c = cfg_.c();
@@ -541,9 +627,16 @@ class PointConvOp {
     const Key key{in_cloud.positions().data(), out_cloud.positions().data(), in_cloud.n_points(),
                   out_cloud.n_points()};
     if (nb_ && key == key_) return;  // conv_op.hpp:109-111 identity cache
-    nb_ = detail::build(out_cloud, in_cloud, geom_.radius, geom_.t);
+    if (geom_.mode == ConvMode::native) {
+      nb_ = detail::build(out_cloud, in_cloud, geom_.radius, geom_.t);
+      n_out_ = out_cloud.n_points();
+      sites_.reset();
+    } else {  // conv_op.hpp:116-120
+      nb_ = detail::build_degraded(in_cloud, geom_.voxel_size, geom_.t);
+      sites_ = std::make_unique<std::pair<PointCloud, DownsampleMap>>(detail::sites_of(*nb_));
+      n_out_ = sites_->first.n_points();
+    }
     key_ = key;
-    n_out_ = out_cloud.n_points();
     sorted_.reset();
     has_forward_ = false;
   }
@@ -559,9 +652,117 @@ class PointConvOp {
   detail::Dev<T> dw_, dfin_;
   std::shared_ptr<detail::Neighbors> nb_;
   mutable std::unique_ptr<TripletList> sorted_;
+  std::unique_ptr<std::pair<PointCloud, DownsampleMap>> sites_;
   Key key_;
   int64_t n_out_ = 0, n_in_ = 0;
   bool has_forward_ = false;
 };
+
+// ---- file formats (io.hpp; triplets.hpp:84-93) -- host side, little-endian -------------
+namespace detail {
+inline void put_u32(std::ostream& os, uint32_t v) { os.write(reinterpret_cast<const char*>(&v), 4); }
+inline uint32_t get_u32(std::istream& is, const char* what) {
+  uint32_t v = 0;
+  if (!is.read(reinterpret_cast<char*>(&v), 4)) throw IOError(std::string("truncated ") + what);
+  return v;
+}
+inline bool ends_with_xyz(const std::string& p) { return p.size() >= 4 && p.compare(p.size() - 4, 4, ".xyz") == 0; }
+}  // namespace detail
+
+// ASCII "x y z" per point, 17 significant digits (io.hpp:11-16)
+inline void write_xyz(const std::string& path, const PointCloud& cloud) {
+  std::ofstream os(path);
+  if (!os) throw IOError("cannot open for writing: " + path);
+  char line[96];
+  for (const Vec3& p : cloud.positions()) {
+    std::snprintf(line, sizeof line, "%.17g %.17g %.17g\n", p[0], p[1], p[2]);
+    os << line;
+  }
+  if (!os) throw IOError("write failed: " + path);
+}
+inline PointCloud read_xyz(const std::string& path) {
+  std::ifstream is(path);
+  if (!is) throw IOError("cannot open: " + path);
+  std::vector<Vec3> pts;
+  std::string line;
+  int64_t no = 0;
+  while (std::getline(is, line)) {
+    ++no;
+    if (line.empty() || line[0] == '#') continue;
+    std::istringstream ss(line);
+    Vec3 p{};
+    if (!(ss >> p[0] >> p[1] >> p[2])) throw IOError(path + ":" + std::to_string(no) + ": expected 'x y z'");
+    pts.push_back(p);
+  }
+  return make_point_cloud(std::move(pts));
+}
+// "NPC1" | u32 N | u32 B | u32 0 | u32 offsets[B+1] | f64 xyz[N][3] (io.hpp:18-26)
+inline void write_npc(const std::string& path, const PointCloud& cloud) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw IOError("cannot open for writing: " + path);
+  os.write("NPC1", 4);
+  detail::put_u32(os, static_cast<uint32_t>(cloud.n_points()));
+  detail::put_u32(os, static_cast<uint32_t>(cloud.n_batches()));
+  detail::put_u32(os, 0);
+  for (int64_t o : cloud.batch_offsets()) detail::put_u32(os, static_cast<uint32_t>(o));
+  if (cloud.n_points())
+    os.write(reinterpret_cast<const char*>(cloud.positions().data()),
+             static_cast<std::streamsize>(cloud.n_points() * 3 * sizeof(double)));
+  if (!os) throw IOError("write failed: " + path);
+}
+inline PointCloud read_npc(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw IOError("cannot open: " + path);
+  char magic[4];
+  if (!is.read(magic, 4) || std::memcmp(magic, "NPC1", 4) != 0) throw IOError(path + ": bad magic, expected NPC1");
+  const uint32_t n = detail::get_u32(is, "point count"), b = detail::get_u32(is, "batch count");
+  (void)detail::get_u32(is, "reserved field");
+  std::vector<int64_t> off(static_cast<size_t>(b) + 1);
+  for (auto& o : off) o = detail::get_u32(is, "batch offset");
+  std::vector<Vec3> pts(n);
+  if (n && !is.read(reinterpret_cast<char*>(pts.data()), static_cast<std::streamsize>(size_t(n) * 24)))
+    throw IOError(path + ": truncated position block");
+  return make_point_cloud(std::move(pts), std::move(off));
+}
+inline void write_cloud(const std::string& path, const PointCloud& c) {
+  detail::ends_with_xyz(path) ? write_xyz(path, c) : write_npc(path, c);
+}
+inline PointCloud read_cloud(const std::string& path) {
+  return detail::ends_with_xyz(path) ? read_xyz(path) : read_npc(path);
+}
+// "TPL1" | u32 size, n_out, n_in, n_kernels, sort_axis | u32 i[] | j[] | k[] (triplets.hpp:84-93)
+inline void write_triplets(const std::string& path, const TripletList& t) {
+  std::ofstream os(path, std::ios::binary);
+  if (!os) throw IOError("cannot open for writing: " + path);
+  os.write("TPL1", 4);
+  for (int64_t v : {t.size(), t.n_out, t.n_in, t.n_kernels, static_cast<int64_t>(t.sort_axis)})
+    detail::put_u32(os, static_cast<uint32_t>(v));
+  for (const auto* a : {&t.i, &t.j, &t.k})
+    os.write(reinterpret_cast<const char*>(a->data()), static_cast<std::streamsize>(a->size() * 4));
+  if (!os) throw IOError("write failed: " + path);
+}
+inline TripletList read_triplets(const std::string& path) {
+  std::ifstream is(path, std::ios::binary);
+  if (!is) throw IOError("cannot open: " + path);
+  char magic[4];
+  if (!is.read(magic, 4) || std::memcmp(magic, "TPL1", 4) != 0) throw IOError(path + ": bad magic, expected TPL1");
+  TripletList t;
+  const uint32_t n = detail::get_u32(is, "triplet count");
+  t.n_out = detail::get_u32(is, "n_out");
+  t.n_in = detail::get_u32(is, "n_in");
+  t.n_kernels = detail::get_u32(is, "n_kernels");
+  const uint32_t axis = detail::get_u32(is, "sort_axis");
+  if (axis > 3) throw IOError(path + ": invalid sort_axis value");
+  t.sort_axis = static_cast<SortAxis>(axis);
+  for (auto* a : {&t.i, &t.j, &t.k}) {
+    a->resize(n);
+    if (n && !is.read(reinterpret_cast<char*>(a->data()), static_cast<std::streamsize>(size_t(n) * 4)))
+      throw IOError(path + ": truncated index array");
+  }
+  for (uint32_t q = 0; q < n; ++q)
+    if (t.i[q] >= t.n_out || t.j[q] >= t.n_in || t.k[q] >= t.n_kernels)
+      throw IOError(path + ": triplet index out of declared range");
+  return t;
+}
 
 }  // namespace npc

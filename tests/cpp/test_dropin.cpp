@@ -185,6 +185,85 @@ int main() {
       }
     }
   }
+  // degraded (voxel) mode: test_triplets.cpp:154-215, test_conv_op.cpp:133-175
+  {
+    ConvGeometry dg;
+    dg.mode = ConvMode::degraded;
+    dg.voxel_size = 1.0;
+    DegradedBuild b = build_triplets_degraded(make_point_cloud({{0.25, 0.25, 0.25}}), dg);
+    CHECK(b.triplets.size() == 1 && b.triplets.k[0] == 13);
+    CHECK((b.snapped.position(0) == Vec3{0.5, 0.5, 0.5}));
+    b = build_triplets_degraded(make_point_cloud({{0.5, 0.5, 0.5}, {1.5, 0.5, 0.5}}), dg);
+    std::vector<uint32_t> ks = b.triplets.k;
+    std::sort(ks.begin(), ks.end());
+    CHECK((ks == std::vector<uint32_t>{4, 13, 13, 22}));
+    b = build_triplets_degraded(make_point_cloud({{0.2, 0.2, 0.2}, {0.8, 0.8, 0.8}, {5, 5, 5}}), dg);
+    CHECK(b.snapped.n_points() == 2 && b.sites.parent_of[0] == b.sites.parent_of[1]);
+    CHECK(b.sites.parent_of[2] != b.sites.parent_of[0]);
+    ConvGeometry bad = dg;
+    bad.voxel_size = 0.0;
+    CHECK_THROWS_AS(build_triplets_degraded(make_point_cloud({{0, 0, 0}}), bad), VoxelError);
+    bad = dg;
+    bad.t = 4;
+    CHECK_THROWS_AS(build_triplets_degraded(make_point_cloud({{0, 0, 0}}), bad), ShapeError);
+    // degraded PointConvOp: gather representative rows, scatter gradients back
+    PointCloud cloud = make_point_cloud({{0.2, 0.2, 0.2}, {0.3, 0.3, 0.3}, {5, 5, 5}});
+    std::vector<double> wv(27 * 2 * 3), fv(3 * 2), gv(2 * 3);
+    orc_make_weights_f64(3, 1, 2, 3, 351, wv.data());
+    orc_gen_features_f64(6, 352, fv.data());
+    orc_gen_features_f64(6, 353, gv.data());
+    ExecConfig cfg;
+    cfg.deterministic = true;
+    PointConvOp<double> op(WeightTensor<double>(3, 1, 2, 3, wv), dg, cfg);
+    CHECK_THROWS_AS(op.snapped_cloud(), StateError);
+    auto out = op.forward(cloud, FeatureTensor<double>(3, 1, 2, fv));
+    CHECK(op.snapped_cloud().n_points() == 2 && out.n() == 2);
+    const auto& kept = op.site_map().kept_index;
+    std::vector<double> sf(2 * 2);
+    for (int m = 0; m < 2; ++m)
+      for (int c = 0; c < 2; ++c) sf[2 * m + c] = fv[2 * kept[m] + c];
+    const TripletList& tl = op.cached_triplets();
+    std::vector<double> fo(2 * 3), gi(2 * 2), gw(27 * 3 * 2);
+    CHECK(orc_dense_conv(wv.data(), 27, 1, 2, 3, sf.data(), 2, tl.i.data(), tl.j.data(), tl.k.data(),
+                         tl.size(), 2, gv.data(), fo.data(), gi.data(), gw.data()) == 0);
+    CHECK(rel(out.values(), fo) <= 1e-13);
+    auto res = op.backward(FeatureTensor<double>(2, 1, 3, gv));
+    CHECK(res.grad_in.n() == 3);
+    for (int p = 0; p < 3; ++p) {
+      const bool rep = p == kept[0] || p == kept[1];
+      const double mag = std::abs(res.grad_in.at(p, 0, 0)) + std::abs(res.grad_in.at(p, 0, 1));
+      CHECK(rep ? mag > 0.0 : mag == 0.0);
+    }
+    CHECK(rel(res.grad_w.values(), gw) <= 1e-13);
+    CHECK_THROWS_AS(op.forward(cloud, cloud, FeatureTensor<double>(3, 1, 2, fv)), StateError);
+  }
+  // voxel_downsample + file formats (io.hpp; triplets.hpp:84-93)
+  {
+    PointCloud c = make_point_cloud({{0.1, 0.1, 0.1}, {0.2, 0.2, 0.2}, {3, 3, 3}, {0.5, 0.5, 0.5}}, {0, 3, 4});
+    auto [coarse, map] = voxel_downsample(c, 1.0);
+    CHECK(coarse.n_points() == 3 && coarse.n_batches() == 2 && map.parent_of.size() == 4);
+    CHECK(map.parent_of[0] == map.parent_of[1]);
+    const std::string dir = "/tmp";
+    write_cloud(dir + "/npcg_dropin.npc", c);
+    PointCloud r = read_cloud(dir + "/npcg_dropin.npc");
+    CHECK(r.n_points() == 4 && r.n_batches() == 2 && r.position(2)[0] == 3.0);
+    write_cloud(dir + "/npcg_dropin.xyz", c);
+    PointCloud x = read_cloud(dir + "/npcg_dropin.xyz");
+    CHECK(x.n_points() == 4 && x.n_batches() == 1 && x.position(1)[2] == 0.2);
+    TripletList t = build_triplets_native(c, c, ConvGeometry{0.5, 3});
+    write_triplets(dir + "/npcg_dropin.tpl", t);
+    TripletList u = read_triplets(dir + "/npcg_dropin.tpl");
+    CHECK(u.i == t.i && u.j == t.j && u.k == t.k && u.n_out == t.n_out && u.n_kernels == 27);
+    {
+      std::ofstream bad(dir + "/npcg_dropin_bad.npc", std::ios::binary);
+      bad.write("NPC2", 4);
+    }
+    CHECK_THROWS_AS(read_npc(dir + "/npcg_dropin_bad.npc"), IOError);
+    TripletList oob = t;
+    oob.n_out = 1;
+    write_triplets(dir + "/npcg_dropin_oob.tpl", oob);
+    CHECK_THROWS_AS(read_triplets(dir + "/npcg_dropin_oob.tpl"), IOError);
+  }
   std::printf("drop-in: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }
