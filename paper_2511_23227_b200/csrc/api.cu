@@ -82,7 +82,7 @@ bool use_tc(const npcg_exec_config* cfg, npcg_dtype dtype, int64_t G, int64_t ci
   if (cfg->math == NPCG_MATH_BF16) {
     if (dtype != NPCG_F32) fail(NPCG_ERR_UNSUPPORTED, "bf16 math requires F32 tensors");
     if (!tc_supported(G, cin, cout, K))
-      fail(NPCG_ERR_UNSUPPORTED, "bf16 tensor-core path needs G=1, C_in=C_out=64, K<=32");
+      fail(NPCG_ERR_UNSUPPORTED, "bf16 tensor-core path needs G=1, C_in, C_out in {64,128,256}, K<=32");
     return true;
   }
   return dtype == NPCG_F32 && tc_supported(G, cin, cout, K);
@@ -146,7 +146,7 @@ void forward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, const
   }
   if (use_tc(cfg, dtype, G, cin, cout, nb->n_kernels)) {
     tc_forward(ctx, nb, static_cast<const float*>(w), static_cast<const float*>(fin),
-               static_cast<float*>(fout));
+               static_cast<float*>(fout), static_cast<int>(cin), static_cast<int>(cout));
     return;
   }
   const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
@@ -182,10 +182,14 @@ void backward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, cons
     return;
   }
   if (use_tc(cfg, dtype, G, cin, cout, nb->n_kernels)) {
+    // wide channels: tensor-core input gradient, exact weight gradient (below)
+    const bool tc_w = grad_w && tc_wgrad_supported(cin, cout);
     tc_backward(ctx, nb, static_cast<const float*>(w), static_cast<const float*>(fin),
                 static_cast<const float*>(gout), static_cast<float*>(grad_in),
-                static_cast<float*>(grad_w));
-    return;
+                tc_w ? static_cast<float*>(grad_w) : nullptr, static_cast<int>(cin),
+                static_cast<int>(cout));
+    if (!grad_w || tc_w) return;
+    grad_in = nullptr;
   }
   if (grad_in) {
     if (dtype == NPCG_F32)

@@ -19,14 +19,17 @@ void vvor_cells(npcg_context* ctx, const CellPlan& cells, const T* gout, const T
                 int cin, int cout, T* grad);
 
 // ---- tensor-core engines (conv_tc.cu) --------------------------------------
-// True when the tcgen05 path handles this shape.
+// True when the tcgen05 forward / input-gradient path handles this shape
+// (G = 1, C_in, C_out in {64, 128, 256}, K <= 32); the weight gradient runs on
+// tensor cores for C_in = C_out = 64 (tc_wgrad_supported), else exactly.
 bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t n_kernels);
+bool tc_wgrad_supported(int64_t cin, int64_t cout);
 // Forward / input-gradient / weight-gradient over a neighbor handle with
 // bf16 operands and fp32 accumulation.  Builds and caches the tile plans.
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                float* fout);
+                float* fout, int cin, int cout);
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                 const float* gout, float* grad_in, float* grad_w);
+                 const float* gout, float* grad_in, float* grad_w, int cin, int cout);
 void tc_prepare(npcg_context* ctx, npcg_neighbors* nb);
 void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12);
 void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,

@@ -108,9 +108,16 @@ void mvmr_rows_subset_f32(npcg_context* ctx, const CsrView& csr, const uint32_t*
                           int cin, int cout, float* out) {
   if (n_list == 0) return;
   const unsigned blocks = static_cast<unsigned>(ceil_div(n_list * 32, 256));
-  if (cout > 64) fail(NPCG_ERR_UNSUPPORTED, "row-subset engine: C_out <= 64");
-  launch(ctx, "mvmr_simt_subset", k_mvmr_rows_subset<float, 2>, dim3(blocks), dim3(256), 0, csr,
-         perm, list, n_list, w, fin, cin, cout, out);
+  if (cout > 256) fail(NPCG_ERR_UNSUPPORTED, "row-subset engine: C_out <= 256");
+  if (cout <= 64)
+    launch(ctx, "mvmr_simt_subset", k_mvmr_rows_subset<float, 2>, dim3(blocks), dim3(256), 0, csr,
+           perm, list, n_list, w, fin, cin, cout, out);
+  else if (cout <= 128)
+    launch(ctx, "mvmr_simt_subset", k_mvmr_rows_subset<float, 4>, dim3(blocks), dim3(256), 0, csr,
+           perm, list, n_list, w, fin, cin, cout, out);
+  else
+    launch(ctx, "mvmr_simt_subset", k_mvmr_rows_subset<float, 8>, dim3(blocks), dim3(256), 0, csr,
+           perm, list, n_list, w, fin, cin, cout, out);
 }
 
 template <typename T>

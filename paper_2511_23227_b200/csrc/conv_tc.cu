@@ -70,20 +70,23 @@ struct GatherPlanDeleter {
 };
 struct TcPlan {
   std::unique_ptr<TcDirPlan> fwd, bwd;  // wgrad reuses the forward plan
+  std::unique_ptr<TcDirPlan> fwd1, bwd1;  // 128-row super-tiles for wide (C > 64) passes
   std::unique_ptr<GatherPlan, GatherPlanDeleter> gfwd, gbwd;  // gather-engine plans
   DevBuf<uint32_t> inv_perm_out, inv_perm_in;
   DevBuf<__nv_bfloat16> feat_in;   // bf16 F_in in perm_in order
   const void* saved_fin = nullptr;  // fin whose image feat_in holds (set by the forward)
   DevBuf<__nv_bfloat16> feat_out;  // bf16 G_out in perm_out order
-  DevBuf<uint8_t> wpack;           // K x 8 KB, SW128 K-major B operand
+  DevBuf<uint8_t> wpack;           // K x nci images of C x 128 B, SW128 K-major B operand
   DevBuf<float> partial;           // wgrad per-CTA partials
 };
 
 void destroy_tc_plan(TcPlan* p);
 
+static bool tc_width(int64_t c) { return c == 64 || c == 128 || c == 256; }
 bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K) {
-  return G == 1 && cin == CH && cout == CH && K >= 1 && K <= KMAX;
+  return G == 1 && tc_width(cin) && tc_width(cout) && K >= 1 && K <= KMAX;
 }
+bool tc_wgrad_supported(int64_t cin, int64_t cout) { return cin == CH && cout == CH; }
 
 // ===========================================================================
 // planner
@@ -433,34 +436,38 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
 // ===========================================================================
 // operand preparation
 // ===========================================================================
-// dst[p][c] = bf16(src[perm[p]][c]), 64 channels, 8 per thread.
+// dst[p][c] = bf16(src[perm[p]][c]), C channels (C % 8 == 0), 8 per thread.
 __global__ void k_to_bf16_perm(const float* __restrict__ src, const uint32_t* __restrict__ perm,
-                               int64_t n, __nv_bfloat16* __restrict__ dst) {
+                               int64_t n, int C, __nv_bfloat16* __restrict__ dst) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  if (x >= n * 8) return;
-  const int64_t p = x >> 3;
-  const int q = static_cast<int>(x & 7);
-  const float4* s = reinterpret_cast<const float4*>(src + static_cast<int64_t>(perm[p]) * CH + q * 8);
+  const int qn = C >> 3;
+  if (x >= n * qn) return;
+  const int64_t p = x / qn;
+  const int q = static_cast<int>(x % qn);
+  const float4* s = reinterpret_cast<const float4*>(src + static_cast<int64_t>(perm[p]) * C + q * 8);
   const float4 a = __ldg(s), b = __ldg(s + 1);
   uint4 o;
   o.x = pack_bf16x2(a.x, a.y);
   o.y = pack_bf16x2(a.z, a.w);
   o.z = pack_bf16x2(b.x, b.y);
   o.w = pack_bf16x2(b.z, b.w);
-  reinterpret_cast<uint4*>(dst + p * CH)[q] = o;
+  reinterpret_cast<uint4*>(dst + p * C)[q] = o;
 }
 
-// B operand images (SW128 K-major, 8 KB per cell).  transpose=false: N = C_out
-// rows, K = C_in (forward); transpose=true: N = C_in rows, K = C_out (dgrad).
-__global__ void k_pack_w(const float* __restrict__ w, int K, bool transpose,
+// B operand images (SW128 K-major), one per (cell, 64-wide chunk of the
+// reduction dim), N x 128 B each.  transpose=false: N = C_out rows, reduction
+// over C_in (forward); transpose=true: N = C_in rows, reduction over C_out (dgrad).
+__global__ void k_pack_w(const float* __restrict__ w, int K, int cin, int cout, bool transpose,
                          uint8_t* __restrict__ out) {
-  const int x = blockIdx.x * blockDim.x + threadIdx.x;
-  if (x >= K * CH * CH) return;
-  const int k = x / (CH * CH), rem = x % (CH * CH);
-  const int c = rem / CH, m = rem % CH;  // W[k][c][m]
-  const float v = w[x];
-  const uint32_t off = transpose ? sw128_off(c, m) : sw128_off(m, c);
-  reinterpret_cast<__nv_bfloat16*>(out + static_cast<int64_t>(k) * 8192 + off)[0] = __float2bfloat16_rn(v);
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= static_cast<int64_t>(K) * cin * cout) return;
+  const int k = static_cast<int>(x / (cin * cout)), rem = static_cast<int>(x % (cin * cout));
+  const int c = rem / cout, m = rem % cout;  // W[k][c][m]
+  const int n = transpose ? c : m, r = transpose ? m : c;  // B row, reduction index
+  const int N = transpose ? cin : cout, nchunk = (transpose ? cout : cin) / CH;
+  const int64_t img = static_cast<int64_t>(k) * nchunk + r / CH;
+  reinterpret_cast<__nv_bfloat16*>(out + img * N * 128 + sw128_off(n, r % CH))[0] =
+      __float2bfloat16_rn(w[x]);
 }
 
 // ===========================================================================
@@ -476,9 +483,10 @@ struct FwdArgs {
   const uint32_t* perm_rows;
   int64_t n_rows;
   int n_sub, n_super, st, hcap, K;
-  const __nv_bfloat16* feat;  // bf16 (n_cols, 64), permuted
-  const uint8_t* wpack;       // K x 8 KB
-  float* out;                 // (n_rows, 64), original order
+  int nci;                    // 64-channel chunks of the gathered features
+  const __nv_bfloat16* feat;  // bf16 (n_cols, 64 nci), permuted
+  const uint8_t* wpack;       // (K x nci) images of NOUT x 128 B
+  float* out;                 // (n_rows, NOUT), original order
   long long* trace;           // debug: per-stage event clocks of CTA 0 (nullptr = off)
 };
 constexpr int TRACE_STAGES = 512;
@@ -495,15 +503,26 @@ constexpr int FWD_W_WARP = FWD_AGG_WARP0 + FWD_AGG_WARPS;
 constexpr int FWD_THREADS = 32 * (FWD_W_WARP + 1);
 constexpr int FWD_ST = 2, FWD_HCAP = 960;  // 256-row super-tiles, halo <= 960 rows (120 KB)
 constexpr int NSA = 4;  // A stages (16 KB)
-constexpr int NSW = 3;  // W stages (8 KB)
+constexpr int NSW = 3;  // W stages (NOUT x 128 B; 2 for NOUT = 256)
 constexpr int NSD = 8;  // stage-descriptor slots
-constexpr int FWD_ACC_COLS = FWD_ST * 64;  // fp32 accumulator columns per TMEM buffer
+// Wide outputs (NOUT = C_out of the pass, 128 or 256) use 128-row tiles: the
+// W stages grow to NOUT x 128 B and TMEM holds 2 x NOUT accumulator columns.
+constexpr int FWD_HCAP1 = 672;  // halo rows of 128-row tiles (what fits beside 256-wide W stages)
+template <int NOUT>
+struct FwdCfg {
+  static constexpr int nsw = NOUT == 256 ? 2 : NSW;
+  static constexpr uint32_t wbytes = NOUT * 128;
+  static constexpr int st = NOUT == 64 ? FWD_ST : 1;
+  static constexpr int acc_cols = st * NOUT;  // per TMEM buffer
+  static constexpr uint32_t tmem_cols = 2 * acc_cols <= 256 ? 256 : 512;
+};
 
 struct FwdSmem {
   uint32_t halo, a, w, d, bar, tmem_slot, offs;
   size_t total;
 };
-__host__ __device__ inline FwdSmem fwd_smem_layout(int hcap) {
+template <int NOUT>
+__host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
   FwdSmem L{};
   uint32_t o = 0;
   L.halo = o;
@@ -512,7 +531,7 @@ __host__ __device__ inline FwdSmem fwd_smem_layout(int hcap) {
   L.a = o;
   o += NSA * 16384;
   L.w = o;
-  o += NSW * 8192;
+  o += FwdCfg<NOUT>::nsw * FwdCfg<NOUT>::wbytes;
   L.d = o;
   o += NSD * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
@@ -526,11 +545,16 @@ __host__ __device__ inline FwdSmem fwd_smem_layout(int hcap) {
   return L;
 }
 
+static_assert(fwd_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
+static_assert(fwd_smem_layout<128>(FWD_HCAP1).total <= 232448, "smem");
+static_assert(fwd_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
+
 // Warm L2 with a super-tile's halo rows: one prefetch.global.L2 per 128-byte
 // row, row indices loaded in batches of 8 per lane before the prefetches.
 template <int NT>
 __device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t H,
-                                                 const __nv_bfloat16* feat, int t) {
+                                                 const __nv_bfloat16* feat, int t,
+                                                 int64_t stride = CH) {
   for (uint32_t h0 = 0; h0 < H; h0 += 8 * NT) {
     uint32_t r[8];
 #pragma unroll
@@ -541,7 +565,8 @@ __device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t 
 #pragma unroll
     for (int x = 0; x < 8; ++x)
       if (r[x] != 0xFFFFFFFFu)
-        asm volatile("prefetch.global.L2 [%0];" ::"l"(feat + static_cast<int64_t>(r[x]) * CH));
+        for (int64_t c = 0; c < stride; c += CH)  // every 64-channel chunk of the row
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(feat + static_cast<int64_t>(r[x]) * stride + c));
   }
 }
 // Cooperative halo load by the aggregation warps: 16-byte cp.async per lane,
@@ -549,11 +574,11 @@ __device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t 
 template <int NT>
 __device__ __forceinline__ void coop_load_halo(const uint32_t* rows, uint32_t H,
                                                const __nv_bfloat16* feat, uint32_t s_halo,
-                                               int t) {
+                                               int t, int64_t stride = CH) {
   const uint32_t q = static_cast<uint32_t>(t & 7);
   for (uint32_t h = static_cast<uint32_t>(t) >> 3; h < H; h += NT / 8)
     cp_async16(s_halo + h * 128u + q * 16u,
-               reinterpret_cast<const uint8_t*>(feat + static_cast<int64_t>(rows[h]) * CH) + q * 16u);
+               reinterpret_cast<const uint8_t*>(feat + static_cast<int64_t>(rows[h]) * stride) + q * 16u);
   cp_async_wait_all();
 }
 // Issue the bulk copies of one super-tile halo (runs of consecutive rows).
@@ -658,12 +683,21 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_h
   }
 }
 
+// Input channels come in a.nci chunks of 64: each super-tile runs the cells
+// once per chunk (the halo reloaded with that chunk's 128-byte row slices),
+// all accumulating into the same TMEM accumulators; W_k is packed per (cell,
+// chunk) as an NOUT x 64 image.
+template <int NOUT>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
+  using Cfg = FwdCfg<NOUT>;
+  constexpr int NSWt = Cfg::nsw;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const FwdSmem L = fwd_smem_layout(a.hcap);
+  const FwdSmem L = fwd_smem_layout<NOUT>(a.hcap);
+  const int nci = a.nci;
+  const int64_t fstride = static_cast<int64_t>(nci) * CH;
   const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_w = base + L.w, s_d = base + L.d;
   const uint32_t s_bar = base + L.bar;
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
@@ -678,7 +712,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       mbar_init(bar(B_A_FULL + i), AGG_GROUP_WARPS);
       mbar_init(bar(B_A_EMPTY + i), 1);
     }
-    for (int i = 0; i < NSW; ++i) {
+    for (int i = 0; i < NSWt; ++i) {
       mbar_init(bar(B_W_FULL + i), 1);
       mbar_init(bar(B_W_EMPTY + i), 1);
     }
@@ -692,7 +726,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     }
     fence_barrier_init();
   }
-  if (warp == 5) tmem_alloc<256>(smem_u32(tmem_slot));
+  if (warp == 5) tmem_alloc<Cfg::tmem_cols>(smem_u32(tmem_slot));
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -710,6 +744,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       const int64_t ob = static_cast<int64_t>(s) * a.st * K;
       for (int x = lane; x <= nsub * K; x += 32) offs[x] = a.blk_off[ob + x];
       __syncwarp();
+      for (int c = 0; c < nci; ++c)
       for (int k = 0; k < K; ++k) {
         for (int g = 0; g < nsub; ++g) {
           if (lane == 0) {
@@ -731,11 +766,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       uint32_t w_it = 0;
       for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
         if (a.halo_len[s] == kOverflow) continue;
+        for (int c = 0; c < nci; ++c)
         for (int k = 0; k < K; ++k) {
-          const uint32_t ws = w_it % NSW;
-          mbar_wait_sleep(bar(B_W_EMPTY + ws), ((w_it / NSW) & 1) ^ 1);
-          mbar_expect_tx(bar(B_W_FULL + ws), 8192u);
-          bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u,
+          const uint32_t ws = w_it % NSWt;
+          mbar_wait_sleep(bar(B_W_EMPTY + ws), ((w_it / NSWt) & 1) ^ 1);
+          mbar_expect_tx(bar(B_W_FULL + ws), Cfg::wbytes);
+          bulk_g2s(s_w + ws * Cfg::wbytes,
+                   a.wpack + (static_cast<int64_t>(k) * nci + c) * Cfg::wbytes, Cfg::wbytes,
                    bar(B_W_FULL + ws));
           ++w_it;
         }
@@ -746,7 +783,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     // ------------------------------ MMA issuer -----------------------------
     // The whole warp runs the loop converged (warp-uniform descriptors); one
     // elected lane issues tcgen05.mma / commit.
-    constexpr uint32_t idesc = idesc_bf16(128, 64, false, false);
+    constexpr uint32_t idesc = idesc_bf16(128, NOUT, false, false);
     const uint64_t a_desc0 = sdesc_sw128(s_a, 16, 1024), b_desc0 = sdesc_sw128(s_w, 16, 1024);
     uint32_t w_it = 0, a_it = 0, t_it = 0;
     // The epilogue warps block on named barrier 2 + (tile & 1) (no polling);
@@ -765,24 +802,25 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       const uint32_t ab = t_it & 1;
       mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
       tc_fence_after();
+      for (int c = 0; c < nci; ++c)
       for (int k = 0; k < K; ++k) {
-        if (pending && k == 1) release_epilogue();
-        const uint32_t ws = w_it % NSW;
-        mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
+        if (pending && (c > 0 || k == 1)) release_epilogue();
+        const uint32_t ws = w_it % NSWt;
+        mbar_wait(bar(B_W_FULL + ws), (w_it / NSWt) & 1);
         if (lane == 0) trace_ev(a.trace, a_it, 6);
         for (int g = 0; g < nsub; ++g) {
           const uint32_t as = a_it % NSA;
           mbar_wait(bar(B_A_FULL + as), (a_it / NSA) & 1);
           if (lane == 0) trace_ev(a.trace, a_it, 4);
           tc_fence_after();
-          const uint32_t d = tmem + ab * FWD_ACC_COLS + g * 64;
+          const uint32_t d = tmem + ab * Cfg::acc_cols + g * NOUT;
           // descriptor start-address field is in 16-byte units
           const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
-          const uint64_t bd = b_desc0 + ((ws * 8192u) >> 4);
+          const uint64_t bd = b_desc0 + ((ws * Cfg::wbytes) >> 4);
           if (elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc, (k > 0 || ks > 0) ? 1u : 0u);
+              umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc, (c > 0 || k > 0 || ks > 0) ? 1u : 0u);
             umma_commit(bar(B_A_EMPTY + as));
           }
           __syncwarp();
@@ -810,9 +848,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       const int nsub = min(a.st, a.n_sub - s * a.st);
       const uint32_t H = a.halo_len[s];
       if (H == kOverflow) continue;
+      for (int c = 0; c < nci; ++c) {
       named_bar_sync(1, 32 * FWD_AGG_WARPS);  // all aggregation warps done with the previous halo
-      coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat,
-                                         s_halo, 32 * aw + lane);
+      coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat + c * CH,
+                                         s_halo, 32 * aw + lane, fstride);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
       for (int k = 0; k < K; ++k) {
         for (int g = 0; g < nsub; ++g) {
@@ -836,6 +875,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           ++d_it;
         }
       }
+      }
     }
   } else {
     // ------------------------------ epilogue (warps 0-3) -------------------
@@ -849,18 +889,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         const int s_next = s + gridDim.x;
         if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
           prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
-                                a.halo_len[s_next], a.feat, 32 * e + lane);
+                                a.halo_len[s_next], a.feat, 32 * e + lane, fstride);
       }
       named_bar_sync(2 + ab, 32 * 5);  // released by the MMA warp once T_FULL(tile) landed
       tc_fence_after();
       for (int g = 0; g < nsub; ++g) {
-        const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * FWD_ACC_COLS + g * 64;
+        const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * Cfg::acc_cols + g * NOUT;
         const int64_t row = (static_cast<int64_t>(s) * a.st + g) * TM + 32 * e + lane;
         float4* o = row < a.n_rows
-                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * CH)
+                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * NOUT)
                         : nullptr;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
+#pragma unroll 4
+        for (int q = 0; q < NOUT / 16; ++q) {
           uint32_t v[16];
           tmem_ld16(t0 + 16 * q, v);
           tmem_ld_wait();
@@ -880,7 +920,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
-  if (warp == 5) tmem_free<256>(tmem);
+  if (warp == 5) tmem_free<Cfg::tmem_cols>(tmem);
 }
 
 // ===========================================================================
@@ -1787,23 +1827,28 @@ static TcPlan* get_plan(npcg_context* ctx, npcg_neighbors* nb) {
   return nb->tc.get();
 }
 
-static TcDirPlan* plan_fwd(npcg_context* ctx, npcg_neighbors* nb) {
+// wide = the pass writes more than 64 channels: 128-row super-tiles (st = 1)
+static TcDirPlan* plan_fwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = false) {
   TcPlan* p = get_plan(ctx, nb);
-  if (!p->fwd)
-    p->fwd = build_dir_plan(ctx, nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out,
-                            nb->n_in, nb->perm_out.get(), p->inv_perm_in.get(),
-                            static_cast<int>(nb->n_kernels), FWD_ST, FWD_HCAP);
-  return p->fwd.get();
+  auto& slot = wide ? p->fwd1 : p->fwd;
+  if (!slot)
+    slot = build_dir_plan(ctx, nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out,
+                          nb->n_in, nb->perm_out.get(), p->inv_perm_in.get(),
+                          static_cast<int>(nb->n_kernels), wide ? 1 : FWD_ST,
+                          wide ? FWD_HCAP1 : FWD_HCAP);
+  return slot.get();
 }
-static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
+static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = false) {
   TcPlan* p = get_plan(ctx, nb);
-  if (!p->bwd) {
+  auto& slot = wide ? p->bwd1 : p->bwd;
+  if (!slot) {
     build_tcsr(ctx, nb);
-    p->bwd = build_dir_plan(ctx, nb->tcsr->row_ptr.get(), nb->tcsr->col.get(), nb->tcsr->k.get(),
-                            nb->n_in, nb->n_out, nb->perm_in.get(), p->inv_perm_out.get(),
-                            static_cast<int>(nb->n_kernels), FWD_ST, FWD_HCAP);
+    slot = build_dir_plan(ctx, nb->tcsr->row_ptr.get(), nb->tcsr->col.get(), nb->tcsr->k.get(),
+                          nb->n_in, nb->n_out, nb->perm_in.get(), p->inv_perm_out.get(),
+                          static_cast<int>(nb->n_kernels), wide ? 1 : FWD_ST,
+                          wide ? FWD_HCAP1 : FWD_HCAP);
   }
-  return p->bwd.get();
+  return slot.get();
 }
 
 static bool use_gather_engine();
@@ -1820,22 +1865,35 @@ void tc_prepare(npcg_context* ctx, npcg_neighbors* nb) {
 }
 
 static void convert(npcg_context* ctx, const float* src, const uint32_t* perm, int64_t n,
-                    DevBuf<__nv_bfloat16>& dst) {
-  if (dst.size() < n * CH) dst.alloc(ctx, n * CH);
+                    DevBuf<__nv_bfloat16>& dst, int C = CH) {
+  if (dst.size() < n * C) dst.alloc(ctx, n * C);
   if (n == 0) return;
-  launch(ctx, "to_bf16_perm", k_to_bf16_perm, dim3(static_cast<unsigned>(ceil_div(n * 8, 256))),
-         dim3(256), 0, src, perm, n, dst.get());
+  launch(ctx, "to_bf16_perm", k_to_bf16_perm, dim3(static_cast<unsigned>(ceil_div(n * (C / 8), 256))),
+         dim3(256), 0, src, perm, n, C, dst.get());
 }
 
-static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose) {
-  if (p->wpack.size() < static_cast<int64_t>(K) * 8192) p->wpack.alloc(ctx, static_cast<int64_t>(K) * 8192);
-  launch(ctx, "pack_w", k_pack_w, dim3(static_cast<unsigned>(ceil_div(K * CH * CH, 256))), dim3(256),
-         0, w, K, transpose, p->wpack.get());
+static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose,
+                   int cin = CH, int cout = CH) {
+  const int64_t n = static_cast<int64_t>(K) * cin * cout;
+  if (p->wpack.size() < n * 2) p->wpack.alloc(ctx, n * 2);
+  launch(ctx, "pack_w", k_pack_w, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256), 0, w,
+         K, cin, cout, transpose, p->wpack.get());
 }
 
+template <int NOUT>
+static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, const char* name) {
+  const FwdSmem L = fwd_smem_layout<NOUT>(hcap);
+  NPCG_CUDA(cudaFuncSetAttribute(k_conv_fwd_tc<NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(L.total)));
+  launch(ctx, name, k_conv_fwd_tc<NOUT>, dim3(grid), dim3(FWD_THREADS), L.total, a);
+}
+
+// One gather-side pass (forward or dgrad): cin_g gathered channels -> nout
+// written channels per row.
 static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16* feat,
                            const uint8_t* wpack, const uint32_t* perm_rows, float* out,
-                           const char* name, long long* trace = nullptr) {
+                           const char* name, long long* trace = nullptr, int cin_g = CH,
+                           int nout = CH) {
   if (P->n_super == 0) return;
   FwdArgs a{};
   a.halo = P->halo.get();
@@ -1851,15 +1909,15 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   a.st = P->st;
   a.hcap = P->hcap;
   a.K = P->K;
+  a.nci = cin_g / CH;
   a.feat = feat;
   a.wpack = wpack;
   a.out = out;
   a.trace = trace;
-  const FwdSmem L = fwd_smem_layout(P->hcap);
-  NPCG_CUDA(cudaFuncSetAttribute(k_conv_fwd_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(L.total)));
   const int grid = std::min(P->n_super, ctx->num_sms);
-  launch(ctx, name, k_conv_fwd_tc, dim3(grid), dim3(FWD_THREADS), L.total, a);
+  if (nout == 64) launch_fwd<64>(ctx, a, P->hcap, grid, name);
+  else if (nout == 128) launch_fwd<128>(ctx, a, P->hcap, grid, name);
+  else launch_fwd<256>(ctx, a, P->hcap, grid, name);
 }
 
 
@@ -1899,8 +1957,8 @@ static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
 }
 
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                float* fout) {
-  if (use_gather_engine()) {
+                float* fout, int cin, int cout) {
+  if (use_gather_engine() && cin == CH && cout == CH) {
     GatherPlan* G = gplan_fwd(ctx, nb);
     TcPlan* p = nb->tc.get();
     if (G->n_overflow < G->n_super) {
@@ -1915,19 +1973,19 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const flo
                          CH, fout);
     return;
   }
-  TcDirPlan* P = plan_fwd(ctx, nb);
+  TcDirPlan* P = plan_fwd(ctx, nb, cout > CH);
   TcPlan* p = nb->tc.get();
   if (P->n_overflow < P->n_super) {
-    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
-    p->saved_fin = fin;  // PointConvOp saves its input at forward (conv_op.hpp:138)
-    pack_w(ctx, p, w, P->K, false);
+    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
+    p->saved_fin = cin == CH ? fin : nullptr;  // PointConvOp saves its input (conv_op.hpp:138)
+    pack_w(ctx, p, w, P->K, false, cin, cout);
     run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
-                   "conv_fwd_tc");
+                   "conv_fwd_tc", nullptr, cin, cout);
   }
   // rows of super-tiles beyond the tile capacities: exact engine on those rows only
   const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
-  mvmr_rows_subset_f32(ctx, v, nb->perm_out.get(), P->spill_rows.get(), P->n_spill, w, fin, CH,
-                       CH, fout);
+  mvmr_rows_subset_f32(ctx, v, nb->perm_out.get(), P->spill_rows.get(), P->n_spill, w, fin, cin,
+                       cout, fout);
 }
 
 __global__ void k_add_inplace(float* __restrict__ a, const float* __restrict__ b, int64_t n) {
@@ -1997,11 +2055,13 @@ static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, con
 }
 
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                 const float* gout, float* grad_in, float* grad_w) {
+                 const float* gout, float* grad_in, float* grad_w, int cin, int cout) {
   TcPlan* p = get_plan(ctx, nb);
   const int K = static_cast<int>(nb->n_kernels);
   bool g_converted = false;
-  if (grad_in && use_gather_engine()) {
+  if (grad_w && !tc_wgrad_supported(cin, cout))
+    fail(NPCG_ERR_UNSUPPORTED, "tensor-core weight gradient needs C_in = C_out = 64");
+  if (grad_in && use_gather_engine() && cin == CH && cout == CH) {
     GatherPlan* G = gplan_bwd(ctx, nb);
     if (G->n_overflow < G->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
@@ -2017,19 +2077,19 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
                            G->n_spill, wt.get(), gout, CH, CH, grad_in);
     }
   } else if (grad_in) {
-    TcDirPlan* P = plan_bwd(ctx, nb);
+    TcDirPlan* P = plan_bwd(ctx, nb, cin > CH);
     if (P->n_overflow < P->n_super) {
-      convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
-      g_converted = true;
-      pack_w(ctx, p, w, K, true);
+      convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
+      g_converted = cout == CH;
+      pack_w(ctx, p, w, K, true, cin, cout);
       run_fwd_kernel(ctx, P, p->feat_out.get(), p->wpack.get(), nb->perm_in.get(), grad_in,
-                     "conv_dgrad_tc");
+                     "conv_dgrad_tc", nullptr, cout, cin);
     }
     if (P->n_spill) {
-      DevBuf<float> wt(ctx, static_cast<int64_t>(K) * CH * CH);
-      transpose_w<float>(ctx, w, K, CH, CH, wt.get());
+      DevBuf<float> wt(ctx, static_cast<int64_t>(K) * cin * cout);
+      transpose_w<float>(ctx, w, K, cin, cout, wt.get());
       mvmr_rows_subset_f32(ctx, nb->tcsr->view(), nb->perm_in.get(), P->spill_rows.get(),
-                           P->n_spill, wt.get(), gout, CH, CH, grad_in);
+                           P->n_spill, wt.get(), gout, cout, cin, grad_in);
     }
   }
   if (grad_w) {

@@ -140,20 +140,20 @@ def _emulate_tc(ti, tj, tk, n_out, n_in, w, f, g):
     aggregation of bf16-rounded neighbor rows with fp32 accumulation in CSR order,
     rounded to bf16, then GEMMs against bf16-rounded weights (fp64 here; the
     device accumulates in fp32, so agreement is ~1e-6)."""
-    K = w.shape[0]
+    K, ci, co = w.shape[0], w.shape[2], w.shape[3]
     wb = _bf16(w[:, 0]).astype(np.float64)          # (K, Cin, Cout)
     fb, gb = _bf16(f[:, 0]), _bf16(g[:, 0])
     ti, tj, tk = ti.astype(np.int64), tj.astype(np.int64), tk.astype(np.int64)
     # forward aggregation over (i, k), CSR order = (i, j) order of the build
-    A = np.zeros((n_out, K, 64), np.float32)
+    A = np.zeros((n_out, K, ci), np.float32)
     np.add.at(A, (ti, tk), fb[tj])
-    A = _bf16(A.reshape(-1, 64)).reshape(n_out, K, 64).astype(np.float64)
+    A = _bf16(A.reshape(-1, ci)).reshape(n_out, K, ci).astype(np.float64)
     fout = np.einsum("nkc,kcm->nm", A, wb)
     # dgrad aggregation over (j, k) in (j, i) order
     o = np.lexsort((ti, tj))
-    B = np.zeros((n_in, K, 64), np.float32)
+    B = np.zeros((n_in, K, co), np.float32)
     np.add.at(B, (tj[o], tk[o]), gb[ti[o]])
-    B = _bf16(B.reshape(-1, 64)).reshape(n_in, K, 64).astype(np.float64)
+    B = _bf16(B.reshape(-1, co)).reshape(n_in, K, co).astype(np.float64)
     gin = np.einsum("nkm,kcm->nc", B, wb)
     gw = np.einsum("nm,nkc->kmc", gb.astype(np.float64), A)
     return fout, gin, gw
@@ -220,14 +220,15 @@ def test_bf16_raw_triplets_api(npc, orc):
     assert rel(npc.vvor(T(go), T(f), tl, 27, c).grad.cpu(), gw) <= 1e-2
 
 
-def test_bf16_clustered_cloud(npc, orc, ref):
+@pytest.mark.parametrize("cin,cout", [(64, 64), (128, 256)])
+def test_bf16_clustered_cloud(npc, orc, ref, cin, cout):
     """Dense clusters stress the tile capacities; super-tiles beyond them are
     served by the exact engine, results stay within the bf16 bound."""
     xyz = ref.gen_gaussian_clusters(30000, 20, 4.0, 0.15, 21)
     r = 0.08
-    w = orc.make_weights(3, 1, 64, 64, 2)
-    f = orc.gen_features(30000, 1, 64, 3)
-    go = orc.gen_features(30000, 1, 64, 4)
+    w = orc.make_weights(3, 1, cin, cout, 2)
+    f = orc.gen_features(30000, 1, cin, 3)
+    go = orc.gen_features(30000, 1, cout, 4)
     ti, tj, tk = orc.build_triplets(xyz, xyz, r, 3)
     cl = npc.make_point_cloud(xyz)
     op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
@@ -238,6 +239,36 @@ def test_bf16_clustered_cloud(npc, orc, ref):
     assert rel(out.cpu(), fo) <= 1e-2
     assert rel(res.grad_in.cpu(), gi) <= 1e-2
     assert rel(res.grad_w.cpu(), gw) <= 1e-2
+
+
+@pytest.mark.parametrize("cin,cout", [(64, 128), (128, 64), (128, 128), (256, 256), (64, 256),
+                                      (256, 128)])
+def test_bf16_wide_channels(npc, orc, cin, cout):
+    """C_in, C_out in {64, 128, 256} on the tensor-core forward / input
+    gradient (input channels in 64-wide chunks accumulated in TMEM; outputs
+    up to 256 columns per tile); the weight gradient of a wide layer runs on
+    the exact engine (fp32)."""
+    n = 6000
+    xyz = orc.gen_uniform_cube(n, 1.0, 31)
+    r = 1.8 * n ** (-1 / 3)
+    w = orc.make_weights(3, 1, cin, cout, 32)
+    f = orc.gen_features(n, 1, cin, 33)
+    go = orc.gen_features(n, 1, cout, 34)
+    ti, tj, tk = orc.build_triplets(xyz, xyz, r, 3)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
+    cl = npc.make_point_cloud(xyz)
+    out = op.forward(cl, T(f))
+    res = op.backward(T(go))
+    assert out.shape == (n, 1, cout) and res.grad_in.shape == (n, 1, cin)
+    efo, egi, _ = _emulate_tc(ti, tj, tk, n, n, w, f, go)
+    assert rel(out.cpu().numpy()[:, 0], efo) <= 2e-5
+    assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= 2e-5
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
+                                go.astype(np.float64))
+    assert rel(out.cpu(), fo) <= 1e-2
+    assert rel(res.grad_in.cpu(), gi) <= 1e-2
+    assert rel(res.grad_w.cpu(), gw) <= 1e-5  # exact fp32 engine
+    assert torch.equal(op.forward(cl, T(f)), out)  # deterministic
 
 
 @pytest.mark.slow
