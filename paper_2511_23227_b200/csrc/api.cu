@@ -182,14 +182,10 @@ void backward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, cons
     return;
   }
   if (use_tc(cfg, dtype, G, cin, cout, nb->n_kernels)) {
-    // wide channels: tensor-core input gradient, exact weight gradient (below)
-    const bool tc_w = grad_w && tc_wgrad_supported(cin, cout);
     tc_backward(ctx, nb, static_cast<const float*>(w), static_cast<const float*>(fin),
                 static_cast<const float*>(gout), static_cast<float*>(grad_in),
-                tc_w ? static_cast<float*>(grad_w) : nullptr, static_cast<int>(cin),
-                static_cast<int>(cout));
-    if (!grad_w || tc_w) return;
-    grad_in = nullptr;
+                static_cast<float*>(grad_w), static_cast<int>(cin), static_cast<int>(cout));
+    return;
   }
   if (grad_in) {
     if (dtype == NPCG_F32)
@@ -684,7 +680,7 @@ npcg_status npcg_vvor(npcg_context* ctx, npcg_dtype dtype, const void* gout, int
       backward_impl(ctx, nb.get(), dtype, nullptr, groups, c_in, c_out, fin, gout, cfg, nullptr,
                     grad);
     } else {
-      if (cfg->math == NPCG_MATH_BF16) fail(NPCG_ERR_UNSUPPORTED, "bf16 vvor needs K = t^3, G=1, C=64");
+      if (cfg->math == NPCG_MATH_BF16) fail(NPCG_ERR_UNSUPPORTED, "bf16 vvor needs K = t^3, G=1, C in {64,128,256}");
       CellPlan cells;
       cells_from_triplets(ctx, T, n_kernels, &cells);
       if (dtype == NPCG_F32)

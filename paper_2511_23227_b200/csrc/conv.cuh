@@ -19,11 +19,9 @@ void vvor_cells(npcg_context* ctx, const CellPlan& cells, const T* gout, const T
                 int cin, int cout, T* grad);
 
 // ---- tensor-core engines (conv_tc.cu) --------------------------------------
-// True when the tcgen05 forward / input-gradient path handles this shape
-// (G = 1, C_in, C_out in {64, 128, 256}, K <= 32); the weight gradient runs on
-// tensor cores for C_in = C_out = 64 (tc_wgrad_supported), else exactly.
+// True when the tcgen05 path handles this shape (G = 1, C_in, C_out in
+// {64, 128, 256}, K <= 32).
 bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t n_kernels);
-bool tc_wgrad_supported(int64_t cin, int64_t cout);
 // Forward / input-gradient / weight-gradient over a neighbor handle with
 // bf16 operands and fp32 accumulation.  Builds and caches the tile plans.
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,

@@ -86,7 +86,6 @@ static bool tc_width(int64_t c) { return c == 64 || c == 128 || c == 256; }
 bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K) {
   return G == 1 && tc_width(cin) && tc_width(cout) && K >= 1 && K <= KMAX;
 }
-bool tc_wgrad_supported(int64_t cin, int64_t cout) { return cin == CH && cout == CH; }
 
 // ===========================================================================
 // planner
@@ -554,7 +553,7 @@ static_assert(fwd_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
 template <int NT>
 __device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t H,
                                                  const __nv_bfloat16* feat, int t,
-                                                 int64_t stride = CH) {
+                                                 int64_t stride = CH, int nchunk = 1) {
   for (uint32_t h0 = 0; h0 < H; h0 += 8 * NT) {
     uint32_t r[8];
 #pragma unroll
@@ -565,8 +564,8 @@ __device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t 
 #pragma unroll
     for (int x = 0; x < 8; ++x)
       if (r[x] != 0xFFFFFFFFu)
-        for (int64_t c = 0; c < stride; c += CH)  // every 64-channel chunk of the row
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(feat + static_cast<int64_t>(r[x]) * stride + c));
+        for (int c = 0; c < nchunk; ++c)  // 64-channel chunks of the row
+          asm volatile("prefetch.global.L2 [%0];" ::"l"(feat + static_cast<int64_t>(r[x]) * stride + c * CH));
   }
 }
 // Cooperative halo load by the aggregation warps: 16-byte cp.async per lane,
@@ -889,7 +888,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         const int s_next = s + gridDim.x;
         if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
           prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
-                                a.halo_len[s_next], a.feat, 32 * e + lane, fstride);
+                                a.halo_len[s_next], a.feat, 32 * e + lane, fstride, nci);
       }
       named_bar_sync(2 + ab, 32 * 5);  // released by the MMA warp once T_FULL(tile) landed
       tc_fence_after();
@@ -924,8 +923,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
 }
 
 // ===========================================================================
-// weight-gradient kernel (st = 1: one 128-row tile per super-tile)
-//   D_pair[(2 cells x 64 c_in) x 64 c_out] += A_pair^T (MN-major) x G_tile (MN-major)
+// weight-gradient kernel over the forward plan's super-tiles
+//   D_pair[(2 cells x 64 c_in) x NOUT c_out] += A_pair^T (MN-major) x G_tile (MN-major)
+// Work items are (cell, 64-wide C_in chunk) A tiles; blockIdx.y selects a
+// chunk and a run of 2 x WgCfg::pairs cells, whose pair accumulators stay in
+// TMEM for the whole sweep (NOUT columns each).
 // ===========================================================================
 struct WgArgs {
   const uint32_t* halo;
@@ -936,23 +938,31 @@ struct WgArgs {
   const uint8_t* blocks;
   int64_t n_rows;
   int n_sub, n_super, st, hcap, K;  // the forward plan's super-tiles (st sub-tiles share a halo)
-  const __nv_bfloat16* feat;   // bf16 F_in (n_cols, 64), permuted
-  const __nv_bfloat16* dense;  // bf16 G_out (n_rows, 64), permuted (row = sub-tile order)
-  float* partial;              // [gridDim.x][K][64 c][64 m]
+  int nci, gpc;                // C_in chunks; cell groups per chunk (blockIdx.y = c * gpc + group)
+  const __nv_bfloat16* feat;   // bf16 F_in (n_cols, 64 nci), permuted
+  const __nv_bfloat16* dense;  // bf16 G_out (n_rows, NOUT), permuted (row = sub-tile order)
+  float* partial;              // [gridDim.x][K][64 nci c][NOUT m]
 };
 
 constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
 constexpr int WG_PAIRS = 7;      // cell pairs per CTA (cell group = 14 cells)
 constexpr int WG_NSA = 2;        // A pair stages (32 KB)
 constexpr int WG_NSD = 3;        // descriptor slots (2 blocks each)
-constexpr int WG_NSG = 2;        // dense G sub-tile slots (16 KB)
+constexpr int WG_NSG = 2;        // dense G sub-tile slots (NOUT x 256 B; 1 for NOUT = 256)
 constexpr int WG_GROUPS = 2;     // stage (cell pair) s is aggregated by warp group s % 2
 
+template <int NOUT>
+struct WgCfg {
+  static constexpr int pairs = NOUT == 64 ? WG_PAIRS : 512 / NOUT;  // TMEM: pairs x NOUT columns
+  static constexpr int nsg = NOUT == 256 ? 1 : WG_NSG;
+  static constexpr uint32_t gbytes = NOUT * 256;  // 128 rows x NOUT bf16, 64-column blocks
+};
 struct WgSmem {
   uint32_t halo, a, gt, d, bar, tmem_slot, offs;
   size_t total;
 };
-__host__ __device__ inline WgSmem wg_smem_layout(int hcap) {
+template <int NOUT>
+__host__ __device__ constexpr WgSmem wg_smem_layout(int hcap) {
   WgSmem L{};
   uint32_t o = 0;
   L.halo = o;
@@ -961,7 +971,7 @@ __host__ __device__ inline WgSmem wg_smem_layout(int hcap) {
   L.a = o;
   o += WG_NSA * 32768;
   L.gt = o;
-  o += WG_NSG * 16384;
+  o += WgCfg<NOUT>::nsg * WgCfg<NOUT>::gbytes;
   L.d = o;
   o += WG_NSD * 2 * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
@@ -989,12 +999,20 @@ enum : int {
 };
 static_assert(W_COUNT <= 24, "wgrad barrier region");
 
+static_assert(wg_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
+static_assert(wg_smem_layout<128>(FWD_HCAP1).total <= 232448, "smem");
+static_assert(wg_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
+
+template <int NOUT>
 __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
+  using Cfg = WgCfg<NOUT>;
+  constexpr int NP = Cfg::pairs, NSG = Cfg::nsg;
+  constexpr uint32_t GB = Cfg::gbytes;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const WgSmem L = wg_smem_layout(a.hcap);
+  const WgSmem L = wg_smem_layout<NOUT>(a.hcap);
   const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_g = base + L.gt, s_d = base + L.d;
   const uint32_t s_bar = base + L.bar;
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
@@ -1004,9 +1022,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K;
-  const int cg = blockIdx.y;                 // cell group
-  const int k_begin = cg * 2 * WG_PAIRS;     // first cell of this CTA
-  const int n_pairs = max(0, min(WG_PAIRS, (K - k_begin + 1) / 2));
+  const int chunk = blockIdx.y / a.gpc;      // C_in chunk
+  const int k_begin = (blockIdx.y % a.gpc) * 2 * NP;  // first cell of this CTA
+  const int n_pairs = max(0, min(NP, (K - k_begin + 1) / 2));
+  const int64_t fstride = static_cast<int64_t>(a.nci) * CH;
   if (threadIdx.x == 0) {
     mbar_init(bar(W_HALO_FULL), 1);
     mbar_init(bar(W_HALO_EMPTY), FWD_AGG_WARPS);
@@ -1018,7 +1037,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       mbar_init(bar(W_D_FULL + i), 1);
       mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS / WG_GROUPS);
     }
-    for (int i = 0; i < WG_NSG; ++i) {
+    for (int i = 0; i < NSG; ++i) {
       mbar_init(bar(W_G_FULL + i), 4);
       mbar_init(bar(W_G_EMPTY + i), 1);
     }
@@ -1061,25 +1080,25 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     }
   } else if (warp == 5) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, 64, true, true);
+      constexpr uint32_t idesc = idesc_bf16(128, NOUT, true, true);
       uint32_t a_it = 0, g_it = 0;
       bool first = true;
       for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
         if (a.halo_len[s] == kOverflow) continue;
         const int nsub = min(a.st, a.n_sub - s * a.st);
         for (int g = 0; g < nsub; ++g) {
-        const uint32_t gs = g_it % WG_NSG;
-        mbar_wait(bar(W_G_FULL + gs), (g_it / WG_NSG) & 1);
+        const uint32_t gs = g_it % NSG;
+        mbar_wait(bar(W_G_FULL + gs), (g_it / NSG) & 1);
         for (int p = 0; p < n_pairs; ++p) {
           const uint32_t as = a_it % WG_NSA;
           mbar_wait(bar(W_A_FULL + as), (a_it / WG_NSA) & 1);
           tc_fence_after();
-          const uint32_t d = tmem + p * 64;
+          const uint32_t d = tmem + p * NOUT;
 #pragma unroll
           for (int ks = 0; ks < 8; ++ks) {
             // K = points: 16 rows per step (2 x 8-row groups of 1024 B)
             const uint64_t ad = sdesc_sw128(s_a + as * 32768u + 2048u * ks, 16384, 1024);
-            const uint64_t bd = sdesc_sw128(s_g + gs * 16384u + 2048u * ks, 16384, 1024);
+            const uint64_t bd = sdesc_sw128(s_g + gs * GB + 2048u * ks, 16384, 1024);
             umma_bf16(d, ad, bd, idesc, (first && ks == 0) ? 0u : 1u);
           }
           umma_commit(bar(W_A_EMPTY + as));
@@ -1102,8 +1121,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       if (H == kOverflow) continue;
       const int nsub = min(a.st, a.n_sub - s * a.st);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
-      coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat,
-                                         s_halo, 32 * aw + lane);
+      coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H,
+                                         a.feat + chunk * CH, s_halo, 32 * aw + lane, fstride);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
       for (int g = 0; g < nsub; ++g)
       for (int p = 0; p < n_pairs; ++p) {
@@ -1137,19 +1156,19 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         const int s_next = s + gridDim.x;
         if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
           prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
-                                a.halo_len[s_next], a.feat, 32 * warp + lane);
+                                a.halo_len[s_next], a.feat + chunk * CH, 32 * warp + lane, fstride);
       }
       for (int g = 0; g < nsub; ++g) {
-        const uint32_t gs = g_it % WG_NSG;
-        mbar_wait_sleep(bar(W_G_EMPTY + gs), ((g_it / WG_NSG) & 1) ^ 1);
-        // 128 rows x 8 chunks of 16 B; warp e copies rows 32e..32e+31
-        uint8_t* gt = g_gt + gs * 16384u;
-        for (int x = lane; x < 32 * 8; x += 32) {
-          const int r = 32 * warp + (x >> 3), q = x & 7;
+        const uint32_t gs = g_it % NSG;
+        mbar_wait_sleep(bar(W_G_EMPTY + gs), ((g_it / NSG) & 1) ^ 1);
+        // 128 rows x NOUT/64 blocks x 8 chunks of 16 B; warp e copies rows 32e..32e+31
+        uint8_t* gt = g_gt + gs * GB;
+        for (int x = lane; x < 32 * 8 * (NOUT / 64); x += 32) {
+          const int j = x >> 8, r = 32 * warp + ((x >> 3) & 31), q = x & 7;
           const int64_t row = (static_cast<int64_t>(s) * a.st + g) * TM + r;
           uint4 v = make_uint4(0, 0, 0, 0);
-          if (row < a.n_rows) v = reinterpret_cast<const uint4*>(a.dense + row * CH)[q];
-          *reinterpret_cast<uint4*>(gt + r * 128 + (((q ^ (r & 7)) & 7) << 4)) = v;
+          if (row < a.n_rows) v = reinterpret_cast<const uint4*>(a.dense + row * NOUT)[j * 8 + q];
+          *reinterpret_cast<uint4*>(gt + j * 16384 + r * 128 + (((q ^ (r & 7)) & 7) << 4)) = v;
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -1167,14 +1186,14 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     tc_fence_after();
     const int e = warp;
     for (int p = 0; p < n_pairs; ++p) {
-      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + p * 64;
+      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + p * NOUT;
       const int k = k_begin + 2 * p + (e >> 1);
-      const int c = 32 * (e & 1) + lane;
+      const int c = chunk * CH + 32 * (e & 1) + lane;
       float4* o = k < K ? reinterpret_cast<float4*>(
-                              a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * CH + c) * CH)
+                              a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * fstride + c) * NOUT)
                         : nullptr;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
+#pragma unroll 4
+      for (int q = 0; q < NOUT / 16; ++q) {
         uint32_t v[16];
         tmem_ld16(t0 + 16 * q, v);
         tmem_ld_wait();
@@ -1194,13 +1213,15 @@ done:
 }
 
 // grad_w[k][m][c] = sum over CTAs x (fixed order) of partial[x][k][c][m]
-__global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, int K,
-                               float* __restrict__ grad_w) {
-  const int idx = blockIdx.x * blockDim.x + threadIdx.x;  // (k, m, c)
-  if (idx >= K * CH * CH) return;
-  const int k = idx / (CH * CH), m = (idx / CH) % CH, c = idx % CH;
+__global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, int K, int cin,
+                               int cout, float* __restrict__ grad_w) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (k, m, c)
+  if (idx >= static_cast<int64_t>(K) * cin * cout) return;
+  const int k = static_cast<int>(idx / (cin * cout)), m = static_cast<int>((idx / cin) % cout),
+            c = static_cast<int>(idx % cin);
   float s = 0.f;
-  for (int x = 0; x < n_part; ++x) s += partial[((static_cast<int64_t>(x) * K + k) * CH + c) * CH + m];
+  for (int x = 0; x < n_part; ++x)
+    s += partial[((static_cast<int64_t>(x) * K + k) * cin + c) * cout + m];
   grad_w[idx] = s;
 }
 
@@ -2022,8 +2043,16 @@ __global__ void k_row_lens(const int64_t* __restrict__ row_ptr, const uint32_t* 
   }
 }
 
+template <int NOUT>
+static void launch_wgrad(npcg_context* ctx, const WgArgs& a, int hcap, dim3 grid) {
+  const WgSmem L = wg_smem_layout<NOUT>(hcap);
+  NPCG_CUDA(cudaFuncSetAttribute(k_conv_wgrad_tc<NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(L.total)));
+  launch(ctx, "conv_wgrad_tc", k_conv_wgrad_tc<NOUT>, grid, dim3(WG_THREADS), L.total, a);
+}
+
 static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, const float* fin,
-                        const float* gout, float* grad_w, bool accumulate) {
+                        const float* gout, float* grad_w, bool accumulate, int cin, int cout) {
   const int K = static_cast<int>(nb->n_kernels);
   DevBuf<int64_t> len(ctx, P->n_spill + 1), off(ctx, P->n_spill + 1);
   NPCG_CUDA(cudaMemsetAsync(len.get(), 0, (P->n_spill + 1) * 8, ctx->stream));
@@ -2044,14 +2073,14 @@ static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, con
   CellPlan cells;
   cells_from_triplets(ctx, &T, K, &cells);
   if (!accumulate) {
-    vvor_cells<float>(ctx, cells, gout, fin, 1, CH, CH, grad_w);
+    vvor_cells<float>(ctx, cells, gout, fin, 1, cin, cout, grad_w);
     return;
   }
-  DevBuf<float> tmp(ctx, static_cast<int64_t>(K) * CH * CH);
-  vvor_cells<float>(ctx, cells, gout, fin, 1, CH, CH, tmp.get());
-  launch(ctx, "add_inplace", k_add_inplace, dim3(static_cast<unsigned>(ceil_div(K * CH * CH, 256))),
-         dim3(256), 0, grad_w, static_cast<const float*>(tmp.get()),
-         static_cast<int64_t>(K) * CH * CH);
+  const int64_t nw = static_cast<int64_t>(K) * cin * cout;
+  DevBuf<float> tmp(ctx, nw);
+  vvor_cells<float>(ctx, cells, gout, fin, 1, cin, cout, tmp.get());
+  launch(ctx, "add_inplace", k_add_inplace, dim3(static_cast<unsigned>(ceil_div(nw, 256))),
+         dim3(256), 0, grad_w, static_cast<const float*>(tmp.get()), nw);
 }
 
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
@@ -2059,8 +2088,6 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
   TcPlan* p = get_plan(ctx, nb);
   const int K = static_cast<int>(nb->n_kernels);
   bool g_converted = false;
-  if (grad_w && !tc_wgrad_supported(cin, cout))
-    fail(NPCG_ERR_UNSUPPORTED, "tensor-core weight gradient needs C_in = C_out = 64");
   if (grad_in && use_gather_engine() && cin == CH && cout == CH) {
     GatherPlan* G = gplan_bwd(ctx, nb);
     if (G->n_overflow < G->n_super) {
@@ -2080,7 +2107,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     TcDirPlan* P = plan_bwd(ctx, nb, cin > CH);
     if (P->n_overflow < P->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
-      g_converted = cout == CH;
+      g_converted = true;
       pack_w(ctx, p, w, K, true, cin, cout);
       run_fwd_kernel(ctx, P, p->feat_out.get(), p->wpack.get(), nb->perm_in.get(), grad_in,
                      "conv_dgrad_tc", nullptr, cout, cin);
@@ -2093,20 +2120,25 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     }
   }
   if (grad_w) {
-    TcDirPlan* P = plan_fwd(ctx, nb);  // same rows and gathers as the forward
+    TcDirPlan* P = plan_fwd(ctx, nb, cout > CH);  // same rows and gathers as the forward
     if (P->n_overflow == P->n_super) {
-      wgrad_spill(ctx, nb, P, fin, gout, grad_w, false);
+      wgrad_spill(ctx, nb, P, fin, gout, grad_w, false, cin, cout);
       return;
     }
     // the bf16 input image saved by the forward on this handle is reused when
     // the backward is handed the same input (the operator's saved copy)
     if (fin != p->saved_fin) {
-      convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
-      p->saved_fin = fin;
+      convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
+      p->saved_fin = cin == CH ? fin : nullptr;
     }
-    if (!g_converted) convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
-    const int gx = std::max(1, std::min(P->n_super, ctx->num_sms / 2));
-    const int64_t need = static_cast<int64_t>(gx) * K * CH * CH;
+    if (!g_converted) convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
+    const int nci = cin / CH;
+    const int np = cout == 64 ? WgCfg<64>::pairs : cout == 128 ? WgCfg<128>::pairs : WgCfg<256>::pairs;
+    const int gpc = (K + 2 * np - 1) / (2 * np);  // cell groups per C_in chunk
+    const int groups = nci * gpc;
+    // one CTA per SM in total over (super-tile slices x groups)
+    const int gx = std::max(1, std::min(P->n_super, ctx->num_sms / groups));
+    const int64_t need = static_cast<int64_t>(gx) * K * cin * cout;
     if (p->partial.size() < need) p->partial.alloc(ctx, need);
     NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
     WgArgs a{};
@@ -2122,17 +2154,19 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     a.st = P->st;
     a.hcap = P->hcap;
     a.K = K;
+    a.nci = nci;
+    a.gpc = gpc;
     a.feat = p->feat_in.get();
     a.dense = p->feat_out.get();
     a.partial = p->partial.get();
-    const WgSmem L = wg_smem_layout(P->hcap);
-    NPCG_CUDA(cudaFuncSetAttribute(k_conv_wgrad_tc, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   static_cast<int>(L.total)));
-    const int groups = (K + 2 * WG_PAIRS - 1) / (2 * WG_PAIRS);
-    launch(ctx, "conv_wgrad_tc", k_conv_wgrad_tc, dim3(gx, groups), dim3(WG_THREADS), L.total, a);
-    launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(K * CH * CH, 256))),
-           dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, grad_w);
-    if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true);
+    const dim3 grid(gx, groups);
+    if (cout == 64) launch_wgrad<64>(ctx, a, P->hcap, grid);
+    else if (cout == 128) launch_wgrad<128>(ctx, a, P->hcap, grid);
+    else launch_wgrad<256>(ctx, a, P->hcap, grid);
+    const int64_t nw = static_cast<int64_t>(K) * cin * cout;
+    launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(nw, 256))),
+           dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, grad_w);
+    if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true, cin, cout);
   }
 }
 
