@@ -258,8 +258,9 @@ npcg_status npcg_conv_backward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype
 npcg_status npcg_neighbors_prepare(npcg_context* ctx, npcg_neighbors* nb, int32_t math);
 /* Tensor-core tile-plan statistics (instrumentation; builds the plans): for
  * the forward, input-gradient and weight-gradient plans, four values each --
- * [super-tiles, super-tiles beyond tile capacity (served by the exact engine),
- *  max halo rows, mean halo rows x 100].  stats: HOST int64[12]. */
+ * [super-tiles over all planning levels, rows beyond the capacity of 8-row
+ *  tiles (served by the exact engine), max halo rows, mean halo rows x 100].
+ * stats: HOST int64[12]. */
 npcg_status npcg_neighbors_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* stats);
 /* Debug instrumentation: runs one tensor-core forward with per-stage pipeline
  * event clocks recorded for CTA 0; trace: HOST int64[512 x 8] (SM clock64 of

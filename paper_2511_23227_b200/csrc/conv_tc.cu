@@ -45,17 +45,32 @@ constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sor
 constexpr int MAX_BLOCK_ENTRIES = 512;   // entries per (sub-tile, cell) block
 constexpr int BLOCK_MAX_BYTES = 512 + 2 * MAX_BLOCK_ENTRIES;
 constexpr uint32_t kOverflow = 0xFFFFFFFFu;
+constexpr uint32_t SUP_FIRST = 1u << 8, SUP_LAST = 1u << 9;  // record flags in sup[].y
 
+// A direction plan: super-tiles of 1..st sub-tiles sharing one shared-memory
+// halo.  Level 0 tiles the permuted rows into 128-row sub-tiles, st per
+// super-tile; a super-tile beyond the capacities (halo > hcap rows, > 512
+// entries in a (sub-tile, cell) block, > 254 entries of one row in one cell,
+// > MAXE_ST entries) is re-planned at the next level as single sub-tiles of
+// half as many rows (128, 64, ..., 8), so dense or strided neighborhoods stay
+// on the tensor cores with partially filled tiles; only rows that fail at
+// 8-row tiles go to the exact engine.  Failed super-tiles stay in the arrays
+// with halo_len = kOverflow (skipped by the kernels).
 struct TcDirPlan {
   int st = 3;
   int hcap = 1280;
   int64_t n_rows = 0, n_cols = 0;
-  int n_sub = 0, n_super = 0, K = 0;
+  int n_sub = 0, n_super = 0, K = 0;  // n_sub = sub-tiles over all levels
+  int levels = 0;
+  DevBuf<uint2> sup;          // n_super records {first sub-tile, sub-tiles | SUP_FIRST | SUP_LAST}
+  DevBuf<uint32_t> item_start;  // n_items + 1 (records of an item share rows, accumulate)
+  int n_items = 0;
+  DevBuf<uint2> tiles;        // n_sub {first permuted row, rows (<= 128)}
   DevBuf<uint32_t> halo;      // n_super * hcap permuted source row of each halo row
   DevBuf<uint2> runs;         // n_super * hcap copy runs {src row, dst row | len << 16}
   DevBuf<uint32_t> n_runs;    // n_super
   DevBuf<uint32_t> halo_len;  // n_super (kOverflow marks a super-tile the planner rejected)
-  DevBuf<uint32_t> blk_off;   // n_sub*K + 1 byte offsets of the stage-descriptor blocks
+  DevBuf<uint32_t> blk_off;   // n_sub*K (+1) byte offsets of the stage-descriptor blocks
   DevBuf<uint8_t> blocks;
   int n_overflow = 0;
   int max_halo = 0;
@@ -96,34 +111,60 @@ __global__ void k_inverse_perm(const uint32_t* __restrict__ perm, int64_t n,
   if (p < n) inv[perm[p]] = static_cast<uint32_t>(p);
 }
 
+// Rank filter of a plan record: only the entries of each (row, cell) whose
+// rank (order among that row's entries of that cell, CSR order) lies in
+// [lo, hi).  Records of one 8-row tile that no single plan can hold split its
+// entries by rank; the kernels accumulate such records in TMEM.
+struct RankFilter {
+  uint32_t lo, hi;
+  __device__ __forceinline__ bool all() const { return lo == 0 && hi == 0xFFFFFFFFu; }
+};
+
 // Per sub-tile: entries per (sub-tile, cell) block -> block byte sizes; flags
 // sub-tiles whose blocks exceed the stage-descriptor slot or whose per-(row,
-// cell) counts exceed the 5-bit item field.
+// cell) counts exceed the 8-bit item field; reports the largest per-(row,
+// cell) count (unfiltered), which sizes rank-split records.
 __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ row_ptr,
                                                     const uint32_t* __restrict__ kk,
                                                     const uint32_t* __restrict__ perm_rows,
-                                                    int64_t n_rows, int K,
+                                                    const uint2* __restrict__ tiles,
+                                                    const uint2* __restrict__ tfilter, int K,
                                                     uint32_t* __restrict__ blk_size,
-                                                    uint32_t* __restrict__ sub_bad) {
+                                                    uint32_t* __restrict__ sub_bad,
+                                                    uint32_t* __restrict__ tile_maxc) {
   __shared__ uint32_t cnt[KMAX];
-  __shared__ uint8_t rc[TM][KMAX];
+  __shared__ uint16_t rc[TM][KMAX];   // all entries seen per (row, cell)
+  __shared__ uint16_t inc[TM][KMAX];  // entries within the rank filter
   __shared__ int bad;
+  __shared__ uint32_t s_maxc;
   const int r = threadIdx.x;
   if (r < KMAX) cnt[r] = 0;
-  if (r == 0) bad = 0;
-  for (int k = 0; k < KMAX; ++k) rc[r][k] = 0;
+  if (r == 0) {
+    bad = 0;
+    s_maxc = 0;
+  }
+  for (int k = 0; k < KMAX; ++k) rc[r][k] = inc[r][k] = 0;
   __syncthreads();
-  const int64_t p = static_cast<int64_t>(blockIdx.x) * TM + r;
-  if (p < n_rows) {
-    const uint32_t i = perm_rows[p];
+  const uint2 tl = tiles[blockIdx.x];
+  const RankFilter f{tfilter[blockIdx.x].x, tfilter[blockIdx.x].y};
+  if (static_cast<uint32_t>(r) < tl.y) {
+    const uint32_t i = perm_rows[tl.x + r];
     for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
       const uint32_t k = kk[e];
-      atomicAdd(&cnt[k], 1u);
-      if (rc[r][k] < 255) rc[r][k]++;
+      const uint32_t rank = rc[r][k];
+      if (rc[r][k] < 0xFFFFu) rc[r][k]++;
+      if (rank >= f.lo && rank < f.hi) {
+        atomicAdd(&cnt[k], 1u);
+        inc[r][k]++;
+      }
     }
   }
-  for (int k = 0; k < K; ++k)
-    if (rc[r][k] > 31) bad = 1;
+  uint32_t mx = 0;
+  for (int k = 0; k < K; ++k) {
+    if (inc[r][k] > 254) bad = 1;
+    mx = max(mx, static_cast<uint32_t>(rc[r][k]));
+  }
+  atomicMax(&s_maxc, mx);
   __syncthreads();
   if (r < K) {
     const uint32_t E = cnt[r];
@@ -131,17 +172,40 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
     blk_size[static_cast<int64_t>(blockIdx.x) * K + r] = 512u + ((2u * E + 15u) / 16u) * 16u;
   }
   __syncthreads();
-  if (r == 0) sub_bad[blockIdx.x] = bad;
+  if (r == 0) {
+    sub_bad[blockIdx.x] = bad;
+    tile_maxc[blockIdx.x] = s_maxc;
+  }
+}
+
+// Entries of one row passing a rank filter, in CSR order: fn(e, k).
+template <typename F>
+__device__ __forceinline__ void for_row_entries(const int64_t* row_ptr, const uint32_t* kk,
+                                                uint32_t row, const RankFilter& f, F&& fn) {
+  const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
+  if (f.all()) {
+    for (int64_t e = e0; e < e1; ++e) fn(e, static_cast<int>(kk[e]));
+    return;
+  }
+  uint16_t seen[KMAX];
+#pragma unroll
+  for (int k = 0; k < KMAX; ++k) seen[k] = 0;
+  for (int64_t e = e0; e < e1; ++e) {
+    const int k = static_cast<int>(kk[e]);
+    const uint32_t rank = seen[k]++;
+    if (rank >= f.lo && rank < f.hi) fn(e, k);
+  }
 }
 
 // Per super-tile: halo (sorted unique permuted neighbor rows), per-(sub-tile,
 // cell) item lists (rows ordered by entry count, descending) and u16 halo
 // indices of the entries.  Block layout: u32 item[128] | u16 entry[E] (pad 16 B)
-//   item = r | count << 7 | entry_offset << 12
+//   item = r | count << 7 | entry_offset << 16   (count <= 254)
 __global__ void __launch_bounds__(512) k_plan_super(
     const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
     const uint32_t* __restrict__ kk, const uint32_t* __restrict__ perm_rows,
-    const uint32_t* __restrict__ inv_perm_cols, int64_t n_rows, int K, int n_sub, int st, int hcap,
+    const uint32_t* __restrict__ inv_perm_cols, const uint2* __restrict__ sup,
+    const uint2* __restrict__ tiles, const uint2* __restrict__ tfilter, int K, int st, int hcap,
     const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ sub_bad,
     uint32_t* __restrict__ halo_out, uint2* __restrict__ runs_out, uint32_t* __restrict__ n_runs,
     uint32_t* __restrict__ halo_len,
@@ -155,8 +219,8 @@ __global__ void __launch_bounds__(512) k_plan_super(
   __shared__ int wsum[16];
 
   const int s = blockIdx.x;
-  const int sub0 = s * st;
-  const int nsub = min(st, n_sub - sub0);
+  const int sub0 = static_cast<int>(sup[s].x);
+  const int nsub = static_cast<int>(sup[s].y & 0xFFu);
   const int R = nsub * TM;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   if (tid == 0) {
@@ -172,11 +236,14 @@ __global__ void __launch_bounds__(512) k_plan_super(
   // 1. row lengths -> offsets (block scan over R <= 512 rows)
   int len = 0;
   uint32_t row_i = 0;
+  RankFilter filt{0, 0xFFFFFFFFu};
   if (tid < R) {
-    const int64_t p = static_cast<int64_t>(sub0) * TM + tid;
-    if (p < n_rows) {
-      row_i = perm_rows[p];
-      len = static_cast<int>(row_ptr[row_i + 1] - row_ptr[row_i]);
+    const uint2 tl = tiles[sub0 + tid / TM];
+    filt = RankFilter{tfilter[sub0 + tid / TM].x, tfilter[sub0 + tid / TM].y};
+    if (static_cast<uint32_t>(tid % TM) < tl.y) {
+      row_i = perm_rows[tl.x + tid % TM];
+      if (filt.all()) len = static_cast<int>(row_ptr[row_i + 1] - row_ptr[row_i]);
+      else for_row_entries(row_ptr, kk, row_i, filt, [&](int64_t, int) { ++len; });
     }
   }
   int incl = len;
@@ -207,11 +274,11 @@ __global__ void __launch_bounds__(512) k_plan_super(
   // 2. permuted neighbor ids + per-(sub, cell, row) counts
   if (tid < R && len > 0) {
     const int g = tid / TM, r = tid % TM;
-    const int64_t e0 = row_ptr[row_i];
-    for (int q = 0; q < len; ++q) {
-      buf[my_off + q] = inv_perm_cols[col[e0 + q]];
-      cnt[(g * K + static_cast<int>(kk[e0 + q])) * TM + r]++;
-    }
+    int q = 0;
+    for_row_entries(row_ptr, kk, row_i, filt, [&](int64_t e, int k) {
+      buf[my_off + q++] = inv_perm_cols[col[e]];
+      cnt[(g * K + k) * TM + r]++;
+    });
   }
   int P = 1;
   while (P < E) P <<= 1;
@@ -324,7 +391,10 @@ __global__ void __launch_bounds__(512) k_plan_super(
     const int64_t boff = blk_off[static_cast<int64_t>(sub0 + g) * K + k];
     uint32_t* items = reinterpret_cast<uint32_t*>(blocks + boff);
     int pos = 0, ebase = 0;
-    for (int v = 31; v >= 0; --v) {
+    int vmax = 0;
+    for (int ch = 0; ch < TM / 32; ++ch) vmax = max(vmax, static_cast<int>(cnt[(g * K + k) * TM + ch * 32 + lane]));
+    vmax = __reduce_max_sync(0xffffffffu, vmax);
+    for (int v = vmax; v >= 0; --v) {
       for (int ch = 0; ch < TM / 32; ++ch) {
         const int r = ch * 32 + lane;
         const int c = cnt[(g * K + k) * TM + r];
@@ -333,7 +403,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
           const int before = __popc(m & lt);
           const int eo = ebase + v * before;
           items[pos + before] = static_cast<uint32_t>(r) | (static_cast<uint32_t>(c) << 7) |
-                                (static_cast<uint32_t>(eo) << 12);
+                                (static_cast<uint32_t>(eo) << 16);
           eoff[(g * K + k) * TM + r] = static_cast<uint16_t>(eo);
         }
         pos += __popc(m);
@@ -347,10 +417,8 @@ __global__ void __launch_bounds__(512) k_plan_super(
   // 6. entries: halo index of each neighbor, written at its item's offset
   if (tid < R && len > 0) {
     const int g = tid / TM, r = tid % TM;
-    const int64_t e0 = row_ptr[row_i];
-    for (int q = 0; q < len; ++q) {
-      const int k = static_cast<int>(kk[e0 + q]);
-      const uint32_t pj = inv_perm_cols[col[e0 + q]];
+    for_row_entries(row_ptr, kk, row_i, filt, [&](int64_t e, int k) {
+      const uint32_t pj = inv_perm_cols[col[e]];
       int lo = 0, hi = H;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
@@ -361,9 +429,70 @@ __global__ void __launch_bounds__(512) k_plan_super(
       const int pos = eoff[idx] + cnt[idx]++;
       const int64_t boff = blk_off[static_cast<int64_t>(sub0 + g) * K + k];
       reinterpret_cast<uint16_t*>(blocks + boff + 512)[pos] = static_cast<uint16_t>(lo);
-    }
+    });
   }
   if (tid == 0) halo_len[s] = static_cast<uint32_t>(H);
+}
+
+__global__ void k_add_u32(uint32_t* __restrict__ p, int64_t n, uint32_t add) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x < n) p[x] += add;
+}
+
+// One planning level over a host list of super-tiles (tiles in level-local
+// numbering).  Results stay in the level's own buffers until concatenation.
+struct PlanLevel {
+  std::vector<uint2> sup, tiles, tfilter;  // tfilter: per tile rank filter {lo, hi}
+  std::vector<uint32_t> maxc;              // per tile largest (row, cell) entry count
+  DevBuf<uint32_t> halo, n_runs, halo_len, blk_off;
+  DevBuf<uint2> runs;
+  DevBuf<uint8_t> blocks;
+  uint32_t block_bytes = 0;
+  std::vector<uint32_t> hl;  // halo_len on the host
+};
+
+static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, const uint32_t* col,
+                       const uint32_t* kk, const uint32_t* perm_rows, const uint32_t* inv_perm_cols,
+                       int K, int st, int hcap) {
+  const int ns = static_cast<int>(L.sup.size()), nt = static_cast<int>(L.tiles.size());
+  if (L.tfilter.empty()) L.tfilter.assign(nt, make_uint2(0, 0xFFFFFFFFu));
+  DevBuf<uint2> d_sup(ctx, ns), d_tiles(ctx, nt), d_filt(ctx, nt);
+  DevBuf<uint32_t> d_maxc(ctx, nt);
+  NPCG_CUDA(cudaMemcpyAsync(d_sup.get(), L.sup.data(), ns * sizeof(uint2), cudaMemcpyHostToDevice,
+                            ctx->stream));
+  NPCG_CUDA(cudaMemcpyAsync(d_tiles.get(), L.tiles.data(), nt * sizeof(uint2),
+                            cudaMemcpyHostToDevice, ctx->stream));
+  NPCG_CUDA(cudaMemcpyAsync(d_filt.get(), L.tfilter.data(), nt * sizeof(uint2),
+                            cudaMemcpyHostToDevice, ctx->stream));
+  const int64_t nblk = static_cast<int64_t>(nt) * K;
+  DevBuf<uint32_t> blk_size(ctx, nblk + 1), sub_bad(ctx, nt);
+  NPCG_CUDA(cudaMemsetAsync(blk_size.get() + nblk, 0, 4, ctx->stream));
+  launch(ctx, "plan_counts", k_plan_counts, dim3(nt), dim3(TM), 0, row_ptr, kk, perm_rows,
+         static_cast<const uint2*>(d_tiles.get()), static_cast<const uint2*>(d_filt.get()), K,
+         blk_size.get(), sub_bad.get(), d_maxc.get());
+  L.blk_off.alloc(ctx, nblk + 1);
+  exclusive_scan_u32(ctx, blk_size.get(), L.blk_off.get(), nblk + 1, &L.block_bytes);
+  L.blocks.alloc(ctx, L.block_bytes);
+  L.halo.alloc(ctx, static_cast<int64_t>(ns) * hcap);
+  L.runs.alloc(ctx, static_cast<int64_t>(ns) * hcap);
+  L.n_runs.alloc(ctx, ns);
+  L.halo_len.alloc(ctx, ns);
+  const size_t smem = MAXE_ST * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
+  NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(smem)));
+  launch(ctx, "plan_super", k_plan_super, dim3(ns), dim3(512), smem, row_ptr, col, kk, perm_rows,
+         inv_perm_cols, static_cast<const uint2*>(d_sup.get()),
+         static_cast<const uint2*>(d_tiles.get()), static_cast<const uint2*>(d_filt.get()), K, st,
+         hcap,
+         static_cast<const uint32_t*>(L.blk_off.get()), static_cast<const uint32_t*>(sub_bad.get()),
+         L.halo.get(), L.runs.get(), L.n_runs.get(), L.halo_len.get(), L.blocks.get());
+  L.hl.resize(ns);
+  L.maxc.resize(nt);
+  NPCG_CUDA(cudaMemcpyAsync(L.hl.data(), L.halo_len.get(), ns * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  NPCG_CUDA(cudaMemcpyAsync(L.maxc.data(), d_maxc.get(), nt * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
+  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
 static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_t* row_ptr,
@@ -378,57 +507,159 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   P->n_rows = n_rows;
   P->n_cols = n_cols;
   P->K = K;
-  P->n_sub = static_cast<int>(ceil_div(n_rows, TM));
-  P->n_super = static_cast<int>(ceil_div(P->n_sub, st));
-  if (P->n_sub == 0) return P;
-  const int64_t nblk = static_cast<int64_t>(P->n_sub) * K;
-  DevBuf<uint32_t> blk_size(ctx, nblk + 1), sub_bad(ctx, P->n_sub);
-  NPCG_CUDA(cudaMemsetAsync(blk_size.get() + nblk, 0, 4, ctx->stream));
-  launch(ctx, "plan_counts", k_plan_counts, dim3(P->n_sub), dim3(TM), 0, row_ptr, kk, perm_rows,
-         n_rows, K, blk_size.get(), sub_bad.get());
-  P->blk_off.alloc(ctx, nblk + 1);
-  uint32_t total = 0;
-  exclusive_scan_u32(ctx, blk_size.get(), P->blk_off.get(), nblk + 1, &total);
-  P->blocks.alloc(ctx, total);
-  P->halo.alloc(ctx, static_cast<int64_t>(P->n_super) * hcap);
-  P->runs.alloc(ctx, static_cast<int64_t>(P->n_super) * hcap);
-  P->n_runs.alloc(ctx, P->n_super);
-  P->halo_len.alloc(ctx, P->n_super);
-  const size_t smem = MAXE_ST * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
-  NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(smem)));
-  launch(ctx, "plan_super", k_plan_super, dim3(P->n_super), dim3(512), smem, row_ptr, col, kk,
-         perm_rows, inv_perm_cols, n_rows, K, P->n_sub, st, hcap,
-         static_cast<const uint32_t*>(P->blk_off.get()), static_cast<const uint32_t*>(sub_bad.get()),
-         P->halo.get(), P->runs.get(), P->n_runs.get(), P->halo_len.get(), P->blocks.get());
-  std::vector<uint32_t> hl(P->n_super);
-  NPCG_CUDA(cudaMemcpyAsync(hl.data(), P->halo_len.get(), hl.size() * 4, cudaMemcpyDeviceToHost,
-                            ctx->stream));
-  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
-  double sum = 0;
-  for (uint32_t h : hl) {
-    if (h == kOverflow) {
-      P->n_overflow++;
-    } else {
-      P->max_halo = std::max<int>(P->max_halo, static_cast<int>(h));
-      sum += h;
-    }
+  if (n_rows == 0) return P;
+  // level 0: 128-row sub-tiles, st per super-tile
+  std::vector<PlanLevel> lv(1);
+  {
+    const int nt = static_cast<int>(ceil_div(n_rows, TM));
+    for (int t = 0; t < nt; ++t)
+      lv[0].tiles.push_back(make_uint2(static_cast<uint32_t>(t) * TM,
+                                       static_cast<uint32_t>(std::min<int64_t>(TM, n_rows - int64_t(t) * TM))));
+    for (int t = 0; t < nt; t += st)
+      lv[0].sup.push_back(make_uint2(t, std::min(st, nt - t)));
   }
+  // Levels: st x 128 rows, then single sub-tiles of 128 (if st > 1), 64, ...,
+  // 8 rows; an 8-row tile that still fails becomes one item of rank-split
+  // records (entries of rank [qQ, (q+1)Q) per (row, cell), Q sized so that
+  // any record fits the halo: 8 rows x K cells x Q <= hcap).
+  std::vector<uint32_t> spill;
+  std::vector<uint8_t> rank_level{0};  // per level: records are rank splits
+  uint32_t cur = TM;                // rows per sub-tile at this level
+  for (int level = 0;; ++level) {
+    PlanLevel& L = lv[level];
+    plan_level(ctx, L, row_ptr, col, kk, perm_rows, inv_perm_cols, K, st, hcap);
+    const bool is_rank = rank_level[level] != 0;
+    PlanLevel next;
+    if (is_rank) {
+      // an item fails as a whole: its rows go to the exact engine
+      for (size_t x = 0; x < L.sup.size();) {
+        size_t y = x + 1;
+        while (y < L.sup.size() && !(L.sup[y].y & SUP_FIRST)) ++y;
+        bool bad = false;
+        for (size_t z = x; z < y; ++z) bad |= L.hl[z] == kOverflow;
+        if (bad) {
+          const uint2 tl = L.tiles[L.sup[x].x];
+          for (uint32_t p = tl.x; p < tl.x + tl.y; ++p) spill.push_back(p);
+          for (size_t z = x; z < y; ++z) L.hl[z] = kOverflow;
+          std::vector<uint32_t> ov(y - x, kOverflow);
+          NPCG_CUDA(cudaMemcpyAsync(L.halo_len.get() + x, ov.data(), ov.size() * 4,
+                                    cudaMemcpyHostToDevice, ctx->stream));
+          NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+        }
+        x = y;
+      }
+      break;
+    }
+    const uint32_t sz = level == 0 && st > 1 ? TM : cur / 2;
+    cur = sz;
+    const bool to_rank = sz < 8;
+    const uint32_t Q = std::max<uint32_t>(1, static_cast<uint32_t>(hcap) / (8u * K));
+    for (size_t x = 0; x < L.sup.size(); ++x) {
+      if (L.hl[x] != kOverflow) continue;
+      const uint2 sp = L.sup[x];
+      const uint32_t a = L.tiles[sp.x].x;
+      const uint2 last = L.tiles[sp.x + (sp.y & 0xFFu) - 1];
+      const uint32_t b = last.x + last.y;
+      if (to_rank) {
+        uint32_t maxc = 0;
+        for (uint32_t t = sp.x; t < sp.x + (sp.y & 0xFFu); ++t) maxc = std::max(maxc, L.maxc[t]);
+        const uint32_t nq = std::max<uint32_t>(1, (maxc + Q - 1) / Q);
+        for (uint32_t q = 0; q < nq; ++q) {
+          const uint32_t fl = (q == 0 ? SUP_FIRST : 0u) | (q + 1 == nq ? SUP_LAST : 0u);
+          next.sup.push_back(make_uint2(static_cast<uint32_t>(next.tiles.size()), 1u | fl));
+          next.tiles.push_back(make_uint2(a, b - a));
+          next.tfilter.push_back(make_uint2(q * Q, (q + 1) * Q));
+        }
+        continue;
+      }
+      for (uint32_t p = a; p < b; p += sz) {
+        next.sup.push_back(make_uint2(static_cast<uint32_t>(next.tiles.size()), 1));
+        next.tiles.push_back(make_uint2(p, std::min(sz, b - p)));
+      }
+    }
+    if (next.sup.empty()) break;
+    lv.push_back(std::move(next));
+    rank_level.push_back(to_rank ? 1 : 0);
+  }
+  P->levels = static_cast<int>(lv.size());
+  // concatenate the levels
+  int64_t ns = 0, nt = 0, bytes = 0;
+  for (auto& L : lv) {
+    ns += L.sup.size();
+    nt += L.tiles.size();
+    bytes += L.block_bytes;
+  }
+  P->n_super = static_cast<int>(ns);
+  P->n_sub = static_cast<int>(nt);
+  P->halo.alloc(ctx, ns * hcap);
+  P->runs.alloc(ctx, ns * hcap);
+  P->n_runs.alloc(ctx, ns);
+  P->halo_len.alloc(ctx, ns);
+  P->blk_off.alloc(ctx, nt * K + 1);
+  P->blocks.alloc(ctx, bytes);
+  std::vector<uint2> sup_all, tiles_all;
+  int64_t s0 = 0, t0 = 0, b0 = 0;
+  double sum = 0;
+  std::vector<uint32_t> items;
+  for (size_t li = 0; li < lv.size(); ++li) {
+    PlanLevel& L = lv[li];
+    const int64_t lns = L.sup.size(), lnt = L.tiles.size();
+    for (const uint2& sp : L.sup) {
+      // plain super-tiles are single-record items
+      const uint32_t fl = rank_level[li] ? (sp.y & (SUP_FIRST | SUP_LAST)) : (SUP_FIRST | SUP_LAST);
+      if (fl & SUP_FIRST) items.push_back(static_cast<uint32_t>(sup_all.size()));
+      sup_all.push_back(make_uint2(sp.x + static_cast<uint32_t>(t0), (sp.y & 0xFFu) | fl));
+    }
+    tiles_all.insert(tiles_all.end(), L.tiles.begin(), L.tiles.end());
+    NPCG_CUDA(cudaMemcpyAsync(P->halo.get() + s0 * hcap, L.halo.get(), lns * hcap * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    NPCG_CUDA(cudaMemcpyAsync(P->runs.get() + s0 * hcap, L.runs.get(), lns * hcap * 8,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    NPCG_CUDA(cudaMemcpyAsync(P->n_runs.get() + s0, L.n_runs.get(), lns * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    NPCG_CUDA(cudaMemcpyAsync(P->halo_len.get() + s0, L.halo_len.get(), lns * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    NPCG_CUDA(cudaMemcpyAsync(P->blk_off.get() + t0 * K, L.blk_off.get(), (lnt * K + 1) * 4,
+                              cudaMemcpyDeviceToDevice, ctx->stream));
+    if (b0)
+      launch(ctx, "plan_rebase", k_add_u32, dim3(static_cast<unsigned>(ceil_div(lnt * K + 1, 256))),
+             dim3(256), 0, P->blk_off.get() + t0 * K, lnt * K + 1, static_cast<uint32_t>(b0));
+    if (L.block_bytes)
+      NPCG_CUDA(cudaMemcpyAsync(P->blocks.get() + b0, L.blocks.get(), L.block_bytes,
+                                cudaMemcpyDeviceToDevice, ctx->stream));
+    for (uint32_t h : L.hl) {
+      if (h == kOverflow) {
+        P->n_overflow++;
+      } else {
+        P->max_halo = std::max<int>(P->max_halo, static_cast<int>(h));
+        sum += h;
+      }
+    }
+    s0 += lns;
+    t0 += lnt;
+    b0 += L.block_bytes;
+  }
+  if (bytes >= (int64_t(1) << 32)) fail(NPCG_ERR_UNSUPPORTED, "tile plan exceeds 4 GB of descriptors");
+  items.push_back(static_cast<uint32_t>(ns));
+  P->n_items = static_cast<int>(items.size()) - 1;
+  P->item_start.alloc(ctx, items.size());
+  NPCG_CUDA(cudaMemcpyAsync(P->item_start.get(), items.data(), items.size() * 4,
+                            cudaMemcpyHostToDevice, ctx->stream));
+  P->sup.alloc(ctx, ns);
+  P->tiles.alloc(ctx, nt);
+  NPCG_CUDA(cudaMemcpyAsync(P->sup.get(), sup_all.data(), ns * sizeof(uint2), cudaMemcpyHostToDevice,
+                            ctx->stream));
+  NPCG_CUDA(cudaMemcpyAsync(P->tiles.get(), tiles_all.data(), nt * sizeof(uint2),
+                            cudaMemcpyHostToDevice, ctx->stream));
   const int ok = P->n_super - P->n_overflow;
   P->mean_halo = ok ? sum / ok : 0.0;
-  if (P->n_overflow) {
-    std::vector<uint32_t> rows;
-    const int64_t per = static_cast<int64_t>(st) * TM;
-    for (int s2 = 0; s2 < P->n_super; ++s2)
-      if (hl[s2] == kOverflow)
-        for (int64_t p = s2 * per; p < std::min(n_rows, (s2 + 1) * per); ++p)
-          rows.push_back(static_cast<uint32_t>(p));
-    P->n_spill = static_cast<int64_t>(rows.size());
+  P->n_spill = static_cast<int64_t>(spill.size());
+  if (P->n_spill) {
     P->spill_rows.alloc(ctx, P->n_spill);
-    NPCG_CUDA(cudaMemcpyAsync(P->spill_rows.get(), rows.data(), rows.size() * 4,
+    NPCG_CUDA(cudaMemcpyAsync(P->spill_rows.get(), spill.data(), spill.size() * 4,
                               cudaMemcpyHostToDevice, ctx->stream));
-    NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
   }
+  NPCG_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
   return P;
 }
 
@@ -480,6 +711,10 @@ struct FwdArgs {
   const uint32_t* blk_off;
   const uint8_t* blocks;
   const uint32_t* perm_rows;
+  const uint2* sup;           // per record {first sub-tile, sub-tiles | SUP_FIRST | SUP_LAST}
+  const uint2* tiles;         // per sub-tile {first permuted row, rows}
+  const uint32_t* item_start; // n_items + 1: records [item_start[w], item_start[w + 1]) share rows
+  int n_items;
   int64_t n_rows;
   int n_sub, n_super, st, hcap, K;
   int nci;                    // 64-channel chunks of the gathered features
@@ -629,7 +864,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_h
   for (int qb = 0; qb < NQ; qb += 4) {
     uint32_t packed = 0;
 #pragma unroll
-    for (int x = 0; x < 4 && qb + x < NQ; ++x) packed |= ((it[qb + x] >> 7) & 31u) << (8 * x);
+    for (int x = 0; x < 4 && qb + x < NQ; ++x) packed |= ((it[qb + x] >> 7) & 255u) << (8 * x);
     packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 8));
     packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 16));
 #pragma unroll
@@ -640,8 +875,8 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_h
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     v[qi] = make_uint4(0, 0, 0, 0);
-    if (cm[qi] <= 1u && ((it[qi] >> 7) & 31u) == 1u)
-      v[qi] = lds128(s_halo + static_cast<uint32_t>(ents[it[qi] >> 12]) * 128u + l8x16);
+    if (cm[qi] <= 1u && ((it[qi] >> 7) & 255u) == 1u)
+      v[qi] = lds128(s_halo + static_cast<uint32_t>(ents[it[qi] >> 16]) * 128u + l8x16);
   }
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
@@ -654,7 +889,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_h
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     if (cm[qi] >= 2u) {
-      const uint32_t c = (it[qi] >> 7) & 31u, eo = it[qi] >> 12;
+      const uint32_t c = (it[qi] >> 7) & 255u, eo = it[qi] >> 16;
       float acc[8];
 #pragma unroll
       for (int x = 0; x < 8; ++x) acc[x] = 0.f;
@@ -736,11 +971,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     // ------------------------ producer: halo + descriptors -----------------
     uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
     uint32_t d_it = 0;
-    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
-      const int nsub = min(a.st, a.n_sub - s * a.st);
+    for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
+    for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+      const uint2 sp = a.sup[s];
+      const int nsub = static_cast<int>(sp.y & 0xFFu);
       if (a.halo_len[s] == kOverflow) continue;
       // stage this super-tile's descriptor offsets in smem
-      const int64_t ob = static_cast<int64_t>(s) * a.st * K;
+      const int64_t ob = static_cast<int64_t>(sp.x) * K;
       for (int x = lane; x <= nsub * K; x += 32) offs[x] = a.blk_off[ob + x];
       __syncwarp();
       for (int c = 0; c < nci; ++c)
@@ -763,7 +1000,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     // ------------------------ producer: W_k per super-tile and cell ---------
     if (lane == 0) {
       uint32_t w_it = 0;
-      for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
+      for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
+    for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
         if (a.halo_len[s] == kOverflow) continue;
         for (int c = 0; c < nci; ++c)
         for (int k = 0; k < K; ++k) {
@@ -795,15 +1033,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       named_bar_arrive(2 + (pend_t & 1), 32 * 5);
       pending = false;
     };
-    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
-      const int nsub = min(a.st, a.n_sub - s * a.st);
+    for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
+    for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+      const uint2 sp = a.sup[s];
+      const int nsub = static_cast<int>(sp.y & 0xFFu);
       if (a.halo_len[s] == kOverflow) continue;
+      const bool first = (sp.y & SUP_FIRST) != 0, last = (sp.y & SUP_LAST) != 0;
       const uint32_t ab = t_it & 1;
-      mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
+      if (first) mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
       tc_fence_after();
       for (int c = 0; c < nci; ++c)
       for (int k = 0; k < K; ++k) {
-        if (pending && (c > 0 || k == 1)) release_epilogue();
+        if (pending && (c > 0 || k == 1 || !first)) release_epilogue();
         const uint32_t ws = w_it % NSWt;
         mbar_wait(bar(B_W_FULL + ws), (w_it / NSWt) & 1);
         if (lane == 0) trace_ev(a.trace, a_it, 6);
@@ -819,7 +1060,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           if (elect_one()) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
-              umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc, (c > 0 || k > 0 || ks > 0) ? 1u : 0u);
+              umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
+                        (!first || c > 0 || k > 0 || ks > 0) ? 1u : 0u);
             umma_commit(bar(B_A_EMPTY + as));
           }
           __syncwarp();
@@ -830,6 +1072,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         __syncwarp();
         ++w_it;
       }
+      if (!last) continue;  // the next record of this item accumulates on
       if (elect_one()) umma_commit(bar(B_T_FULL + ab));
       __syncwarp();
       if (pending) release_epilogue();  // K == 1
@@ -843,8 +1086,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     const int aw = warp - FWD_AGG_WARP0;
     const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
     uint32_t a_it = 0, d_it = 0;
-    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
-      const int nsub = min(a.st, a.n_sub - s * a.st);
+    for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
+    for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+      const uint2 sp = a.sup[s];
+      const int nsub = static_cast<int>(sp.y & 0xFFu);
       const uint32_t H = a.halo_len[s];
       if (H == kOverflow) continue;
       for (int c = 0; c < nci; ++c) {
@@ -880,12 +1125,15 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     // ------------------------------ epilogue (warps 0-3) -------------------
     const int e = warp;
     uint32_t t_it = 0;
-    for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
-      const int nsub = min(a.st, a.n_sub - s * a.st);
+    for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
+      const int s = static_cast<int>(a.item_start[w + 1]) - 1;  // last record: the rows
+      const uint2 sp = a.sup[s];
+      const int nsub = static_cast<int>(sp.y & 0xFFu);
       if (a.halo_len[s] == kOverflow) continue;
       const uint32_t ab = t_it & 1;
-      {  // warm L2 with the next super-tile's halo while this one is aggregated
-        const int s_next = s + gridDim.x;
+      {  // warm L2 with the next item's halo while this one is aggregated
+        const int s_next = w + static_cast<int>(gridDim.x) < a.n_items
+                               ? static_cast<int>(a.item_start[w + gridDim.x]) : a.n_super;
         if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
           prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap,
                                 a.halo_len[s_next], a.feat, 32 * e + lane, fstride, nci);
@@ -894,8 +1142,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       tc_fence_after();
       for (int g = 0; g < nsub; ++g) {
         const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * Cfg::acc_cols + g * NOUT;
-        const int64_t row = (static_cast<int64_t>(s) * a.st + g) * TM + 32 * e + lane;
-        float4* o = row < a.n_rows
+        const uint2 tl = a.tiles[sp.x + g];
+        const int64_t row = static_cast<int64_t>(tl.x) + 32 * e + lane;
+        float4* o = static_cast<uint32_t>(32 * e + lane) < tl.y
                         ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * NOUT)
                         : nullptr;
 #pragma unroll 4
@@ -936,6 +1185,8 @@ struct WgArgs {
   const uint32_t* halo_len;
   const uint32_t* blk_off;
   const uint8_t* blocks;
+  const uint2* sup;            // per super-tile {first sub-tile, sub-tiles}
+  const uint2* tiles;          // per sub-tile {first permuted row, rows}
   int64_t n_rows;
   int n_sub, n_super, st, hcap, K;  // the forward plan's super-tiles (st sub-tiles share a halo)
   int nci, gpc;                // C_in chunks; cell groups per chunk (blockIdx.y = c * gpc + group)
@@ -1056,9 +1307,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     uint32_t d_it = 0;
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       if (a.halo_len[s] == kOverflow) continue;
-      const int nsub = min(a.st, a.n_sub - s * a.st);
+      const uint2 sp = a.sup[s];
+      const int nsub = static_cast<int>(sp.y & 0xFFu);
       for (int x = lane; x <= nsub * K; x += 32)
-        offs[x] = a.blk_off[static_cast<int64_t>(s) * a.st * K + x];
+        offs[x] = a.blk_off[static_cast<int64_t>(sp.x) * K + x];
       __syncwarp();
       for (int g = 0; g < nsub; ++g)
       for (int p = 0; p < n_pairs; ++p) {
@@ -1085,7 +1337,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       bool first = true;
       for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
         if (a.halo_len[s] == kOverflow) continue;
-        const int nsub = min(a.st, a.n_sub - s * a.st);
+        const uint2 sp = a.sup[s];
+        const int nsub = static_cast<int>(sp.y & 0xFFu);
         for (int g = 0; g < nsub; ++g) {
         const uint32_t gs = g_it % NSG;
         mbar_wait(bar(W_G_FULL + gs), (g_it / NSG) & 1);
@@ -1119,7 +1372,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       const uint32_t H = a.halo_len[s];
       if (H == kOverflow) continue;
-      const int nsub = min(a.st, a.n_sub - s * a.st);
+      const uint2 sp = a.sup[s];
+      const int nsub = static_cast<int>(sp.y & 0xFFu);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
       coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H,
                                          a.feat + chunk * CH, s_halo, 32 * aw + lane, fstride);
@@ -1151,7 +1405,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     uint32_t g_it = 0;
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       if (a.halo_len[s] == kOverflow) continue;
-      const int nsub = min(a.st, a.n_sub - s * a.st);
+      const uint2 sp = a.sup[s];
+      const int nsub = static_cast<int>(sp.y & 0xFFu);
       {
         const int s_next = s + gridDim.x;
         if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
@@ -1165,9 +1420,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         uint8_t* gt = g_gt + gs * GB;
         for (int x = lane; x < 32 * 8 * (NOUT / 64); x += 32) {
           const int j = x >> 8, r = 32 * warp + ((x >> 3) & 31), q = x & 7;
-          const int64_t row = (static_cast<int64_t>(s) * a.st + g) * TM + r;
+          const uint2 tl = a.tiles[sp.x + g];
+          const int64_t row = static_cast<int64_t>(tl.x) + r;
           uint4 v = make_uint4(0, 0, 0, 0);
-          if (row < a.n_rows) v = reinterpret_cast<const uint4*>(a.dense + row * NOUT)[j * 8 + q];
+          if (static_cast<uint32_t>(r) < tl.y) v = reinterpret_cast<const uint4*>(a.dense + row * NOUT)[j * 8 + q];
           *reinterpret_cast<uint4*>(gt + j * 16384 + r * 128 + (((q ^ (r & 7)) & 7) << 4)) = v;
         }
         fence_proxy_async_smem();
@@ -1924,6 +2180,10 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   a.blk_off = P->blk_off.get();
   a.blocks = P->blocks.get();
   a.perm_rows = perm_rows;
+  a.sup = P->sup.get();
+  a.tiles = P->tiles.get();
+  a.item_start = P->item_start.get();
+  a.n_items = P->n_items;
   a.n_rows = P->n_rows;
   a.n_sub = P->n_sub;
   a.n_super = P->n_super;
@@ -2148,6 +2408,8 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     a.halo_len = P->halo_len.get();
     a.blk_off = P->blk_off.get();
     a.blocks = P->blocks.get();
+    a.sup = P->sup.get();
+    a.tiles = P->tiles.get();
     a.n_rows = P->n_rows;
     a.n_sub = P->n_sub;
     a.n_super = P->n_super;
@@ -2203,7 +2465,7 @@ void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12) {
   const TcDirPlan* ds[3] = {p->fwd.get(), p->bwd.get(), p->fwd.get()};  // wgrad runs on the forward plan
   for (int i = 0; i < 3; ++i) {
     out12[4 * i + 0] = ds[i]->n_super;
-    out12[4 * i + 1] = ds[i]->n_overflow;
+    out12[4 * i + 1] = ds[i]->n_spill;
     out12[4 * i + 2] = ds[i]->max_halo;
     out12[4 * i + 3] = static_cast<int64_t>(ds[i]->mean_halo * 100);
   }

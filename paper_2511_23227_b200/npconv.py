@@ -376,6 +376,7 @@ class Neighbors:
         h = self.ctx.bind()
         self.ctx.check(L.lib().npcg_neighbors_plan_stats(h, self.h, out), "plan_stats")
         v = list(out)
+        # overflow = rows the tensor-core plan leaves to the exact engine
         return {name: {"super_tiles": v[4 * i], "overflow": v[4 * i + 1], "max_halo": v[4 * i + 2],
                        "mean_halo": v[4 * i + 3] / 100.0}
                 for i, name in enumerate(("fwd", "dgrad", "wgrad"))}
