@@ -42,7 +42,7 @@ constexpr int TM = 128;
 constexpr int CH = 64;
 constexpr int KMAX = 32;
 constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sorts in smem
-constexpr int MAX_BLOCK_ENTRIES = 512;   // entries per (sub-tile, cell) block
+constexpr int MAX_BLOCK_ENTRIES = 768;   // entries per (sub-tile, cell) block
 constexpr int BLOCK_MAX_BYTES = 512 + 2 * MAX_BLOCK_ENTRIES;
 constexpr uint32_t kOverflow = 0xFFFFFFFFu;
 constexpr uint32_t SUP_FIRST = 1u << 8, SUP_LAST = 1u << 9;  // record flags in sup[].y
@@ -735,7 +735,7 @@ constexpr int AGG_GROUPS = 4;                           // stage s is aggregated
 constexpr int AGG_GROUP_WARPS = FWD_AGG_WARPS / AGG_GROUPS;
 constexpr int FWD_W_WARP = FWD_AGG_WARP0 + FWD_AGG_WARPS;
 constexpr int FWD_THREADS = 32 * (FWD_W_WARP + 1);
-constexpr int FWD_ST = 2, FWD_HCAP = 960;  // 256-row super-tiles, halo <= 960 rows (120 KB)
+constexpr int FWD_ST = 2, FWD_HCAP = 928;  // 256-row super-tiles, halo <= 928 rows (116 KB)
 constexpr int NSA = 4;  // A stages (16 KB)
 constexpr int NSW = 3;  // W stages (NOUT x 128 B; 2 for NOUT = 256)
 constexpr int NSD = 8;  // stage-descriptor slots
@@ -745,6 +745,7 @@ constexpr int FWD_HCAP1 = 672;  // halo rows of 128-row tiles (what fits beside 
 template <int NOUT>
 struct FwdCfg {
   static constexpr int nsw = NOUT == 256 ? 2 : NSW;
+  static constexpr int nsd = NOUT == 256 ? 6 : NSD;  // descriptor slots
   static constexpr uint32_t wbytes = NOUT * 128;
   static constexpr int st = NOUT == 64 ? FWD_ST : 1;
   static constexpr int acc_cols = st * NOUT;  // per TMEM buffer
@@ -767,7 +768,7 @@ __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
   L.w = o;
   o += FwdCfg<NOUT>::nsw * FwdCfg<NOUT>::wbytes;
   L.d = o;
-  o += NSD * BLOCK_MAX_BYTES;
+  o += FwdCfg<NOUT>::nsd * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
   L.bar = o;
   o += 48 * 8;
@@ -924,7 +925,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_h
 template <int NOUT>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   using Cfg = FwdCfg<NOUT>;
-  constexpr int NSWt = Cfg::nsw;
+  constexpr int NSWt = Cfg::nsw, NSDt = Cfg::nsd;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
@@ -950,7 +951,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       mbar_init(bar(B_W_FULL + i), 1);
       mbar_init(bar(B_W_EMPTY + i), 1);
     }
-    for (int i = 0; i < NSD; ++i) {
+    for (int i = 0; i < NSDt; ++i) {
       mbar_init(bar(B_D_FULL + i), 1);
       mbar_init(bar(B_D_EMPTY + i), AGG_GROUP_WARPS);
     }
@@ -984,8 +985,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       for (int k = 0; k < K; ++k) {
         for (int g = 0; g < nsub; ++g) {
           if (lane == 0) {
-            const uint32_t ds = d_it % NSD;
-            mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
+            const uint32_t ds = d_it % NSDt;
+            mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSDt) & 1) ^ 1);
             const uint32_t o0 = offs[g * K + k], o1 = offs[g * K + k + 1];
             mbar_expect_tx(bar(B_D_FULL + ds), o1 - o0);
             bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(B_D_FULL + ds));
@@ -1100,8 +1101,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       for (int k = 0; k < K; ++k) {
         for (int g = 0; g < nsub; ++g) {
           if (static_cast<int>(a_it % AGG_GROUPS) == grp) {
-            const uint32_t ds = d_it % NSD, as = a_it % NSA;
-            mbar_wait(bar(B_D_FULL + ds), (d_it / NSD) & 1);
+            const uint32_t ds = d_it % NSDt, as = a_it % NSA;
+            mbar_wait(bar(B_D_FULL + ds), (d_it / NSDt) & 1);
             if (wig == 0 && lane == 0) trace_ev(a.trace, d_it, 1);
             mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
             if (wig == 0 && lane == 0) trace_ev(a.trace, a_it, 2);
@@ -1206,6 +1207,7 @@ template <int NOUT>
 struct WgCfg {
   static constexpr int pairs = NOUT == 64 ? WG_PAIRS : 512 / NOUT;  // TMEM: pairs x NOUT columns
   static constexpr int nsg = NOUT == 256 ? 1 : WG_NSG;
+  static constexpr int nsd = WG_NSD;
   static constexpr uint32_t gbytes = NOUT * 256;  // 128 rows x NOUT bf16, 64-column blocks
 };
 struct WgSmem {
@@ -1224,7 +1226,7 @@ __host__ __device__ constexpr WgSmem wg_smem_layout(int hcap) {
   L.gt = o;
   o += WgCfg<NOUT>::nsg * WgCfg<NOUT>::gbytes;
   L.d = o;
-  o += WG_NSD * 2 * BLOCK_MAX_BYTES;
+  o += WgCfg<NOUT>::nsd * 2 * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
   L.bar = o;
   o += 24 * 8;
@@ -1257,7 +1259,7 @@ static_assert(wg_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
 template <int NOUT>
 __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   using Cfg = WgCfg<NOUT>;
-  constexpr int NP = Cfg::pairs, NSG = Cfg::nsg;
+  constexpr int NP = Cfg::pairs, NSG = Cfg::nsg, WNSD = Cfg::nsd;
   constexpr uint32_t GB = Cfg::gbytes;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -1284,7 +1286,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       mbar_init(bar(W_A_FULL + i), FWD_AGG_WARPS / WG_GROUPS);
       mbar_init(bar(W_A_EMPTY + i), 1);
     }
-    for (int i = 0; i < WG_NSD; ++i) {
+    for (int i = 0; i < WNSD; ++i) {
       mbar_init(bar(W_D_FULL + i), 1);
       mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS / WG_GROUPS);
     }
@@ -1315,8 +1317,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       for (int g = 0; g < nsub; ++g)
       for (int p = 0; p < n_pairs; ++p) {
         if (lane == 0) {
-          const uint32_t ds = d_it % WG_NSD;
-          mbar_wait(bar(W_D_EMPTY + ds), ((d_it / WG_NSD) & 1) ^ 1);
+          const uint32_t ds = d_it % WNSD;
+          mbar_wait(bar(W_D_EMPTY + ds), ((d_it / WNSD) & 1) ^ 1);
           const int k0 = g * K + k_begin + 2 * p;
           const uint32_t o0 = offs[k0], o1 = offs[k0 + 1];
           const uint32_t o2 = (k_begin + 2 * p + 1 < K) ? offs[k0 + 2] : o1;
@@ -1381,8 +1383,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       for (int g = 0; g < nsub; ++g)
       for (int p = 0; p < n_pairs; ++p) {
         if (static_cast<int>(a_it % WG_GROUPS) == grp) {
-          const uint32_t ds = d_it % WG_NSD, as = a_it % WG_NSA;
-          mbar_wait(bar(W_D_FULL + ds), (d_it / WG_NSD) & 1);
+          const uint32_t ds = d_it % WNSD, as = a_it % WG_NSA;
+          mbar_wait(bar(W_D_FULL + ds), (d_it / WNSD) & 1);
           mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
           const int ncell = (k_begin + 2 * p + 1 < K) ? 2 : 1;
           for (int half = 0; half < ncell; ++half)

@@ -111,6 +111,32 @@ def run_stack(layers, fin, math, steps, warmup):
     return time_steps(step, steps, warmup)
 
 
+def per_layer(layers, fin, math, steps):
+    """Device ms of each layer's forward + backward alone (same buffers)."""
+    cfg = npc.ExecConfig(math=math)
+    o = Oracle()
+    out = []
+    h = fin
+    for l in layers:
+        x = h if h.shape[2] == l.cin and h.shape[0] == l.n_in else \
+            torch.from_numpy(o.gen_features(l.n_in, 1, l.cin, 5)).cuda()
+        y = torch.empty((l.n_out, 1, l.cout), device="cuda")
+        g = torch.from_numpy(o.gen_features(l.n_out, 1, l.cout, 6)).cuda()
+        gi = torch.empty((l.n_in, 1, l.cin), device="cuda")
+        gw = torch.empty((27, 1, l.cin, l.cout), device="cuda")
+
+        def step():
+            npc.conv_forward(l.nb, l.w, x, cfg, out=y)
+            npc.conv_backward(l.nb, l.w, x, g, cfg, grad_in=gi, grad_w=gw)
+        ms, prof = time_steps(step, steps, 2)
+        st = l.nb.plan_stats() if (l.cin, l.cout) == (64, 64) else None
+        out.append({"name": l.name, "ms": round(ms, 4),
+                    "kernels": {k: round(v[1] / steps, 4) for k, v in prof.items() if v[1] / steps > 0.01},
+                    "plan": st})
+        h = y
+    return out
+
+
 def result(name, desc, unit_points, ms, prof, layers, bf16, extra):
     flop = sum(3 * 2 * l.nb.size * l.cin * l.cout for l in layers)
     return {"config": name, "workload": desc, "value": round(unit_points / (ms / 1e3) / 1e6, 3),
@@ -197,7 +223,8 @@ def main():
                        "64-128-256-128-64, fwd+bwd; Mpoints/s over input points",
                        n, ms, prof, layers, bf16,
                        {"levels": [c0.n_points(), c1.n_points(), c2.n_points()],
-                        "radii": [r0, r1, r2], "voxels": [v1, v2]})
+                        "radii": [r0, r1, r2], "voxels": [v1, v2],
+                        "per_layer": per_layer(layers, f, auto, a.steps)})
         else:
             raise SystemExit(f"unknown config {c}")
         r["setup_s"] = round(time.time() - t0, 2)
