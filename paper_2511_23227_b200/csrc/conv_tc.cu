@@ -1,28 +1,34 @@
 // conv_tc.cu -- tcgen05 / TMEM engines for the point-centric convolution
-// (bf16 operands, fp32 accumulate), C_in = C_out = 64, G = 1, K = t^3 <= 32.
+// (bf16 operands, fp32 accumulate), G = 1, C_in, C_out in {64, 128, 256},
+// K = t^3 <= 32.
 //
 // Formulation (output-stationary cell aggregation):
 //     F_out[i] = sum_k W_k^T A_k[i],   A_k[i] = sum_{j in N_k(i)} F_in[j]
 // Rows are processed in spatial (Morton) order in 128-row sub-tiles grouped
-// into super-tiles.  Per super-tile the union of all neighbor rows (the halo,
-// ~2.6x the rows at 384 rows/super-tile) is bulk-copied into shared memory
-// once; every A_k is then aggregated from shared memory (fp32 accumulate via
-// FHADD.BF16) into a SWIZZLE_128B K-major tile and multiplied on the tensor
-// core against W_k, which is loaded once per super-tile and cell (W traffic
-// amortised over 384 rows).  Accumulators live in TMEM (3 x 64 columns,
-// double-buffered); one epilogue store per output value, no atomics.
+// into super-tiles (2 x 128 rows when 64 channels are written, 1 x 128
+// otherwise).  Per super-tile the union of all neighbor rows (the halo,
+// ~2.9x the rows) is loaded into shared memory once per 64-channel chunk;
+// every A_k is then aggregated from shared memory (fp32 accumulate via
+// FHADD.BF16, rounded once) into a SWIZZLE_128B K-major tile and multiplied on
+// the tensor core against W_k (M128 x N{64,128,256} x K16 UMMAs), which is
+// loaded once per super-tile, chunk and cell.  Accumulators live in TMEM
+// (double-buffered); one epilogue store per output value, no atomics.
+// Dense or strided neighborhoods are re-tiled by the planner (128..8-row
+// tiles, then rank-split records accumulated in TMEM; see TcDirPlan).
 //
 //   forward   : rows = output points, gathered features = F_in, B = W_k
 //   dgrad     : rows = input points (transposed CSR), features = G_out, B = W_k^T
-//   wgrad     : rows = output points, A_k^T (MN-major, two cells stacked to
-//               M = 128) x dense G_out tile (MN-major) into per-cell TMEM
-//               accumulators; per-CTA partials reduced in a fixed order.
+//   wgrad     : rows = output points, A_k^T (MN-major, two (cell, C_in chunk)
+//               tiles stacked to M = 128) x dense G_out tile (MN-major) into
+//               per-pair TMEM accumulators; per-CTA partials reduced in a
+//               fixed order.
 //
-// Warp roles (fwd / dgrad kernel, 448 threads):
-//   warps 0-3  epilogue (TMEM lane quadrant = warp id)
-//   warp 4     producer: halo / W_k / stage-descriptor bulk copies
-//   warp 5     MMA issuer (one elected lane) + TMEM allocator
-//   warps 6-13 aggregation (quarter-warp per row, 4 rows per step)
+// Warp roles (fwd / dgrad kernel, 736 threads):
+//   warps 0-3   epilogue (TMEM lane quadrant = warp id) + L2 halo prefetch
+//   warp 4      producer: stage-descriptor bulk copies
+//   warp 5      MMA issuer (one elected lane) + TMEM allocator
+//   warps 6-21  aggregation (4 groups x 4 warps; quarter-warp per row)
+//   warp 22     producer: W_k bulk copies
 #include <cuda.h>
 #include <cuda_bf16.h>
 
