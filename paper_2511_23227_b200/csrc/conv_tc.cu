@@ -745,15 +745,17 @@ constexpr int FWD_ST = 2, FWD_HCAP = 928;  // 256-row super-tiles, halo <= 928 r
 constexpr int NSA = 4;  // A stages (16 KB)
 constexpr int NSW = 3;  // W stages (NOUT x 128 B; 2 for NOUT = 256)
 constexpr int NSD = 8;  // stage-descriptor slots
-// Wide outputs (NOUT = C_out of the pass, 128 or 256) use 128-row tiles: the
-// W stages grow to NOUT x 128 B and TMEM holds 2 x NOUT accumulator columns.
+// Wide outputs (NOUT = channels the pass writes): the W stages grow to
+// NOUT x 128 B (two stages, six descriptor slots); NOUT = 128 keeps the
+// 256-row super-tiles (TMEM 2 x 2 x 128 columns), NOUT = 256 uses 128-row
+// super-tiles (TMEM 2 x 256 columns) with a smaller halo.
 constexpr int FWD_HCAP1 = 672;  // halo rows of 128-row tiles (what fits beside 256-wide W stages)
 template <int NOUT>
 struct FwdCfg {
-  static constexpr int nsw = NOUT == 256 ? 2 : NSW;
-  static constexpr int nsd = NOUT == 256 ? 6 : NSD;  // descriptor slots
+  static constexpr int nsw = NOUT == 64 ? NSW : 2;
+  static constexpr int nsd = NOUT == 64 ? NSD : 6;  // descriptor slots
   static constexpr uint32_t wbytes = NOUT * 128;
-  static constexpr int st = NOUT == 64 ? FWD_ST : 1;
+  static constexpr int st = NOUT <= 128 ? FWD_ST : 1;
   static constexpr int acc_cols = st * NOUT;  // per TMEM buffer
   static constexpr uint32_t tmem_cols = 2 * acc_cols <= 256 ? 256 : 512;
 };
@@ -787,7 +789,7 @@ __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
 }
 
 static_assert(fwd_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
-static_assert(fwd_smem_layout<128>(FWD_HCAP1).total <= 232448, "smem");
+static_assert(fwd_smem_layout<128>(FWD_HCAP).total <= 232448, "smem");
 static_assert(fwd_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
 
 // Warm L2 with a super-tile's halo rows: one prefetch.global.L2 per 128-byte
@@ -1212,7 +1214,7 @@ constexpr int WG_GROUPS = 2;     // stage (cell pair) s is aggregated by warp gr
 template <int NOUT>
 struct WgCfg {
   static constexpr int pairs = NOUT == 64 ? WG_PAIRS : 512 / NOUT;  // TMEM: pairs x NOUT columns
-  static constexpr int nsg = NOUT == 256 ? 1 : WG_NSG;
+  static constexpr int nsg = NOUT == 64 ? WG_NSG : 1;
   static constexpr int nsd = WG_NSD;
   static constexpr uint32_t gbytes = NOUT * 256;  // 128 rows x NOUT bf16, 64-column blocks
 };
@@ -1259,7 +1261,7 @@ enum : int {
 static_assert(W_COUNT <= 24, "wgrad barrier region");
 
 static_assert(wg_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
-static_assert(wg_smem_layout<128>(FWD_HCAP1).total <= 232448, "smem");
+static_assert(wg_smem_layout<128>(FWD_HCAP).total <= 232448, "smem");
 static_assert(wg_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
 
 template <int NOUT>
@@ -2112,7 +2114,8 @@ static TcPlan* get_plan(npcg_context* ctx, npcg_neighbors* nb) {
   return nb->tc.get();
 }
 
-// wide = the pass writes more than 64 channels: 128-row super-tiles (st = 1)
+// wide = the pass writes 256 channels: 128-row super-tiles (st = 1); 64- and
+// 128-channel passes share the 256-row plan
 static TcDirPlan* plan_fwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = false) {
   TcPlan* p = get_plan(ctx, nb);
   auto& slot = wide ? p->fwd1 : p->fwd;
@@ -2262,7 +2265,7 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const flo
                          CH, fout);
     return;
   }
-  TcDirPlan* P = plan_fwd(ctx, nb, cout > CH);
+  TcDirPlan* P = plan_fwd(ctx, nb, cout > 2 * CH);
   TcPlan* p = nb->tc.get();
   if (P->n_overflow < P->n_super) {
     convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
@@ -2372,7 +2375,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
                            G->n_spill, wt.get(), gout, CH, CH, grad_in);
     }
   } else if (grad_in) {
-    TcDirPlan* P = plan_bwd(ctx, nb, cin > CH);
+    TcDirPlan* P = plan_bwd(ctx, nb, cin > 2 * CH);
     if (P->n_overflow < P->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
       g_converted = true;
@@ -2388,7 +2391,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     }
   }
   if (grad_w) {
-    TcDirPlan* P = plan_fwd(ctx, nb, cout > CH);  // same rows and gathers as the forward
+    TcDirPlan* P = plan_fwd(ctx, nb, cout > 2 * CH);  // same rows and gathers as the forward
     if (P->n_overflow == P->n_super) {
       wgrad_spill(ctx, nb, P, fin, gout, grad_w, false, cin, cout);
       return;
