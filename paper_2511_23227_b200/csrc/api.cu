@@ -263,6 +263,13 @@ npcg_status npcg_context_create(int device, void* stream, npcg_context** out) {
     ctx->num_sms = p.multiProcessorCount;
     ctx->max_smem_optin = static_cast<int>(p.sharedMemPerBlockOptin);
     ctx->stream = static_cast<cudaStream_t>(stream);
+    // stream-ordered allocations come from the device's default pool; keep
+    // freed blocks cached there (a caching allocator, like torch's) instead
+    // of returning them to the driver at every synchronisation
+    cudaMemPool_t pool;
+    NPCG_CUDA(cudaDeviceGetDefaultMemPool(&pool, device));
+    uint64_t keep = ~0ull;
+    NPCG_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep));
   });
   if (s != NPCG_OK) return s;
   *out = ctx.release();

@@ -588,6 +588,45 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     rank_level.push_back(to_rank ? 1 : 0);
   }
   P->levels = static_cast<int>(lv.size());
+  if (lv.size() == 1) {  // one level: adopt its buffers as they are
+    PlanLevel& L = lv[0];
+    P->n_super = static_cast<int>(L.sup.size());
+    P->n_sub = static_cast<int>(L.tiles.size());
+    P->halo = std::move(L.halo);
+    P->runs = std::move(L.runs);
+    P->n_runs = std::move(L.n_runs);
+    P->halo_len = std::move(L.halo_len);
+    P->blk_off = std::move(L.blk_off);
+    P->blocks = std::move(L.blocks);
+    std::vector<uint2> sup_all(L.sup.size());
+    std::vector<uint32_t> items(L.sup.size() + 1);
+    double sum = 0;
+    for (size_t x = 0; x < L.sup.size(); ++x) {
+      sup_all[x] = make_uint2(L.sup[x].x, (L.sup[x].y & 0xFFu) | SUP_FIRST | SUP_LAST);
+      items[x] = static_cast<uint32_t>(x);
+      if (L.hl[x] == kOverflow) {
+        P->n_overflow++;
+      } else {
+        P->max_halo = std::max<int>(P->max_halo, static_cast<int>(L.hl[x]));
+        sum += L.hl[x];
+      }
+    }
+    items[L.sup.size()] = static_cast<uint32_t>(L.sup.size());
+    P->n_items = static_cast<int>(L.sup.size());
+    P->item_start.alloc(ctx, items.size());
+    P->sup.alloc(ctx, P->n_super);
+    P->tiles.alloc(ctx, P->n_sub);
+    NPCG_CUDA(cudaMemcpyAsync(P->item_start.get(), items.data(), items.size() * 4,
+                              cudaMemcpyHostToDevice, ctx->stream));
+    NPCG_CUDA(cudaMemcpyAsync(P->sup.get(), sup_all.data(), sup_all.size() * sizeof(uint2),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    NPCG_CUDA(cudaMemcpyAsync(P->tiles.get(), L.tiles.data(), L.tiles.size() * sizeof(uint2),
+                              cudaMemcpyHostToDevice, ctx->stream));
+    const int ok = P->n_super - P->n_overflow;
+    P->mean_halo = ok ? sum / ok : 0.0;
+    NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    return P;
+  }
   // concatenate the levels
   int64_t ns = 0, nt = 0, bytes = 0;
   for (auto& L : lv) {
