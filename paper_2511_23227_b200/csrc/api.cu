@@ -81,8 +81,9 @@ bool use_tc(const npcg_exec_config* cfg, npcg_dtype dtype, int64_t G, int64_t ci
   if (cfg->math == NPCG_MATH_EXACT) return false;
   if (cfg->math == NPCG_MATH_BF16) {
     if (dtype != NPCG_F32) fail(NPCG_ERR_UNSUPPORTED, "bf16 math requires F32 tensors");
-    if (!tc_supported(G, cin, cout, K))
-      fail(NPCG_ERR_UNSUPPORTED, "bf16 tensor-core path needs G=1, C_in, C_out in {64,128,256}, K<=32");
+    if (!tc_supported(G, cin, cout, K, true))
+      fail(NPCG_ERR_UNSUPPORTED,
+           "bf16 tensor-core path needs G=1, C_in, C_out multiples of 16 up to 256, K<=32");
     return true;
   }
   return dtype == NPCG_F32 && tc_supported(G, cin, cout, K);
@@ -687,7 +688,7 @@ npcg_status npcg_vvor(npcg_context* ctx, npcg_dtype dtype, const void* gout, int
       backward_impl(ctx, nb.get(), dtype, nullptr, groups, c_in, c_out, fin, gout, cfg, nullptr,
                     grad);
     } else {
-      if (cfg->math == NPCG_MATH_BF16) fail(NPCG_ERR_UNSUPPORTED, "bf16 vvor needs K = t^3, G=1, C in {64,128,256}");
+      if (cfg->math == NPCG_MATH_BF16) fail(NPCG_ERR_UNSUPPORTED, "bf16 vvor needs K = t^3, G=1, C multiples of 16 up to 256");
       CellPlan cells;
       cells_from_triplets(ctx, T, n_kernels, &cells);
       if (dtype == NPCG_F32)

@@ -96,6 +96,7 @@ struct TcPlan {
   DevBuf<uint32_t> inv_perm_out, inv_perm_in;
   DevBuf<__nv_bfloat16> feat_in;   // bf16 F_in in perm_in order
   const void* saved_fin = nullptr;  // fin whose image feat_in holds (set by the forward)
+  int saved_c = 0;                  // and its channel count
   DevBuf<__nv_bfloat16> feat_out;  // bf16 G_out in perm_out order
   DevBuf<uint8_t> wpack;           // K x nci images of C x 128 B, SW128 K-major B operand
   DevBuf<float> partial;           // wgrad per-CTA partials
@@ -103,9 +104,17 @@ struct TcPlan {
 
 void destroy_tc_plan(TcPlan* p);
 
-static bool tc_width(int64_t c) { return c == 64 || c == 128 || c == 256; }
-bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K) {
-  return G == 1 && tc_width(cin) && tc_width(cout) && K >= 1 && K <= KMAX;
+// Channel widths run on the tensor cores padded to 64 / 128 / 256 (zero
+// channels in the bf16 images and packed weights; outputs written unpadded).
+// The automatic choice keeps narrow layers (C < 64, where the contraction is
+// not dense enough to pay for the padding) on the CUDA-core engines;
+// math = bf16 forces the tensor cores for any multiple of 16 up to 256.
+static bool tc_width(int64_t c, bool forced) {
+  return c >= (forced ? 16 : 64) && c <= 256 && c % 16 == 0;
+}
+static int tc_pad(int c) { return c <= 64 ? 64 : c <= 128 ? 128 : 256; }
+bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K, bool forced) {
+  return G == 1 && tc_width(cin, forced) && tc_width(cout, forced) && K >= 1 && K <= KMAX;
 }
 
 // ===========================================================================
@@ -711,14 +720,19 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
 // ===========================================================================
 // operand preparation
 // ===========================================================================
-// dst[p][c] = bf16(src[perm[p]][c]), C channels (C % 8 == 0), 8 per thread.
+// dst[p][c] = bf16(src[perm[p]][c]) for c < C, 0 for C <= c < CP (C % 8 == 0),
+// 8 channels per thread.
 __global__ void k_to_bf16_perm(const float* __restrict__ src, const uint32_t* __restrict__ perm,
-                               int64_t n, int C, __nv_bfloat16* __restrict__ dst) {
+                               int64_t n, int C, int CP, __nv_bfloat16* __restrict__ dst) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
-  const int qn = C >> 3;
+  const int qn = CP >> 3;
   if (x >= n * qn) return;
   const int64_t p = x / qn;
   const int q = static_cast<int>(x % qn);
+  if (q * 8 >= C) {
+    reinterpret_cast<uint4*>(dst + p * CP)[q] = make_uint4(0, 0, 0, 0);
+    return;
+  }
   const float4* s = reinterpret_cast<const float4*>(src + static_cast<int64_t>(perm[p]) * C + q * 8);
   const float4 a = __ldg(s), b = __ldg(s + 1);
   uint4 o;
@@ -726,20 +740,20 @@ __global__ void k_to_bf16_perm(const float* __restrict__ src, const uint32_t* __
   o.y = pack_bf16x2(a.z, a.w);
   o.z = pack_bf16x2(b.x, b.y);
   o.w = pack_bf16x2(b.z, b.w);
-  reinterpret_cast<uint4*>(dst + p * C)[q] = o;
+  reinterpret_cast<uint4*>(dst + p * CP)[q] = o;
 }
 
 // B operand images (SW128 K-major), one per (cell, 64-wide chunk of the
 // reduction dim), N x 128 B each.  transpose=false: N = C_out rows, reduction
 // over C_in (forward); transpose=true: N = C_in rows, reduction over C_out (dgrad).
-__global__ void k_pack_w(const float* __restrict__ w, int K, int cin, int cout, bool transpose,
-                         uint8_t* __restrict__ out) {
+__global__ void k_pack_w(const float* __restrict__ w, int K, int cin, int cout, int cinp,
+                         int coutp, bool transpose, uint8_t* __restrict__ out) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= static_cast<int64_t>(K) * cin * cout) return;
   const int k = static_cast<int>(x / (cin * cout)), rem = static_cast<int>(x % (cin * cout));
   const int c = rem / cout, m = rem % cout;  // W[k][c][m]
   const int n = transpose ? c : m, r = transpose ? m : c;  // B row, reduction index
-  const int N = transpose ? cin : cout, nchunk = (transpose ? cout : cin) / CH;
+  const int N = transpose ? cinp : coutp, nchunk = (transpose ? coutp : cinp) / CH;
   const int64_t img = static_cast<int64_t>(k) * nchunk + r / CH;
   reinterpret_cast<__nv_bfloat16*>(out + img * N * 128 + sw128_off(n, r % CH))[0] =
       __float2bfloat16_rn(w[x]);
@@ -765,7 +779,8 @@ struct FwdArgs {
   int nci;                    // 64-channel chunks of the gathered features
   const __nv_bfloat16* feat;  // bf16 (n_cols, 64 nci), permuted
   const uint8_t* wpack;       // (K x nci) images of NOUT x 128 B
-  float* out;                 // (n_rows, NOUT), original order
+  float* out;                 // (n_rows, ncols), original order
+  int ncols;                  // channels written per row (<= NOUT; the rest is padding)
   long long* trace;           // debug: per-stage event clocks of CTA 0 (nullptr = off)
 };
 constexpr int TRACE_STAGES = 512;
@@ -1193,10 +1208,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         const uint2 tl = a.tiles[sp.x + g];
         const int64_t row = static_cast<int64_t>(tl.x) + 32 * e + lane;
         float4* o = static_cast<uint32_t>(32 * e + lane) < tl.y
-                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * NOUT)
+                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * a.ncols)
                         : nullptr;
 #pragma unroll 4
         for (int q = 0; q < NOUT / 16; ++q) {
+          if (q * 16 >= a.ncols) break;
           uint32_t v[16];
           tmem_ld16(t0 + 16 * q, v);
           tmem_ld_wait();
@@ -1519,14 +1535,14 @@ done:
 
 // grad_w[k][m][c] = sum over CTAs x (fixed order) of partial[x][k][c][m]
 __global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, int K, int cin,
-                               int cout, float* __restrict__ grad_w) {
+                               int cout, int cinp, int coutp, float* __restrict__ grad_w) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (k, m, c)
   if (idx >= static_cast<int64_t>(K) * cin * cout) return;
   const int k = static_cast<int>(idx / (cin * cout)), m = static_cast<int>((idx / cin) % cout),
             c = static_cast<int>(idx % cin);
   float s = 0.f;
   for (int x = 0; x < n_part; ++x)
-    s += partial[((static_cast<int64_t>(x) * K + k) * cin + c) * cout + m];
+    s += partial[((static_cast<int64_t>(x) * K + k) * cinp + c) * coutp + m];
   grad_w[idx] = s;
 }
 
@@ -2191,20 +2207,26 @@ void tc_prepare(npcg_context* ctx, npcg_neighbors* nb) {
   plan_bwd(ctx, nb);
 }
 
+// bf16 image of C-channel rows, padded with zero channels to CP = tc_pad(C)
 static void convert(npcg_context* ctx, const float* src, const uint32_t* perm, int64_t n,
                     DevBuf<__nv_bfloat16>& dst, int C = CH) {
-  if (dst.size() < n * C) dst.alloc(ctx, n * C);
+  const int CP = tc_pad(C);
+  if (dst.size() < n * CP) dst.alloc(ctx, n * CP);
   if (n == 0) return;
-  launch(ctx, "to_bf16_perm", k_to_bf16_perm, dim3(static_cast<unsigned>(ceil_div(n * (C / 8), 256))),
-         dim3(256), 0, src, perm, n, C, dst.get());
+  launch(ctx, "to_bf16_perm", k_to_bf16_perm, dim3(static_cast<unsigned>(ceil_div(n * (CP / 8), 256))),
+         dim3(256), 0, src, perm, n, C, CP, dst.get());
 }
 
 static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose,
                    int cin = CH, int cout = CH) {
+  const int cinp = tc_pad(cin), coutp = tc_pad(cout);
   const int64_t n = static_cast<int64_t>(K) * cin * cout;
-  if (p->wpack.size() < n * 2) p->wpack.alloc(ctx, n * 2);
+  const int64_t bytes = static_cast<int64_t>(K) * cinp * coutp * 2;
+  if (p->wpack.size() < bytes) p->wpack.alloc(ctx, bytes);
+  if (cinp != cin || coutp != cout)
+    NPCG_CUDA(cudaMemsetAsync(p->wpack.get(), 0, bytes, ctx->stream));
   launch(ctx, "pack_w", k_pack_w, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256), 0, w,
-         K, cin, cout, transpose, p->wpack.get());
+         K, cin, cout, cinp, coutp, transpose, p->wpack.get());
 }
 
 template <int NOUT>
@@ -2221,6 +2243,10 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
                            const uint8_t* wpack, const uint32_t* perm_rows, float* out,
                            const char* name, long long* trace = nullptr, int cin_g = CH,
                            int nout = CH) {
+  // cin_g / nout: real gathered / written channels; the kernel runs padded
+  const int ncols = nout;
+  cin_g = tc_pad(cin_g);
+  nout = tc_pad(nout);
   if (P->n_super == 0) return;
   FwdArgs a{};
   a.halo = P->halo.get();
@@ -2244,6 +2270,7 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   a.feat = feat;
   a.wpack = wpack;
   a.out = out;
+  a.ncols = ncols;
   a.trace = trace;
   const int grid = std::min(P->n_super, ctx->num_sms);
   if (nout == 64) launch_fwd<64>(ctx, a, P->hcap, grid, name);
@@ -2295,6 +2322,7 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const flo
     if (G->n_overflow < G->n_super) {
       convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
       p->saved_fin = fin;  // PointConvOp saves its input at forward (conv_op.hpp:138)
+      p->saved_c = CH;
       pack_w(ctx, p, w, G->K, false);
       run_gather_kernel(ctx, G, p->feat_in.get(), nb->n_in, p->wpack.get(), nb->perm_out.get(),
                         fout, "conv_fwd_tc");
@@ -2304,11 +2332,12 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const flo
                          CH, fout);
     return;
   }
-  TcDirPlan* P = plan_fwd(ctx, nb, cout > 2 * CH);
+  TcDirPlan* P = plan_fwd(ctx, nb, tc_pad(cout) > 2 * CH);
   TcPlan* p = nb->tc.get();
   if (P->n_overflow < P->n_super) {
     convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
-    p->saved_fin = cin == CH ? fin : nullptr;  // PointConvOp saves its input (conv_op.hpp:138)
+    p->saved_fin = fin;  // PointConvOp saves its input (conv_op.hpp:138)
+    p->saved_c = cin;
     pack_w(ctx, p, w, P->K, false, cin, cout);
     run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
                    "conv_fwd_tc", nullptr, cin, cout);
@@ -2414,7 +2443,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
                            G->n_spill, wt.get(), gout, CH, CH, grad_in);
     }
   } else if (grad_in) {
-    TcDirPlan* P = plan_bwd(ctx, nb, cin > 2 * CH);
+    TcDirPlan* P = plan_bwd(ctx, nb, tc_pad(cin) > 2 * CH);
     if (P->n_overflow < P->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
       g_converted = true;
@@ -2430,25 +2459,27 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     }
   }
   if (grad_w) {
-    TcDirPlan* P = plan_fwd(ctx, nb, cout > 2 * CH);  // same rows and gathers as the forward
+    TcDirPlan* P = plan_fwd(ctx, nb, tc_pad(cout) > 2 * CH);  // same rows and gathers as the forward
     if (P->n_overflow == P->n_super) {
       wgrad_spill(ctx, nb, P, fin, gout, grad_w, false, cin, cout);
       return;
     }
     // the bf16 input image saved by the forward on this handle is reused when
     // the backward is handed the same input (the operator's saved copy)
-    if (fin != p->saved_fin) {
+    if (fin != p->saved_fin || cin != p->saved_c) {
       convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
-      p->saved_fin = cin == CH ? fin : nullptr;
+      p->saved_fin = fin;
+      p->saved_c = cin;
     }
     if (!g_converted) convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
-    const int nci = cin / CH;
-    const int np = cout == 64 ? WgCfg<64>::pairs : cout == 128 ? WgCfg<128>::pairs : WgCfg<256>::pairs;
+    const int cinp = tc_pad(cin), coutp = tc_pad(cout);
+    const int nci = cinp / CH;
+    const int np = coutp == 64 ? WgCfg<64>::pairs : coutp == 128 ? WgCfg<128>::pairs : WgCfg<256>::pairs;
     const int gpc = (K + 2 * np - 1) / (2 * np);  // cell groups per C_in chunk
     const int groups = nci * gpc;
     // one CTA per SM in total over (super-tile slices x groups)
     const int gx = std::max(1, std::min(P->n_super, ctx->num_sms / groups));
-    const int64_t need = static_cast<int64_t>(gx) * K * cin * cout;
+    const int64_t need = static_cast<int64_t>(gx) * K * cinp * coutp;
     if (p->partial.size() < need) p->partial.alloc(ctx, need);
     NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
     WgArgs a{};
@@ -2472,12 +2503,13 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     a.dense = p->feat_out.get();
     a.partial = p->partial.get();
     const dim3 grid(gx, groups);
-    if (cout == 64) launch_wgrad<64>(ctx, a, P->hcap, grid);
-    else if (cout == 128) launch_wgrad<128>(ctx, a, P->hcap, grid);
+    if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid);
+    else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid);
     else launch_wgrad<256>(ctx, a, P->hcap, grid);
     const int64_t nw = static_cast<int64_t>(K) * cin * cout;
     launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(nw, 256))),
-           dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, grad_w);
+           dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, cinp, coutp,
+           grad_w);
     if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true, cin, cout);
   }
 }
@@ -2492,6 +2524,7 @@ void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, con
     GatherPlan* G = gplan_fwd(ctx, nb);
     convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
     p->saved_fin = fin;
+    p->saved_c = CH;
     pack_w(ctx, p, w, G->K, false);
     run_gather_kernel(ctx, G, p->feat_in.get(), nb->n_in, p->wpack.get(), nb->perm_out.get(), fout,
                       "conv_fwd_tc_traced", tr.get());
@@ -2499,6 +2532,7 @@ void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, con
     TcDirPlan* P = plan_fwd(ctx, nb);
     convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
     p->saved_fin = fin;
+    p->saved_c = CH;
     pack_w(ctx, p, w, P->K, false);
     run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
                    "conv_fwd_tc_traced", tr.get());

@@ -92,7 +92,8 @@ def test_strided_two_cloud_forward(npc, orc, ref):
 
 
 def test_c1_forward_parity(npc, orc):
-    """BASELINE config 1: 16K points, C=32, fp32 exact vs the fp64 oracle."""
+    """BASELINE config 1: 16K points, C=32, fp32 exact vs the fp64 oracle (the
+    automatic engine choice keeps C < 64 on the CUDA cores)."""
     n = 16384
     xyz = orc.gen_uniform_cube(n, 1.0, 1)
     r = 1.8 * n ** (-1 / 3)
@@ -242,12 +243,14 @@ def test_bf16_clustered_cloud(npc, orc, ref, cin, cout):
 
 
 @pytest.mark.parametrize("cin,cout", [(64, 128), (128, 64), (128, 128), (256, 256), (64, 256),
-                                      (256, 128)])
+                                      (256, 128), (32, 32), (48, 80), (96, 160), (16, 256)])
 def test_bf16_wide_channels(npc, orc, cin, cout):
     """C_in, C_out in {64, 128, 256} on the tensor-core engines: forward /
     input gradient gather 64-channel chunks accumulated in TMEM with up to 256
     output columns per tile; the weight gradient pairs (cell, C_in chunk) A
-    tiles against G tiles of C_out columns."""
+    tiles against G tiles of C_out columns.  Other multiples of 16 are
+    zero-padded to 64 / 128 / 256 (math = bf16 forces narrow widths onto the
+    tensor cores; the automatic choice keeps C < 64 on the exact engines)."""
     n = 6000
     xyz = orc.gen_uniform_cube(n, 1.0, 31)
     r = 1.8 * n ** (-1 / 3)
