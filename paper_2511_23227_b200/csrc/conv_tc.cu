@@ -48,8 +48,12 @@ constexpr int TM = 128;
 constexpr int CH = 64;
 constexpr int KMAX = 32;
 constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sorts in smem
-constexpr int MAX_BLOCK_ENTRIES = 768;   // entries per (sub-tile, cell) block
-constexpr int BLOCK_MAX_BYTES = 512 + 2 * MAX_BLOCK_ENTRIES;
+// A (sub-tile, cell) descriptor block: u32 item[128] | u16 entry[E].  Its
+// first BLOCK_MAX_BYTES (items + up to 768 entries) are staged in a shared-
+// memory slot; the entries of larger blocks are read from L2 (global).
+constexpr int SLOT_ENTRIES = 768;
+constexpr int BLOCK_MAX_BYTES = 512 + 2 * SLOT_ENTRIES;
+constexpr int MAX_BLOCK_ENTRIES = 8192;  // planner cap per block
 constexpr uint32_t kOverflow = 0xFFFFFFFFu;
 constexpr uint32_t SUP_FIRST = 1u << 8, SUP_LAST = 1u << 9;  // record flags in sup[].y
 
@@ -68,6 +72,7 @@ struct TcDirPlan {
   int64_t n_rows = 0, n_cols = 0;
   int n_sub = 0, n_super = 0, K = 0;  // n_sub = sub-tiles over all levels
   int levels = 0;
+  bool big_blocks = false;    // some descriptor block exceeds its shared-memory slot
   DevBuf<uint2> sup;          // n_super records {first sub-tile, sub-tiles | SUP_FIRST | SUP_LAST}
   DevBuf<uint32_t> item_start;  // n_items + 1 (records of an item share rows, accumulate)
   int n_items = 0;
@@ -146,7 +151,8 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
                                                     const uint2* __restrict__ tfilter, int K,
                                                     uint32_t* __restrict__ blk_size,
                                                     uint32_t* __restrict__ sub_bad,
-                                                    uint32_t* __restrict__ tile_maxc) {
+                                                    uint32_t* __restrict__ tile_maxc,
+                                                    uint32_t* __restrict__ max_blk) {
   __shared__ uint32_t cnt[KMAX];
   __shared__ uint16_t rc[TM][KMAX];   // all entries seen per (row, cell)
   __shared__ uint16_t inc[TM][KMAX];  // entries within the rank filter
@@ -184,7 +190,9 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
   if (r < K) {
     const uint32_t E = cnt[r];
     if (E > MAX_BLOCK_ENTRIES) bad = 1;
-    blk_size[static_cast<int64_t>(blockIdx.x) * K + r] = 512u + ((2u * E + 15u) / 16u) * 16u;
+    const uint32_t bytes = 512u + ((2u * E + 15u) / 16u) * 16u;
+    blk_size[static_cast<int64_t>(blockIdx.x) * K + r] = bytes;
+    atomicMax(max_blk, bytes);
   }
   __syncthreads();
   if (r == 0) {
@@ -463,6 +471,7 @@ struct PlanLevel {
   DevBuf<uint2> runs;
   DevBuf<uint8_t> blocks;
   uint32_t block_bytes = 0;
+  uint32_t max_blk = 0;      // largest descriptor block (bytes)
   std::vector<uint32_t> hl;  // halo_len on the host
 };
 
@@ -472,7 +481,8 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   const int ns = static_cast<int>(L.sup.size()), nt = static_cast<int>(L.tiles.size());
   if (L.tfilter.empty()) L.tfilter.assign(nt, make_uint2(0, 0xFFFFFFFFu));
   DevBuf<uint2> d_sup(ctx, ns), d_tiles(ctx, nt), d_filt(ctx, nt);
-  DevBuf<uint32_t> d_maxc(ctx, nt);
+  DevBuf<uint32_t> d_maxc(ctx, nt), d_maxblk(ctx, 1);
+  NPCG_CUDA(cudaMemsetAsync(d_maxblk.get(), 0, 4, ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(d_sup.get(), L.sup.data(), ns * sizeof(uint2), cudaMemcpyHostToDevice,
                             ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(d_tiles.get(), L.tiles.data(), nt * sizeof(uint2),
@@ -484,7 +494,7 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   NPCG_CUDA(cudaMemsetAsync(blk_size.get() + nblk, 0, 4, ctx->stream));
   launch(ctx, "plan_counts", k_plan_counts, dim3(nt), dim3(TM), 0, row_ptr, kk, perm_rows,
          static_cast<const uint2*>(d_tiles.get()), static_cast<const uint2*>(d_filt.get()), K,
-         blk_size.get(), sub_bad.get(), d_maxc.get());
+         blk_size.get(), sub_bad.get(), d_maxc.get(), d_maxblk.get());
   L.blk_off.alloc(ctx, nblk + 1);
   exclusive_scan_u32(ctx, blk_size.get(), L.blk_off.get(), nblk + 1, &L.block_bytes);
   L.blocks.alloc(ctx, L.block_bytes);
@@ -507,6 +517,7 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
                             ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(L.maxc.data(), d_maxc.get(), nt * 4, cudaMemcpyDeviceToHost,
                             ctx->stream));
+  NPCG_CUDA(cudaMemcpyAsync(&L.max_blk, d_maxblk.get(), 4, cudaMemcpyDeviceToHost, ctx->stream));
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -539,6 +550,20 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   // any record fits the halo: 8 rows x K cells x Q <= hcap).
   std::vector<uint32_t> spill;
   std::vector<uint8_t> rank_level{0};  // per level: records are rank splits
+  // rank step that always fits (8 rows x K cells x Q entries <= hcap halo
+  // rows, <= 768 block entries) and the optimistic first step
+  const uint32_t q_safe = std::max<uint32_t>(1, static_cast<uint32_t>(hcap) / (8u * K));
+  const uint32_t q_first = std::max<uint32_t>(q_safe, 64);
+  // one item of rank-split records over a tile's rows
+  auto push_rank_item = [](PlanLevel& nx, uint2 tile, uint32_t maxc, uint32_t Q) {
+    const uint32_t nq = std::max<uint32_t>(1, (maxc + Q - 1) / Q);
+    for (uint32_t q = 0; q < nq; ++q) {
+      const uint32_t fl = (q == 0 ? SUP_FIRST : 0u) | (q + 1 == nq ? SUP_LAST : 0u);
+      nx.sup.push_back(make_uint2(static_cast<uint32_t>(nx.tiles.size()), 1u | fl));
+      nx.tiles.push_back(tile);
+      nx.tfilter.push_back(make_uint2(q * Q, (q + 1) * Q));
+    }
+  };
   uint32_t cur = TM;                // rows per sub-tile at this level
   for (int level = 0;; ++level) {
     PlanLevel& L = lv[level];
@@ -546,7 +571,11 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     const bool is_rank = rank_level[level] != 0;
     PlanLevel next;
     if (is_rank) {
-      // an item fails as a whole: its rows go to the exact engine
+      // an item fails as a whole: it is split again with a smaller rank step
+      // (down to the step that always fits), else its rows go to the exact engine
+      const uint32_t q_now = L.tfilter[0].y - L.tfilter[0].x;
+      const uint32_t q_next = q_now > q_safe ? std::max(q_safe, q_now / 4) : 0;
+      PlanLevel again;
       for (size_t x = 0; x < L.sup.size();) {
         size_t y = x + 1;
         while (y < L.sup.size() && !(L.sup[y].y & SUP_FIRST)) ++y;
@@ -554,7 +583,11 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
         for (size_t z = x; z < y; ++z) bad |= L.hl[z] == kOverflow;
         if (bad) {
           const uint2 tl = L.tiles[L.sup[x].x];
-          for (uint32_t p = tl.x; p < tl.x + tl.y; ++p) spill.push_back(p);
+          if (q_next) {
+            push_rank_item(again, tl, L.maxc[L.sup[x].x], q_next);
+          } else {
+            for (uint32_t p = tl.x; p < tl.x + tl.y; ++p) spill.push_back(p);
+          }
           for (size_t z = x; z < y; ++z) L.hl[z] = kOverflow;
           std::vector<uint32_t> ov(y - x, kOverflow);
           NPCG_CUDA(cudaMemcpyAsync(L.halo_len.get() + x, ov.data(), ov.size() * 4,
@@ -563,12 +596,14 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
         }
         x = y;
       }
-      break;
+      if (again.sup.empty()) break;
+      lv.push_back(std::move(again));
+      rank_level.push_back(1);
+      continue;
     }
     const uint32_t sz = level == 0 && st > 1 ? TM : cur / 2;
     cur = sz;
     const bool to_rank = sz < 8;
-    const uint32_t Q = std::max<uint32_t>(1, static_cast<uint32_t>(hcap) / (8u * K));
     for (size_t x = 0; x < L.sup.size(); ++x) {
       if (L.hl[x] != kOverflow) continue;
       const uint2 sp = L.sup[x];
@@ -578,13 +613,7 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
       if (to_rank) {
         uint32_t maxc = 0;
         for (uint32_t t = sp.x; t < sp.x + (sp.y & 0xFFu); ++t) maxc = std::max(maxc, L.maxc[t]);
-        const uint32_t nq = std::max<uint32_t>(1, (maxc + Q - 1) / Q);
-        for (uint32_t q = 0; q < nq; ++q) {
-          const uint32_t fl = (q == 0 ? SUP_FIRST : 0u) | (q + 1 == nq ? SUP_LAST : 0u);
-          next.sup.push_back(make_uint2(static_cast<uint32_t>(next.tiles.size()), 1u | fl));
-          next.tiles.push_back(make_uint2(a, b - a));
-          next.tfilter.push_back(make_uint2(q * Q, (q + 1) * Q));
-        }
+        push_rank_item(next, make_uint2(a, b - a), maxc, q_first);
         continue;
       }
       for (uint32_t p = a; p < b; p += sz) {
@@ -597,6 +626,18 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     rank_level.push_back(to_rank ? 1 : 0);
   }
   P->levels = static_cast<int>(lv.size());
+  for (const PlanLevel& L : lv) P->big_blocks |= L.max_blk > static_cast<uint32_t>(BLOCK_MAX_BYTES);
+  if (std::getenv("NPCG_PLAN_DEBUG")) {  // planner instrumentation (stderr)
+    std::fprintf(stderr, "[npcg plan] rows %lld st %d hcap %d:", static_cast<long long>(n_rows), st, hcap);
+    for (size_t li = 0; li < lv.size(); ++li) {
+      size_t bad = 0;
+      for (uint32_t h : lv[li].hl) bad += h == kOverflow;
+      std::fprintf(stderr, " L%zu%s %zu recs (%zu tiles of %u rows) %zu failed;", li,
+                   rank_level[li] ? "(rank)" : "", lv[li].sup.size(), lv[li].tiles.size(),
+                   lv[li].tiles.empty() ? 0u : lv[li].tiles[0].y, bad);
+    }
+    std::fprintf(stderr, " spill rows %zu\n", spill.size());
+  }
   if (lv.size() == 1) {  // one level: adopt its buffers as they are
     PlanLevel& L = lv[0];
     P->n_super = static_cast<int>(L.sup.size());
@@ -837,7 +878,7 @@ __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
   L.tmem_slot = o;
   o += 16;
   L.offs = o;
-  o += 128 * 4;
+  o += 128 * 4;  // block offsets of the super-tile; [96, 128): slot sources
   L.total = o + 1024;  // alignment slack
   return L;
 }
@@ -889,6 +930,11 @@ __device__ __forceinline__ void load_halo(const uint2* runs, uint32_t nr,
   }
 }
 
+// Entries of a staged block are in the slot, or in global memory (L2) when
+// the block did not fit (src = its byte offset, kFitsSlot when it fit).  The
+// L2 variant is an out-of-line call, keeping the hot loop's code compact.
+constexpr uint32_t kFitsSlot = 0xFFFFFFFFu;
+
 // barrier indices
 enum : int {
   B_HALO_FULL = 0,
@@ -913,11 +959,10 @@ static_assert(B_COUNT <= 48, "barrier region");
 // (FHADD.BF16) rounded once to bf16.  All loads of the warp's quads are issued
 // before their uses (ILP), stores go to the SW128 K-major A tile.
 template <int NW>
-__device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_halo, uint32_t s_A,
-                                                int wig, int lane) {
+__device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16_t* ents,
+                                                uint32_t s_halo, uint32_t s_A, int wig, int lane) {
   constexpr int NQ = (TM / 4) / NW;  // quads per warp, round-robin over count-sorted items
   const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
-  const uint16_t* ents = reinterpret_cast<const uint16_t*>(blk + 512);
   const int sub_l = lane >> 3;
   const uint32_t l8x16 = static_cast<uint32_t>(lane & 7) << 4;
   uint32_t it[NQ], cm[NQ];
@@ -979,12 +1024,19 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, uint32_t s_h
     }
   }
 }
+template <int NW>
+__device__ __noinline__ void aggregate_stage_l2(const uint8_t* blk, const uint16_t* ents,
+                                                uint32_t s_halo, uint32_t s_A, int wig, int lane) {
+  aggregate_stage<NW>(blk, ents, s_halo, s_A, wig, lane);
+}
 
 // Input channels come in a.nci chunks of 64: each super-tile runs the cells
 // once per chunk (the halo reloaded with that chunk's 128-byte row slices),
 // all accumulating into the same TMEM accumulators; W_k is packed per (cell,
 // chunk) as an NOUT x 64 image.
-template <int NOUT>
+// BIG: the plan has descriptor blocks beyond the shared-memory slot (their
+// entries are read from L2); plans without them run the leaner variant.
+template <int NOUT, bool BIG>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   using Cfg = FwdCfg<NOUT>;
   constexpr int NSWt = Cfg::nsw, NSDt = Cfg::nsd;
@@ -1000,6 +1052,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
   const uint8_t* g_d = gbase + L.d;
+  uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + 96;  // per descriptor slot
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -1050,8 +1103,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             const uint32_t ds = d_it % NSDt;
             mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSDt) & 1) ^ 1);
             const uint32_t o0 = offs[g * K + k], o1 = offs[g * K + k + 1];
-            mbar_expect_tx(bar(B_D_FULL + ds), o1 - o0);
-            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(B_D_FULL + ds));
+            const uint32_t nb = min(o1 - o0, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+            if (BIG) dsrc[ds] = o1 - o0 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
+            mbar_expect_tx(bar(B_D_FULL + ds), nb);
+            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, nb, bar(B_D_FULL + ds));
             trace_ev(a.trace, d_it, 0);
           }
           ++d_it;
@@ -1168,8 +1223,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             if (wig == 0 && lane == 0) trace_ev(a.trace, d_it, 1);
             mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
             if (wig == 0 && lane == 0) trace_ev(a.trace, a_it, 2);
-            aggregate_stage<AGG_GROUP_WARPS>(g_d + ds * BLOCK_MAX_BYTES, s_halo,
-                                             s_a + as * 16384u, wig, lane);
+            const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
+            const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
+            if (src == kFitsSlot)  // (separate instantiations keep shared-memory loads)
+              aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512),
+                                               s_halo, s_a + as * 16384u, wig, lane);
+            else
+              aggregate_stage_l2<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512),
+                                                  s_halo, s_a + as * 16384u, wig, lane);
             fence_proxy_async_smem();
             __syncwarp();
             if (wig == 0 && lane == 0) trace_ev(a.trace, a_it, 3);
@@ -1296,7 +1357,7 @@ __host__ __device__ constexpr WgSmem wg_smem_layout(int hcap) {
   L.tmem_slot = o;
   o += 16;
   L.offs = o;
-  o += (2 * KMAX + 1) * 4;
+  o += 128 * 4;  // block offsets of the super-tile; [96, 128): slot sources
   L.total = o + 1024;
   return L;
 }
@@ -1319,7 +1380,7 @@ static_assert(wg_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
 static_assert(wg_smem_layout<128>(FWD_HCAP).total <= 232448, "smem");
 static_assert(wg_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
 
-template <int NOUT>
+template <int NOUT, bool BIG>
 __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   using Cfg = WgCfg<NOUT>;
   constexpr int NP = Cfg::pairs, NSG = Cfg::nsg, WNSD = Cfg::nsd;
@@ -1335,6 +1396,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
   uint8_t* g_gt = gbase + L.gt;
   const uint8_t* g_d = gbase + L.d;
+  uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + 96;  // per descriptor half-slot
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K;
@@ -1385,10 +1447,16 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
           const int k0 = g * K + k_begin + 2 * p;
           const uint32_t o0 = offs[k0], o1 = offs[k0 + 1];
           const uint32_t o2 = (k_begin + 2 * p + 1 < K) ? offs[k0 + 2] : o1;
-          mbar_expect_tx(bar(W_D_FULL + ds), o2 - o0);
-          bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + o0, o1 - o0, bar(W_D_FULL + ds));
-          if (o2 > o1)
-            bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES + BLOCK_MAX_BYTES, a.blocks + o1, o2 - o1,
+          const uint32_t n0 = min(o1 - o0, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+          const uint32_t n1 = min(o2 - o1, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+          if (BIG) {
+            dsrc[2 * ds] = o1 - o0 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
+            dsrc[2 * ds + 1] = o2 - o1 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o1 : kFitsSlot;
+          }
+          mbar_expect_tx(bar(W_D_FULL + ds), n0 + n1);
+          bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + o0, n0, bar(W_D_FULL + ds));
+          if (n1)
+            bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES + BLOCK_MAX_BYTES, a.blocks + o1, n1,
                      bar(W_D_FULL + ds));
         }
         ++d_it;
@@ -1450,10 +1518,18 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
           mbar_wait(bar(W_D_FULL + ds), (d_it / WNSD) & 1);
           mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
           const int ncell = (k_begin + 2 * p + 1 < K) ? 2 : 1;
-          for (int half = 0; half < ncell; ++half)
-            aggregate_stage<FWD_AGG_WARPS / WG_GROUPS>(
-                g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES, s_halo,
-                s_a + as * 32768u + half * 16384u, wig, lane);
+          for (int half = 0; half < ncell; ++half) {
+            const uint8_t* slot = g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES;
+            const uint32_t src = BIG ? dsrc[2 * ds + half] : kFitsSlot;
+            if (src == kFitsSlot)
+              aggregate_stage<FWD_AGG_WARPS / WG_GROUPS>(
+                  slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
+                  s_a + as * 32768u + half * 16384u, wig, lane);
+            else
+              aggregate_stage_l2<FWD_AGG_WARPS / WG_GROUPS>(
+                  slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512), s_halo,
+                  s_a + as * 32768u + half * 16384u, wig, lane);
+          }
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -2230,11 +2306,13 @@ static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool tra
 }
 
 template <int NOUT>
-static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, const char* name) {
+static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, const char* name,
+                       bool big) {
   const FwdSmem L = fwd_smem_layout<NOUT>(hcap);
-  NPCG_CUDA(cudaFuncSetAttribute(k_conv_fwd_tc<NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = big ? k_conv_fwd_tc<NOUT, true> : k_conv_fwd_tc<NOUT, false>;
+  NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
-  launch(ctx, name, k_conv_fwd_tc<NOUT>, dim3(grid), dim3(FWD_THREADS), L.total, a);
+  launch(ctx, name, kern, dim3(grid), dim3(FWD_THREADS), L.total, a);
 }
 
 // One gather-side pass (forward or dgrad): cin_g gathered channels -> nout
@@ -2273,9 +2351,9 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   a.ncols = ncols;
   a.trace = trace;
   const int grid = std::min(P->n_super, ctx->num_sms);
-  if (nout == 64) launch_fwd<64>(ctx, a, P->hcap, grid, name);
-  else if (nout == 128) launch_fwd<128>(ctx, a, P->hcap, grid, name);
-  else launch_fwd<256>(ctx, a, P->hcap, grid, name);
+  if (nout == 64) launch_fwd<64>(ctx, a, P->hcap, grid, name, P->big_blocks);
+  else if (nout == 128) launch_fwd<128>(ctx, a, P->hcap, grid, name, P->big_blocks);
+  else launch_fwd<256>(ctx, a, P->hcap, grid, name, P->big_blocks);
 }
 
 
@@ -2383,11 +2461,12 @@ __global__ void k_row_lens(const int64_t* __restrict__ row_ptr, const uint32_t* 
 }
 
 template <int NOUT>
-static void launch_wgrad(npcg_context* ctx, const WgArgs& a, int hcap, dim3 grid) {
+static void launch_wgrad(npcg_context* ctx, const WgArgs& a, int hcap, dim3 grid, bool big) {
   const WgSmem L = wg_smem_layout<NOUT>(hcap);
-  NPCG_CUDA(cudaFuncSetAttribute(k_conv_wgrad_tc<NOUT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  auto kern = big ? k_conv_wgrad_tc<NOUT, true> : k_conv_wgrad_tc<NOUT, false>;
+  NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
-  launch(ctx, "conv_wgrad_tc", k_conv_wgrad_tc<NOUT>, grid, dim3(WG_THREADS), L.total, a);
+  launch(ctx, "conv_wgrad_tc", kern, grid, dim3(WG_THREADS), L.total, a);
 }
 
 static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, const float* fin,
@@ -2503,9 +2582,9 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     a.dense = p->feat_out.get();
     a.partial = p->partial.get();
     const dim3 grid(gx, groups);
-    if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid);
-    else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid);
-    else launch_wgrad<256>(ctx, a, P->hcap, grid);
+    if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid, P->big_blocks);
+    else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid, P->big_blocks);
+    else launch_wgrad<256>(ctx, a, P->hcap, grid, P->big_blocks);
     const int64_t nw = static_cast<int64_t>(K) * cin * cout;
     launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(nw, 256))),
            dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, cinp, coutp,
