@@ -272,6 +272,21 @@ def run_ours(args):
         data.append((cl, nb, f, g, fo, gi, gw))
         n_t_total += nb.size
     gw_sum = torch.zeros((27, 1, C, C), device=dev)
+    # dW all-reduce: the library's NCCL communicator (npcg_allreduce_dw); the
+    # torch.distributed all-reduce only if the library's cannot be created
+    comm = None
+    if world > 1:
+        try:
+            comm = shard.DwComm(rank, world, local)
+        except Exception as e:  # noqa: BLE001
+            print(f"[bench] rank {rank}: library NCCL comm unavailable ({e}); torch all-reduce",
+                  file=sys.stderr)
+
+    def allreduce(t):
+        if comm is not None:
+            comm.allreduce(t)
+        else:
+            shard.allreduce_weight_grad(t)
 
     def step():
         gw_sum.zero_()
@@ -280,7 +295,7 @@ def run_ours(args):
             npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw)
             gw_sum.add_(gw)
         if world > 1:
-            shard.allreduce_weight_grad(gw_sum)
+            allreduce(gw_sum)
 
     sampler = ClockSampler(local)
     if rank == 0:
@@ -384,7 +399,7 @@ def run_ours(args):
                     s_d2h.wait_event(last_b)
                     hi[s_].copy_(gi, non_blocking=True)
             if world > 1:
-                shard.allreduce_weight_grad(gs)
+                allreduce(gs)
             ev_w = torch.cuda.Event()
             ev_w.record(comp)
             with torch.cuda.stream(s_d2h):

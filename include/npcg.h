@@ -21,6 +21,9 @@
  *   npcg_voxel_downsample         spatial.hpp:47-48   voxel_downsample
  *   npcg_build_triplets_degraded  triplets.hpp:63-76  build_triplets_degraded
  *   npcg_neighbors_export_sites   conv_op.hpp:56-57   snapped_cloud / site_map
+ *   npcg_allreduce_dw             SURVEY.md §8(b,e): the one multi-GPU exchange
+ *                                  (no reference counterpart: the reference is
+ *                                  single-process; dW is a sum, vvor.hpp:79-84)
  *
  * Conventions
  *  - All tensor / index arrays are DEVICE pointers on the context's device.
@@ -123,6 +126,7 @@ typedef struct npcg_triplets {
 } npcg_triplets;
 
 typedef struct npcg_context npcg_context;     /* device, stream, scratch, profiler */
+typedef struct npcg_comm npcg_comm;           /* NCCL communicator (dW all-reduce) */
 typedef struct npcg_neighbors npcg_neighbors; /* device-resident neighbor structure */
 
 /* ---- context ------------------------------------------------------------ */
@@ -276,6 +280,23 @@ npcg_status npcg_debug_trace_forward(npcg_context* ctx, npcg_neighbors* nb, cons
 npcg_status npcg_voxel_downsample(npcg_context* ctx, const npcg_cloud* cloud, double voxel,
                                   int64_t* kept, int64_t* parent, int64_t* out_offsets,
                                   int64_t* n_kept);
+
+/* ---- multi-GPU: dW all-reduce over NCCL -------------------
+ * Whole point clouds are sharded per GPU; the weight gradient is the one
+ * exchange: sum over ranks, in place, on the context stream.  NCCL is loaded
+ * at first use (libnccl.so.2; the one a PyTorch process already has).
+ * npcg_comm_unique_id: rank 0 creates the id (HOST bytes), the caller
+ * broadcasts it (e.g. torch.distributed), every rank calls npcg_comm_create
+ * (collective; synchronises).  NPCG_ERR_UNSUPPORTED when NCCL is absent. */
+#define NPCG_COMM_ID_BYTES 128
+npcg_status npcg_comm_unique_id(uint8_t* id);
+npcg_status npcg_comm_create(npcg_context* ctx, int nranks, int rank, const uint8_t* id,
+                             npcg_comm** out);
+npcg_status npcg_comm_destroy(npcg_comm* comm);
+/* dw: DEVICE (K, G, C_out, C_in) weight gradient, count elements, summed over
+ * ranks in place (asynchronous, stream-ordered). */
+npcg_status npcg_allreduce_dw(npcg_context* ctx, npcg_comm* comm, npcg_dtype dtype, void* dw,
+                              int64_t count);
 
 #ifdef __cplusplus
 }

@@ -85,6 +85,10 @@ _SIGS = {
     "npcg_neighbors_plan_stats": (C.c_int, [_P, _P, _P]),
     "npcg_debug_trace_forward": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "npcg_voxel_downsample": (C.c_int, [_P, C.POINTER(npcg_cloud), _D, _P, _P, _P, _PI64]),
+    "npcg_comm_unique_id": (C.c_int, [_P]),
+    "npcg_comm_create": (C.c_int, [_P, C.c_int, C.c_int, _P, C.POINTER(_P)]),
+    "npcg_comm_destroy": (C.c_int, [_P]),
+    "npcg_allreduce_dw": (C.c_int, [_P, _P, C.c_int, _P, _I64]),
     "npcg_build_triplets_degraded": (C.c_int, [_P, C.POINTER(npcg_cloud), _D, _I64, C.POINTER(_P)]),
     "npcg_neighbors_sites": (C.c_int, [_P, _PI64, _PI64, _PI64]),
     "npcg_neighbors_export_sites": (C.c_int, [_P, _P, _P, _P, _P, _P]),

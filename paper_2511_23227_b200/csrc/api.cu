@@ -26,27 +26,6 @@ __global__ void k_widen(const uint32_t* a, int64_t n, int64_t* o) {
   if (p < n) o[p] = a[p];
 }
 
-template <typename F>
-npcg_status guard(npcg_context* ctx, F&& f) {
-  try {
-    if (ctx) {
-      NPCG_CUDA(cudaSetDevice(ctx->device));
-      ctx->last_error.clear();
-    }
-    f();
-    return NPCG_OK;
-  } catch (const Error& e) {
-    if (ctx) ctx->last_error = e.msg;
-    return e.code;
-  } catch (const std::bad_alloc&) {
-    if (ctx) ctx->last_error = "host allocation failed";
-    return NPCG_ERR_OOM;
-  } catch (const std::exception& e) {
-    if (ctx) ctx->last_error = e.what();
-    return NPCG_ERR_CUDA;
-  }
-}
-
 void need(const void* p, const char* what) {
   if (!p) fail(NPCG_ERR_INVALID, std::string(what) + " is null");
 }

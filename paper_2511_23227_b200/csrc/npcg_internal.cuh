@@ -63,6 +63,29 @@ namespace npcg {
 
 cudaEvent_t take_event(npcg_context* ctx);
 
+// Runs an entry point's body: C++ exceptions become status codes (they never
+// cross the ABI); the message is kept for npcg_last_error.
+template <typename F>
+npcg_status guard(npcg_context* ctx, F&& f) {
+  try {
+    if (ctx) {
+      NPCG_CUDA(cudaSetDevice(ctx->device));
+      ctx->last_error.clear();
+    }
+    f();
+    return NPCG_OK;
+  } catch (const Error& e) {
+    if (ctx) ctx->last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    if (ctx) ctx->last_error = "host allocation failed";
+    return NPCG_ERR_OOM;
+  } catch (const std::exception& e) {
+    if (ctx) ctx->last_error = e.what();
+    return NPCG_ERR_CUDA;
+  }
+}
+
 // Every kernel launch of the library goes through here: counted, optionally
 // bracketed by events for the in-library profiler, error-checked.
 template <typename... KArgs, typename... Args>

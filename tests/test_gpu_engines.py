@@ -204,3 +204,20 @@ def test_vvor_linearity(npc, orc):
     a = npc.vvor(go, f, tl, 27).grad
     b = npc.vvor(2 * go, f, tl, 27).grad
     assert torch.equal(b, 2 * a)
+
+
+def test_library_dw_allreduce_single_rank(npc):
+    """npcg_allreduce_dw through the library's own NCCL
+    communicator: with one rank the sum is the identity, fp32 and fp64; bad
+    dtype / arguments are rejected like the reference's errors."""
+    from paper_2511_23227_b200.shard import DwComm
+    comm = DwComm(0, 1, 0)
+    for dt in (torch.float32, torch.float64):
+        g = torch.randn(27, 1, 64, 64, device="cuda", dtype=dt)
+        ref = g.clone()
+        comm.allreduce(g)
+        torch.cuda.synchronize()
+        assert torch.equal(g, ref)
+    with pytest.raises(npc.ShapeError):
+        comm.allreduce(torch.zeros(4, device="cuda", dtype=torch.float16))
+    comm.close()
