@@ -822,7 +822,7 @@ struct FwdArgs {
   const uint8_t* wpack;       // (K x nci) images of NOUT x 128 B
   float* out;                 // (n_rows, ncols), original order
   int ncols;                  // channels written per row (<= NOUT; the rest is padding)
-  long long* trace;           // debug: per-stage event clocks of CTA 0 (nullptr = off)
+  long long* trace;           // debug: per-stage event clocks of CTA 0 (traced variant only)
 };
 constexpr int TRACE_STAGES = 512;
 constexpr int TRACE_EV = 8;  // 0 d_issue, 1 d_full, 2 a_empty, 3 agg_done, 4 mma_start, 5 mma_issued, 6 w_full
@@ -1036,8 +1036,13 @@ __device__ __noinline__ void aggregate_stage_l2(const uint8_t* blk, const uint16
 // chunk) as an NOUT x 64 image.
 // BIG: the plan has descriptor blocks beyond the shared-memory slot (their
 // entries are read from L2); plans without them run the leaner variant.
-template <int NOUT, bool BIG>
+template <int NOUT, bool BIG, bool TRACE = false>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
+  // pipeline event clocks only in the traced debug variant (the checks cost
+  // issue slots in the product kernel)
+  auto tev = [&](uint32_t stage, int ev) {
+    if constexpr (TRACE) trace_ev(a.trace, stage, ev);
+  };
   using Cfg = FwdCfg<NOUT>;
   constexpr int NSWt = Cfg::nsw, NSDt = Cfg::nsd;
   extern __shared__ uint8_t smem_raw[];
@@ -1107,7 +1112,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             if (BIG) dsrc[ds] = o1 - o0 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
             mbar_expect_tx(bar(B_D_FULL + ds), nb);
             bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, nb, bar(B_D_FULL + ds));
-            trace_ev(a.trace, d_it, 0);
+            tev(d_it, 0);
           }
           ++d_it;
         }
@@ -1165,11 +1170,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         if (pending && (c > 0 || k == 1 || !first)) release_epilogue();
         const uint32_t ws = w_it % NSWt;
         mbar_wait(bar(B_W_FULL + ws), (w_it / NSWt) & 1);
-        if (lane == 0) trace_ev(a.trace, a_it, 6);
+        if (lane == 0) tev(a_it, 6);
         for (int g = 0; g < nsub; ++g) {
           const uint32_t as = a_it % NSA;
           mbar_wait(bar(B_A_FULL + as), (a_it / NSA) & 1);
-          if (lane == 0) trace_ev(a.trace, a_it, 4);
+          if (lane == 0) tev(a_it, 4);
           tc_fence_after();
           const uint32_t d = tmem + ab * Cfg::acc_cols + g * NOUT;
           // descriptor start-address field is in 16-byte units
@@ -1183,7 +1188,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             umma_commit(bar(B_A_EMPTY + as));
           }
           __syncwarp();
-          if (lane == 0) trace_ev(a.trace, a_it, 5);
+          if (lane == 0) tev(a_it, 5);
           ++a_it;
         }
         if (elect_one()) umma_commit(bar(B_W_EMPTY + ws));
@@ -1220,9 +1225,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           if (static_cast<int>(a_it % AGG_GROUPS) == grp) {
             const uint32_t ds = d_it % NSDt, as = a_it % NSA;
             mbar_wait(bar(B_D_FULL + ds), (d_it / NSDt) & 1);
-            if (wig == 0 && lane == 0) trace_ev(a.trace, d_it, 1);
+            if (wig == 0 && lane == 0) tev(d_it, 1);
             mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
-            if (wig == 0 && lane == 0) trace_ev(a.trace, a_it, 2);
+            if (wig == 0 && lane == 0) tev(a_it, 2);
             const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
             const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
             if (src == kFitsSlot)  // (separate instantiations keep shared-memory loads)
@@ -1233,7 +1238,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
                                                   s_halo, s_a + as * 16384u, wig, lane);
             fence_proxy_async_smem();
             __syncwarp();
-            if (wig == 0 && lane == 0) trace_ev(a.trace, a_it, 3);
+            if (wig == 0 && lane == 0) tev(a_it, 3);
             if (lane == 0) {
               mbar_arrive(bar(B_A_FULL + as));
               mbar_arrive(bar(B_D_EMPTY + ds));
@@ -2310,6 +2315,9 @@ static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, 
                        bool big) {
   const FwdSmem L = fwd_smem_layout<NOUT>(hcap);
   auto kern = big ? k_conv_fwd_tc<NOUT, true> : k_conv_fwd_tc<NOUT, false>;
+  if constexpr (NOUT == 64)
+    if (a.trace) kern = big ? k_conv_fwd_tc<64, true, true> : k_conv_fwd_tc<64, false, true>;
+  if (a.trace && NOUT != 64) fail(NPCG_ERR_UNSUPPORTED, "trace: 64-channel passes only");
   NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
   launch(ctx, name, kern, dim3(grid), dim3(FWD_THREADS), L.total, a);
