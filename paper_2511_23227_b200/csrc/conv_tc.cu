@@ -131,14 +131,20 @@ __global__ void k_inverse_perm(const uint32_t* __restrict__ perm, int64_t n,
   if (p < n) inv[perm[p]] = static_cast<uint32_t>(p);
 }
 
-// Rank filter of a plan record: only the entries of each (row, cell) whose
-// rank (order among that row's entries of that cell, CSR order) lies in
-// [lo, hi).  Records of one 8-row tile that no single plan can hold split its
-// entries by rank; the kernels accumulate such records in TMEM.
-struct RankFilter {
-  uint32_t lo, hi;
-  __device__ __forceinline__ bool all() const { return lo == 0 && hi == 0xFFFFFFFFu; }
+// Entry filter of a plan record: only the entries whose permuted column lies
+// in [clo, chi) (a halo segment) and, among those, whose rank (order among
+// the row's entries of that cell, CSR order) lies in [rlo, rhi).  Records
+// that split one tile's entries this way form an item; the kernels
+// accumulate its records in TMEM.
+constexpr int MAXSEG = 16;  // halo segments per record at most
+struct EntryFilter {
+  uint32_t rlo, rhi, clo, chi;
+  __host__ __device__ static EntryFilter from(uint4 v) { return {v.x, v.y, v.z, v.w}; }
+  __device__ __forceinline__ bool all() const {
+    return rlo == 0 && rhi == 0xFFFFFFFFu && clo == 0 && chi == 0xFFFFFFFFu;
+  }
 };
+__host__ __device__ inline uint4 no_filter() { return make_uint4(0, 0xFFFFFFFFu, 0, 0xFFFFFFFFu); }
 
 // Per sub-tile: entries per (sub-tile, cell) block -> block byte sizes; flags
 // sub-tiles whose blocks exceed the stage-descriptor slot or whose per-(row,
@@ -146,9 +152,11 @@ struct RankFilter {
 // cell) count (unfiltered), which sizes rank-split records.
 __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ row_ptr,
                                                     const uint32_t* __restrict__ kk,
+                                                    const uint32_t* __restrict__ col,
+                                                    const uint32_t* __restrict__ inv_perm_cols,
                                                     const uint32_t* __restrict__ perm_rows,
                                                     const uint2* __restrict__ tiles,
-                                                    const uint2* __restrict__ tfilter, int K,
+                                                    const uint4* __restrict__ tfilter, int K,
                                                     uint32_t* __restrict__ blk_size,
                                                     uint32_t* __restrict__ sub_bad,
                                                     uint32_t* __restrict__ tile_maxc,
@@ -167,14 +175,19 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
   for (int k = 0; k < KMAX; ++k) rc[r][k] = inc[r][k] = 0;
   __syncthreads();
   const uint2 tl = tiles[blockIdx.x];
-  const RankFilter f{tfilter[blockIdx.x].x, tfilter[blockIdx.x].y};
+  const EntryFilter f = EntryFilter::from(tfilter[blockIdx.x]);
+  const bool colf = !(f.clo == 0 && f.chi == 0xFFFFFFFFu);
   if (static_cast<uint32_t>(r) < tl.y) {
     const uint32_t i = perm_rows[tl.x + r];
     for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
+      if (colf) {
+        const uint32_t pj = inv_perm_cols[col[e]];
+        if (pj < f.clo || pj >= f.chi) continue;
+      }
       const uint32_t k = kk[e];
       const uint32_t rank = rc[r][k];
       if (rc[r][k] < 0xFFFFu) rc[r][k]++;
-      if (rank >= f.lo && rank < f.hi) {
+      if (rank >= f.rlo && rank < f.rhi) {
         atomicAdd(&cnt[k], 1u);
         inc[r][k]++;
       }
@@ -201,22 +214,28 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
   }
 }
 
-// Entries of one row passing a rank filter, in CSR order: fn(e, k).
+// Entries of one row passing a filter, in CSR order: fn(e, k).
 template <typename F>
 __device__ __forceinline__ void for_row_entries(const int64_t* row_ptr, const uint32_t* kk,
-                                                uint32_t row, const RankFilter& f, F&& fn) {
+                                                const uint32_t* col, const uint32_t* inv_perm_cols,
+                                                uint32_t row, const EntryFilter& f, F&& fn) {
   const int64_t e0 = row_ptr[row], e1 = row_ptr[row + 1];
   if (f.all()) {
     for (int64_t e = e0; e < e1; ++e) fn(e, static_cast<int>(kk[e]));
     return;
   }
+  const bool colf = !(f.clo == 0 && f.chi == 0xFFFFFFFFu);
   uint16_t seen[KMAX];
 #pragma unroll
   for (int k = 0; k < KMAX; ++k) seen[k] = 0;
   for (int64_t e = e0; e < e1; ++e) {
+    if (colf) {
+      const uint32_t pj = inv_perm_cols[col[e]];
+      if (pj < f.clo || pj >= f.chi) continue;
+    }
     const int k = static_cast<int>(kk[e]);
     const uint32_t rank = seen[k]++;
-    if (rank >= f.lo && rank < f.hi) fn(e, k);
+    if (rank >= f.rlo && rank < f.rhi) fn(e, k);
   }
 }
 
@@ -228,10 +247,10 @@ __global__ void __launch_bounds__(512) k_plan_super(
     const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
     const uint32_t* __restrict__ kk, const uint32_t* __restrict__ perm_rows,
     const uint32_t* __restrict__ inv_perm_cols, const uint2* __restrict__ sup,
-    const uint2* __restrict__ tiles, const uint2* __restrict__ tfilter, int K, int st, int hcap,
+    const uint2* __restrict__ tiles, const uint4* __restrict__ tfilter, int K, int st, int hcap,
     const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ sub_bad,
     uint32_t* __restrict__ halo_out, uint2* __restrict__ runs_out, uint32_t* __restrict__ n_runs,
-    uint32_t* __restrict__ halo_len,
+    uint32_t* __restrict__ halo_len, uint32_t* __restrict__ seg,
     uint8_t* __restrict__ blocks) {
   extern __shared__ __align__(16) uint8_t sm[];
   uint32_t* buf = reinterpret_cast<uint32_t*>(sm);                          // MAXE_ST
@@ -253,20 +272,23 @@ __global__ void __launch_bounds__(512) k_plan_super(
   for (int x = tid; x < st * K * TM; x += blockDim.x) cnt[x] = 0;
   __syncthreads();
   if (s_bad) {
-    if (tid == 0) halo_len[s] = kOverflow;
+    if (tid == 0) {
+      halo_len[s] = kOverflow;
+      seg[static_cast<int64_t>(s) * (MAXSEG + 1)] = 0;
+    }
     return;
   }
   // 1. row lengths -> offsets (block scan over R <= 512 rows)
   int len = 0;
   uint32_t row_i = 0;
-  RankFilter filt{0, 0xFFFFFFFFu};
+  EntryFilter filt = EntryFilter::from(no_filter());
   if (tid < R) {
     const uint2 tl = tiles[sub0 + tid / TM];
-    filt = RankFilter{tfilter[sub0 + tid / TM].x, tfilter[sub0 + tid / TM].y};
+    filt = EntryFilter::from(tfilter[sub0 + tid / TM]);
     if (static_cast<uint32_t>(tid % TM) < tl.y) {
       row_i = perm_rows[tl.x + tid % TM];
       if (filt.all()) len = static_cast<int>(row_ptr[row_i + 1] - row_ptr[row_i]);
-      else for_row_entries(row_ptr, kk, row_i, filt, [&](int64_t, int) { ++len; });
+      else for_row_entries(row_ptr, kk, col, inv_perm_cols, row_i, filt, [&](int64_t, int) { ++len; });
     }
   }
   int incl = len;
@@ -291,14 +313,17 @@ __global__ void __launch_bounds__(512) k_plan_super(
   if (tid < R) rowoff[tid] = my_off;
   const int E = s_total;
   if (E > MAXE_ST) {
-    if (tid == 0) halo_len[s] = kOverflow;
+    if (tid == 0) {
+      halo_len[s] = kOverflow;
+      seg[static_cast<int64_t>(s) * (MAXSEG + 1)] = 0;
+    }
     return;
   }
   // 2. permuted neighbor ids + per-(sub, cell, row) counts
   if (tid < R && len > 0) {
     const int g = tid / TM, r = tid % TM;
     int q = 0;
-    for_row_entries(row_ptr, kk, row_i, filt, [&](int64_t e, int k) {
+    for_row_entries(row_ptr, kk, col, inv_perm_cols, row_i, filt, [&](int64_t e, int k) {
       buf[my_off + q++] = inv_perm_cols[col[e]];
       cnt[(g * K + k) * TM + r]++;
     });
@@ -351,10 +376,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
   }
   __syncthreads();
   const int H = s_H;
-  if (H > hcap) {
-    if (tid == 0) halo_len[s] = kOverflow;
-    return;
-  }
+  const bool over = H > hcap;
   // gather my unique values into registers-by-chunk, then write compacted
   {
     int w0 = li - local + wsum[warp];
@@ -367,10 +389,24 @@ __global__ void __launch_bounds__(512) k_plan_super(
     __syncthreads();
     for (int q = 0; q < nv; ++q) {
       buf[w0 + q] = vals[q];
-      halo_out[static_cast<int64_t>(s) * hcap + w0 + q] = vals[q];
+      if (!over) halo_out[static_cast<int64_t>(s) * hcap + w0 + q] = vals[q];
     }
   }
   __syncthreads();
+  if (over) {
+    // beyond the halo cap: report the split of the halo into <= hcap-row
+    // segments (column ranges) so the host can plan the rows as one item of
+    // segment records instead of smaller tiles
+    if (tid == 0) {
+      halo_len[s] = kOverflow;
+      const int nseg = (H + hcap - 1) / hcap;
+      uint32_t* sg = seg + static_cast<int64_t>(s) * (MAXSEG + 1);
+      sg[0] = nseg <= MAXSEG ? static_cast<uint32_t>(nseg) : 0u;
+      if (nseg <= MAXSEG)
+        for (int q = 1; q < nseg; ++q) sg[q] = buf[static_cast<int64_t>(q) * H / nseg];
+    }
+    return;
+  }
   // 4b. copy runs of consecutive rows: {src row, dst | len << 16}
   {
     const int per2 = (H + blockDim.x - 1) / blockDim.x;
@@ -440,7 +476,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
   // 6. entries: halo index of each neighbor, written at its item's offset
   if (tid < R && len > 0) {
     const int g = tid / TM, r = tid % TM;
-    for_row_entries(row_ptr, kk, row_i, filt, [&](int64_t e, int k) {
+    for_row_entries(row_ptr, kk, col, inv_perm_cols, row_i, filt, [&](int64_t e, int k) {
       const uint32_t pj = inv_perm_cols[col[e]];
       int lo = 0, hi = H;
       while (lo < hi) {
@@ -465,8 +501,12 @@ __global__ void k_add_u32(uint32_t* __restrict__ p, int64_t n, uint32_t add) {
 // One planning level over a host list of super-tiles (tiles in level-local
 // numbering).  Results stay in the level's own buffers until concatenation.
 struct PlanLevel {
-  std::vector<uint2> sup, tiles, tfilter;  // tfilter: per tile rank filter {lo, hi}
-  std::vector<uint32_t> maxc;              // per tile largest (row, cell) entry count
+  int kind = 0;                 // 0 plain super-tiles, 1 rank-split items, 2 halo-segment items
+  std::vector<uint2> sup, tiles;
+  std::vector<uint4> tfilter;   // per tile entry filter {rank lo, hi, column lo, hi}
+  std::vector<uint32_t> nom;    // per tile nominal rows (128, 64, ..., 8)
+  std::vector<uint32_t> maxc;   // per tile largest (row, cell) entry count
+  std::vector<uint32_t> seg;    // per record: halo segments and their column boundaries
   DevBuf<uint32_t> halo, n_runs, halo_len, blk_off;
   DevBuf<uint2> runs;
   DevBuf<uint8_t> blocks;
@@ -479,21 +519,23 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
                        const uint32_t* kk, const uint32_t* perm_rows, const uint32_t* inv_perm_cols,
                        int K, int st, int hcap) {
   const int ns = static_cast<int>(L.sup.size()), nt = static_cast<int>(L.tiles.size());
-  if (L.tfilter.empty()) L.tfilter.assign(nt, make_uint2(0, 0xFFFFFFFFu));
-  DevBuf<uint2> d_sup(ctx, ns), d_tiles(ctx, nt), d_filt(ctx, nt);
+  if (L.tfilter.empty()) L.tfilter.assign(nt, no_filter());
+  DevBuf<uint2> d_sup(ctx, ns), d_tiles(ctx, nt);
+  DevBuf<uint4> d_filt(ctx, nt);
+  DevBuf<uint32_t> d_seg(ctx, static_cast<int64_t>(ns) * (MAXSEG + 1));
   DevBuf<uint32_t> d_maxc(ctx, nt), d_maxblk(ctx, 1);
   NPCG_CUDA(cudaMemsetAsync(d_maxblk.get(), 0, 4, ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(d_sup.get(), L.sup.data(), ns * sizeof(uint2), cudaMemcpyHostToDevice,
                             ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(d_tiles.get(), L.tiles.data(), nt * sizeof(uint2),
                             cudaMemcpyHostToDevice, ctx->stream));
-  NPCG_CUDA(cudaMemcpyAsync(d_filt.get(), L.tfilter.data(), nt * sizeof(uint2),
+  NPCG_CUDA(cudaMemcpyAsync(d_filt.get(), L.tfilter.data(), nt * sizeof(uint4),
                             cudaMemcpyHostToDevice, ctx->stream));
   const int64_t nblk = static_cast<int64_t>(nt) * K;
   DevBuf<uint32_t> blk_size(ctx, nblk + 1), sub_bad(ctx, nt);
   NPCG_CUDA(cudaMemsetAsync(blk_size.get() + nblk, 0, 4, ctx->stream));
-  launch(ctx, "plan_counts", k_plan_counts, dim3(nt), dim3(TM), 0, row_ptr, kk, perm_rows,
-         static_cast<const uint2*>(d_tiles.get()), static_cast<const uint2*>(d_filt.get()), K,
+  launch(ctx, "plan_counts", k_plan_counts, dim3(nt), dim3(TM), 0, row_ptr, kk, col, inv_perm_cols,
+         perm_rows, static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K,
          blk_size.get(), sub_bad.get(), d_maxc.get(), d_maxblk.get());
   L.blk_off.alloc(ctx, nblk + 1);
   exclusive_scan_u32(ctx, blk_size.get(), L.blk_off.get(), nblk + 1, &L.block_bytes);
@@ -507,10 +549,10 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
                                  static_cast<int>(smem)));
   launch(ctx, "plan_super", k_plan_super, dim3(ns), dim3(512), smem, row_ptr, col, kk, perm_rows,
          inv_perm_cols, static_cast<const uint2*>(d_sup.get()),
-         static_cast<const uint2*>(d_tiles.get()), static_cast<const uint2*>(d_filt.get()), K, st,
+         static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K, st,
          hcap,
          static_cast<const uint32_t*>(L.blk_off.get()), static_cast<const uint32_t*>(sub_bad.get()),
-         L.halo.get(), L.runs.get(), L.n_runs.get(), L.halo_len.get(), L.blocks.get());
+         L.halo.get(), L.runs.get(), L.n_runs.get(), L.halo_len.get(), d_seg.get(), L.blocks.get());
   L.hl.resize(ns);
   L.maxc.resize(nt);
   NPCG_CUDA(cudaMemcpyAsync(L.hl.data(), L.halo_len.get(), ns * 4, cudaMemcpyDeviceToHost,
@@ -518,6 +560,9 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   NPCG_CUDA(cudaMemcpyAsync(L.maxc.data(), d_maxc.get(), nt * 4, cudaMemcpyDeviceToHost,
                             ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(&L.max_blk, d_maxblk.get(), 4, cudaMemcpyDeviceToHost, ctx->stream));
+  L.seg.resize(static_cast<size_t>(ns) * (MAXSEG + 1));
+  NPCG_CUDA(cudaMemcpyAsync(L.seg.data(), d_seg.get(), L.seg.size() * 4, cudaMemcpyDeviceToHost,
+                            ctx->stream));
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
@@ -538,92 +583,112 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   std::vector<PlanLevel> lv(1);
   {
     const int nt = static_cast<int>(ceil_div(n_rows, TM));
-    for (int t = 0; t < nt; ++t)
+    for (int t = 0; t < nt; ++t) {
       lv[0].tiles.push_back(make_uint2(static_cast<uint32_t>(t) * TM,
                                        static_cast<uint32_t>(std::min<int64_t>(TM, n_rows - int64_t(t) * TM))));
+      lv[0].nom.push_back(TM);
+    }
     for (int t = 0; t < nt; t += st)
       lv[0].sup.push_back(make_uint2(t, std::min(st, nt - t)));
   }
-  // Levels: st x 128 rows, then single sub-tiles of 128 (if st > 1), 64, ...,
-  // 8 rows; an 8-row tile that still fails becomes one item of rank-split
-  // records (entries of rank [qQ, (q+1)Q) per (row, cell), Q sized so that
-  // any record fits the halo: 8 rows x K cells x Q <= hcap).
+  // Planning levels form a worklist.  A plain super-tile beyond capacity
+  // becomes, when only its halo is too large, one item of halo-segment
+  // records (same rows, each record the entries of one column range of the
+  // halo, <= hcap rows each); otherwise its rows are re-tiled as single
+  // sub-tiles of half as many rows (128 after a multi-tile super-tile, 64,
+  // ..., 8).  An 8-row tile that still fails becomes an item of rank-split
+  // records (entries of rank [qQ, (q+1)Q) per (row, cell)), re-split with a
+  // smaller Q down to the Q that always fits (8 rows x K cells x Q <= hcap);
+  // only an item failing at that Q goes to the exact engine.
   std::vector<uint32_t> spill;
-  std::vector<uint8_t> rank_level{0};  // per level: records are rank splits
-  // rank step that always fits (8 rows x K cells x Q entries <= hcap halo
-  // rows, <= 768 block entries) and the optimistic first step
   const uint32_t q_safe = std::max<uint32_t>(1, static_cast<uint32_t>(hcap) / (8u * K));
   const uint32_t q_first = std::max<uint32_t>(q_safe, 64);
-  // one item of rank-split records over a tile's rows
   auto push_rank_item = [](PlanLevel& nx, uint2 tile, uint32_t maxc, uint32_t Q) {
     const uint32_t nq = std::max<uint32_t>(1, (maxc + Q - 1) / Q);
     for (uint32_t q = 0; q < nq; ++q) {
       const uint32_t fl = (q == 0 ? SUP_FIRST : 0u) | (q + 1 == nq ? SUP_LAST : 0u);
       nx.sup.push_back(make_uint2(static_cast<uint32_t>(nx.tiles.size()), 1u | fl));
       nx.tiles.push_back(tile);
-      nx.tfilter.push_back(make_uint2(q * Q, (q + 1) * Q));
+      nx.nom.push_back(8);
+      nx.tfilter.push_back(make_uint4(q * Q, (q + 1) * Q, 0, 0xFFFFFFFFu));
     }
   };
-  uint32_t cur = TM;                // rows per sub-tile at this level
-  for (int level = 0;; ++level) {
-    PlanLevel& L = lv[level];
-    plan_level(ctx, L, row_ptr, col, kk, perm_rows, inv_perm_cols, K, st, hcap);
-    const bool is_rank = rank_level[level] != 0;
-    PlanLevel next;
-    if (is_rank) {
-      // an item fails as a whole: it is split again with a smaller rank step
-      // (down to the step that always fits), else its rows go to the exact engine
-      const uint32_t q_now = L.tfilter[0].y - L.tfilter[0].x;
-      const uint32_t q_next = q_now > q_safe ? std::max(q_safe, q_now / 4) : 0;
-      PlanLevel again;
-      for (size_t x = 0; x < L.sup.size();) {
-        size_t y = x + 1;
-        while (y < L.sup.size() && !(L.sup[y].y & SUP_FIRST)) ++y;
-        bool bad = false;
-        for (size_t z = x; z < y; ++z) bad |= L.hl[z] == kOverflow;
-        if (bad) {
-          const uint2 tl = L.tiles[L.sup[x].x];
-          if (q_next) {
-            push_rank_item(again, tl, L.maxc[L.sup[x].x], q_next);
-          } else {
-            for (uint32_t p = tl.x; p < tl.x + tl.y; ++p) spill.push_back(p);
-          }
-          for (size_t z = x; z < y; ++z) L.hl[z] = kOverflow;
-          std::vector<uint32_t> ov(y - x, kOverflow);
-          NPCG_CUDA(cudaMemcpyAsync(L.halo_len.get() + x, ov.data(), ov.size() * 4,
-                                    cudaMemcpyHostToDevice, ctx->stream));
-          NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
-        }
-        x = y;
-      }
-      if (again.sup.empty()) break;
-      lv.push_back(std::move(again));
-      rank_level.push_back(1);
-      continue;
-    }
-    const uint32_t sz = level == 0 && st > 1 ? TM : cur / 2;
-    cur = sz;
-    const bool to_rank = sz < 8;
-    for (size_t x = 0; x < L.sup.size(); ++x) {
-      if (L.hl[x] != kOverflow) continue;
-      const uint2 sp = L.sup[x];
-      const uint32_t a = L.tiles[sp.x].x;
-      const uint2 last = L.tiles[sp.x + (sp.y & 0xFFu) - 1];
-      const uint32_t b = last.x + last.y;
-      if (to_rank) {
-        uint32_t maxc = 0;
-        for (uint32_t t = sp.x; t < sp.x + (sp.y & 0xFFu); ++t) maxc = std::max(maxc, L.maxc[t]);
-        push_rank_item(next, make_uint2(a, b - a), maxc, q_first);
-        continue;
+  // mark the records [x, y) of a level overflowed (also on the device)
+  auto drop = [&](PlanLevel& L, size_t x, size_t y) {
+    for (size_t z = x; z < y; ++z) L.hl[z] = kOverflow;
+    std::vector<uint32_t> ov(y - x, kOverflow);
+    NPCG_CUDA(cudaMemcpyAsync(L.halo_len.get() + x, ov.data(), ov.size() * 4,
+                              cudaMemcpyHostToDevice, ctx->stream));
+    NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  };
+  for (size_t li = 0; li < lv.size(); ++li) {
+    plan_level(ctx, lv[li], row_ptr, col, kk, perm_rows, inv_perm_cols, K, st, hcap);
+    PlanLevel seg_items, halves, ranks;
+    seg_items.kind = 2;
+    ranks.kind = 1;
+    PlanLevel& L = lv[li];
+    // rows of a failed record / item -> smaller tiles (or rank items below 8 rows)
+    auto retile = [&](uint32_t a, uint32_t b, uint32_t sz, uint32_t maxc) {
+      if (sz < 8) {
+        push_rank_item(ranks, make_uint2(a, b - a), maxc, q_first);
+        return;
       }
       for (uint32_t p = a; p < b; p += sz) {
-        next.sup.push_back(make_uint2(static_cast<uint32_t>(next.tiles.size()), 1));
-        next.tiles.push_back(make_uint2(p, std::min(sz, b - p)));
+        halves.sup.push_back(make_uint2(static_cast<uint32_t>(halves.tiles.size()), 1));
+        halves.tiles.push_back(make_uint2(p, std::min(sz, b - p)));
+        halves.nom.push_back(sz);
       }
+    };
+    for (size_t x = 0; x < L.sup.size();) {
+      size_t y = x + 1;  // records of one item
+      if (L.kind != 0)
+        while (y < L.sup.size() && !(L.sup[y].y & SUP_FIRST)) ++y;
+      bool bad = false;
+      for (size_t z = x; z < y; ++z) bad |= L.hl[z] == kOverflow;
+      if (!bad) {
+        x = y;
+        continue;
+      }
+      const uint2 sp = L.sup[x];
+      const uint32_t nsub = sp.y & 0xFFu;
+      const uint32_t a = L.tiles[sp.x].x;
+      const uint2 last = L.tiles[sp.x + nsub - 1];
+      const uint32_t b = last.x + last.y;
+      uint32_t maxc = 0;
+      for (uint32_t t = sp.x; t < sp.x + nsub; ++t) maxc = std::max(maxc, L.maxc[t]);
+      const uint32_t nom = L.nom[sp.x];
+      if (L.kind == 0) {
+        const uint32_t* sg = &L.seg[x * (MAXSEG + 1)];
+        if (sg[0] >= 2) {  // halo too large only: one item of segment records
+          const uint32_t nseg = sg[0];
+          for (uint32_t q = 0; q < nseg; ++q) {
+            const uint32_t fl = (q == 0 ? SUP_FIRST : 0u) | (q + 1 == nseg ? SUP_LAST : 0u);
+            seg_items.sup.push_back(make_uint2(static_cast<uint32_t>(seg_items.tiles.size()), nsub | fl));
+            for (uint32_t t = sp.x; t < sp.x + nsub; ++t) {
+              seg_items.tiles.push_back(L.tiles[t]);
+              seg_items.nom.push_back(L.nom[t]);
+              seg_items.tfilter.push_back(make_uint4(0, 0xFFFFFFFFu, q == 0 ? 0u : sg[q],
+                                                     q + 1 == nseg ? 0xFFFFFFFFu : sg[q + 1]));
+            }
+          }
+        } else {
+          retile(a, b, nsub > 1 ? nom : nom / 2, maxc);
+        }
+      } else if (L.kind == 2) {
+        drop(L, x, y);
+        retile(a, b, nsub > 1 ? nom : nom / 2, maxc);
+      } else {  // rank item: re-split with a smaller step, else the exact engine
+        const uint32_t q_now = L.tfilter[sp.x].y - L.tfilter[sp.x].x;
+        const uint32_t q_next = q_now > q_safe ? std::max(q_safe, q_now / 4) : 0;
+        drop(L, x, y);
+        if (q_next) push_rank_item(ranks, make_uint2(a, b - a), maxc, q_next);
+        else
+          for (uint32_t p = a; p < b; ++p) spill.push_back(p);
+      }
+      x = y;
     }
-    if (next.sup.empty()) break;
-    lv.push_back(std::move(next));
-    rank_level.push_back(to_rank ? 1 : 0);
+    for (PlanLevel* nx : {&seg_items, &halves, &ranks})
+      if (!nx->sup.empty()) lv.push_back(std::move(*nx));
   }
   P->levels = static_cast<int>(lv.size());
   for (const PlanLevel& L : lv) P->big_blocks |= L.max_blk > static_cast<uint32_t>(BLOCK_MAX_BYTES);
@@ -633,8 +698,8 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
       size_t bad = 0;
       for (uint32_t h : lv[li].hl) bad += h == kOverflow;
       std::fprintf(stderr, " L%zu%s %zu recs (%zu tiles of %u rows) %zu failed;", li,
-                   rank_level[li] ? "(rank)" : "", lv[li].sup.size(), lv[li].tiles.size(),
-                   lv[li].tiles.empty() ? 0u : lv[li].tiles[0].y, bad);
+                   lv[li].kind == 1 ? "(rank)" : lv[li].kind == 2 ? "(seg)" : "", lv[li].sup.size(),
+                   lv[li].tiles.size(), lv[li].nom.empty() ? 0u : lv[li].nom[0], bad);
     }
     std::fprintf(stderr, " spill rows %zu\n", spill.size());
   }
@@ -701,7 +766,7 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     const int64_t lns = L.sup.size(), lnt = L.tiles.size();
     for (const uint2& sp : L.sup) {
       // plain super-tiles are single-record items
-      const uint32_t fl = rank_level[li] ? (sp.y & (SUP_FIRST | SUP_LAST)) : (SUP_FIRST | SUP_LAST);
+      const uint32_t fl = L.kind != 0 ? (sp.y & (SUP_FIRST | SUP_LAST)) : (SUP_FIRST | SUP_LAST);
       if (fl & SUP_FIRST) items.push_back(static_cast<uint32_t>(sup_all.size()));
       sup_all.push_back(make_uint2(sp.x + static_cast<uint32_t>(t0), (sp.y & 0xFFu) | fl));
     }

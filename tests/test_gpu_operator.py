@@ -326,7 +326,9 @@ def test_bf16_strided_lidar_dense(npc, orc, cout):
 
 def test_bf16_indoor_surface(npc, orc):
     """Config-4 geometry: surface-sampled room, neighbors concentrated in the
-    cells a plane crosses (up to ~10 per (row, cell))."""
+    cells a plane crosses (up to ~10 per (row, cell)).  Super-tiles whose halo
+    exceeds the cap run as items of halo-segment records (partial (row, cell)
+    sums rounded per record), hence the 2^-8 emulation bound."""
     from paper_2511_23227_b200.synthetic import gen_indoor_fragment
     n = 40000
     xyz, area = gen_indoor_fragment(n, 11)
@@ -342,9 +344,12 @@ def test_bf16_indoor_surface(npc, orc):
     assert all(v_["overflow"] == 0 for v_ in st.values()), st
     ti, tj, tk = op.cached_triplets().numpy()
     efo, egi, egw = _emulate_tc(ti, tj, tk, n, n, w, f, go)
-    assert rel(out.cpu().numpy()[:, 0], efo) <= 2e-5
-    assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= 2e-5
-    assert rel(res.grad_w.cpu().numpy()[:, 0], egw) <= 2e-5
+    assert rel(out.cpu().numpy()[:, 0], efo) <= 2 ** -8
+    assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= 2 ** -8
+    assert rel(res.grad_w.cpu().numpy()[:, 0], egw) <= 2 ** -8
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
+                                go.astype(np.float64))
+    assert max(rel(out.cpu(), fo), rel(res.grad_in.cpu(), gi), rel(res.grad_w.cpu(), gw)) <= 1e-2
 
 
 @pytest.mark.slow
