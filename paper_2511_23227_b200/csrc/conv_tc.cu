@@ -1063,6 +1063,19 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
   for (int qi = 0; qi < NQ; ++qi) {
     if (cm[qi] >= 2u) {
       const uint32_t c = (it[qi] >> 7) & 255u, eo = it[qi] >> 16;
+      if (cm[qi] == 2u) {  // at most two entries per row: one packed bf16x2 add
+        uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
+        if (c > 0u) w0 = lds128(s_halo + static_cast<uint32_t>(ents[eo]) * 128u + l8x16);
+        if (c > 1u) w1 = lds128(s_halo + static_cast<uint32_t>(ents[eo + 1]) * 128u + l8x16);
+        uint4 o;
+        o.x = add_bf16x2_rn(w0.x, w1.x);
+        o.y = add_bf16x2_rn(w0.y, w1.y);
+        o.z = add_bf16x2_rn(w0.z, w1.z);
+        o.w = add_bf16x2_rn(w0.w, w1.w);
+        const uint32_t r = it[qi] & 127u;
+        sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), o);
+        continue;
+      }
       float acc[8];
 #pragma unroll
       for (int x = 0; x < 8; ++x) acc[x] = 0.f;

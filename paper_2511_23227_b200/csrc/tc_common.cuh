@@ -215,6 +215,13 @@ __device__ __forceinline__ void acc_bf16x2(float& lo_acc, float& hi_acc, uint32_
   asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(lo_acc) : "h"(lo));
   asm("add.rn.f32.bf16 %0, %1, %0;" : "+f"(hi_acc) : "h"(hi));
 }
+// a + b per bf16 lane, rounded once (exact sums of two bf16 values round
+// identically through fp32, so this matches the fp32-accumulate path)
+__device__ __forceinline__ uint32_t add_bf16x2_rn(uint32_t a, uint32_t b) {
+  uint32_t r;
+  asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   uint32_t r;
   asm("cvt.rn.bf16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
