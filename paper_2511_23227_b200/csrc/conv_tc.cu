@@ -1033,16 +1033,10 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
   uint32_t it[NQ], cm[NQ];
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) it[qi] = items[(wig + NW * qi) * 4 + sub_l];
+  // items are sorted by count (descending), so a quad's largest count is
+  // its first item's (a broadcast load)
 #pragma unroll
-  for (int qb = 0; qb < NQ; qb += 4) {
-    uint32_t packed = 0;
-#pragma unroll
-    for (int x = 0; x < 4 && qb + x < NQ; ++x) packed |= ((it[qb + x] >> 7) & 255u) << (8 * x);
-    packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 8));
-    packed = __vmaxu4(packed, __shfl_xor_sync(0xffffffffu, packed, 16));
-#pragma unroll
-    for (int x = 0; x < 4 && qb + x < NQ; ++x) cm[qb + x] = (packed >> (8 * x)) & 0xFFu;
-  }
+  for (int qi = 0; qi < NQ; ++qi) cm[qi] = (items[(wig + NW * qi) * 4] >> 7) & 255u;
   // pass 1: quads whose rows have at most one entry: zero rows / exact bf16 copies
   uint4 v[NQ];
 #pragma unroll
