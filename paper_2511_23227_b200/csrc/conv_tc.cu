@@ -1023,9 +1023,12 @@ static_assert(B_COUNT <= 48, "barrier region");
 // count 1 -> exact bf16 copy of the halo row, count >= 2 -> fp32 sum
 // (FHADD.BF16) rounded once to bf16.  All loads of the warp's quads are issued
 // before their uses (ILP), stores go to the SW128 K-major A tile.
-template <int NW>
+// wait_slot() is called once, before the first store into the A slot, so the
+// item / halo loads of the copy pass overlap the wait for the slot.
+template <int NW, typename WaitSlot>
 __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16_t* ents,
-                                                uint32_t s_halo, uint32_t s_A, int wig, int lane) {
+                                                uint32_t s_halo, uint32_t s_A, int wig, int lane,
+                                                WaitSlot&& wait_slot) {
   constexpr int NQ = (TM / 4) / NW;  // quads per warp, round-robin over count-sorted items
   const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
   const int sub_l = lane >> 3;
@@ -1045,6 +1048,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
     if (cm[qi] <= 1u && ((it[qi] >> 7) & 255u) == 1u)
       v[qi] = lds128(s_halo + static_cast<uint32_t>(ents[it[qi] >> 16]) * 128u + l8x16);
   }
+  wait_slot();
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     if (cm[qi] <= 1u) {
@@ -1099,7 +1103,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
 template <int NW>
 __device__ __noinline__ void aggregate_stage_l2(const uint8_t* blk, const uint16_t* ents,
                                                 uint32_t s_halo, uint32_t s_A, int wig, int lane) {
-  aggregate_stage<NW>(blk, ents, s_halo, s_A, wig, lane);
+  aggregate_stage<NW>(blk, ents, s_halo, s_A, wig, lane, [] {});
 }
 
 // Input channels come in a.nci chunks of 64: each super-tile runs the cells
@@ -1298,16 +1302,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             const uint32_t ds = d_it % NSDt, as = a_it % NSA;
             mbar_wait(bar(B_D_FULL + ds), (d_it / NSDt) & 1);
             if (wig == 0 && lane == 0) tev(d_it, 1);
-            mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
-            if (wig == 0 && lane == 0) tev(a_it, 2);
             const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
             const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
-            if (src == kFitsSlot)  // (separate instantiations keep shared-memory loads)
+            auto wait_a = [&] {
+              mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
+              if (wig == 0 && lane == 0) tev(a_it, 2);
+            };
+            if (src == kFitsSlot) {  // (separate instantiations keep shared-memory loads)
               aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512),
-                                               s_halo, s_a + as * 16384u, wig, lane);
-            else
+                                               s_halo, s_a + as * 16384u, wig, lane, wait_a);
+            } else {
+              wait_a();
               aggregate_stage_l2<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512),
                                                   s_halo, s_a + as * 16384u, wig, lane);
+            }
             fence_proxy_async_smem();
             __syncwarp();
             if (wig == 0 && lane == 0) tev(a_it, 3);
@@ -1593,16 +1601,20 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         if (static_cast<int>(a_it % WG_GROUPS) == grp) {
           const uint32_t ds = d_it % WNSD, as = a_it % WG_NSA;
           mbar_wait(bar(W_D_FULL + ds), (d_it / WNSD) & 1);
-          mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
           const int ncell = (k_begin + 2 * p + 1 < K) ? 2 : 1;
+          bool waited = false;
+          auto wait_a = [&] {
+            if (!waited) mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
+            waited = true;
+          };
           for (int half = 0; half < ncell; ++half) {
             const uint8_t* slot = g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES;
             const uint32_t src = BIG ? dsrc[2 * ds + half] : kFitsSlot;
             if (src == kFitsSlot)
               aggregate_stage<FWD_AGG_WARPS / WG_GROUPS>(
                   slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
-                  s_a + as * 32768u + half * 16384u, wig, lane);
-            else
+                  s_a + as * 32768u + half * 16384u, wig, lane, wait_a);
+            else if ((wait_a(), true))
               aggregate_stage_l2<FWD_AGG_WARPS / WG_GROUPS>(
                   slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512), s_halo,
                   s_a + as * 32768u + half * 16384u, wig, lane);
