@@ -131,6 +131,17 @@ __global__ void k_inverse_perm(const uint32_t* __restrict__ perm, int64_t n,
   if (p < n) inv[perm[p]] = static_cast<uint32_t>(p);
 }
 
+__host__ __device__ __forceinline__ uint32_t item_encode(uint32_t r, uint32_t count, uint32_t eo) {
+  return (8u * r + (r & 7u)) | (count << 10) | (eo << 18);
+}
+__device__ __forceinline__ uint32_t item_count(uint32_t it) { return (it >> 10) & 255u; }
+__device__ __forceinline__ uint32_t item_eo(uint32_t it) { return it >> 18; }
+// byte offset of the item's row, 16-byte chunk `l8x16` (= (lane & 7) << 4), in
+// a SWIZZLE_128B K-major tile
+__device__ __forceinline__ uint32_t item_sw128(uint32_t it, uint32_t l8x16) {
+  return ((it << 4) & 0x3FF0u) ^ l8x16;
+}
+
 // Entry filter of a plan record: only the entries whose permuted column lies
 // in [clo, chi) (a halo segment) and, among those, whose rank (order among
 // the row's entries of that cell, CSR order) lies in [rlo, rhi).  Records
@@ -242,7 +253,9 @@ __device__ __forceinline__ void for_row_entries(const int64_t* row_ptr, const ui
 // Per super-tile: halo (sorted unique permuted neighbor rows), per-(sub-tile,
 // cell) item lists (rows ordered by entry count, descending) and u16 halo
 // indices of the entries.  Block layout: u32 item[128] | u16 entry[E] (pad 16 B)
-//   item = r | count << 7 | entry_offset << 16   (count <= 254)
+//   item = rs | count << 10 | entry_offset << 18   (count <= 254, offset < 16384)
+//   rs = 8 r + (r & 7): rs << 4 is row r's byte offset in a SWIZZLE_128B tile
+//   before the lane's 16-byte chunk is XOR-ed in
 __global__ void __launch_bounds__(512) k_plan_super(
     const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
     const uint32_t* __restrict__ kk, const uint32_t* __restrict__ perm_rows,
@@ -461,8 +474,8 @@ __global__ void __launch_bounds__(512) k_plan_super(
         if (c == v) {
           const int before = __popc(m & lt);
           const int eo = ebase + v * before;
-          items[pos + before] = static_cast<uint32_t>(r) | (static_cast<uint32_t>(c) << 7) |
-                                (static_cast<uint32_t>(eo) << 16);
+          items[pos + before] = item_encode(static_cast<uint32_t>(r), static_cast<uint32_t>(c),
+                                            static_cast<uint32_t>(eo));
           eoff[(g * K + k) * TM + r] = static_cast<uint16_t>(eo);
         }
         pos += __popc(m);
@@ -1039,28 +1052,27 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
   // items are sorted by count (descending), so a quad's largest count is
   // its first item's (a broadcast load)
 #pragma unroll
-  for (int qi = 0; qi < NQ; ++qi) cm[qi] = (items[(wig + NW * qi) * 4] >> 7) & 255u;
+  for (int qi = 0; qi < NQ; ++qi) cm[qi] = item_count(items[(wig + NW * qi) * 4]);
   // pass 1: quads whose rows have at most one entry: zero rows / exact bf16 copies
   uint4 v[NQ];
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     v[qi] = make_uint4(0, 0, 0, 0);
-    if (cm[qi] <= 1u && ((it[qi] >> 7) & 255u) == 1u)
-      v[qi] = lds128(s_halo + static_cast<uint32_t>(ents[it[qi] >> 16]) * 128u + l8x16);
+    if (cm[qi] <= 1u && item_count(it[qi]) == 1u)
+      v[qi] = lds128(s_halo + static_cast<uint32_t>(ents[item_eo(it[qi])]) * 128u + l8x16);
   }
   wait_slot();
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     if (cm[qi] <= 1u) {
-      const uint32_t r = it[qi] & 127u;
-      sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), v[qi]);
+      sts128(s_A + item_sw128(it[qi], l8x16), v[qi]);
     }
   }
   // pass 2: quads with a row of >= 2 entries: fp32 sums rounded once to bf16
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     if (cm[qi] >= 2u) {
-      const uint32_t c = (it[qi] >> 7) & 255u, eo = it[qi] >> 16;
+      const uint32_t c = item_count(it[qi]), eo = item_eo(it[qi]);
       if (cm[qi] == 2u) {  // at most two entries per row: one packed bf16x2 add
         uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
         if (c > 0u) w0 = lds128(s_halo + static_cast<uint32_t>(ents[eo]) * 128u + l8x16);
@@ -1070,8 +1082,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
         o.y = add_bf16x2_rn(w0.y, w1.y);
         o.z = add_bf16x2_rn(w0.z, w1.z);
         o.w = add_bf16x2_rn(w0.w, w1.w);
-        const uint32_t r = it[qi] & 127u;
-        sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), o);
+        sts128(s_A + item_sw128(it[qi], l8x16), o);
         continue;
       }
       float acc[8];
@@ -1095,8 +1106,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
       o.y = pack_bf16x2(acc[2], acc[3]);
       o.z = pack_bf16x2(acc[4], acc[5]);
       o.w = pack_bf16x2(acc[6], acc[7]);
-      const uint32_t r = it[qi] & 127u;
-      sts128(s_A + r * 128u + ((l8x16 ^ ((r & 7u) << 4)) & 0x70u), o);
+      sts128(s_A + item_sw128(it[qi], l8x16), o);
     }
   }
 }
