@@ -1294,7 +1294,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     // ------------------------------ aggregation ----------------------------
     const int aw = warp - FWD_AGG_WARP0;
     const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
-    uint32_t a_it = 0, d_it = 0;
+    uint32_t a_it = 0;  // pipeline position of the current (record, chunk)'s first stage
     for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
     for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
       const uint2 sp = a.sup[s];
@@ -1306,38 +1306,37 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat + c * CH,
                                          s_halo, 32 * aw + lane, fstride);
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
-      for (int k = 0; k < K; ++k) {
-        for (int g = 0; g < nsub; ++g) {
-          if (static_cast<int>(a_it % AGG_GROUPS) == grp) {
-            const uint32_t ds = d_it % NSDt, as = a_it % NSA;
-            mbar_wait(bar(B_D_FULL + ds), (d_it / NSDt) & 1);
-            if (wig == 0 && lane == 0) tev(d_it, 1);
-            const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
-            const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
-            auto wait_a = [&] {
-              mbar_wait(bar(B_A_EMPTY + as), ((a_it / NSA) & 1) ^ 1);
-              if (wig == 0 && lane == 0) tev(a_it, 2);
-            };
-            if (src == kFitsSlot) {  // (separate instantiations keep shared-memory loads)
-              aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512),
-                                               s_halo, s_a + as * 16384u, wig, lane, wait_a);
-            } else {
-              wait_a();
-              aggregate_stage_l2<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512),
-                                                  s_halo, s_a + as * 16384u, wig, lane);
-            }
-            fence_proxy_async_smem();
-            __syncwarp();
-            if (wig == 0 && lane == 0) tev(a_it, 3);
-            if (lane == 0) {
-              mbar_arrive(bar(B_A_FULL + as));
-              mbar_arrive(bar(B_D_EMPTY + ds));
-            }
-          }
-          ++a_it;
-          ++d_it;
+      // this group's stages of the (record, chunk): every AGG_GROUPS-th one
+      // (stage index = pipeline position; slot / parity derive from it)
+      const uint32_t n_st = static_cast<uint32_t>(K * nsub);
+      const uint32_t first = a_it + ((static_cast<uint32_t>(grp) - a_it) & (AGG_GROUPS - 1));
+      for (uint32_t j = first; j < a_it + n_st; j += AGG_GROUPS) {
+        const uint32_t ds = j % NSDt, as = j % NSA;
+        mbar_wait(bar(B_D_FULL + ds), (j / NSDt) & 1);
+        if (wig == 0 && lane == 0) tev(j, 1);
+        const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
+        const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
+        auto wait_a = [&] {
+          mbar_wait(bar(B_A_EMPTY + as), ((j / NSA) & 1) ^ 1);
+          if (wig == 0 && lane == 0) tev(j, 2);
+        };
+        if (src == kFitsSlot) {  // (separate instantiations keep shared-memory loads)
+          aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512),
+                                           s_halo, s_a + as * 16384u, wig, lane, wait_a);
+        } else {
+          wait_a();
+          aggregate_stage_l2<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512),
+                                              s_halo, s_a + as * 16384u, wig, lane);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (wig == 0 && lane == 0) tev(j, 3);
+        if (lane == 0) {
+          mbar_arrive(bar(B_A_FULL + as));
+          mbar_arrive(bar(B_D_EMPTY + ds));
         }
       }
+      a_it += n_st;
       }
     }
   } else {
