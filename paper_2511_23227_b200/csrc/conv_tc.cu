@@ -49,9 +49,9 @@ constexpr int CH = 64;
 constexpr int KMAX = 32;
 constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sorts in smem
 // A (sub-tile, cell) descriptor block: u32 item[128] | u16 entry[E].  Its
-// first BLOCK_MAX_BYTES (items + up to 768 entries) are staged in a shared-
+// first BLOCK_MAX_BYTES (items + up to 512 entries) are staged in a shared-
 // memory slot; the entries of larger blocks are read from L2 (global).
-constexpr int SLOT_ENTRIES = 768;
+constexpr int SLOT_ENTRIES = 512;
 constexpr int BLOCK_MAX_BYTES = 512 + 2 * SLOT_ENTRIES;
 constexpr int MAX_BLOCK_ENTRIES = 8192;  // planner cap per block
 constexpr uint32_t kOverflow = 0xFFFFFFFFu;
@@ -917,7 +917,7 @@ constexpr int FWD_THREADS = 32 * (FWD_W_WARP + 1);
 constexpr int FWD_ST = 2, FWD_HCAP = 928;  // 256-row super-tiles, halo <= 928 rows (116 KB)
 constexpr int NSA = 4;  // A stages (16 KB)
 constexpr int NSW = 3;  // W stages (NOUT x 128 B; 2 for NOUT = 256)
-constexpr int NSD = 8;  // stage-descriptor slots
+constexpr int NSD = 8;  // stage-descriptor slots (a multiple of AGG_GROUPS)
 // Wide outputs (NOUT = channels the pass writes): the W stages grow to
 // NOUT x 128 B (two stages, six descriptor slots); NOUT = 128 keeps the
 // 256-row super-tiles (TMEM 2 x 2 x 128 columns), NOUT = 256 uses 128-row
@@ -926,7 +926,10 @@ constexpr int FWD_HCAP1 = 672;  // halo rows of 128-row tiles (what fits beside 
 template <int NOUT>
 struct FwdCfg {
   static constexpr int nsw = NOUT == 64 ? NSW : 2;
-  static constexpr int nsd = NOUT == 64 ? NSD : 6;  // descriptor slots
+  // descriptor slots: a multiple of the aggregation groups, so a slot is
+  // always consumed by the same group (a waiter can then never be two
+  // barrier phases ahead, which a parity wait cannot tell apart)
+  static constexpr int nsd = NSD;
   static constexpr uint32_t wbytes = NOUT * 128;
   static constexpr int st = NOUT <= 128 ? FWD_ST : 1;
   static constexpr int acc_cols = st * NOUT;  // per TMEM buffer
@@ -961,6 +964,7 @@ __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
   return L;
 }
 
+static_assert(NSD % AGG_GROUPS == 0, "descriptor slots per group");
 static_assert(fwd_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
 static_assert(fwd_smem_layout<128>(FWD_HCAP).total <= 232448, "smem");
 static_assert(fwd_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
@@ -1417,7 +1421,7 @@ struct WgArgs {
 constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
 constexpr int WG_PAIRS = 7;      // cell pairs per CTA (cell group = 14 cells)
 constexpr int WG_NSA = 2;        // A pair stages (32 KB)
-constexpr int WG_NSD = 3;        // descriptor slots (2 blocks each)
+constexpr int WG_NSD = 4;        // descriptor slots (2 blocks each; a multiple of WG_GROUPS)
 constexpr int WG_NSG = 2;        // dense G sub-tile slots (NOUT x 256 B; 1 for NOUT = 256)
 constexpr int WG_GROUPS = 2;     // stage (cell pair) s is aggregated by warp group s % 2
 
@@ -1470,6 +1474,7 @@ enum : int {
 };
 static_assert(W_COUNT <= 24, "wgrad barrier region");
 
+static_assert(WG_NSD % WG_GROUPS == 0, "descriptor slots per group");
 static_assert(wg_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
 static_assert(wg_smem_layout<128>(FWD_HCAP).total <= 232448, "smem");
 static_assert(wg_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");

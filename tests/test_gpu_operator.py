@@ -352,6 +352,31 @@ def test_bf16_indoor_surface(npc, orc):
     assert max(rel(out.cpu(), fo), rel(res.grad_in.cpu(), gi), rel(res.grad_w.cpu(), gw)) <= 1e-2
 
 
+def test_bf16_wide_pipeline_repeated(npc, orc):
+    """Regression: with descriptor slots shared between aggregation groups, a
+    group could wait on a slot two barrier phases ahead (parity waits cannot
+    tell) and read a stale descriptor -- an intermittent illegal address on
+    128-channel passes.  Slots are now a multiple of the groups; repeated
+    128 -> 128 fwd+bwd steps on a surface cloud must run and agree bitwise."""
+    from paper_2511_23227_b200.synthetic import gen_indoor_fragment
+    n = 150000
+    xyz, area = gen_indoor_fragment(n, 11)
+    r = 2 * (25.0 / (np.pi * n / area)) ** 0.5
+    cl = npc.make_point_cloud(xyz)
+    w = orc.make_weights(3, 1, 128, 128, 5)
+    f, go = T(orc.gen_features(n, 1, 128, 6)), T(orc.gen_features(n, 1, 128, 7))
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
+    ref = None
+    for _ in range(8):
+        out = op.forward(cl, f)
+        res = op.backward(go)
+        torch.cuda.synchronize()
+        cur = (out.clone(), res.grad_in.clone(), res.grad_w.clone())
+        if ref is None:
+            ref = cur
+        assert all(torch.equal(a, b) for a, b in zip(cur, ref))
+
+
 @pytest.mark.slow
 def test_c2_bf16_fwd_bwd(npc, orc):
     """BASELINE config 2 (100K, C=64) on the tensor-core path, bound 1e-2."""
