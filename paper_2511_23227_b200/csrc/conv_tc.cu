@@ -1621,17 +1621,20 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
             if (!waited) mbar_wait(bar(W_A_EMPTY + as), ((a_it / WG_NSA) & 1) ^ 1);
             waited = true;
           };
-          for (int half = 0; half < ncell; ++half) {
+          // the group's warps split in two teams, one per cell of the pair
+          constexpr int TW = FWD_AGG_WARPS / WG_GROUPS / 2;
+          const int half = wig / TW, wq = wig % TW;
+          if (half < ncell) {
             const uint8_t* slot = g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES;
             const uint32_t src = BIG ? dsrc[2 * ds + half] : kFitsSlot;
             if (src == kFitsSlot)
-              aggregate_stage<FWD_AGG_WARPS / WG_GROUPS>(
-                  slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
-                  s_a + as * 32768u + half * 16384u, wig, lane, wait_a);
+              aggregate_stage<TW>(slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
+                                  s_a + as * 32768u + half * 16384u, wq, lane, wait_a);
             else if ((wait_a(), true))
-              aggregate_stage_l2<FWD_AGG_WARPS / WG_GROUPS>(
-                  slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512), s_halo,
-                  s_a + as * 32768u + half * 16384u, wig, lane);
+              aggregate_stage_l2<TW>(slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512),
+                                     s_halo, s_a + as * 32768u + half * 16384u, wq, lane);
+          } else {
+            wait_a();
           }
           fence_proxy_async_smem();
           __syncwarp();
