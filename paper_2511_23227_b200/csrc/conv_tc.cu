@@ -142,6 +142,14 @@ __device__ __forceinline__ uint32_t item_sw128(uint32_t it, uint32_t l8x16) {
   return ((it << 4) & 0x3FF0u) ^ l8x16;
 }
 
+// Position of the p-th item (count-sorted order) in the block: quad q = p / 4
+// goes to aggregation warp q % 4 as its quad q / 4; a warp's items are stored
+// [sub-row][quad], so a lane's eight items are 32 contiguous bytes and the
+// quads' first items (their largest counts) are the warp's first eight.
+__host__ __device__ __forceinline__ int item_slot(int p) {
+  return ((p >> 2) & 3) * 32 + (p & 3) * 8 + (p >> 4);
+}
+
 // Entry filter of a plan record: only the entries whose permuted column lies
 // in [clo, chi) (a halo segment) and, among those, whose rank (order among
 // the row's entries of that cell, CSR order) lies in [rlo, rhi).  Records
@@ -474,8 +482,9 @@ __global__ void __launch_bounds__(512) k_plan_super(
         if (c == v) {
           const int before = __popc(m & lt);
           const int eo = ebase + v * before;
-          items[pos + before] = item_encode(static_cast<uint32_t>(r), static_cast<uint32_t>(c),
-                                            static_cast<uint32_t>(eo));
+          items[item_slot(pos + before)] = item_encode(static_cast<uint32_t>(r),
+                                                       static_cast<uint32_t>(c),
+                                                       static_cast<uint32_t>(eo));
           eoff[(g * K + k) * TM + r] = static_cast<uint16_t>(eo);
         }
         pos += __popc(m);
@@ -1046,17 +1055,23 @@ template <int NW, typename WaitSlot>
 __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16_t* ents,
                                                 uint32_t s_halo, uint32_t s_A, int wig, int lane,
                                                 WaitSlot&& wait_slot) {
+  static_assert(NW == 4, "item layout (item_slot) is for four warps per A tile");
   constexpr int NQ = (TM / 4) / NW;  // quads per warp, round-robin over count-sorted items
   const uint32_t* items = reinterpret_cast<const uint32_t*>(blk);
   const int sub_l = lane >> 3;
   const uint32_t l8x16 = static_cast<uint32_t>(lane & 7) << 4;
   uint32_t it[NQ], cm[NQ];
-#pragma unroll
-  for (int qi = 0; qi < NQ; ++qi) it[qi] = items[(wig + NW * qi) * 4 + sub_l];
-  // items are sorted by count (descending), so a quad's largest count is
-  // its first item's (a broadcast load)
-#pragma unroll
-  for (int qi = 0; qi < NQ; ++qi) cm[qi] = item_count(items[(wig + NW * qi) * 4]);
+  {  // a lane's eight items (two 16-byte loads); the quads' first items
+     // (count-sorted: their largest counts) by broadcast loads
+    const uint4* iv = reinterpret_cast<const uint4*>(items + wig * 32 + sub_l * 8);
+    const uint4* fv = reinterpret_cast<const uint4*>(items + wig * 32);
+    const uint4 a0 = iv[0], a1 = iv[1], f0 = fv[0], f1 = fv[1];
+    it[0] = a0.x; it[1] = a0.y; it[2] = a0.z; it[3] = a0.w;
+    it[4] = a1.x; it[5] = a1.y; it[6] = a1.z; it[7] = a1.w;
+    cm[0] = item_count(f0.x); cm[1] = item_count(f0.y); cm[2] = item_count(f0.z);
+    cm[3] = item_count(f0.w); cm[4] = item_count(f1.x); cm[5] = item_count(f1.y);
+    cm[6] = item_count(f1.z); cm[7] = item_count(f1.w);
+  }
   // pass 1: quads whose rows have at most one entry: zero rows / exact bf16 copies
   uint4 v[NQ];
 #pragma unroll
