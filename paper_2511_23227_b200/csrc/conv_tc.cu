@@ -261,7 +261,9 @@ __device__ __forceinline__ void for_row_entries(const int64_t* row_ptr, const ui
 // Per super-tile: halo (sorted unique permuted neighbor rows), per-(sub-tile,
 // cell) item lists (rows ordered by entry count, descending) and u16 halo
 // indices of the entries.  Block layout: u32 item[128] | u16 entry[E] (pad 16 B)
-//   item = rs | count << 10 | entry_offset << 18   (count <= 254, offset < 16384)
+//   item = rs | count << 10 | x << 18   (count <= 254, x < 16384): x is the
+//   entry offset, or, in a quad whose rows have at most one entry, the row's
+//   one entry itself (its halo index)
 //   rs = 8 r + (r & 7): rs << 4 is row r's byte offset in a SWIZZLE_128B tile
 //   before the lane's 16-byte chunk is XOR-ed in
 __global__ void __launch_bounds__(512) k_plan_super(
@@ -511,6 +513,20 @@ __global__ void __launch_bounds__(512) k_plan_super(
       const int64_t boff = blk_off[static_cast<int64_t>(sub0 + g) * K + k];
       reinterpret_cast<uint16_t*>(blocks + boff + 512)[pos] = static_cast<uint16_t>(lo);
     });
+  }
+  __syncthreads();
+  // 7. in quads whose rows have at most one entry (the copy pass), a row's
+  //    item carries its entry's halo index instead of the entry offset
+  for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
+    const int64_t boff = blk_off[static_cast<int64_t>(sub0 + b / K) * K + b % K];
+    uint32_t* items = reinterpret_cast<uint32_t*>(blocks + boff);
+    const uint16_t* ents = reinterpret_cast<const uint16_t*>(blocks + boff + 512);
+    for (int p = lane; p < TM; p += 32) {
+      const uint32_t first = items[item_slot(p & ~3)];  // the quad's largest count
+      const uint32_t it = items[item_slot(p)];
+      if (((first >> 10) & 255u) <= 1u && ((it >> 10) & 255u) == 1u)
+        items[item_slot(p)] = (it & 0x3FFFFu) | (static_cast<uint32_t>(ents[it >> 18]) << 18);
+    }
   }
   if (tid == 0) halo_len[s] = static_cast<uint32_t>(H);
 }
@@ -1077,8 +1093,8 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
 #pragma unroll
   for (int qi = 0; qi < NQ; ++qi) {
     v[qi] = make_uint4(0, 0, 0, 0);
-    if (cm[qi] <= 1u && item_count(it[qi]) == 1u)
-      v[qi] = lds128(s_halo + static_cast<uint32_t>(ents[item_eo(it[qi])]) * 128u + l8x16);
+    if (cm[qi] <= 1u && item_count(it[qi]) == 1u)  // copy quads: x = the halo index
+      v[qi] = lds128(s_halo + item_eo(it[qi]) * 128u + l8x16);
   }
   wait_slot();
 #pragma unroll
