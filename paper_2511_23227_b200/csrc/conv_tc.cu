@@ -78,8 +78,6 @@ struct TcDirPlan {
   int n_items = 0;
   DevBuf<uint2> tiles;        // n_sub {first permuted row, rows (<= 128)}
   DevBuf<uint32_t> halo;      // n_super * hcap permuted source row of each halo row
-  DevBuf<uint2> runs;         // n_super * hcap copy runs {src row, dst row | len << 16}
-  DevBuf<uint32_t> n_runs;    // n_super
   DevBuf<uint32_t> halo_len;  // n_super (kOverflow marks a super-tile the planner rejected)
   DevBuf<uint32_t> blk_off;   // n_sub*K (+1) byte offsets of the stage-descriptor blocks
   DevBuf<uint8_t> blocks;
@@ -272,7 +270,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
     const uint32_t* __restrict__ inv_perm_cols, const uint2* __restrict__ sup,
     const uint2* __restrict__ tiles, const uint4* __restrict__ tfilter, int K, int st, int hcap,
     const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ sub_bad,
-    uint32_t* __restrict__ halo_out, uint2* __restrict__ runs_out, uint32_t* __restrict__ n_runs,
+    uint32_t* __restrict__ halo_out,
     uint32_t* __restrict__ halo_len, uint32_t* __restrict__ seg,
     uint8_t* __restrict__ blocks) {
   extern __shared__ __align__(16) uint8_t sm[];
@@ -430,42 +428,6 @@ __global__ void __launch_bounds__(512) k_plan_super(
     }
     return;
   }
-  // 4b. copy runs of consecutive rows: {src row, dst | len << 16}
-  {
-    const int per2 = (H + blockDim.x - 1) / blockDim.x;
-    const int a0 = tid * per2, a1 = min(H, a0 + per2);
-    int nst = 0;
-    for (int x = a0; x < a1; ++x)
-      if (x == 0 || buf[x] != buf[x - 1] + 1) ++nst;
-    int ri = nst;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int n = __shfl_up_sync(0xffffffffu, ri, o);
-      if (lane >= o) ri += n;
-    }
-    if (lane == 31) wsum[warp] = ri;
-    __syncthreads();
-    if (tid == 0) {
-      int acc = 0;
-      for (int w = 0; w < 16; ++w) {
-        const int v = wsum[w];
-        wsum[w] = acc;
-        acc += v;
-      }
-      n_runs[s] = acc;
-    }
-    __syncthreads();
-    int r0 = ri - nst + wsum[warp];
-    for (int x = a0; x < a1; ++x) {
-      if (x == 0 || buf[x] != buf[x - 1] + 1) {
-        int e = x + 1;
-        while (e < H && buf[e] == buf[e - 1] + 1) ++e;
-        runs_out[static_cast<int64_t>(s) * hcap + r0++] =
-            make_uint2(buf[x], static_cast<uint32_t>(x) | (static_cast<uint32_t>(e - x) << 16));
-      }
-    }
-  }
-  __syncthreads();
   // 5. items per (sub, cell) block: rows by count descending (stable in r)
   const unsigned lt = (1u << lane) - 1u;
   for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
@@ -545,8 +507,7 @@ struct PlanLevel {
   std::vector<uint32_t> nom;    // per tile nominal rows (128, 64, ..., 8)
   std::vector<uint32_t> maxc;   // per tile largest (row, cell) entry count
   std::vector<uint32_t> seg;    // per record: halo segments and their column boundaries
-  DevBuf<uint32_t> halo, n_runs, halo_len, blk_off;
-  DevBuf<uint2> runs;
+  DevBuf<uint32_t> halo, halo_len, blk_off;
   DevBuf<uint8_t> blocks;
   uint32_t block_bytes = 0;
   uint32_t max_blk = 0;      // largest descriptor block (bytes)
@@ -579,8 +540,6 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   exclusive_scan_u32(ctx, blk_size.get(), L.blk_off.get(), nblk + 1, &L.block_bytes);
   L.blocks.alloc(ctx, L.block_bytes);
   L.halo.alloc(ctx, static_cast<int64_t>(ns) * hcap);
-  L.runs.alloc(ctx, static_cast<int64_t>(ns) * hcap);
-  L.n_runs.alloc(ctx, ns);
   L.halo_len.alloc(ctx, ns);
   const size_t smem = MAXE_ST * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
   NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -590,7 +549,7 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
          static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K, st,
          hcap,
          static_cast<const uint32_t*>(L.blk_off.get()), static_cast<const uint32_t*>(sub_bad.get()),
-         L.halo.get(), L.runs.get(), L.n_runs.get(), L.halo_len.get(), d_seg.get(), L.blocks.get());
+         L.halo.get(), L.halo_len.get(), d_seg.get(), L.blocks.get());
   L.hl.resize(ns);
   L.maxc.resize(nt);
   NPCG_CUDA(cudaMemcpyAsync(L.hl.data(), L.halo_len.get(), ns * 4, cudaMemcpyDeviceToHost,
@@ -746,8 +705,6 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     P->n_super = static_cast<int>(L.sup.size());
     P->n_sub = static_cast<int>(L.tiles.size());
     P->halo = std::move(L.halo);
-    P->runs = std::move(L.runs);
-    P->n_runs = std::move(L.n_runs);
     P->halo_len = std::move(L.halo_len);
     P->blk_off = std::move(L.blk_off);
     P->blocks = std::move(L.blocks);
@@ -790,8 +747,6 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   P->n_super = static_cast<int>(ns);
   P->n_sub = static_cast<int>(nt);
   P->halo.alloc(ctx, ns * hcap);
-  P->runs.alloc(ctx, ns * hcap);
-  P->n_runs.alloc(ctx, ns);
   P->halo_len.alloc(ctx, ns);
   P->blk_off.alloc(ctx, nt * K + 1);
   P->blocks.alloc(ctx, bytes);
@@ -810,10 +765,6 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     }
     tiles_all.insert(tiles_all.end(), L.tiles.begin(), L.tiles.end());
     NPCG_CUDA(cudaMemcpyAsync(P->halo.get() + s0 * hcap, L.halo.get(), lns * hcap * 4,
-                              cudaMemcpyDeviceToDevice, ctx->stream));
-    NPCG_CUDA(cudaMemcpyAsync(P->runs.get() + s0 * hcap, L.runs.get(), lns * hcap * 8,
-                              cudaMemcpyDeviceToDevice, ctx->stream));
-    NPCG_CUDA(cudaMemcpyAsync(P->n_runs.get() + s0, L.n_runs.get(), lns * 4,
                               cudaMemcpyDeviceToDevice, ctx->stream));
     NPCG_CUDA(cudaMemcpyAsync(P->halo_len.get() + s0, L.halo_len.get(), lns * 4,
                               cudaMemcpyDeviceToDevice, ctx->stream));
@@ -908,8 +859,6 @@ __global__ void k_pack_w(const float* __restrict__ w, int K, int cin, int cout, 
 // ===========================================================================
 struct FwdArgs {
   const uint32_t* halo;
-  const uint2* runs;
-  const uint32_t* n_runs;
   const uint32_t* halo_len;
   const uint32_t* blk_off;
   const uint8_t* blocks;
@@ -1026,17 +975,6 @@ __device__ __forceinline__ void coop_load_halo(const uint32_t* rows, uint32_t H,
                reinterpret_cast<const uint8_t*>(feat + static_cast<int64_t>(rows[h]) * stride) + q * 16u);
   cp_async_wait_all();
 }
-// Issue the bulk copies of one super-tile halo (runs of consecutive rows).
-__device__ __forceinline__ void load_halo(const uint2* runs, uint32_t nr,
-                                          const __nv_bfloat16* feat, uint32_t s_halo,
-                                          uint32_t bar_full, int lane) {
-  for (uint32_t r = lane; r < nr; r += 32) {
-    const uint2 v = runs[r];
-    bulk_g2s(s_halo + (v.y & 0xFFFFu) * 128u, feat + static_cast<int64_t>(v.x) * CH,
-             (v.y >> 16) * 128u, bar_full);
-  }
-}
-
 // Entries of a staged block are in the slot, or in global memory (L2) when
 // the block did not fit (src = its byte offset, kFitsSlot when it fit).  The
 // L2 variant is an out-of-line call, keeping the hot loop's code compact.
@@ -1434,8 +1372,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
 // ===========================================================================
 struct WgArgs {
   const uint32_t* halo;
-  const uint2* runs;
-  const uint32_t* n_runs;
   const uint32_t* halo_len;
   const uint32_t* blk_off;
   const uint8_t* blocks;
@@ -2468,8 +2404,6 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   if (P->n_super == 0) return;
   FwdArgs a{};
   a.halo = P->halo.get();
-  a.runs = P->runs.get();
-  a.n_runs = P->n_runs.get();
   a.halo_len = P->halo_len.get();
   a.blk_off = P->blk_off.get();
   a.blocks = P->blocks.get();
@@ -2703,8 +2637,6 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
     WgArgs a{};
     a.halo = P->halo.get();
-    a.runs = P->runs.get();
-    a.n_runs = P->n_runs.get();
     a.halo_len = P->halo_len.get();
     a.blk_off = P->blk_off.get();
     a.blocks = P->blocks.get();
