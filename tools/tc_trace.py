@@ -25,3 +25,12 @@ d = lambda e: np.median(np.diff([t[s, e] for s in range(20, 400) if t[s, e] > 0]
 print("median per-stage interval: mma_start %.0f  agg_done %.0f  d_issue %.0f" % (d(4), d(3), d(0)))
 print("median latencies: d_issue->d_full %.0f  a_empty->agg_done %.0f  agg_done->mma_start %.0f  mma_start->mma_issued %.0f" % (v(0,1), v(2,3), v(3,4), v(4,5)))
 print("median d_full->a_empty %.0f" % v(1, 2))
+# halo switches: gap between consecutive MMA starts, at super-tile boundaries (54 stages per 2 x 128-row super-tile)
+ms = np.array([t[s, 4] for s in range(512) if t[s, 4] > 0])
+gaps = np.diff(ms)
+per = 2 * 27
+bnd = [gaps[i] for i in range(len(gaps)) if (i + 1) % per == 0]
+inner = [gaps[i] for i in range(len(gaps)) if (i + 1) % per != 0]
+print("MMA-start gaps: inner median %.0f mean %.0f | super-tile boundary median %.0f mean %.0f (n=%d)"
+      % (np.median(inner), np.mean(inner), np.median(bnd), np.mean(bnd), len(bnd)))
+print("boundary share of time: %.1f%%" % (100 * np.sum(bnd) / np.sum(gaps)))
