@@ -377,6 +377,45 @@ def test_bf16_wide_pipeline_repeated(npc, orc):
         assert all(torch.equal(a, b) for a, b in zip(cur, ref))
 
 
+@pytest.mark.parametrize("case", ["one_point", "five_points", "partial_tile", "isolated",
+                                  "empty_batch", "two_cloud_tiny"])
+def test_bf16_edge_cases(npc, orc, case):
+    """Tensor-core path on degenerate shapes: a single point, fewer rows than a
+    tile, partial last tiles, rows with only the self-neighbor, an empty batch
+    in a jagged cloud, a strided conv onto a handful of sites."""
+    rng_seed = {"one_point": 1, "five_points": 2, "partial_tile": 3, "isolated": 4,
+                "empty_batch": 5, "two_cloud_tiny": 6}[case]
+    off = None
+    if case == "one_point":
+        xyz = orc.gen_uniform_cube(1, 1.0, rng_seed); r = 0.3
+    elif case == "five_points":
+        xyz = orc.gen_uniform_cube(5, 1.0, rng_seed); r = 0.6
+    elif case == "partial_tile":
+        xyz = orc.gen_uniform_cube(300, 1.0, rng_seed); r = 0.25
+    elif case == "isolated":
+        xyz = orc.gen_uniform_cube(700, 1.0, rng_seed); r = 1e-4  # self-neighbor only
+    elif case == "empty_batch":
+        xyz = orc.gen_uniform_cube(900, 1.0, rng_seed); r = 0.2
+        off = np.array([0, 400, 400, 900], dtype=np.int64)
+    else:
+        xyz = orc.gen_uniform_cube(2000, 1.0, rng_seed); r = 0.3
+    cl = npc.make_point_cloud(xyz, off)
+    out_cl = npc.make_point_cloud(xyz[:7]) if case == "two_cloud_tiny" else cl
+    n_in, n_out = len(xyz), out_cl.n_points()
+    w = orc.make_weights(3, 1, 64, 64, 9)
+    f = orc.gen_features(n_in, 1, 64, 10)
+    go = orc.gen_features(n_out, 1, 64, 11)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
+    out = op.forward(cl, out_cl, T(f)) if out_cl is not cl else op.forward(cl, T(f))
+    res = op.backward(T(go))
+    ti, tj, tk = op.cached_triplets().numpy()
+    efo, egi, egw = _emulate_tc(ti, tj, tk, n_out, n_in, w, f, go)
+    assert out.shape == (n_out, 1, 64) and res.grad_in.shape == (n_in, 1, 64)
+    assert rel(out.cpu().numpy()[:, 0], efo) <= 2e-5
+    assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= 2e-5
+    assert rel(res.grad_w.cpu().numpy()[:, 0], egw) <= 2e-5
+
+
 @pytest.mark.slow
 def test_c2_bf16_fwd_bwd(npc, orc):
     """BASELINE config 2 (100K, C=64) on the tensor-core path, bound 1e-2."""
