@@ -6,7 +6,8 @@ repetition) plus the median row (repetition = -1).
 
     python tools/replay.py workload.tpl --c-in 64 --c-out 64 --reps 5 [--cpu] > rows.csv
 
-GPU executors: `gpu_tc` (tcgen05 bf16-operand path; C = 64, G = 1 only) and
+GPU executors: `gpu_tc` (tcgen05 bf16-operand path; G = 1, C_in and C_out
+multiples of 16 up to 256) and
 `gpu_exact` (fp32 CUDA-core engines).  The access counters and closed-form
 predictions of the reference's CPU executors have no GPU analogue and are
 written as 0; aux_bytes is the library's peak scratch allocation."""
@@ -64,7 +65,7 @@ def main():
     print(HEADER)
     kernels = ["mvmr", "vvor"] if a.kernel == "both" else [a.kernel]
     execs = [("gpu_exact", npc.Math.exact)]
-    if a.c_in == 64 and a.c_out == 64:
+    if all(c % 16 == 0 and 16 <= c <= 256 for c in (a.c_in, a.c_out)):
         execs.insert(0, ("gpu_tc", npc.Math.bf16))
     for kern in kernels:
         for name, math in execs:
