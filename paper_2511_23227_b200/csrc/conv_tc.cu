@@ -1230,10 +1230,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         const uint32_t ws = w_it % NSWt;
         mbar_wait(bar(B_W_FULL + ws), (w_it / NSWt) & 1);
         if (lane == 0) tev(a_it, 6);
-        for (int g = 0; g < nsub; ++g) {
-          const uint32_t as = a_it % NSA;
-          mbar_wait(bar(B_A_FULL + as), (a_it / NSA) & 1);
-          if (lane == 0) tev(a_it, 4);
+        // The sub-tiles' stages of cell k feed different accumulators, so
+        // whichever is aggregated first is issued first (each accumulator
+        // still sums its cells in plan order: deterministic).
+        auto issue = [&](int g) {
+          const uint32_t st = a_it + static_cast<uint32_t>(g);
+          const uint32_t as = st % NSA;
+          if (lane == 0) tev(st, 4);
           tc_fence_after();
           const uint32_t d = tmem + ab * Cfg::acc_cols + g * NOUT;
           // descriptor start-address field is in 16-byte units
@@ -1247,9 +1250,29 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             umma_commit(bar(B_A_EMPTY + as));
           }
           __syncwarp();
-          if (lane == 0) tev(a_it, 5);
-          ++a_it;
+          if (lane == 0) tev(st, 5);
+        };
+        if (nsub == 2) {
+          uint32_t todo = 3u;
+          while (todo) {
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              const uint32_t st = a_it + static_cast<uint32_t>(g);
+              if ((todo >> g) & 1u)
+                if (__shfl_sync(0xffffffffu, mbar_test(bar(B_A_FULL + st % NSA), (st / NSA) & 1), 0)) {
+                  issue(g);
+                  todo &= ~(1u << g);
+                }
+            }
+          }
+        } else {
+          for (int g = 0; g < nsub; ++g) {
+            const uint32_t st = a_it + static_cast<uint32_t>(g);
+            mbar_wait(bar(B_A_FULL + st % NSA), (st / NSA) & 1);
+            issue(g);
+          }
         }
+        a_it += static_cast<uint32_t>(nsub);
         if (elect_one()) umma_commit(bar(B_W_EMPTY + ws));
         __syncwarp();
         ++w_it;
