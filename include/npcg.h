@@ -84,7 +84,7 @@ typedef enum npcg_sort_axis {
 
 /* Arithmetic of the MVMR / VVOR engines. */
 typedef enum npcg_math {
-  NPCG_MATH_AUTO = 0,  /* tensor-core path where it applies (F32, G=1, K<=32, C_in and C_out
+  NPCG_MATH_AUTO = 0,  /* tensor-core path where it applies (F32, G=1, K<=128, C_in and C_out
                           multiples of 16 in [64, 256]), else EXACT */
   NPCG_MATH_EXACT = 1, /* CUDA cores in the API dtype (fp32 / fp64 FMA, fp32 accumulate for F32) */
   NPCG_MATH_BF16 = 2   /* tcgen05 tensor cores: bf16 operands, fp32 accumulate (F32 API only;

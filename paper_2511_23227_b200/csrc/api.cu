@@ -62,7 +62,7 @@ bool use_tc(const npcg_exec_config* cfg, npcg_dtype dtype, int64_t G, int64_t ci
     if (dtype != NPCG_F32) fail(NPCG_ERR_UNSUPPORTED, "bf16 math requires F32 tensors");
     if (!tc_supported(G, cin, cout, K, true))
       fail(NPCG_ERR_UNSUPPORTED,
-           "bf16 tensor-core path needs G=1, C_in, C_out multiples of 16 up to 256, K<=32");
+           "bf16 tensor-core path needs G=1, C_in, C_out multiples of 16 up to 256, K<=128");
     return true;
   }
   return dtype == NPCG_F32 && tc_supported(G, cin, cout, K);
@@ -780,7 +780,7 @@ npcg_status npcg_debug_trace_forward(npcg_context* ctx, npcg_neighbors* nb, cons
   if (!ctx || !nb || !trace) return NPCG_ERR_INVALID;
   return guard(ctx, [&] {
     if (nb->t == 0 || !tc_supported(1, 64, 64, nb->n_kernels))
-      fail(NPCG_ERR_UNSUPPORTED, "trace: tensor-core plan needs C=64, K<=32");
+      fail(NPCG_ERR_UNSUPPORTED, "trace: tensor-core plan needs K<=128");
     tc_trace_forward(ctx, nb, w, fin, fout, trace);
   });
 }

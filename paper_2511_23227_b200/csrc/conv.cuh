@@ -19,7 +19,7 @@ void vvor_cells(npcg_context* ctx, const CellPlan& cells, const T* gout, const T
                 int cin, int cout, T* grad);
 
 // ---- tensor-core engines (conv_tc.cu) --------------------------------------
-// True when the tcgen05 path handles this shape: G = 1, K <= 32, C_in and
+// True when the tcgen05 path handles this shape: G = 1, K <= 128 (t <= 5), C_in and
 // C_out multiples of 16 in [64, 256] (automatic choice) or [16, 256] (forced,
 // math = bf16); widths are zero-padded to 64 / 128 / 256 inside.
 bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t n_kernels, bool forced = false);

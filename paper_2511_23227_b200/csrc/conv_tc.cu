@@ -46,7 +46,8 @@ using namespace tc;
 
 constexpr int TM = 128;
 constexpr int CH = 64;
-constexpr int KMAX = 32;
+constexpr int KMAX = 128;   // kernel cells (t^3 <= 125: t = 1, 3, 5)
+constexpr int G_KMAX = 32;  // the gather engine's planner keeps per-cell arrays in static smem
 constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sorts in smem
 // A (sub-tile, cell) descriptor block: u32 item[128] | u16 entry[E].  Its
 // first BLOCK_MAX_BYTES (items + up to 512 entries) are staged in a shared-
@@ -179,8 +180,9 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
                                                     uint32_t* __restrict__ tile_maxc,
                                                     uint32_t* __restrict__ max_blk) {
   __shared__ uint32_t cnt[KMAX];
-  __shared__ uint16_t rc[TM][KMAX];   // all entries seen per (row, cell)
-  __shared__ uint16_t inc[TM][KMAX];  // entries within the rank filter
+  extern __shared__ uint16_t pc_dyn[];  // rc[TM][K]: all entries per (row, cell); inc[TM][K]: filtered
+  uint16_t* rc = pc_dyn;
+  uint16_t* inc = pc_dyn + TM * K;
   __shared__ int bad;
   __shared__ uint32_t s_maxc;
   const int r = threadIdx.x;
@@ -189,7 +191,7 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
     bad = 0;
     s_maxc = 0;
   }
-  for (int k = 0; k < KMAX; ++k) rc[r][k] = inc[r][k] = 0;
+  for (int k = 0; k < K; ++k) rc[r * K + k] = inc[r * K + k] = 0;
   __syncthreads();
   const uint2 tl = tiles[blockIdx.x];
   const EntryFilter f = EntryFilter::from(tfilter[blockIdx.x]);
@@ -202,22 +204,22 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
         if (pj < f.clo || pj >= f.chi) continue;
       }
       const uint32_t k = kk[e];
-      const uint32_t rank = rc[r][k];
-      if (rc[r][k] < 0xFFFFu) rc[r][k]++;
+      const uint32_t rank = rc[r * K + k];
+      if (rank < 0xFFFFu) rc[r * K + k] = static_cast<uint16_t>(rank + 1);
       if (rank >= f.rlo && rank < f.rhi) {
         atomicAdd(&cnt[k], 1u);
-        inc[r][k]++;
+        inc[r * K + k]++;
       }
     }
   }
   uint32_t mx = 0;
   for (int k = 0; k < K; ++k) {
-    if (inc[r][k] > 254) bad = 1;
-    mx = max(mx, static_cast<uint32_t>(rc[r][k]));
+    if (inc[r * K + k] > 254) bad = 1;
+    mx = max(mx, static_cast<uint32_t>(rc[r * K + k]));
   }
   atomicMax(&s_maxc, mx);
   __syncthreads();
-  if (r < K) {
+  if (r < K) {  // K <= KMAX = TM
     const uint32_t E = cnt[r];
     if (E > MAX_BLOCK_ENTRIES) bad = 1;
     const uint32_t bytes = 512u + ((2u * E + 15u) / 16u) * 16u;
@@ -533,7 +535,10 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   const int64_t nblk = static_cast<int64_t>(nt) * K;
   DevBuf<uint32_t> blk_size(ctx, nblk + 1), sub_bad(ctx, nt);
   NPCG_CUDA(cudaMemsetAsync(blk_size.get() + nblk, 0, 4, ctx->stream));
-  launch(ctx, "plan_counts", k_plan_counts, dim3(nt), dim3(TM), 0, row_ptr, kk, col, inv_perm_cols,
+  const size_t pc_smem = 2u * TM * static_cast<size_t>(K) * sizeof(uint16_t);
+  NPCG_CUDA(cudaFuncSetAttribute(k_plan_counts, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(pc_smem)));
+  launch(ctx, "plan_counts", k_plan_counts, dim3(nt), dim3(TM), pc_smem, row_ptr, kk, col, inv_perm_cols,
          perm_rows, static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K,
          blk_size.get(), sub_bad.get(), d_maxc.get(), d_maxblk.get());
   L.blk_off.alloc(ctx, nblk + 1);
@@ -892,6 +897,10 @@ constexpr int FWD_ST = 2, FWD_HCAP = 928;  // 256-row super-tiles, halo <= 928 r
 constexpr int NSA = 4;  // A stages (16 KB)
 constexpr int NSW = 3;  // W stages (NOUT x 128 B; 2 for NOUT = 256)
 constexpr int NSD = 8;  // stage-descriptor slots (a multiple of AGG_GROUPS)
+// per-CTA smem words: a super-tile's block offsets (st * K + 1 <= 2 * KMAX + 1)
+// followed by the descriptor slots' sources (<= 2 * WG_NSD)
+constexpr int OFFS_DSRC = 2 * KMAX + 4;
+constexpr int OFFS_WORDS = OFFS_DSRC + 8;
 // Wide outputs (NOUT = channels the pass writes): the W stages grow to
 // NOUT x 128 B (two stages, six descriptor slots); NOUT = 128 keeps the
 // 256-row super-tiles (TMEM 2 x 2 x 128 columns), NOUT = 256 uses 128-row
@@ -933,8 +942,8 @@ __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
   L.tmem_slot = o;
   o += 16;
   L.offs = o;
-  o += 128 * 4;  // block offsets of the super-tile; [96, 128): slot sources
-  L.total = o + 1024;  // alignment slack
+  o += OFFS_WORDS * 4;  // block offsets of the super-tile, then the slot sources
+  L.total = o + 1024;   // alignment slack
   return L;
 }
 
@@ -1116,7 +1125,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
   const uint8_t* g_d = gbase + L.d;
-  uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + 96;  // per descriptor slot
+  uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + OFFS_DSRC;  // per descriptor slot
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) {
@@ -1445,7 +1454,7 @@ __host__ __device__ constexpr WgSmem wg_smem_layout(int hcap) {
   L.tmem_slot = o;
   o += 16;
   L.offs = o;
-  o += 128 * 4;  // block offsets of the super-tile; [96, 128): slot sources
+  o += OFFS_WORDS * 4;  // block offsets of the super-tile, then the slot sources
   L.total = o + 1024;
   return L;
 }
@@ -1485,7 +1494,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
   uint8_t* g_gt = gbase + L.gt;
   const uint8_t* g_d = gbase + L.d;
-  uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + 96;  // per descriptor half-slot
+  uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + OFFS_DSRC;  // per descriptor half-slot
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int K = a.K;
@@ -1775,12 +1784,12 @@ __global__ void __launch_bounds__(TM) k_gplan(const int64_t* __restrict__ row_pt
                                               uint32_t* __restrict__ blk_size,
                                               uint32_t* __restrict__ sub_bad,
                                               uint8_t* __restrict__ blocks) {
-  __shared__ uint8_t cnt[KMAX][TM], run[KMAX][TM];
-  __shared__ uint16_t fpos[KMAX][TM], xpos[KMAX][TM];
-  __shared__ int nfix_k[KMAX], next_k[KMAX], wsum[2][4], bad;
+  __shared__ uint8_t cnt[G_KMAX][TM], run[G_KMAX][TM];
+  __shared__ uint16_t fpos[G_KMAX][TM], xpos[G_KMAX][TM];
+  __shared__ int nfix_k[G_KMAX], next_k[G_KMAX], wsum[2][4], bad;
   const int r = threadIdx.x, lane = r & 31, warp = r >> 5;
   const int sub = blockIdx.x;
-  for (int k = 0; k < KMAX; ++k) {
+  for (int k = 0; k < G_KMAX; ++k) {
     cnt[k][r] = 0;
     run[k][r] = 0;
   }
@@ -1953,7 +1962,7 @@ __host__ __device__ inline GSmem g_smem_layout() {
   L.tmem_slot = o;
   o += 16;
   L.offs = o;
-  o += (G_ST * KMAX + 1) * 4;
+  o += (G_ST * G_KMAX + 1) * 4;
   L.total = o + 1024;
   return L;
 }
@@ -2366,12 +2375,13 @@ static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = fa
   return slot.get();
 }
 
-static bool use_gather_engine();
+static bool use_gather_engine_env();
+static bool use_gather_engine(int64_t K) { return use_gather_engine_env() && K <= G_KMAX; }
 static GatherPlan* gplan_fwd(npcg_context* ctx, npcg_neighbors* nb);
 static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb);
 
 void tc_prepare(npcg_context* ctx, npcg_neighbors* nb) {
-  if (use_gather_engine()) {
+  if (use_gather_engine(nb->n_kernels)) {
     gplan_fwd(ctx, nb);
     gplan_bwd(ctx, nb);
   }
@@ -2461,7 +2471,7 @@ void destroy_tc_plan(TcPlan* p) { delete p; }
 // default: 0.85 ms per 1M-point pass) or "gather" (A tiles gathered from L2
 // by cp.async, fixups on the SM: 0.99 ms; profiles/r1_pipeline_experiments.md).
 // NPCG_TC_ENGINE=gather selects the latter (read once per process).
-static bool use_gather_engine() {
+static bool use_gather_engine_env() {
   static int v = -1;
   if (v < 0) {
     const char* e = std::getenv("NPCG_TC_ENGINE");
@@ -2491,7 +2501,7 @@ static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
 
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
                 float* fout, int cin, int cout) {
-  if (use_gather_engine() && cin == CH && cout == CH) {
+  if (use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
     GatherPlan* G = gplan_fwd(ctx, nb);
     TcPlan* p = nb->tc.get();
     if (G->n_overflow < G->n_super) {
@@ -2603,7 +2613,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
   TcPlan* p = get_plan(ctx, nb);
   const int K = static_cast<int>(nb->n_kernels);
   bool g_converted = false;
-  if (grad_in && use_gather_engine() && cin == CH && cout == CH) {
+  if (grad_in && use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
     GatherPlan* G = gplan_bwd(ctx, nb);
     if (G->n_overflow < G->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
@@ -2694,7 +2704,7 @@ void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, con
   TcPlan* p = get_plan(ctx, nb);
   DevBuf<long long> tr(ctx, TRACE_STAGES * TRACE_EV);
   NPCG_CUDA(cudaMemsetAsync(tr.get(), 0, TRACE_STAGES * TRACE_EV * 8, ctx->stream));
-  if (use_gather_engine()) {
+  if (use_gather_engine(nb->n_kernels)) {
     GatherPlan* G = gplan_fwd(ctx, nb);
     convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in);
     p->saved_fin = fin;

@@ -416,6 +416,33 @@ def test_bf16_edge_cases(npc, orc, case):
     assert rel(res.grad_w.cpu().numpy()[:, 0], egw) <= 2e-5
 
 
+@pytest.mark.parametrize("t,cin,cout", [(5, 64, 64), (5, 128, 64), (1, 64, 128)])
+def test_bf16_kernel_resolutions(npc, orc, t, cin, cout):
+    """t = 5 (125 kernel cells) and t = 1 on the tensor cores (the reference's
+    geometry supports any odd t; K <= 128 runs on tcgen05).  The radius here
+    (~70 neighbors) overflows the 256-row halo cap and, at t = 1, puts all of
+    them in one cell, so rows run as split records (partial sums rounded per
+    record): emulation bound 2^-8."""
+    n = 6000
+    xyz = orc.gen_uniform_cube(n, 1.0, 41)
+    r = (1.8 if t == 3 else 2.6) * n ** (-1 / 3)
+    w = orc.make_weights(t, 1, cin, cout, 42)
+    f = orc.gen_features(n, 1, cin, 43)
+    go = orc.gen_features(n, 1, cout, 44)
+    ti, tj, tk = orc.build_triplets(xyz, xyz, r, t)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=t), npc.ExecConfig(math=npc.Math.bf16))
+    out = op.forward(npc.make_point_cloud(xyz), T(f))
+    res = op.backward(T(go))
+    efo, egi, egw = _emulate_tc(ti, tj, tk, n, n, w, f, go)
+    bound = 2 ** -8
+    assert rel(out.cpu().numpy()[:, 0], efo) <= bound
+    assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= bound
+    assert rel(res.grad_w.cpu().numpy()[:, 0], egw) <= bound
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
+                                go.astype(np.float64))
+    assert max(rel(out.cpu(), fo), rel(res.grad_in.cpu(), gi), rel(res.grad_w.cpu(), gw)) <= 1e-2
+
+
 @pytest.mark.slow
 def test_c2_bf16_fwd_bwd(npc, orc):
     """BASELINE config 2 (100K, C=64) on the tensor-core path, bound 1e-2."""
