@@ -1717,14 +1717,16 @@ done:
 // grad_w[k][m][c] = sum over CTAs x (fixed order) of partial[x][k][c][m]
 __global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, int K, int cin,
                                int cout, int cinp, int coutp, float* __restrict__ grad_w) {
-  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;  // (k, m, c)
+  // thread = (k, c, m) with m fastest: the partial reads are coalesced (the
+  // large side); the transposed grad_w stores are the small side
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<int64_t>(K) * cin * cout) return;
-  const int k = static_cast<int>(idx / (cin * cout)), m = static_cast<int>((idx / cin) % cout),
-            c = static_cast<int>(idx % cin);
+  const int k = static_cast<int>(idx / (cin * cout)), c = static_cast<int>((idx / cout) % cin),
+            m = static_cast<int>(idx % cout);
   float s = 0.f;
   for (int x = 0; x < n_part; ++x)
     s += partial[((static_cast<int64_t>(x) * K + k) * cinp + c) * coutp + m];
-  grad_w[idx] = s;
+  grad_w[(static_cast<int64_t>(k) * cout + m) * cin + c] = s;
 }
 
 // ===========================================================================
