@@ -1,0 +1,58 @@
+"""GPU: seeded random shapes through the tensor-core path (bf16 operands,
+fp32 accumulate) -- cloud size, density, clustering, two-cloud strided
+builds, channel widths (multiples of 16 up to 256) and kernel resolution --
+each checked against the exact numpy emulation of the engine's arithmetic
+(<= 2^-8: split records round partial sums per record) and the fp64 dense
+oracle (<= 1e-2), plus bitwise determinism."""
+import numpy as np
+import pytest
+import torch
+
+from test_gpu_operator import T, _emulate_tc, rel
+
+pytestmark = pytest.mark.gpu
+
+WIDTHS = [16, 32, 48, 64, 96, 128, 192, 256]
+
+
+def _case(seed):
+    rng = np.random.default_rng(seed)
+    n = int(rng.choice([1, 17, 129, 700, 3000, 5000]))
+    t = int(rng.choice([1, 3, 3, 3, 5]))
+    cin, cout = (int(x) for x in rng.choice(WIDTHS, 2))
+    dens = float(rng.choice([0.6, 1.0, 1.8, 2.4]))
+    clustered = bool(rng.integers(0, 2))
+    strided = bool(rng.integers(0, 2)) and n > 20
+    return n, t, cin, cout, dens, clustered, strided
+
+
+@pytest.mark.parametrize("seed", range(32))
+def test_fuzz_tensor_core_path(npc, orc, ref, seed):
+    n, t, cin, cout, dens, clustered, strided = _case(seed)
+    if clustered:
+        xyz = ref.gen_gaussian_clusters(n, max(1, n // 300), 2.0, 0.25, 100 + seed)
+    else:
+        xyz = orc.gen_uniform_cube(n, 1.0, 100 + seed)
+    r = dens * max(n, 1) ** (-1 / 3)
+    cl = npc.make_point_cloud(xyz)
+    out_cl = npc.make_point_cloud(xyz[: max(1, n // 4)]) if strided else cl
+    n_out = out_cl.n_points()
+    w = orc.make_weights(t, 1, cin, cout, 200 + seed)
+    f = orc.gen_features(n, 1, cin, 300 + seed)
+    go = orc.gen_features(n_out, 1, cout, 400 + seed)
+    ti, tj, tk = orc.build_triplets(out_cl.xyz.cpu().numpy(), xyz, r, t)
+    if len(ti) * max(cin, cout) > 60_000_000:  # keep the numpy references in memory / seconds
+        pytest.skip(f"{len(ti)} pairs x {max(cin, cout)} channels: beyond the numpy check size")
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=t), npc.ExecConfig(math=npc.Math.bf16))
+    out = op.forward(cl, out_cl, T(f)) if strided else op.forward(cl, T(f))
+    res = op.backward(T(go))
+    out2 = op.forward(cl, out_cl, T(f)) if strided else op.forward(cl, T(f))
+    assert torch.equal(out, out2)
+    ti, tj, tk = op.cached_triplets().numpy()  # the library's own triplets (by_k order)
+    efo, egi, egw = _emulate_tc(ti, tj, tk, n_out, n, w, f, go)
+    assert rel(out.cpu().numpy()[:, 0], efo) <= 2 ** -8
+    assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= 2 ** -8
+    assert rel(res.grad_w.cpu().numpy()[:, 0], egw) <= 2 ** -8
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n_out,
+                                go.astype(np.float64))
+    assert max(rel(out.cpu(), fo), rel(res.grad_in.cpu(), gi), rel(res.grad_w.cpu(), gw)) <= 1e-2
