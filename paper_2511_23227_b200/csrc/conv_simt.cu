@@ -45,13 +45,26 @@ __global__ void __launch_bounds__(256) k_mvmr_rows(CsrView csr, const T* __restr
     for (int c0 = 0; c0 < cin; c0 += 32) {
       const T fv = (c0 + lane < cin) ? f[c0 + lane] : T(0);
       const int cn = cin - c0 < 32 ? cin - c0 : 32;
-      for (int cc = 0; cc < cn; ++cc) {
-        const T fc = __shfl_sync(0xffffffffu, fv, cc);
-        const T* wr = wm + static_cast<int64_t>(c0 + cc) * cout;
+      if (cn == 32) {  // full chunk: unrolled, so the W loads of several channels are in flight
+#pragma unroll 8
+        for (int cc = 0; cc < 32; ++cc) {
+          const T fc = __shfl_sync(0xffffffffu, fv, cc);
+          const T* wr = wm + static_cast<int64_t>(c0 + cc) * cout;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-          const int m = lane + 32 * r;
-          if (m_base + m < cout) acc[r] = fma(wr[m], fc, acc[r]);
+          for (int r = 0; r < R; ++r) {
+            const int m = lane + 32 * r;
+            if (m_base + m < cout) acc[r] = fma(__ldg(wr + m), fc, acc[r]);
+          }
+        }
+      } else {
+        for (int cc = 0; cc < cn; ++cc) {
+          const T fc = __shfl_sync(0xffffffffu, fv, cc);
+          const T* wr = wm + static_cast<int64_t>(c0 + cc) * cout;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int m = lane + 32 * r;
+            if (m_base + m < cout) acc[r] = fma(wr[m], fc, acc[r]);
+          }
         }
       }
     }
