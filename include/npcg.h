@@ -243,6 +243,20 @@ npcg_status npcg_vvor(npcg_context* ctx, npcg_dtype dtype, const void* gout, int
                       const void* fin, int64_t n_fin, int64_t groups, int64_t c_in,
                       int64_t c_out, const npcg_triplets* triplets, int64_t n_kernels,
                       const npcg_exec_config* cfg, void* grad);
+/* The same three engines under the names of SURVEY.md §8(b)'s export list
+ * (identical arguments and behaviour). */
+npcg_status npcg_mvmr_fwd(npcg_context* ctx, npcg_dtype dtype, const void* w, int64_t t,
+                          int64_t groups, int64_t c_in, int64_t c_out, const void* fin,
+                          int64_t n_fin, const npcg_triplets* triplets, int64_t n_out,
+                          const npcg_exec_config* cfg, void* out);
+npcg_status npcg_mvmr_dgrad(npcg_context* ctx, npcg_dtype dtype, const void* w, int64_t t,
+                            int64_t groups, int64_t c_in, int64_t c_out, const void* gout,
+                            int64_t n_gout, const npcg_triplets* triplets, int64_t n_in,
+                            const npcg_exec_config* cfg, void* out);
+npcg_status npcg_vvor_wgrad(npcg_context* ctx, npcg_dtype dtype, const void* gout, int64_t n_gout,
+                            const void* fin, int64_t n_fin, int64_t groups, int64_t c_in,
+                            int64_t c_out, const npcg_triplets* triplets, int64_t n_kernels,
+                            const npcg_exec_config* cfg, void* grad);
 
 /* ---- operator path (PointConvOp with a cached neighbor structure) --------- */
 /* conv_op.hpp:129-175 forward over a triplet handle (the PointConvOp cache,

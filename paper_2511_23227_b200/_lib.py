@@ -77,6 +77,12 @@ _SIGS = {
                                        C.POINTER(npcg_exec_config), _P]),
     "npcg_vvor": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _I64, _I64, _I64,
                             C.POINTER(npcg_triplets), _I64, C.POINTER(npcg_exec_config), _P]),
+    "npcg_mvmr_fwd": (C.c_int, [_P, C.c_int, _P, _I64, _I64, _I64, _I64, _P, _I64,
+                                C.POINTER(npcg_triplets), _I64, C.POINTER(npcg_exec_config), _P]),
+    "npcg_mvmr_dgrad": (C.c_int, [_P, C.c_int, _P, _I64, _I64, _I64, _I64, _P, _I64,
+                                  C.POINTER(npcg_triplets), _I64, C.POINTER(npcg_exec_config), _P]),
+    "npcg_vvor_wgrad": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _I64, _I64, _I64,
+                                  C.POINTER(npcg_triplets), _I64, C.POINTER(npcg_exec_config), _P]),
     "npcg_conv_forward": (C.c_int, [_P, _P, C.c_int, _P, _I64, _I64, _I64, _P,
                                     C.POINTER(npcg_exec_config), _P]),
     "npcg_conv_backward": (C.c_int, [_P, _P, C.c_int, _P, _I64, _I64, _I64, _P, _P,

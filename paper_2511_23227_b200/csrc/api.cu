@@ -799,3 +799,27 @@ npcg_status npcg_voxel_downsample(npcg_context* ctx, const npcg_cloud* cloud, do
 }
 
 }  // extern "C"
+
+// SURVEY.md §8(b) export names for the three engines
+extern "C" {
+npcg_status npcg_mvmr_fwd(npcg_context* ctx, npcg_dtype dtype, const void* w, int64_t t,
+                          int64_t groups, int64_t c_in, int64_t c_out, const void* fin,
+                          int64_t n_fin, const npcg_triplets* triplets, int64_t n_out,
+                          const npcg_exec_config* cfg, void* out) {
+  return npcg_mvmr(ctx, dtype, w, t, groups, c_in, c_out, fin, n_fin, triplets, n_out, cfg, out);
+}
+npcg_status npcg_mvmr_dgrad(npcg_context* ctx, npcg_dtype dtype, const void* w, int64_t t,
+                            int64_t groups, int64_t c_in, int64_t c_out, const void* gout,
+                            int64_t n_gout, const npcg_triplets* triplets, int64_t n_in,
+                            const npcg_exec_config* cfg, void* out) {
+  return npcg_mvmr_transposed(ctx, dtype, w, t, groups, c_in, c_out, gout, n_gout, triplets, n_in,
+                              cfg, out);
+}
+npcg_status npcg_vvor_wgrad(npcg_context* ctx, npcg_dtype dtype, const void* gout, int64_t n_gout,
+                            const void* fin, int64_t n_fin, int64_t groups, int64_t c_in,
+                            int64_t c_out, const npcg_triplets* triplets, int64_t n_kernels,
+                            const npcg_exec_config* cfg, void* grad) {
+  return npcg_vvor(ctx, dtype, gout, n_gout, fin, n_fin, groups, c_in, c_out, triplets, n_kernels,
+                   cfg, grad);
+}
+}  // extern "C"
