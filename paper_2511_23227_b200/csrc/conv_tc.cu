@@ -1421,7 +1421,8 @@ constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
 constexpr int WG_PAIRS = 7;      // cell pairs per CTA (cell group = 14 cells)
 constexpr int WG_NSA = 2;        // A pair stages (32 KB)
 constexpr int WG_NSD = 4;        // descriptor slots (2 blocks each; a multiple of WG_GROUPS)
-constexpr int WG_NSG = 2;        // dense G sub-tile slots (NOUT x 256 B; 1 for NOUT = 256)
+constexpr int WG_NSG = 2;        // dense G sub-tile slots (NOUT x 256 B; 1 for NOUT >= 128;
+                                 // at 256 as two 64-row halves with their own barriers)
 constexpr int WG_GROUPS = 2;     // stage (cell pair) s is aggregated by warp group s % 2
 
 template <int NOUT>
@@ -1482,6 +1483,12 @@ template <int NOUT, bool BIG>
 __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   using Cfg = WgCfg<NOUT>;
   constexpr int NP = Cfg::pairs, NSG = Cfg::nsg, WNSD = Cfg::nsd;
+  // NOUT = 256 (one G slot, two pairs = the two A slots): the slot's 64-row
+  // halves (MMA k-steps 0-3 / 4-7; loader warps 0-1 / 2-3) are filled and
+  // released separately, so the next sub-tile's first half loads while the
+  // MMAs consume the second (NOUT = 128 has four pairs for two A slots)
+  constexpr bool GH = NOUT == 256;
+  static_assert(!GH || (NSG == 1 && NP <= WG_NSA), "G halves: every pair's A slot held across both halves");
   constexpr uint32_t GB = Cfg::gbytes;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
@@ -1492,7 +1499,6 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   const uint32_t s_bar = base + L.bar;
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
-  uint8_t* g_gt = gbase + L.gt;
   const uint8_t* g_d = gbase + L.d;
   uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + OFFS_DSRC;  // per descriptor half-slot
 
@@ -1513,8 +1519,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       mbar_init(bar(W_D_FULL + i), 1);
       mbar_init(bar(W_D_EMPTY + i), FWD_AGG_WARPS / WG_GROUPS);
     }
-    for (int i = 0; i < NSG; ++i) {
-      mbar_init(bar(W_G_FULL + i), 4);
+    for (int i = 0; i < WG_NSG; ++i) {
+      mbar_init(bar(W_G_FULL + i), GH ? 2 : 4);
       mbar_init(bar(W_G_EMPTY + i), 1);
     }
     mbar_init(bar(W_DONE), 1);
@@ -1571,6 +1577,32 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         const uint2 sp = a.sup[s];
         const int nsub = static_cast<int>(sp.y & 0xFFu);
         for (int g = 0; g < nsub; ++g) {
+        if (GH) {
+          for (int h = 0; h < 2; ++h) {
+            mbar_wait(bar(W_G_FULL + h), g_it & 1);
+            tc_fence_after();
+            for (int p = 0; p < n_pairs; ++p) {
+              const uint32_t as = (a_it + p) % WG_NSA;
+              if (h == 0) {
+                mbar_wait(bar(W_A_FULL + as), ((a_it + p) / WG_NSA) & 1);
+                tc_fence_after();
+              }
+              const uint32_t d = tmem + p * NOUT;
+#pragma unroll
+              for (int ks = 4 * h; ks < 4 * h + 4; ++ks) {
+                const uint64_t ad = sdesc_sw128(s_a + as * 32768u + 2048u * ks, 16384, 1024);
+                const uint64_t bd = sdesc_sw128(s_g + 2048u * ks, 16384, 1024);
+                umma_bf16(d, ad, bd, idesc, (first && ks == 0) ? 0u : 1u);
+              }
+              if (h == 1) umma_commit(bar(W_A_EMPTY + as));
+            }
+            umma_commit(bar(W_G_EMPTY + h));
+          }
+          a_it += n_pairs;
+          first = false;
+          ++g_it;
+          continue;
+        }
         const uint32_t gs = g_it % NSG;
         mbar_wait(bar(W_G_FULL + gs), (g_it / NSG) & 1);
         for (int p = 0; p < n_pairs; ++p) {
@@ -1660,21 +1692,28 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
                                 a.halo_len[s_next], a.feat + chunk * CH, 32 * warp + lane, fstride);
       }
       for (int g = 0; g < nsub; ++g) {
-        const uint32_t gs = g_it % NSG;
-        mbar_wait_sleep(bar(W_G_EMPTY + gs), ((g_it / NSG) & 1) ^ 1);
+        const uint32_t gs = g_it % NSG, gu = GH ? (warp >> 1) : gs;  // barrier unit
+        // a single G slot (NOUT >= 128) puts this wait on the MMA's critical path
+        if (NSG == 1)
+          mbar_wait(bar(W_G_EMPTY + gu), (g_it & 1) ^ 1);
+        else
+          mbar_wait_sleep(bar(W_G_EMPTY + gs), ((g_it / NSG) & 1) ^ 1);
         // 128 rows x NOUT/64 blocks x 8 chunks of 16 B; warp e copies rows 32e..32e+31
-        uint8_t* gt = g_gt + gs * GB;
+        // with cp.async (all of a lane's copies in flight; rows past the tile zero-filled)
+        const uint32_t gt = s_g + gs * GB;
+        const uint2 tl = a.tiles[sp.x + g];
+#pragma unroll 8
         for (int x = lane; x < 32 * 8 * (NOUT / 64); x += 32) {
           const int j = x >> 8, r = 32 * warp + ((x >> 3) & 31), q = x & 7;
-          const uint2 tl = a.tiles[sp.x + g];
-          const int64_t row = static_cast<int64_t>(tl.x) + r;
-          uint4 v = make_uint4(0, 0, 0, 0);
-          if (static_cast<uint32_t>(r) < tl.y) v = reinterpret_cast<const uint4*>(a.dense + row * NOUT)[j * 8 + q];
-          *reinterpret_cast<uint4*>(gt + j * 16384 + r * 128 + (((q ^ (r & 7)) & 7) << 4)) = v;
+          const bool in = static_cast<uint32_t>(r) < tl.y;
+          const int64_t row = static_cast<int64_t>(tl.x) + (in ? r : 0);
+          cp_async16_zfill(gt + j * 16384 + r * 128 + (((q ^ (r & 7)) & 7) << 4),
+                           reinterpret_cast<const uint4*>(a.dense + row * NOUT) + j * 8 + q, in ? 16u : 0u);
         }
+        cp_async_wait_all();
         fence_proxy_async_smem();
         __syncwarp();
-        if (lane == 0) mbar_arrive(bar(W_G_FULL + gs));
+        if (lane == 0) mbar_arrive(bar(W_G_FULL + gu));
         ++g_it;
       }
     }

@@ -3,6 +3,8 @@ time (library profiler, CUDA events on the library stream) of the tensor-core
 and exact engines for (C_in, C_out) pairs.
 
     python tools/chan_sweep.py [n_points] [iters] [cin:cout ...]
+
+CHAN_SWEEP_TC_ONLY=1 skips the exact engines.
 """
 import os
 import sys
@@ -33,7 +35,8 @@ for cin, cout in pairs:
     w = T(o.make_weights(3, 1, cin, cout, 2))
     f = T(o.gen_features(n, 1, cin, 3))
     g = T(o.gen_features(n, 1, cout, 4))
-    for math in (npc.Math.bf16, npc.Math.exact):
+    maths = (npc.Math.bf16,) if os.environ.get("CHAN_SWEEP_TC_ONLY") else (npc.Math.bf16, npc.Math.exact)
+    for math in maths:
         cfg = npc.ExecConfig(math=math)
         fo = torch.empty((n, 1, cout), device="cuda")
         gi = torch.empty((n, 1, cin), device="cuda")
