@@ -87,6 +87,7 @@ struct TcDirPlan {
   double mean_halo = 0.0;
   DevBuf<uint32_t> spill_rows;  // permuted positions of rows in overflow super-tiles
   int64_t n_spill = 0;
+  std::vector<unsigned long long> k_count;  // entries per kernel cell (host)
 };
 
 struct GatherPlan;
@@ -568,6 +569,21 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
 }
 
+// entries per kernel cell: shared-memory histogram of the structure's cells
+__global__ void k_cell_hist(const int64_t* __restrict__ row_ptr, int64_t n_rows,
+                            const uint32_t* __restrict__ kk, int K, unsigned long long* __restrict__ out) {
+  __shared__ unsigned int h[KMAX];
+  for (int x = threadIdx.x; x < K; x += blockDim.x) h[x] = 0;
+  __syncthreads();
+  const int64_t n = row_ptr[n_rows];
+  for (int64_t e = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; e < n;
+       e += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    atomicAdd(&h[kk[e]], 1u);
+  __syncthreads();
+  for (int x = threadIdx.x; x < K; x += blockDim.x)
+    if (h[x]) atomicAdd(&out[x], static_cast<unsigned long long>(h[x]));
+}
+
 static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_t* row_ptr,
                                                  const uint32_t* col, const uint32_t* kk,
                                                  int64_t n_rows, int64_t n_cols,
@@ -813,6 +829,13 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     NPCG_CUDA(cudaMemcpyAsync(P->spill_rows.get(), spill.data(), spill.size() * 4,
                               cudaMemcpyHostToDevice, ctx->stream));
   }
+  // per-cell entry counts (the weight gradient balances its cell runs on them)
+  DevBuf<unsigned long long> kc(ctx, K);
+  NPCG_CUDA(cudaMemsetAsync(kc.get(), 0, K * 8, ctx->stream));
+  launch(ctx, "plan_cell_hist", k_cell_hist, dim3(static_cast<unsigned>(ctx->num_sms * 4)), dim3(256), 0,
+         row_ptr, n_rows, kk, K, kc.get());
+  P->k_count.assign(K, 0);
+  NPCG_CUDA(cudaMemcpyAsync(P->k_count.data(), kc.get(), K * 8, cudaMemcpyDeviceToHost, ctx->stream));
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
   return P;
 }
@@ -1415,6 +1438,7 @@ struct WgArgs {
   const __nv_bfloat16* feat;   // bf16 F_in (n_cols, 64 nci), permuted
   const __nv_bfloat16* dense;  // bf16 G_out (n_rows, NOUT), permuted (row = sub-tile order)
   float* partial;              // [gridDim.x][K][64 nci c][NOUT m]
+  uint8_t korder[KMAX];        // run slot -> kernel cell (runs of 2 x pairs slots, load-balanced)
 };
 
 constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
@@ -1548,14 +1572,16 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         if (lane == 0) {
           const uint32_t ds = d_it % WNSD;
           mbar_wait(bar(W_D_EMPTY + ds), ((d_it / WNSD) & 1) ^ 1);
-          const int k0 = g * K + k_begin + 2 * p;
-          const uint32_t o0 = offs[k0], o1 = offs[k0 + 1];
-          const uint32_t o2 = (k_begin + 2 * p + 1 < K) ? offs[k0 + 2] : o1;
-          const uint32_t n0 = min(o1 - o0, static_cast<uint32_t>(BLOCK_MAX_BYTES));
-          const uint32_t n1 = min(o2 - o1, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+          const int ka = g * K + a.korder[k_begin + 2 * p];
+          const bool two = k_begin + 2 * p + 1 < K;
+          const int kb = two ? g * K + a.korder[k_begin + 2 * p + 1] : ka;
+          const uint32_t o0 = offs[ka], e0 = offs[ka + 1];
+          const uint32_t o1 = offs[kb], e1 = two ? offs[kb + 1] : o1;
+          const uint32_t n0 = min(e0 - o0, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+          const uint32_t n1 = min(e1 - o1, static_cast<uint32_t>(BLOCK_MAX_BYTES));
           if (BIG) {
-            dsrc[2 * ds] = o1 - o0 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
-            dsrc[2 * ds + 1] = o2 - o1 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o1 : kFitsSlot;
+            dsrc[2 * ds] = e0 - o0 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
+            dsrc[2 * ds + 1] = e1 - o1 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o1 : kFitsSlot;
           }
           mbar_expect_tx(bar(W_D_FULL + ds), n0 + n1);
           bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + o0, n0, bar(W_D_FULL + ds));
@@ -1728,7 +1754,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     const int e = warp;
     for (int p = 0; p < n_pairs; ++p) {
       const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + p * NOUT;
-      const int k = k_begin + 2 * p + (e >> 1);
+      const int ks = k_begin + 2 * p + (e >> 1);
+      const int k = ks < K ? a.korder[ks] : K;
       const int c = chunk * CH + 32 * (e & 1) + lane;
       float4* o = k < K ? reinterpret_cast<float4*>(
                               a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * fstride + c) * NOUT)
@@ -2391,6 +2418,8 @@ static TcPlan* get_plan(npcg_context* ctx, npcg_neighbors* nb) {
   return nb->tc.get();
 }
 
+static void wgrad_cell_order(const TcDirPlan* P, int K, int np, int gpc, uint8_t* korder);
+
 // wide = the pass writes 256 channels: 128-row super-tiles (st = 1); 64- and
 // 128-channel passes share the 256-row plan
 static TcDirPlan* plan_fwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = false) {
@@ -2727,6 +2756,7 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
     a.feat = p->feat_in.get();
     a.dense = p->feat_out.get();
     a.partial = p->partial.get();
+    wgrad_cell_order(P, K, np, gpc, a.korder);
     const dim3 grid(gx, groups);
     if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid, P->big_blocks);
     else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid, P->big_blocks);
@@ -2737,6 +2767,36 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
            grad_w);
     if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true, cin, cout);
   }
+}
+
+// Cell runs of the weight gradient: gpc runs of 2 x np slots (the last one
+// short), each run swept by its own CTAs over every super-tile, so a run's
+// time follows the entries of its cells -- uneven by ~15 % with index-order
+// runs (the centre and face cells are the dense ones).  Cells go to runs by
+// longest-processing-time greedy on (entries + a per-row cost), and within a
+// run in descending order so the two cells of a pair (aggregated side by
+// side) have similar loads.  Each cell's sum keeps its order (same CTAs, same
+// super-tiles), so the result does not depend on the assignment.
+static void wgrad_cell_order(const TcDirPlan* P, int K, int np, int gpc, uint8_t* korder) {
+  std::vector<double> cost(K, 1.0);
+  if (static_cast<int>(P->k_count.size()) == K)
+    for (int k = 0; k < K; ++k) cost[k] = static_cast<double>(P->k_count[k]) + 0.5 * P->n_rows;
+  std::vector<int> by(K);
+  for (int k = 0; k < K; ++k) by[k] = k;
+  std::stable_sort(by.begin(), by.end(), [&](int x, int y) { return cost[x] > cost[y]; });
+  std::vector<std::vector<int>> run(gpc);
+  std::vector<double> load(gpc, 0.0);
+  for (int k : by) {
+    int best = -1;
+    for (int r = 0; r < gpc; ++r) {
+      const int cap = std::min(2 * np, K - r * 2 * np);
+      if (static_cast<int>(run[r].size()) < cap && (best < 0 || load[r] < load[best])) best = r;
+    }
+    run[best].push_back(k);  // cells arrive in descending cost: each run stays sorted
+    load[best] += cost[k];
+  }
+  for (int r = 0; r < gpc; ++r)
+    for (size_t x = 0; x < run[r].size(); ++x) korder[r * 2 * np + x] = static_cast<uint8_t>(run[r][x]);
 }
 
 // Debug: one traced forward; trace_host receives TRACE_STAGES x TRACE_EV clocks.
