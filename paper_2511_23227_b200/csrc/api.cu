@@ -133,11 +133,11 @@ void forward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, const
   if (dtype == NPCG_F32)
     mvmr_rows<float>(ctx, v, static_cast<const float*>(w), static_cast<const float*>(fin),
                      static_cast<int>(G), static_cast<int>(cin), static_cast<int>(cout),
-                     static_cast<float*>(fout));
+                     static_cast<float*>(fout), nb->n_kernels);
   else
     mvmr_rows<double>(ctx, v, static_cast<const double*>(w), static_cast<const double*>(fin),
                       static_cast<int>(G), static_cast<int>(cin), static_cast<int>(cout),
-                      static_cast<double*>(fout));
+                      static_cast<double*>(fout), nb->n_kernels);
 }
 
 template <typename T>
@@ -147,7 +147,7 @@ void dgrad_exact(npcg_context* ctx, npcg_neighbors* nb, const T* w, int64_t G, i
   DevBuf<T> wt(ctx, nb->n_kernels * G * cin * cout);
   transpose_w<T>(ctx, w, nb->n_kernels * G, static_cast<int>(cin), static_cast<int>(cout), wt.get());
   mvmr_rows<T>(ctx, nb->tcsr->view(), wt.get(), gout, static_cast<int>(G), static_cast<int>(cout),
-               static_cast<int>(cin), grad_in);
+               static_cast<int>(cin), grad_in, nb->n_kernels);
 }
 
 void backward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, const void* w,

@@ -8,7 +8,7 @@ namespace npcg {
 // ---- exact engines (conv_simt.cu) -----------------------------------------
 template <typename T>
 void mvmr_rows(npcg_context* ctx, const CsrView& csr, const T* w, const T* fin, int G, int cin,
-               int cout, T* out);
+               int cout, T* out, int64_t n_kernels = 0);  // n_kernels > 0: W may be staged in smem
 void mvmr_rows_subset_f32(npcg_context* ctx, const CsrView& csr, const uint32_t* perm,
                           const uint32_t* list, int64_t n_list, const float* w, const float* fin,
                           int cin, int cout, float* out);

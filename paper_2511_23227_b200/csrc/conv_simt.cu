@@ -77,6 +77,85 @@ __global__ void __launch_bounds__(256) k_mvmr_rows(CsrView csr, const T* __restr
   }
 }
 
+// Same arithmetic (same FMA order: entries in CSR order, input channels
+// ascending) with W staged once per CTA in shared memory, for the narrow
+// layers whose whole W fits (config 1: 27 x 32 x 32 fp32 = 110 KB): one
+// persistent CTA per SM, warps grid-striding over rows, the next entry's
+// (j, k) and feature slice loaded while the current one is reduced.
+template <typename T, int R>
+__global__ void __launch_bounds__(1024, 1) k_mvmr_rows_ws(CsrView csr, const T* __restrict__ w,
+                                                          int64_t w_elems, const T* __restrict__ fin,
+                                                          int G, int cin, int cout,
+                                                          T* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t ws_raw[];
+  T* ws = reinterpret_cast<T*>(ws_raw);
+  for (int64_t x = threadIdx.x; x < w_elems; x += blockDim.x) ws[x] = w[x];
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t total = csr.n_rows * G;
+  for (int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       warp < total; warp += nw) {
+    const int64_t row = warp / G;
+    const int g = static_cast<int>(warp - row * G);
+    T acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = T(0);
+    const int64_t e0 = csr.row_ptr[row], e1 = csr.row_ptr[row + 1];
+    // the next entry's cell and first feature slice are in flight while the
+    // current entry is reduced
+    int64_t kn = 0;
+    T fn = T(0);
+    if (e0 < e1) {
+      kn = csr.k[e0];
+      if (lane < cin) fn = fin[(static_cast<int64_t>(csr.col[e0]) * G + g) * cin + lane];
+    }
+    for (int64_t e = e0; e < e1; ++e) {
+      const int64_t k = kn;
+      const T f0 = fn;
+      const int64_t j = csr.col[e];
+      if (e + 1 < e1) {
+        kn = csr.k[e + 1];
+        if (lane < cin) fn = fin[(static_cast<int64_t>(csr.col[e + 1]) * G + g) * cin + lane];
+      }
+      const T* f = fin + (j * G + g) * cin;
+      const T* wm = ws + ((k * G + g) * cin) * cout;
+      for (int c0 = 0; c0 < cin; c0 += 32) {
+        const T fv = c0 == 0 ? f0 : (c0 + lane < cin) ? f[c0 + lane] : T(0);
+        const int cn = cin - c0 < 32 ? cin - c0 : 32;
+#pragma unroll 8
+        for (int cc = 0; cc < cn; ++cc) {
+          const T fc = __shfl_sync(0xffffffffu, fv, cc);
+          const T* wr = wm + (c0 + cc) * cout;
+#pragma unroll
+          for (int r = 0; r < R; ++r) {
+            const int m = lane + 32 * r;
+            if (m < cout) acc[r] = fma(wr[m], fc, acc[r]);
+          }
+        }
+      }
+    }
+    T* o = out + (row * G + g) * cout;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int m = lane + 32 * r;
+      if (m < cout) o[m] = acc[r];
+    }
+  }
+}
+
+constexpr int64_t WS_MAX_BYTES = 200 * 1024;
+
+template <typename T, int R>
+static void launch_mvmr_ws(npcg_context* ctx, const CsrView& csr, const T* w, int64_t w_elems,
+                           const T* fin, int G, int cin, int cout, T* out) {
+  const int bytes = static_cast<int>(w_elems * sizeof(T));
+  auto kern = k_mvmr_rows_ws<T, R>;
+  NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  launch(ctx, "mvmr_simt", kern, dim3(static_cast<unsigned>(ctx->num_sms)), dim3(1024), bytes, csr, w,
+         w_elems, fin, G, cin, cout, out);
+}
+
 // Rows given as a list of positions into `perm` (row = perm[list[x]]): the
 // exact engine for the rows of tensor-core super-tiles beyond tile capacity.
 template <typename T, int R>
@@ -135,8 +214,17 @@ void mvmr_rows_subset_f32(npcg_context* ctx, const CsrView& csr, const uint32_t*
 
 template <typename T>
 void mvmr_rows(npcg_context* ctx, const CsrView& csr, const T* w, const T* fin, int G, int cin,
-               int cout, T* out) {
+               int cout, T* out, int64_t n_kernels) {
   if (csr.n_rows == 0) return;
+  const int64_t w_elems = n_kernels * G * cin * cout;
+  if (n_kernels > 0 && cout <= 64 && w_elems * static_cast<int64_t>(sizeof(T)) <= WS_MAX_BYTES &&
+      csr.n_rows * G >= 8 * static_cast<int64_t>(ctx->num_sms)) {
+    if (cout <= 32)
+      launch_mvmr_ws<T, 1>(ctx, csr, w, w_elems, fin, G, cin, cout, out);
+    else
+      launch_mvmr_ws<T, 2>(ctx, csr, w, w_elems, fin, G, cin, cout, out);
+    return;
+  }
   const unsigned blocks = static_cast<unsigned>(ceil_div(csr.n_rows * G * 32, 256));
   for (int m_base = 0; m_base < cout; m_base += 256) {
     const int rem = cout - m_base;
@@ -284,9 +372,9 @@ void vvor_cells(npcg_context* ctx, const CellPlan& cells, const T* gout, const T
 
 // explicit instantiations
 template void mvmr_rows<float>(npcg_context*, const CsrView&, const float*, const float*, int,
-                               int, int, float*);
+                               int, int, float*, int64_t);
 template void mvmr_rows<double>(npcg_context*, const CsrView&, const double*, const double*, int,
-                                int, int, double*);
+                                int, int, double*, int64_t);
 template void transpose_w<float>(npcg_context*, const float*, int64_t, int, int, float*);
 template void transpose_w<double>(npcg_context*, const double*, int64_t, int, int, double*);
 template void vvor_cells<float>(npcg_context*, const CellPlan&, const float*, const float*, int,
