@@ -15,6 +15,8 @@
 //                   entries accumulate dW_k tiles in registers (rows staged
 //                   in shared memory); chunk partials are summed in a fixed
 //                   order by a second kernel (deterministic, no atomics).
+#include <type_traits>
+
 #include "neighbors.cuh"
 #include "conv.cuh"
 
@@ -144,7 +146,92 @@ __global__ void __launch_bounds__(1024, 1) k_mvmr_rows_ws(CsrView csr, const T* 
   }
 }
 
+// fp32, C_in % 4 == 0: W staged transposed ([k][m][c], rows padded to an odd
+// number of 16-byte groups so a warp's 16-byte reads are conflict-free), the
+// input row read four channels at a time with a broadcast load -- per four
+// FMAs one LDG.128 (all lanes one address) and one LDS.128 instead of four
+// shuffles and four loads.  Same products, same order: channel-ascending FMAs
+// per entry, entries in CSR order.
+template <int R>
+__global__ void __launch_bounds__(1024, 1) k_mvmr_rows_ws4(CsrView csr, const float* __restrict__ w,
+                                                           int64_t kg_n, const float* __restrict__ fin,
+                                                           int G, int cin, int cout, int wstride,
+                                                           float* __restrict__ out) {
+  extern __shared__ __align__(16) uint8_t ws_raw[];
+  float* ws = reinterpret_cast<float*>(ws_raw);
+  const int64_t per = static_cast<int64_t>(cin) * cout;
+  for (int64_t x = threadIdx.x; x < kg_n * per; x += blockDim.x) {
+    const int64_t kg = x / per;
+    const int r = static_cast<int>(x - kg * per), c = r / cout, m = r - c * cout;
+    ws[(kg * cout + m) * wstride + c] = w[x];
+  }
+  __syncthreads();
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = static_cast<int64_t>(gridDim.x) * (blockDim.x >> 5);
+  const int64_t total = csr.n_rows * G;
+  int mrow[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) mrow[r] = min(lane + 32 * r, cout - 1) * wstride;  // lanes past C_out: discarded
+  for (int64_t warp = static_cast<int64_t>(blockIdx.x) * (blockDim.x >> 5) + (threadIdx.x >> 5);
+       warp < total; warp += nw) {
+    const int64_t row = warp / G;
+    const int g = static_cast<int>(warp - row * G);
+    float acc[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) acc[r] = 0.f;
+    const int64_t e0 = csr.row_ptr[row], e1 = csr.row_ptr[row + 1];
+    // the row's entries, 32 at a time: one coalesced load of (j, k) per lane,
+    // broadcast by shuffles (no dependent global load per entry)
+    for (int64_t eb = e0; eb < e1; eb += 32) {
+    const int cnt = static_cast<int>(e1 - eb < 32 ? e1 - eb : 32);
+    uint32_t jl = 0, kl = 0;
+    if (lane < cnt) {
+      jl = csr.col[eb + lane];
+      kl = csr.k[eb + lane];
+    }
+    for (int x = 0; x < cnt; ++x) {
+      const int64_t j = __shfl_sync(0xffffffffu, jl, x), k = __shfl_sync(0xffffffffu, kl, x);
+      const float4* f4 = reinterpret_cast<const float4*>(fin + (j * G + g) * cin);
+      const float* wk = ws + (k * G + g) * cout * wstride;
+#pragma unroll 8
+      for (int c = 0; c < cin; c += 4) {
+        const float4 fv = __ldg(f4 + (c >> 2));
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+          const float4 wv = *reinterpret_cast<const float4*>(wk + mrow[r] + c);
+          acc[r] = fmaf(wv.x, fv.x, acc[r]);
+          acc[r] = fmaf(wv.y, fv.y, acc[r]);
+          acc[r] = fmaf(wv.z, fv.z, acc[r]);
+          acc[r] = fmaf(wv.w, fv.w, acc[r]);
+        }
+      }
+    }
+    }
+    float* o = out + (row * G + g) * cout;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      const int m = lane + 32 * r;
+      if (m < cout) o[m] = acc[r];
+    }
+  }
+}
+
 constexpr int64_t WS_MAX_BYTES = 200 * 1024;
+
+// fp32 rows of the transposed W image: C_in floats padded to an odd number of
+// 16-byte groups
+static int ws4_stride(int cin) { return (cin / 4) % 2 ? cin : cin + 4; }
+
+template <int R>
+static void launch_mvmr_ws4(npcg_context* ctx, const CsrView& csr, const float* w, int64_t kg_n,
+                            const float* fin, int G, int cin, int cout, float* out) {
+  const int stride = ws4_stride(cin);
+  const int bytes = static_cast<int>(kg_n * cout * stride * sizeof(float));
+  auto kern = k_mvmr_rows_ws4<R>;
+  NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+  launch(ctx, "mvmr_simt", kern, dim3(static_cast<unsigned>(ctx->num_sms)), dim3(1024), bytes, csr, w,
+         kg_n, fin, G, cin, cout, stride, out);
+}
 
 template <typename T, int R>
 static void launch_mvmr_ws(npcg_context* ctx, const CsrView& csr, const T* w, int64_t w_elems,
@@ -217,6 +304,18 @@ void mvmr_rows(npcg_context* ctx, const CsrView& csr, const T* w, const T* fin, 
                int cout, T* out, int64_t n_kernels) {
   if (csr.n_rows == 0) return;
   const int64_t w_elems = n_kernels * G * cin * cout;
+  if (std::is_same<T, float>::value && n_kernels > 0 && cout <= 64 && cin % 4 == 0 &&
+      n_kernels * G * cout * ws4_stride(cin) * 4 <= WS_MAX_BYTES &&
+      reinterpret_cast<uintptr_t>(fin) % 16 == 0 && csr.n_rows * G >= 8 * static_cast<int64_t>(ctx->num_sms)) {
+    const float* wf = reinterpret_cast<const float*>(w);
+    const float* ff = reinterpret_cast<const float*>(fin);
+    float* of = reinterpret_cast<float*>(out);
+    if (cout <= 32)
+      launch_mvmr_ws4<1>(ctx, csr, wf, n_kernels * G, ff, G, cin, cout, of);
+    else
+      launch_mvmr_ws4<2>(ctx, csr, wf, n_kernels * G, ff, G, cin, cout, of);
+    return;
+  }
   if (n_kernels > 0 && cout <= 64 && w_elems * static_cast<int64_t>(sizeof(T)) <= WS_MAX_BYTES &&
       csr.n_rows * G >= 8 * static_cast<int64_t>(ctx->num_sms)) {
     if (cout <= 32)
