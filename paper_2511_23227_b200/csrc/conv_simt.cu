@@ -159,10 +159,11 @@ __global__ void __launch_bounds__(1024, 1) k_mvmr_rows_ws4(CsrView csr, const fl
                                                            float* __restrict__ out) {
   extern __shared__ __align__(16) uint8_t ws_raw[];
   float* ws = reinterpret_cast<float*>(ws_raw);
-  const int64_t per = static_cast<int64_t>(cin) * cout;
-  for (int64_t x = threadIdx.x; x < kg_n * per; x += blockDim.x) {
-    const int64_t kg = x / per;
-    const int r = static_cast<int>(x - kg * per), c = r / cout, m = r - c * cout;
+  // (the image is < 200 KB: 32-bit index arithmetic)
+  const int per = cin * cout, w_total = static_cast<int>(kg_n) * per;
+#pragma unroll 4
+  for (int x = threadIdx.x; x < w_total; x += blockDim.x) {
+    const int kg = x / per, r = x - kg * per, c = r / cout, m = r - c * cout;
     ws[(kg * cout + m) * wstride + c] = w[x];
   }
   __syncthreads();
