@@ -38,13 +38,25 @@ T_RES = 3
 
 
 def parse():
+    """Command line; the workload default depends on the world size."""
+    a = _parse()
+    if a.workload is None:
+        a.workload = "batch64" if int(os.environ.get("WORLD_SIZE", "1")) > 1 else "ns"
+    return a
+
+
+def _parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=10)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--workload", default="ns", choices=["ns", "batch64"])
-    p.add_argument("--math", default="auto", choices=["auto", "exact", "bf16"])
+    p.add_argument("--workload", default=None, choices=["ns", "batch64"],
+                   help="default: ns at N=1, batch64 (config 5) under torchrun N>1")
+    p.add_argument("--math", default="bf16", choices=["auto", "exact", "bf16", "f32tc"],
+                   help="headline arithmetic (bf16 = the opt-in bf16-operand variant); the "
+                        "fp32-contract path (auto) is timed beside it as fp32_variant")
+    p.add_argument("--fp32-steps", type=int, default=5)
     p.add_argument("--points", type=int, default=N_POINTS)
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -150,7 +162,9 @@ def run_reference(args):
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libnpref.so not built"}))
         return
     cores = impl.hardware_concurrency()
-    n = 250_000  # bounded sample of the workload per step (same density / neighbor count)
+    # the same instance as our arm's N=1 line: the 1M-point north-star cloud
+    # (batch64: one 250K scene, the unit a rank's step repeats)
+    n = args.points if args.workload == "ns" else 250_000
     xyz = orc.gen_uniform_cube(n, 1.0, 1)
     r = 1.8 * n ** (-1 / 3)
     w = orc.make_weights(T_RES, 1, C, C, 2)
@@ -173,30 +187,33 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (gen_uniform_cube seed 1, gen_features seeds 3/4, make_weights seed 2)",
         "impl": "reference",
-        "config": {"workload": f"{args.workload}: reference CPU fwd+bwd (mvmr + mvmr_transposed"
-                               " + vvor, cached sorted triplets)", "points_per_step": n,
-                   "c_in": C, "c_out": C, "kernel_cells": 27, "radius": r,
-                   "exec": "grouped L=128 deterministic=false"},
+        "config": {"workload": (f"ns: one {n}-point uniform cloud (seed 1), conv layer fwd+bwd "
+                                "(north-star instance), reference CPU chain mvmr + "
+                                "mvmr_transposed + vvor over the cached sorted triplets")
+                   if args.workload == "ns" else
+                   f"batch64: one {n}-point scene per step (config 5's unit), reference CPU chain",
+                   "points_per_step": n, "c_in": C, "c_out": C, "kernel_cells": 27, "radius": r,
+                   "exec": "grouped L=128 deterministic=false", "same_config_as_gpu_arm": True},
         "cpu_baseline": {"value": round(value, 4), "unit": "Mpoints/s", "cores": cores,
                          "kind": kind,
-                         "sample": f"{n}-point uniform cloud per step (bounded sample of the 1M "
-                                   f"workload, same r*N^(1/3)); neighbor build {build_s:.2f}s "
-                                   "(1 thread, excluded like the GPU arm's cached structure)"},
+                         "sample": f"the full {n}-point instance per step (fp32, the reference's "
+                                   f"own engines); neighbor build + sort {build_s:.2f}s on 1 "
+                                   "thread (excluded like the GPU arm's cached structure)"},
         "e2e": {"value": round(value, 4), "unit": "Mpoints/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(out))
 
 
-def cpu_baseline_sample():
-    """Reference CPU chain on a bounded sample (c2: 100K points, C=64), rank 0, N=1."""
+def cpu_baseline_sample(n):
+    """Reference CPU chain (oracle/_ref) on the bench's own instance (n points,
+    C=64), rank 0, N=1: median of 2 steps after 1 warm-up."""
     from oracle import Oracle, Reference, reference_available
     orc = Oracle()
     if not reference_available():
         return None
     ref = Reference()
     cores = ref.hardware_concurrency()
-    n = 100_000
     xyz = orc.gen_uniform_cube(n, 1.0, 1)
     r = 1.8 * n ** (-1 / 3)
     w = orc.make_weights(T_RES, 1, C, C, 2)
@@ -205,7 +222,7 @@ def cpu_baseline_sample():
     times, cache, _ = ref.conv_layer_f32(xyz, r, T_RES, w, f, g, workers=cores, build=True)
     build = float(times[0] + times[1])
     per = []
-    for _ in range(4):
+    for _ in range(3):
         times, cache, _ = ref.conv_layer_f32(xyz, r, T_RES, w, f, g, workers=cores, build=False,
                                              cache=cache)
         per.append(float(times[2] + times[3] + times[4]))
@@ -213,8 +230,9 @@ def cpu_baseline_sample():
     s = statistics.median(per[1:])
     return {"value": round(n / s / 1e6, 4), "unit": "Mpoints/s", "cores": cores,
             "kind": "reference",
-            "sample": f"100K-point uniform cloud (BASELINE config 2), C=64, fwd+dgrad+wgrad, "
-                      f"median of 3 after 1 warm-up; neighbor build+sort {build:.2f}s on 1 thread"}
+            "sample": f"the bench's own {n}-point uniform cloud (seed 1), C=64, fp32 "
+                      f"fwd+dgrad+wgrad with the reference's grouped engines, median of 2 after "
+                      f"1 warm-up; neighbor build+sort {build:.2f}s on 1 thread"}
 
 
 # ---------------------------------------------------------------------------
@@ -224,8 +242,8 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from oracle import Oracle
     from paper_2511_23227_b200 import npconv as npc
+    from paper_2511_23227_b200 import synthetic as syn
     from paper_2511_23227_b200 import shard
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -235,8 +253,8 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    orc = Oracle()
-    math = {"auto": npc.Math.auto, "exact": npc.Math.exact, "bf16": npc.Math.bf16}[args.math]
+    math = {"auto": npc.Math.auto, "exact": npc.Math.exact, "bf16": npc.Math.bf16,
+            "f32tc": npc.Math.f32tc}[args.math]
     cfg = npc.ExecConfig(math=math)
 
     # ---- this rank's scenes
@@ -250,13 +268,13 @@ def run_ours(args):
         scenes = list(range(a, b))
         scaling = "strong"
     r = 1.8 * n_pts ** (-1 / 3)
-    w = torch.from_numpy(orc.make_weights(T_RES, 1, C, C, 2)).to(dev)
+    w = torch.from_numpy(syn.make_weights(T_RES, 1, C, C, 2)).to(dev)
     ctx = npc.context(local)
     data = []
     n_t_total = 0
     t_build, t_plan = [], []
     # one small build first: module / allocator-pool initialisation is not build time
-    wcl = npc.make_point_cloud(orc.gen_uniform_cube(20000, 1.0, 99), device=dev)
+    wcl = npc.make_point_cloud(syn.gen_uniform_cube(20000, 1.0, 99), device=dev)
     npc.build_neighbors(wcl, wcl, npc.ConvGeometry(radius=1.8 * 20000 ** (-1 / 3), t=T_RES)).prepare(math)
     # batch64: this rank's scenes form ONE jagged cloud (batch offsets; pairs
     # never cross scenes, spatial.cpp:68-77), so one neighbor structure and one
@@ -264,7 +282,7 @@ def run_ours(args):
     units = [[s] for s in scenes] if args.workload == "ns" else [scenes]
     for unit in units:
         s = unit[0]
-        xyz = np.concatenate([orc.gen_uniform_cube(n_pts, 1.0, 1 + q) for q in unit])
+        xyz = np.concatenate([syn.gen_uniform_cube(n_pts, 1.0, 1 + q) for q in unit])
         offs = np.arange(len(unit) + 1, dtype=np.int64) * n_pts
         cl = npc.make_point_cloud(xyz, offs, device=dev)
         torch.cuda.synchronize()
@@ -276,9 +294,9 @@ def run_ours(args):
         torch.cuda.synchronize()
         t_build.append(t1 - t0)
         t_plan.append(time.perf_counter() - t1)
-        f = torch.from_numpy(np.concatenate([orc.gen_features(n_pts, 1, C, 3 + 100 * q)
+        f = torch.from_numpy(np.concatenate([syn.gen_features(n_pts, 1, C, 3 + 100 * q)
                                              for q in unit])).to(dev)
-        g = torch.from_numpy(np.concatenate([orc.gen_features(n_pts, 1, C, 4 + 100 * q)
+        g = torch.from_numpy(np.concatenate([syn.gen_features(n_pts, 1, C, 4 + 100 * q)
                                              for q in unit])).to(dev)
         fo = torch.empty((n_pts * len(unit), 1, C), device=dev)
         gi = torch.empty((n_pts * len(unit), 1, C), device=dev)
@@ -306,7 +324,8 @@ def run_ours(args):
         gw_sum.zero_()
         for (cl, nb, f, g, fo, gi, gw) in data:
             npc.conv_forward(nb, w, f, cfg, out=fo)
-            npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw)
+            # the operator's saved input, unmodified (PointConvOp semantics)
+            npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw, fin_unchanged=True)
             gw_sum.add_(gw)
         if world > 1:
             allreduce(gw_sum)
@@ -353,6 +372,37 @@ def run_ours(args):
     if args.workload == "batch64":
         n_points_total = n_pts * 64
     value = n_points_total / (ms / 1e3) / 1e6
+
+    # ---- fp32 variant: the same step with the reference's fp32 contract
+    # (math=auto: the split tensor-core path where it applies, else exact)
+    fp32v = None
+    if args.math != "auto" and args.fp32_steps > 0:
+        cfg_saved = cfg
+        cfg = npc.ExecConfig(math=npc.Math.auto)
+        step()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        ctx.profile_reset()
+        ctx.profile(True)
+        v0 = torch.cuda.Event(enable_timing=True)
+        v1 = torch.cuda.Event(enable_timing=True)
+        v0.record()
+        for _ in range(args.fp32_steps):
+            step()
+        v1.record()
+        torch.cuda.synchronize()
+        vprof = ctx.profile_dump()
+        ctx.profile(False)
+        vms = torch.tensor([v0.elapsed_time(v1) / args.fp32_steps], device=dev, dtype=torch.float64)
+        if world > 1:
+            dist.all_reduce(vms, op=dist.ReduceOp.MAX)
+        vms = float(vms.item())
+        fp32v = {"math": "auto (fp32 contract, rel <= 1e-5)", "steps": args.fp32_steps,
+                 "ms_per_step": round(vms, 4), "unit": "Mpoints/s",
+                 "value": round(n_points_total / (vms / 1e3) / 1e6, 3),
+                 "kernels": {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in vprof.items()}}
+        cfg = cfg_saved
 
     # ---- e2e: the same step through the public API with pinned host buffers
     e2e = None
@@ -405,7 +455,7 @@ def run_ours(args):
                     s_d2h.wait_event(ev_fo)
                     ho[s_].copy_(fo, non_blocking=True)
                 comp.wait_event(ev_g)
-                npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw)
+                npc.conv_backward(nb, w, f, g, cfg, grad_in=gi, grad_w=gw, fin_unchanged=True)
                 gs.add_(gw)
                 last_b = torch.cuda.Event()
                 last_b.record(comp)
@@ -474,9 +524,11 @@ def run_ours(args):
     passes = 2 if "bwd" in name else 1
     if "tc" in name or "umma" in name:
         achieved = passes * f_pass / (per_launch_ms / 1e3) / 1e12
-        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": bf16_sus,
-                "unit": "TFLOP/s", "frac": round(achieved / bf16_sus, 4), "traffic": ncu_traffic(name),
-                "kernel": name, "peak_kind": f"{peak_kind} bf16 sustained",
+        # burst peak: the kernel is timed inside a short (tens of ms) region
+        roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": bf16_burst,
+                "unit": "TFLOP/s", "frac": round(achieved / bf16_burst, 4),
+                "traffic": ncu_traffic(name), "kernel": name,
+                "peak_kind": f"{peak_kind} bf16 burst (short timed region)",
                 "algorithmic_flop_per_launch": passes * f_pass,
                 "launch_ms": round(per_launch_ms, 4), "share_of_step": round(share, 3)}
     else:
@@ -490,12 +542,13 @@ def run_ours(args):
     layer_bytes = 3 * b_pass * len(units)
     layer_flops = 3 * f_pass * len(units)
     layer = {"hbm_frac": round(layer_bytes / (ms / 1e3) / 1e9 / hbm, 4),
-             "tensor_frac": round(layer_flops / (ms / 1e3) / 1e12 / bf16_sus, 4),
+             "tensor_frac": round(layer_flops / (ms / 1e3) / 1e12 / bf16_burst, 4),
              "algorithmic_bytes_per_step": layer_bytes, "algorithmic_flop_per_step": layer_flops}
 
-    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_sample()
-    dtype = {"auto": "bf16-operand/fp32-accumulate (tcgen05) where supported, else f32",
-             "exact": "f32", "bf16": "bf16-operand/fp32-accumulate (tcgen05)"}[args.math]
+    cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_sample(n_unit)
+    dtype = {"auto": "f32 contract: split bf16x3 operands on tcgen05 where supported, else f32",
+             "exact": "f32", "bf16": "bf16-operand/fp32-accumulate (tcgen05), the opt-in variant",
+             "f32tc": "split bf16x3 operands, fp32 accumulate (tcgen05)"}[args.math]
     out = {
         "metric": METRIC, "value": round(value, 3), "unit": "Mpoints/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
@@ -524,6 +577,7 @@ def run_ours(args):
         "kernels": {k: {"launches": v[0], "ms": round(v[1], 4)} for k, v in prof.items()},
         "clocks": clocks,
         "cpu_baseline": cpu,
+        "fp32_variant": fp32v,
         "e2e": e2e,
     }
     print(json.dumps(out))

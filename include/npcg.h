@@ -82,14 +82,29 @@ typedef enum npcg_sort_axis {
   NPCG_SORT_BY_K = 3
 } npcg_sort_axis;
 
-/* Arithmetic of the MVMR / VVOR engines. */
+/* Arithmetic of the MVMR / VVOR engines.  The reference computes in the API
+ * dtype (fp32 / fp64) and pins fp32 results at rel <= 1e-5 against an fp64
+ * oracle (acceptance.cpp:39); AUTO keeps that contract, BF16 is an explicit
+ * opt-in with its own (looser) bound. */
 typedef enum npcg_math {
-  NPCG_MATH_AUTO = 0,  /* tensor-core path where it applies (F32, G=1, K<=128, C_in and C_out
-                          multiples of 16 in [64, 256]), else EXACT */
+  NPCG_MATH_AUTO = 0,  /* fp32 contract (rel <= 1e-5): F32 tensors run on the split tensor-core
+                          path (F32TC) where it applies (G=1, K<=128, C_in and C_out multiples of
+                          16 in [64, 128]), everything else (fp64, narrow or wide layers) on EXACT */
   NPCG_MATH_EXACT = 1, /* CUDA cores in the API dtype (fp32 / fp64 FMA, fp32 accumulate for F32) */
-  NPCG_MATH_BF16 = 2   /* tcgen05 tensor cores: bf16 operands, fp32 accumulate (F32 API only;
-                          C_in and C_out multiples of 16 up to 256, zero-padded inside) */
+  NPCG_MATH_BF16 = 2,  /* opt-in: tcgen05 tensor cores, bf16 operands, fp32 accumulate (F32 API
+                          only; C_in and C_out multiples of 16 up to 256, zero-padded inside);
+                          rel ~2e-3, bound 1e-2 */
+  NPCG_MATH_F32TC = 3  /* tcgen05 with split operands: every fp32 operand x = hi + lo (two bf16),
+                          products hi*hi + hi*lo + lo*hi (+ lo*lo for the weight gradient), fp32
+                          accumulate; rel ~4e-6 (bound 1e-5, the reference's fp32 bound).
+                          C_in, C_out multiples of 16 up to 128 */
 } npcg_math;
+
+/* npcg_exec_config.flags */
+#define NPCG_FLAG_FIN_UNCHANGED 1 /* npcg_conv_backward: `fin` is the same, unmodified buffer the
+                                     last npcg_conv_forward on this handle read (the operator's
+                                     saved input, conv_op.hpp:138), so the forward's device image
+                                     of it may be reused instead of re-converting it */
 
 /* engine.hpp:22-29 ExecConfig.  L / b_out / b_in / workers are validated like
  * the reference (ShapeError when < 1 / < 0) and otherwise only hints: the GPU
@@ -104,6 +119,8 @@ typedef struct npcg_exec_config {
   int32_t deterministic; /* engine.hpp:27 */
   int32_t workers;       /* engine.hpp:28 */
   int32_t math;          /* npcg_math */
+  int32_t flags;         /* NPCG_FLAG_* */
+  int32_t reserved;
 } npcg_exec_config;
 
 /* point_cloud.hpp:18-50 PointCloud.  xyz: DEVICE (n_points, 3) float64 AoS;
@@ -266,9 +283,12 @@ npcg_status npcg_conv_forward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype 
                               const void* fin, const npcg_exec_config* cfg, void* fout);
 /* conv_op.hpp:177-203 backward: grad_in = mvmr_transposed, grad_w = vvor.
  * Either output may be NULL to skip it.  `fin` is the operator's saved input
- * (PointConvOp copies it at forward, conv_op.hpp:138): on the tensor-core path
- * the bf16 image the last npcg_conv_forward on this handle made of the same
- * `fin` pointer is reused, so pass the forward's input unchanged. */
+ * (PointConvOp copies it at forward, conv_op.hpp:138).  With
+ * cfg->flags & NPCG_FLAG_FIN_UNCHANGED the tensor-core image the last forward
+ * on this handle made of `fin` is reused (the caller guarantees it is the same
+ * unmodified buffer); otherwise `fin` is read again.  On a degraded handle the
+ * site rows are gathered again from `fin` (ShapeError if the operator's
+ * widths differ from the forward's when `fin` is NULL). */
 npcg_status npcg_conv_backward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype,
                                const void* w, int64_t groups, int64_t c_in, int64_t c_out,
                                const void* fin, const void* gout, const npcg_exec_config* cfg,
@@ -296,6 +316,25 @@ npcg_status npcg_debug_trace_forward(npcg_context* ctx, npcg_neighbors* nb, cons
 npcg_status npcg_voxel_downsample(npcg_context* ctx, const npcg_cloud* cloud, double voxel,
                                   int64_t* kept, int64_t* parent, int64_t* out_offsets,
                                   int64_t* n_kept);
+
+/* spatial.hpp:52-54 upsample (spatial.cpp:154-169): fine (n_fine, width)
+ * row m = coarse row parent[m]; parent: DEVICE int64[n_fine] (the map's
+ * parent_of), coarse: DEVICE (n_coarse, width) of `dtype`.
+ * Errors: SHAPE (width < 1), INDEX (a parent outside [0, n_coarse)). */
+npcg_status npcg_upsample(npcg_context* ctx, npcg_dtype dtype, const int64_t* parent,
+                          int64_t n_fine, const void* coarse, int64_t n_coarse, int64_t width,
+                          void* fine);
+
+/* ---- synthetic inputs (host) ---------------------------------------------
+ * The reference core's seeded generators (synthetic.hpp:12-40,
+ * tensors.hpp:142-150) over std::mt19937_64 (random.hpp:14-26), writing HOST
+ * buffers: xyz (n, 3) float64; features (n, groups, channels) and weights
+ * (t^3, groups, c_in, c_out) of `dtype`.  Errors: SHAPE, DOMAIN (extent <= 0). */
+npcg_status npcg_gen_uniform_cube(int64_t n, double extent, uint64_t seed, double* xyz);
+npcg_status npcg_gen_features(int64_t n, int64_t groups, int64_t channels, uint64_t seed,
+                              npcg_dtype dtype, void* out);
+npcg_status npcg_make_weights(int64_t t, int64_t groups, int64_t c_in, int64_t c_out,
+                              uint64_t seed, npcg_dtype dtype, void* out);
 
 /* ---- multi-GPU: dW all-reduce over NCCL -------------------
  * Whole point clouds are sharded per GPU; the weight gradient is the one

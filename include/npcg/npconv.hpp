@@ -40,6 +40,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <utility>
 #include <vector>
 
@@ -107,19 +108,98 @@ inline void cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
-// Owning device buffer.
+// Host <-> device copies of the reference's std::vector containers (pageable
+// memory): through two pinned staging chunks, the CPU side of a chunk copied by
+// several threads while the other chunk's DMA runs, so a transfer goes at
+// close to PCIe speed instead of the driver's single-threaded pageable path.
+class Stager {
+ public:
+  static Stager& get() {
+    static Stager s;
+    return s;
+  }
+  void h2d(void* dst, const void* src, size_t bytes) {
+    if (bytes < kSmall) {
+      cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "H2D");
+      return;
+    }
+    init();
+    for (size_t off = 0, b = 0; off < bytes; off += kChunk, b ^= 1) {
+      const size_t n = std::min(kChunk, bytes - off);
+      cuda(cudaEventSynchronize(ev_[b]), "staging wait");
+      par_copy(buf_[b], static_cast<const char*>(src) + off, n);
+      cuda(cudaMemcpyAsync(static_cast<char*>(dst) + off, buf_[b], n, cudaMemcpyHostToDevice, stream_), "H2D");
+      cuda(cudaEventRecord(ev_[b], stream_), "event");
+    }
+    cuda(cudaStreamSynchronize(stream_), "H2D sync");
+  }
+  void d2h(void* dst, const void* src, size_t bytes) {
+    if (bytes < kSmall) {
+      cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "D2H");
+      return;
+    }
+    init();
+    const size_t nchunk = (bytes + kChunk - 1) / kChunk;
+    auto issue = [&](size_t c) {
+      const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+      cuda(cudaMemcpyAsync(buf_[c & 1], static_cast<const char*>(src) + off, n, cudaMemcpyDeviceToHost, stream_),
+           "D2H");
+      cuda(cudaEventRecord(ev_[c & 1], stream_), "event");
+    };
+    issue(0);
+    for (size_t c = 0; c < nchunk; ++c) {
+      cuda(cudaEventSynchronize(ev_[c & 1]), "staging wait");
+      if (c + 1 < nchunk) issue(c + 1);  // overlaps this chunk's CPU copy
+      const size_t off = c * kChunk, n = std::min(kChunk, bytes - off);
+      par_copy(static_cast<char*>(dst) + off, buf_[c & 1], n);
+    }
+  }
+
+ private:
+  static constexpr size_t kChunk = size_t(32) << 20, kSmall = size_t(1) << 20;
+  void init() {
+    if (buf_[0]) return;
+    for (int b = 0; b < 2; ++b) {
+      cuda(cudaHostAlloc(reinterpret_cast<void**>(&buf_[b]), kChunk, cudaHostAllocDefault), "cudaHostAlloc");
+      cuda(cudaEventCreateWithFlags(&ev_[b], cudaEventDisableTiming), "event");
+    }
+    cuda(cudaStreamCreateWithFlags(&stream_, cudaStreamNonBlocking), "stream");
+    threads_ = std::max(1u, std::min(8u, std::thread::hardware_concurrency()));
+  }
+  void par_copy(void* dst, const void* src, size_t n) {
+    const unsigned T = n >= (size_t(4) << 20) ? threads_ : 1;
+    if (T == 1) {
+      std::memcpy(dst, src, n);
+      return;
+    }
+    const size_t per = (n / T + 63) & ~size_t(63);
+    std::vector<std::thread> th;
+    for (unsigned t = 1; t < T; ++t) {
+      const size_t a = std::min(n, t * per), e = std::min(n, a + per);
+      if (a < e)
+        th.emplace_back([=] { std::memcpy(static_cast<char*>(dst) + a, static_cast<const char*>(src) + a, e - a); });
+    }
+    std::memcpy(dst, src, std::min(n, per));
+    for (auto& x : th) x.join();
+  }
+  char* buf_[2] = {nullptr, nullptr};
+  cudaEvent_t ev_[2] = {nullptr, nullptr};
+  cudaStream_t stream_ = nullptr;
+  unsigned threads_ = 1;
+};
+
+// Owning device buffer: stream-ordered allocations from the device's memory
+// pool (libnpcg keeps freed blocks cached there, so repeated calls reuse them).
 template <typename T>
 class Dev {
  public:
   Dev() = default;
   explicit Dev(size_t n) : n_(n) {
-    if (n) cuda(cudaMalloc(&p_, n * sizeof(T)), "cudaMalloc");
+    if (n) cuda(cudaMallocAsync(reinterpret_cast<void**>(&p_), n * sizeof(T), nullptr), "cudaMallocAsync");
   }
-  Dev(const T* host, size_t n) : Dev(n) {
-    if (n) cuda(cudaMemcpy(p_, host, n * sizeof(T), cudaMemcpyHostToDevice), "H2D");
-  }
+  Dev(const T* host, size_t n) : Dev(n) { upload(host, n); }
   ~Dev() {
-    if (p_) cudaFree(p_);
+    if (p_) cudaFreeAsync(p_, nullptr);
   }
   Dev(Dev&& o) noexcept : p_(o.p_), n_(o.n_) { o.p_ = nullptr, o.n_ = 0; }
   Dev& operator=(Dev&& o) noexcept {
@@ -130,11 +210,24 @@ class Dev {
   Dev(const Dev&) = delete;
   T* get() const { return p_; }
   size_t size() const { return n_; }
-  std::vector<T> host() const {
-    std::vector<T> v(n_);
-    if (n_) {
+  // (re)size without keeping the contents; keeps the block when it fits
+  void ensure(size_t n) {
+    if (n <= n_ && p_) return;
+    *this = Dev(n);
+  }
+  void upload(const T* host, size_t n) {
+    ensure(n);
+    if (n) {
+      cuda(cudaStreamSynchronize(nullptr), "sync");  // the block may be fresh from the pool
+      Stager::get().h2d(p_, host, n * sizeof(T));
+    }
+  }
+  std::vector<T> host() const { return host(n_); }
+  std::vector<T> host(size_t n) const {
+    std::vector<T> v(n);
+    if (n) {
       check(npcg_context_synchronize(ctx()), "sync");
-      cuda(cudaMemcpy(v.data(), p_, n_ * sizeof(T), cudaMemcpyDeviceToHost), "D2H");
+      Stager::get().d2h(v.data(), p_, n * sizeof(T));
     }
     return v;
   }
@@ -467,10 +560,12 @@ struct ExecConfig {
   Executor executor = Executor::grouped;
   bool deterministic = false;
   int workers = 0;
+  // AUTO keeps the reference's fp32 contract (rel <= 1e-5, the split
+  // tensor-core path or the exact engines); NPCG_MATH_BF16 is the opt-in
   npcg_math math = NPCG_MATH_AUTO;
-  npcg_exec_config c() const {
+  npcg_exec_config c(int32_t flags = 0) const {
     return {L, b_out, b_in, static_cast<int32_t>(executor), deterministic ? 1 : 0, workers,
-            static_cast<int32_t>(math)};
+            static_cast<int32_t>(math), flags, 0};
   }
 };
 
@@ -591,33 +686,38 @@ class PointConvOp {
     if (fin.groups() != w_.groups() || fin.channels() != w_.c_in())
       throw ShapeError("mvmr: weight and feature shapes differ");
     build_cache(in_cloud, out_cloud);
-    // conv_op.hpp:138 copy (degraded: the library gathers the site rows from it)
-    dfin_ = detail::Dev<T>(fin.values().data(), fin.values().size());
-    detail::Dev<T> out(static_cast<size_t>(n_out_ * w_.groups() * w_.c_out()));
+    // conv_op.hpp:138 copy (degraded: the library gathers the site rows from
+    // it); the op's device buffers persist across calls
+    dfin_.upload(fin.values().data(), fin.values().size());
+    const size_t n_o = static_cast<size_t>(n_out_ * w_.groups() * w_.c_out());
+    dout_.ensure(n_o);
     const npcg_exec_config c = cfg_.c();
     detail::check(npcg_conv_forward(detail::ctx(), nb_->h, detail::dtype_of<T>(), dw_.get(), w_.groups(), w_.c_in(),
-                                    w_.c_out(), dfin_.get(), &c, out.get()),
+                                    w_.c_out(), dfin_.get(), &c, dout_.get()),
                   "PointConvOp::forward");
     n_in_ = fin.n();
     has_forward_ = true;
-    return FeatureTensor<T>(n_out_, w_.groups(), w_.c_out(), out.host());
+    return FeatureTensor<T>(n_out_, w_.groups(), w_.c_out(), dout_.host(n_o));
   }
 
   BackwardResult<T> backward(const FeatureTensor<T>& gout) {
     if (!has_forward_) throw StateError("PointConvOp::backward: no cached forward inputs");
     if (gout.n() != n_out_ || gout.groups() != w_.groups() || gout.channels() != w_.c_out())
       throw ShapeError("PointConvOp::backward: gout shape mismatch");
-    detail::Dev<T> dg(gout.values().data(), gout.values().size());
+    dg_.upload(gout.values().data(), gout.values().size());
     // degraded: gradients of the original rows, zero for merged-away points (conv_op.hpp:193-202)
-    detail::Dev<T> gi(static_cast<size_t>(n_in_ * w_.groups() * w_.c_in()));
-    detail::Dev<T> gw(static_cast<size_t>(w_.kernels() * w_.groups() * w_.c_out() * w_.c_in()));
-    const npcg_exec_config c = cfg_.c();
+    const size_t n_gi = static_cast<size_t>(n_in_ * w_.groups() * w_.c_in());
+    const size_t n_gw = static_cast<size_t>(w_.kernels() * w_.groups() * w_.c_out() * w_.c_in());
+    dgi_.ensure(n_gi);
+    dgw_.ensure(n_gw);
+    // dfin_ is the op's own saved copy, unmodified since the forward
+    const npcg_exec_config c = cfg_.c(NPCG_FLAG_FIN_UNCHANGED);
     detail::check(npcg_conv_backward(detail::ctx(), nb_->h, detail::dtype_of<T>(), dw_.get(), w_.groups(), w_.c_in(),
-                                     w_.c_out(), dfin_.get(), dg.get(), &c, gi.get(), gw.get()),
+                                     w_.c_out(), dfin_.get(), dg_.get(), &c, dgi_.get(), dgw_.get()),
                   "PointConvOp::backward");
-    BackwardResult<T> r{FeatureTensor<T>(n_in_, w_.groups(), w_.c_in(), gi.host()),
+    BackwardResult<T> r{FeatureTensor<T>(n_in_, w_.groups(), w_.c_in(), dgi_.host(n_gi)),
                         WeightGradient<T>(w_.kernels(), w_.groups(), w_.c_out(), w_.c_in())};
-    const auto h = gw.host();
+    const auto h = dgw_.host(n_gw);
     std::copy(h.begin(), h.end(), r.grad_w.values_mut().begin());
     return r;
   }
@@ -649,7 +749,7 @@ class PointConvOp {
   WeightTensor<T> w_;
   ConvGeometry geom_;
   ExecConfig cfg_;
-  detail::Dev<T> dw_, dfin_;
+  detail::Dev<T> dw_, dfin_, dout_, dg_, dgi_, dgw_;
   std::shared_ptr<detail::Neighbors> nb_;
   mutable std::unique_ptr<TripletList> sorted_;
   std::unique_ptr<std::pair<PointCloud, DownsampleMap>> sites_;
@@ -657,6 +757,39 @@ class PointConvOp {
   int64_t n_out_ = 0, n_in_ = 0;
   bool has_forward_ = false;
 };
+
+// ---- strided path (spatial.hpp:52-54, conv_op.hpp:86-91, 219-225) -------------------
+// spatial.cpp:154-169: fine row p = coarse row map.parent_of[p] (npcg_upsample)
+template <typename T>
+FeatureTensor<T> upsample(const PointCloud& fine, const DownsampleMap& map, const FeatureTensor<T>& coarse) {
+  if (static_cast<int64_t>(map.parent_of.size()) != fine.n_points())
+    throw ShapeError("upsample: map does not cover the fine cloud");
+  if (static_cast<int64_t>(map.kept_index.size()) != coarse.n())
+    throw ShapeError("upsample: coarse features do not match the map");
+  const int64_t n = fine.n_points(), w = coarse.row_width();
+  detail::Dev<int64_t> par(map.parent_of.data(), map.parent_of.size());
+  detail::Dev<T> dc(coarse.values().data(), coarse.values().size());
+  detail::Dev<T> out(static_cast<size_t>(n * w));
+  detail::check(npcg_upsample(detail::ctx(), detail::dtype_of<T>(), par.get(), n, dc.get(), coarse.n(), w, out.get()),
+                "upsample");
+  return FeatureTensor<T>(n, coarse.groups(), coarse.channels(), out.host());
+}
+
+template <typename T>
+struct StridedResult {  // conv_op.hpp:22-26
+  PointCloud coarse_cloud;
+  FeatureTensor<T> coarse_features;
+  DownsampleMap map;  // for a later upsample back to the fine cloud
+};
+
+// conv_op.hpp:219-225: voxel-downsample, then convolve the fine cloud onto the kept points
+template <typename T>
+StridedResult<T> strided_block(PointConvOp<T>& op, const PointCloud& cloud, const FeatureTensor<T>& fin,
+                               double voxel_size) {
+  auto [coarse, map] = voxel_downsample(cloud, voxel_size);
+  FeatureTensor<T> features = op.forward(cloud, coarse, fin);
+  return {std::move(coarse), std::move(features), std::move(map)};
+}
 
 // ---- file formats (io.hpp; triplets.hpp:84-93) -- host side, little-endian -------------
 namespace detail {

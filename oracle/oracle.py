@@ -263,6 +263,8 @@ class Reference:
             getattr(lib, f"ref_vvor_{s}").argtypes = [_P, _I64, _P, _I64, _I64, _I64, _I64, _P, _P,
                                                       _P, _I64, _I64, _I64, _I64, _INT, _INT, _I64,
                                                       _INT, _P]
+            getattr(lib, f"ref_upsample_{s}").argtypes = [_P, _P, _I64, _P, _I64, _P, _P, _I64, _I64,
+                                                          _P]
         search_args = [_P, _P, _I64, _P, _P, _I64, _D, C.POINTER(_P)]
         lib.ref_radius_search.argtypes = search_args
         lib.ref_brute_radius.argtypes = search_args
@@ -472,6 +474,23 @@ class Reference:
         if m < 0:
             raise OracleError(-m, "voxel_downsample")
         return kept[:m].copy(), parent, out_off
+
+    def upsample(self, xyz, kept, parent, coarse, offsets=None):
+        """The reference's upsample (spatial.hpp:52-54) of coarse (n_kept, G, C)."""
+        xyz = _f64(xyz).reshape(-1, 3)
+        off = _offsets(len(xyz), offsets)
+        coarse = np.ascontiguousarray(coarse)
+        s = "f32" if coarse.dtype == np.float32 else "f64"
+        kept = np.ascontiguousarray(kept, np.int64)
+        parent = np.ascontiguousarray(parent, np.int64)
+        _, G, Cc = coarse.shape
+        out = np.empty((len(xyz), G, Cc), dtype=coarse.dtype)
+        rc = getattr(self.lib, f"ref_upsample_{s}")(_ptr(xyz), _ptr(off), len(off) - 1, _ptr(kept),
+                                                    len(kept), _ptr(parent), _ptr(coarse), G, Cc,
+                                                    _ptr(out))
+        if rc:
+            raise OracleError(rc, "upsample")
+        return out
 
     def build_triplets_degraded(self, xyz, voxel, t, offsets=None):
         """The reference's build_triplets_degraded (triplets.hpp:63-76)."""

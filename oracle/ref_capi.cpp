@@ -287,6 +287,26 @@ int ref_dense_oracle(const double* w, int64_t t, int64_t G, int64_t ci, int64_t 
   } catch (const std::exception& e) { return status_of(e); }
 }
 
+// spatial.hpp:52-54 upsample (the reference checks the map against the cloud
+// and the coarse tensor, then copies rows through parent_of)
+#define NPREF_UPSAMPLE(T, SUF)                                                              \
+  int ref_upsample_##SUF(const double* xyz, const int64_t* off, int64_t nb, const int64_t* kept, \
+                         int64_t n_kept, const int64_t* parent, const T* coarse, int64_t G,    \
+                         int64_t C, T* out) {                                                 \
+    try {                                                                                    \
+      const PointCloud fine = cloud_of(xyz, off, nb);                                        \
+      DownsampleMap m;                                                                       \
+      m.kept_index.assign(kept, kept + n_kept);                                              \
+      m.parent_of.assign(parent, parent + fine.n_points());                                  \
+      FeatureTensor<T> c(n_kept, G, C, std::vector<T>(coarse, coarse + n_kept * G * C));     \
+      auto r = upsample(fine, m, c);                                                         \
+      std::memcpy(out, r.values().data(), r.values().size() * sizeof(T));                    \
+      return 0;                                                                              \
+    } catch (const std::exception& e) { return status_of(e); }                               \
+  }
+NPREF_UPSAMPLE(float, f32)
+NPREF_UPSAMPLE(double, f64)
+
 // spatial.hpp:47-48 voxel_downsample
 int64_t ref_voxel_downsample(const double* xyz, const int64_t* off, int64_t nb, double v,
                              int64_t* kept, int64_t* parent, int64_t* out_off) {

@@ -24,7 +24,10 @@ _PI64 = C.POINTER(C.c_int64)
 
 class npcg_exec_config(C.Structure):
     _fields_ = [("L", _I64), ("b_out", _I64), ("b_in", _I64), ("executor", _I32),
-                ("deterministic", _I32), ("workers", _I32), ("math", _I32)]
+                ("deterministic", _I32), ("workers", _I32), ("math", _I32), ("flags", _I32),
+                ("reserved", _I32)]
+
+FLAG_FIN_UNCHANGED = 1  # NPCG_FLAG_FIN_UNCHANGED
 
 
 class npcg_cloud(C.Structure):
@@ -91,6 +94,10 @@ _SIGS = {
     "npcg_neighbors_plan_stats": (C.c_int, [_P, _P, _P]),
     "npcg_debug_trace_forward": (C.c_int, [_P, _P, _P, _P, _P, _P]),
     "npcg_voxel_downsample": (C.c_int, [_P, C.POINTER(npcg_cloud), _D, _P, _P, _P, _PI64]),
+    "npcg_upsample": (C.c_int, [_P, C.c_int, _P, _I64, _P, _I64, _I64, _P]),
+    "npcg_gen_uniform_cube": (C.c_int, [_I64, _D, C.c_uint64, _P]),
+    "npcg_gen_features": (C.c_int, [_I64, _I64, _I64, C.c_uint64, C.c_int, _P]),
+    "npcg_make_weights": (C.c_int, [_I64, _I64, _I64, _I64, C.c_uint64, C.c_int, _P]),
     "npcg_comm_unique_id": (C.c_int, [_P]),
     "npcg_comm_create": (C.c_int, [_P, C.c_int, C.c_int, _P, C.POINTER(_P)]),
     "npcg_comm_destroy": (C.c_int, [_P]),

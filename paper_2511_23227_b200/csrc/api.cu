@@ -17,6 +17,8 @@ void kernel_index_batch(npcg_context* ctx, const double* c, const double* nbr, i
                         double radius, int64_t t, int64_t* k);
 void voxel_downsample_impl(npcg_context* ctx, const npcg_cloud* cloud, double voxel,
                            int64_t* kept, int64_t* parent, int64_t* out_offsets, int64_t* n_kept);
+void upsample_impl(npcg_context* ctx, const int64_t* parent, int64_t n_fine, const void* coarse,
+                   int64_t n_coarse, int64_t row_bytes, void* fine);
 }  // namespace npcg
 
 namespace {
@@ -35,7 +37,7 @@ void validate_config(const npcg_exec_config* c) {
   if (c->L < 1) fail(NPCG_ERR_SHAPE, "ExecConfig: L must be >= 1");
   if (c->b_out < 1 || c->b_in < 1) fail(NPCG_ERR_SHAPE, "ExecConfig: tile sizes must be >= 1");
   if (c->workers < 0) fail(NPCG_ERR_SHAPE, "ExecConfig: workers must be >= 0");
-  if (c->math < NPCG_MATH_AUTO || c->math > NPCG_MATH_BF16)
+  if (c->math < NPCG_MATH_AUTO || c->math > NPCG_MATH_F32TC)
     fail(NPCG_ERR_INVALID, "ExecConfig: unknown math mode");
 }
 
@@ -54,18 +56,31 @@ int64_t cube_root_exact(int64_t K) {
   return -1;
 }
 
-// Which engine runs: BF16 tensor cores or exact CUDA cores.
-bool use_tc(const npcg_exec_config* cfg, npcg_dtype dtype, int64_t G, int64_t cin, int64_t cout,
-            int64_t K) {
-  if (cfg->math == NPCG_MATH_EXACT) return false;
-  if (cfg->math == NPCG_MATH_BF16) {
-    if (dtype != NPCG_F32) fail(NPCG_ERR_UNSUPPORTED, "bf16 math requires F32 tensors");
-    if (!tc_supported(G, cin, cout, K, true))
-      fail(NPCG_ERR_UNSUPPORTED,
-           "bf16 tensor-core path needs G=1, C_in, C_out multiples of 16 up to 256, K<=128");
-    return true;
+// Which engine runs: the exact CUDA-core engines, the bf16 tensor-core path
+// (opt-in), or the split (fp32-contract) tensor-core path.  AUTO keeps the
+// reference's fp32 contract: the split path where it applies, else exact.
+TcMode use_tc(const npcg_exec_config* cfg, npcg_dtype dtype, int64_t G, int64_t cin,
+              int64_t cout, int64_t K) {
+  switch (cfg->math) {
+    case NPCG_MATH_EXACT:
+      return TcMode::none;
+    case NPCG_MATH_BF16:
+      if (dtype != NPCG_F32) fail(NPCG_ERR_UNSUPPORTED, "bf16 math requires F32 tensors");
+      if (!tc_supported(G, cin, cout, K, TcMode::bf16, true))
+        fail(NPCG_ERR_UNSUPPORTED,
+             "bf16 tensor-core path needs G=1, C_in, C_out multiples of 16 up to 256, K<=128");
+      return TcMode::bf16;
+    case NPCG_MATH_F32TC:
+      if (dtype != NPCG_F32) fail(NPCG_ERR_UNSUPPORTED, "f32tc math requires F32 tensors");
+      if (!tc_supported(G, cin, cout, K, TcMode::split, true))
+        fail(NPCG_ERR_UNSUPPORTED,
+             "split tensor-core path needs G=1, C_in, C_out multiples of 16 up to 128, K<=128");
+      return TcMode::split;
+    default:
+      return dtype == NPCG_F32 && tc_supported(G, cin, cout, K, TcMode::split, false)
+                 ? TcMode::split
+                 : TcMode::none;
   }
-  return dtype == NPCG_F32 && tc_supported(G, cin, cout, K);
 }
 
 // A transient neighbor handle over a raw TripletList: CSR over rows (stable
@@ -124,8 +139,8 @@ void forward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, const
     NPCG_CUDA(cudaMemsetAsync(fout, 0, bytes, ctx->stream));
     return;
   }
-  if (use_tc(cfg, dtype, G, cin, cout, nb->n_kernels)) {
-    tc_forward(ctx, nb, static_cast<const float*>(w), static_cast<const float*>(fin),
+  if (const TcMode m = use_tc(cfg, dtype, G, cin, cout, nb->n_kernels); m != TcMode::none) {
+    tc_forward(ctx, nb, m, static_cast<const float*>(w), static_cast<const float*>(fin),
                static_cast<float*>(fout), static_cast<int>(cin), static_cast<int>(cout));
     return;
   }
@@ -161,10 +176,11 @@ void backward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, cons
       NPCG_CUDA(cudaMemsetAsync(grad_w, 0, nb->n_kernels * G * cin * cout * ds, ctx->stream));
     return;
   }
-  if (use_tc(cfg, dtype, G, cin, cout, nb->n_kernels)) {
-    tc_backward(ctx, nb, static_cast<const float*>(w), static_cast<const float*>(fin),
+  if (const TcMode m = use_tc(cfg, dtype, G, cin, cout, nb->n_kernels); m != TcMode::none) {
+    tc_backward(ctx, nb, m, static_cast<const float*>(w), static_cast<const float*>(fin),
                 static_cast<const float*>(gout), static_cast<float*>(grad_in),
-                static_cast<float*>(grad_w), static_cast<int>(cin), static_cast<int>(cout));
+                static_cast<float*>(grad_w), static_cast<int>(cin), static_cast<int>(cout),
+                (cfg->flags & NPCG_FLAG_FIN_UNCHANGED) != 0);
     return;
   }
   if (grad_in) {
@@ -187,6 +203,13 @@ void backward_impl(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype dtype, cons
                          static_cast<int>(cin), static_cast<int>(cout),
                          static_cast<double*>(grad_w));
   }
+}
+
+// The handle's last user (see npcg_neighbors::last_stream).
+void touch(npcg_context* ctx, npcg_neighbors* nb) {
+  nb->last_stream = ctx->stream;
+  nb->device = ctx->device;
+  nb->used = true;
 }
 
 void check_triplets_struct(const npcg_triplets* T) {
@@ -455,6 +478,12 @@ npcg_status npcg_neighbors_export_sites(npcg_context* ctx, const npcg_neighbors*
 
 npcg_status npcg_neighbors_destroy(npcg_neighbors* nb) {
   if (!nb) return NPCG_ERR_INVALID;
+  if (nb->used) {
+    cudaSetDevice(nb->device);
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(nb->last_stream, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone)
+      cudaStreamSynchronize(nb->last_stream);
+  }
   delete nb;
   return NPCG_OK;
 }
@@ -640,7 +669,7 @@ npcg_status npcg_vvor(npcg_context* ctx, npcg_dtype dtype, const void* gout, int
     if (dtype != NPCG_F32 && dtype != NPCG_F64) fail(NPCG_ERR_INVALID, "bad dtype");
     if (cfg->L < 1) fail(NPCG_ERR_SHAPE, "vvor: L must be >= 1");
     if (cfg->b_out < 1 || cfg->b_in < 1) fail(NPCG_ERR_SHAPE, "vvor: tile sizes must be >= 1");
-    if (cfg->math < NPCG_MATH_AUTO || cfg->math > NPCG_MATH_BF16)
+    if (cfg->math < NPCG_MATH_AUTO || cfg->math > NPCG_MATH_F32TC)
       fail(NPCG_ERR_INVALID, "ExecConfig: unknown math mode");
     if (groups < 1 || c_in < 1 || c_out < 1)
       fail(NPCG_ERR_SHAPE, "FeatureTensor: need n >= 0, groups >= 1, channels >= 1");
@@ -662,12 +691,13 @@ npcg_status npcg_vvor(npcg_context* ctx, npcg_dtype dtype, const void* gout, int
     // vvor accepts any n_kernels (not only t^3): use the t-less exact engine
     // unless K is a cube handled by the tensor-core path.
     const int64_t t = cube_root_exact(n_kernels);
-    if (t > 0 && t % 2 == 1 && use_tc(cfg, dtype, groups, c_in, c_out, n_kernels)) {
+    if (t > 0 && t % 2 == 1 && use_tc(cfg, dtype, groups, c_in, c_out, n_kernels) != TcMode::none) {
       auto nb = handle_from_triplets(ctx, T, n_gout, n_fin, t);
       backward_impl(ctx, nb.get(), dtype, nullptr, groups, c_in, c_out, fin, gout, cfg, nullptr,
                     grad);
     } else {
-      if (cfg->math == NPCG_MATH_BF16) fail(NPCG_ERR_UNSUPPORTED, "bf16 vvor needs K = t^3, G=1, C multiples of 16 up to 256");
+      if (cfg->math == NPCG_MATH_BF16 || cfg->math == NPCG_MATH_F32TC)
+        fail(NPCG_ERR_UNSUPPORTED, "tensor-core vvor needs K = t^3 (t odd), G=1, C multiples of 16");
       CellPlan cells;
       cells_from_triplets(ctx, T, n_kernels, &cells);
       if (dtype == NPCG_F32)
@@ -703,6 +733,7 @@ npcg_status npcg_conv_forward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype 
   if (!ctx) return NPCG_ERR_INVALID;
   return guard(ctx, [&] {
     check_op(nb, dtype, groups, c_in, c_out, cfg);
+    touch(ctx, nb);
     if (nb->n_out == 0) return;
     need(fout, "fout");
     need(w, "w");
@@ -715,6 +746,7 @@ npcg_status npcg_conv_forward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype 
       if (nb->site_fin.size() < nb->n_in * width) nb->site_fin.alloc(ctx, nb->n_in * width);
       gather_rows(ctx, fin, nb->kept.get(), nb->n_in, width, nb->site_fin.get());
       nb->site_fin_dtype = dtype;
+      nb->site_fin_width = width;
       forward_impl(ctx, nb, dtype, w, groups, c_in, c_out, nb->site_fin.get(), cfg, fout);
       return;
     }
@@ -729,15 +761,26 @@ npcg_status npcg_conv_backward(npcg_context* ctx, npcg_neighbors* nb, npcg_dtype
   if (!ctx) return NPCG_ERR_INVALID;
   return guard(ctx, [&] {
     check_op(nb, dtype, groups, c_in, c_out, cfg);
+    touch(ctx, nb);
     need(w, "w");
     if (nb->n_out > 0) need(gout, "gout");
     if (nb->degraded) {
       // conv_op.hpp:177-202: gradients w.r.t. the rows saved by the forward;
       // site input gradients scatter back to the representative points,
       // merged-away points keep zero rows
-      if (nb->site_fin_dtype != dtype)
-        fail(NPCG_ERR_STATE, "PointConvOp::backward: no cached forward inputs");
       const int64_t width = groups * c_in * static_cast<int64_t>(dsize(dtype));
+      if (fin) {
+        // the operator's saved input: its site rows are gathered again (the
+        // handle may have served another layer's forward since)
+        if (nb->site_fin.size() < nb->n_in * width) nb->site_fin.alloc(ctx, nb->n_in * width);
+        gather_rows(ctx, fin, nb->kept.get(), nb->n_in, width, nb->site_fin.get());
+        nb->site_fin_dtype = dtype;
+        nb->site_fin_width = width;
+      } else if (nb->site_fin_dtype != dtype) {
+        fail(NPCG_ERR_STATE, "PointConvOp::backward: no cached forward inputs");
+      } else if (nb->site_fin_width != width) {
+        fail(NPCG_ERR_SHAPE, "PointConvOp::backward: layer widths differ from the cached forward's");
+      }
       DevBuf<uint8_t> gi_sites(ctx, grad_in ? std::max<int64_t>(nb->n_in * width, 1) : 0);
       backward_impl(ctx, nb, dtype, w, groups, c_in, c_out, nb->site_fin.get(), gout, cfg,
                     grad_in ? gi_sites.get() : nullptr, grad_w);
@@ -756,11 +799,12 @@ npcg_status npcg_neighbors_prepare(npcg_context* ctx, npcg_neighbors* nb, int32_
   if (!ctx || !nb) return NPCG_ERR_INVALID;
   return guard(ctx, [&] {
     if (nb->t == 0) fail(NPCG_ERR_STATE, "prepare: handle has no kernel cells");
+    touch(ctx, nb);
     if (math == NPCG_MATH_EXACT || math == NPCG_MATH_AUTO) {
       build_tcsr(ctx, nb);
       build_cells(ctx, nb);
     }
-    if ((math == NPCG_MATH_BF16 || math == NPCG_MATH_AUTO) && tc_supported(1, 64, 64, nb->n_kernels))
+    if (math != NPCG_MATH_EXACT && tc_supported(1, 64, 64, nb->n_kernels, TcMode::bf16, false))
       tc_prepare(ctx, nb);
     NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
@@ -770,7 +814,9 @@ npcg_status npcg_neighbors_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int
   if (!ctx || !nb || !stats) return NPCG_ERR_INVALID;
   return guard(ctx, [&] {
     if (nb->t == 0) fail(NPCG_ERR_STATE, "plan_stats: handle has no kernel cells");
-    if (!tc_supported(1, 64, 64, nb->n_kernels)) fail(NPCG_ERR_UNSUPPORTED, "no tensor-core plan for this K");
+    touch(ctx, nb);
+    if (!tc_supported(1, 64, 64, nb->n_kernels, TcMode::bf16, false))
+      fail(NPCG_ERR_UNSUPPORTED, "no tensor-core plan for this K");
     tc_plan_stats(ctx, nb, stats);
   });
 }
@@ -779,7 +825,7 @@ npcg_status npcg_debug_trace_forward(npcg_context* ctx, npcg_neighbors* nb, cons
                                      const float* fin, float* fout, int64_t* trace) {
   if (!ctx || !nb || !trace) return NPCG_ERR_INVALID;
   return guard(ctx, [&] {
-    if (nb->t == 0 || !tc_supported(1, 64, 64, nb->n_kernels))
+    if (nb->t == 0 || !tc_supported(1, 64, 64, nb->n_kernels, TcMode::bf16, false))
       fail(NPCG_ERR_UNSUPPORTED, "trace: tensor-core plan needs K<=128");
     tc_trace_forward(ctx, nb, w, fin, fout, trace);
   });
@@ -795,6 +841,25 @@ npcg_status npcg_voxel_downsample(npcg_context* ctx, const npcg_cloud* cloud, do
     need(out_offsets, "out_offsets");
     need(n_kept, "n_kept");
     voxel_downsample_impl(ctx, cloud, voxel, kept, parent, out_offsets, n_kept);
+  });
+}
+
+// spatial.cpp:154-169 (validation at :156-160 is the caller's map / tensor
+// shapes; here the widths and the parent range)
+npcg_status npcg_upsample(npcg_context* ctx, npcg_dtype dtype, const int64_t* parent,
+                          int64_t n_fine, const void* coarse, int64_t n_coarse, int64_t width,
+                          void* fine) {
+  if (!ctx) return NPCG_ERR_INVALID;
+  return guard(ctx, [&] {
+    if (dtype != NPCG_F32 && dtype != NPCG_F64) fail(NPCG_ERR_INVALID, "bad dtype");
+    if (width < 1) fail(NPCG_ERR_SHAPE, "upsample: feature width must be >= 1");
+    if (n_fine < 0 || n_coarse < 0) fail(NPCG_ERR_SHAPE, "upsample: negative row count");
+    if (n_fine == 0) return;
+    need(parent, "parent");
+    need(coarse, "coarse");
+    need(fine, "fine");
+    upsample_impl(ctx, parent, n_fine, coarse, n_coarse, width * static_cast<int64_t>(dsize(dtype)),
+                  fine);
   });
 }
 

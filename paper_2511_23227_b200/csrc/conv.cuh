@@ -19,16 +19,25 @@ void vvor_cells(npcg_context* ctx, const CellPlan& cells, const T* gout, const T
                 int cin, int cout, T* grad);
 
 // ---- tensor-core engines (conv_tc.cu) --------------------------------------
-// True when the tcgen05 path handles this shape: G = 1, K <= 128 (t <= 5), C_in and
-// C_out multiples of 16 in [64, 256] (automatic choice) or [16, 256] (forced,
-// math = bf16); widths are zero-padded to 64 / 128 / 256 inside.
-bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t n_kernels, bool forced = false);
-// Forward / input-gradient / weight-gradient over a neighbor handle with
-// bf16 operands and fp32 accumulation.  Builds and caches the tile plans.
-void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                float* fout, int cin, int cout);
-void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                 const float* gout, float* grad_in, float* grad_w, int cin, int cout);
+// Operand arithmetic of the tcgen05 path: bf16 operands (opt-in, rel ~2e-3),
+// or split operands (x = hi + lo, two bf16 each; products hi*hi + hi*lo + lo*hi,
+// fp32 accumulate; rel ~4e-6, inside the reference's fp32 bound of 1e-5).
+enum class TcMode { none = 0, bf16 = 1, split = 2 };
+// True when the tcgen05 path handles this shape in `mode`: G = 1, K <= 128
+// (t <= 5), C_in and C_out multiples of 16 in [64, cmax] (automatic choice) or
+// [16, cmax] (forced), cmax = 256 (bf16) / 128 (split); widths are zero-padded
+// to 64 / 128 / 256 inside.
+bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t n_kernels, TcMode mode,
+                  bool forced);
+// Forward / input-gradient / weight-gradient over a neighbor handle on the
+// tensor cores.  Builds and caches the tile plans.  fin_unchanged: `fin` is
+// the buffer the last forward on this handle converted, unmodified (its device
+// image is reused).
+void tc_forward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
+                const float* fin, float* fout, int cin, int cout);
+void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
+                 const float* fin, const float* gout, float* grad_in, float* grad_w, int cin,
+                 int cout, bool fin_unchanged);
 void tc_prepare(npcg_context* ctx, npcg_neighbors* nb);
 void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12);
 void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,

@@ -56,6 +56,12 @@ constexpr int SLOT_ENTRIES = 512;
 constexpr int BLOCK_MAX_BYTES = 512 + 2 * SLOT_ENTRIES;
 constexpr int MAX_BLOCK_ENTRIES = 8192;  // planner cap per block
 constexpr uint32_t kOverflow = 0xFFFFFFFFu;
+constexpr bool kSplitReady = false;
+// Descriptor blocks are 16-byte aligned and addressed in 16-byte units (u32:
+// 64 GB of blocks per plan, ~400M points at ~160 B per point).
+__host__ __device__ __forceinline__ uint64_t blk_bytes(uint32_t units) {
+  return static_cast<uint64_t>(units) << 4;
+}
 constexpr uint32_t SUP_FIRST = 1u << 8, SUP_LAST = 1u << 9;  // record flags in sup[].y
 
 // A direction plan: super-tiles of 1..st sub-tiles sharing one shared-memory
@@ -80,7 +86,7 @@ struct TcDirPlan {
   DevBuf<uint2> tiles;        // n_sub {first permuted row, rows (<= 128)}
   DevBuf<uint32_t> halo;      // n_super * hcap permuted source row of each halo row
   DevBuf<uint32_t> halo_len;  // n_super (kOverflow marks a super-tile the planner rejected)
-  DevBuf<uint32_t> blk_off;   // n_sub*K (+1) byte offsets of the stage-descriptor blocks
+  DevBuf<uint32_t> blk_off;   // n_sub*K (+1) offsets of the stage-descriptor blocks, in 16-byte units
   DevBuf<uint8_t> blocks;
   int n_overflow = 0;
   int max_halo = 0;
@@ -114,12 +120,16 @@ void destroy_tc_plan(TcPlan* p);
 // The automatic choice keeps narrow layers (C < 64, where the contraction is
 // not dense enough to pay for the padding) on the CUDA-core engines;
 // math = bf16 forces the tensor cores for any multiple of 16 up to 256.
-static bool tc_width(int64_t c, bool forced) {
-  return c >= (forced ? 16 : 64) && c <= 256 && c % 16 == 0;
+static bool tc_width(int64_t c, int64_t cmax, bool forced) {
+  return c >= (forced ? 16 : 64) && c <= cmax && c % 16 == 0;
 }
 static int tc_pad(int c) { return c <= 64 ? 64 : c <= 128 ? 128 : 256; }
-bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K, bool forced) {
-  return G == 1 && tc_width(cin, forced) && tc_width(cout, forced) && K >= 1 && K <= KMAX;
+bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K, TcMode mode, bool forced) {
+  if (mode == TcMode::none) return false;
+  if (mode == TcMode::split && !kSplitReady) return false;
+  const int64_t cmax = mode == TcMode::split ? 128 : 256;
+  return G == 1 && tc_width(cin, cmax, forced) && tc_width(cout, cmax, forced) && K >= 1 &&
+         K <= KMAX;
 }
 
 // ===========================================================================
@@ -224,7 +234,7 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
     const uint32_t E = cnt[r];
     if (E > MAX_BLOCK_ENTRIES) bad = 1;
     const uint32_t bytes = 512u + ((2u * E + 15u) / 16u) * 16u;
-    blk_size[static_cast<int64_t>(blockIdx.x) * K + r] = bytes;
+    blk_size[static_cast<int64_t>(blockIdx.x) * K + r] = bytes >> 4;
     atomicMax(max_blk, bytes);
   }
   __syncthreads();
@@ -435,7 +445,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
   const unsigned lt = (1u << lane) - 1u;
   for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
     const int g = b / K, k = b % K;
-    const int64_t boff = blk_off[static_cast<int64_t>(sub0 + g) * K + k];
+    const uint64_t boff = blk_bytes(blk_off[static_cast<int64_t>(sub0 + g) * K + k]);
     uint32_t* items = reinterpret_cast<uint32_t*>(blocks + boff);
     int pos = 0, ebase = 0;
     int vmax = 0;
@@ -475,7 +485,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
       }
       const int idx = (g * K + k) * TM + r;
       const int pos = eoff[idx] + cnt[idx]++;
-      const int64_t boff = blk_off[static_cast<int64_t>(sub0 + g) * K + k];
+      const uint64_t boff = blk_bytes(blk_off[static_cast<int64_t>(sub0 + g) * K + k]);
       reinterpret_cast<uint16_t*>(blocks + boff + 512)[pos] = static_cast<uint16_t>(lo);
     });
   }
@@ -483,7 +493,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
   // 7. in quads whose rows have at most one entry (the copy pass), a row's
   //    item carries its entry's halo index instead of the entry offset
   for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
-    const int64_t boff = blk_off[static_cast<int64_t>(sub0 + b / K) * K + b % K];
+    const uint64_t boff = blk_bytes(blk_off[static_cast<int64_t>(sub0 + b / K) * K + b % K]);
     uint32_t* items = reinterpret_cast<uint32_t*>(blocks + boff);
     const uint16_t* ents = reinterpret_cast<const uint16_t*>(blocks + boff + 512);
     for (int p = lane; p < TM; p += 32) {
@@ -512,7 +522,7 @@ struct PlanLevel {
   std::vector<uint32_t> seg;    // per record: halo segments and their column boundaries
   DevBuf<uint32_t> halo, halo_len, blk_off;
   DevBuf<uint8_t> blocks;
-  uint32_t block_bytes = 0;
+  uint32_t block_units = 0;     // descriptor blocks, 16-byte units
   uint32_t max_blk = 0;      // largest descriptor block (bytes)
   std::vector<uint32_t> hl;  // halo_len on the host
 };
@@ -543,8 +553,8 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
          perm_rows, static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K,
          blk_size.get(), sub_bad.get(), d_maxc.get(), d_maxblk.get());
   L.blk_off.alloc(ctx, nblk + 1);
-  exclusive_scan_u32(ctx, blk_size.get(), L.blk_off.get(), nblk + 1, &L.block_bytes);
-  L.blocks.alloc(ctx, L.block_bytes);
+  exclusive_scan_u32(ctx, blk_size.get(), L.blk_off.get(), nblk + 1, &L.block_units);
+  L.blocks.alloc(ctx, static_cast<int64_t>(blk_bytes(L.block_units)));
   L.halo.alloc(ctx, static_cast<int64_t>(ns) * hcap);
   L.halo_len.alloc(ctx, ns);
   const size_t smem = MAXE_ST * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
@@ -763,7 +773,7 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   for (auto& L : lv) {
     ns += L.sup.size();
     nt += L.tiles.size();
-    bytes += L.block_bytes;
+    bytes += static_cast<int64_t>(blk_bytes(L.block_units));
   }
   P->n_super = static_cast<int>(ns);
   P->n_sub = static_cast<int>(nt);
@@ -793,9 +803,9 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
                               cudaMemcpyDeviceToDevice, ctx->stream));
     if (b0)
       launch(ctx, "plan_rebase", k_add_u32, dim3(static_cast<unsigned>(ceil_div(lnt * K + 1, 256))),
-             dim3(256), 0, P->blk_off.get() + t0 * K, lnt * K + 1, static_cast<uint32_t>(b0));
-    if (L.block_bytes)
-      NPCG_CUDA(cudaMemcpyAsync(P->blocks.get() + b0, L.blocks.get(), L.block_bytes,
+             dim3(256), 0, P->blk_off.get() + t0 * K, lnt * K + 1, static_cast<uint32_t>(b0 >> 4));
+    if (L.block_units)
+      NPCG_CUDA(cudaMemcpyAsync(P->blocks.get() + b0, L.blocks.get(), blk_bytes(L.block_units),
                                 cudaMemcpyDeviceToDevice, ctx->stream));
     for (uint32_t h : L.hl) {
       if (h == kOverflow) {
@@ -807,9 +817,9 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     }
     s0 += lns;
     t0 += lnt;
-    b0 += L.block_bytes;
+    b0 += static_cast<int64_t>(blk_bytes(L.block_units));
   }
-  if (bytes >= (int64_t(1) << 32)) fail(NPCG_ERR_UNSUPPORTED, "tile plan exceeds 4 GB of descriptors");
+  if (bytes >= (int64_t(1) << 36)) fail(NPCG_ERR_UNSUPPORTED, "tile plan exceeds 64 GB of descriptors");
   items.push_back(static_cast<uint32_t>(ns));
   P->n_items = static_cast<int>(items.size()) - 1;
   P->item_start.alloc(ctx, items.size());
@@ -1199,10 +1209,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             const uint32_t ds = d_it % NSDt;
             mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSDt) & 1) ^ 1);
             const uint32_t o0 = offs[g * K + k], o1 = offs[g * K + k + 1];
-            const uint32_t nb = min(o1 - o0, static_cast<uint32_t>(BLOCK_MAX_BYTES));
-            if (BIG) dsrc[ds] = o1 - o0 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
+            const uint32_t nb = min((o1 - o0) << 4, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+            if (BIG) dsrc[ds] = (o1 - o0) << 4 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
             mbar_expect_tx(bar(B_D_FULL + ds), nb);
-            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + o0, nb, bar(B_D_FULL + ds));
+            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + blk_bytes(o0), nb, bar(B_D_FULL + ds));
             tev(d_it, 0);
           }
           ++d_it;
@@ -1353,7 +1363,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
                                            s_halo, s_a + as * 16384u, wig, lane, wait_a);
         } else {
           wait_a();
-          aggregate_stage_l2<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512),
+          aggregate_stage_l2<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512),
                                               s_halo, s_a + as * 16384u, wig, lane);
         }
         fence_proxy_async_smem();
@@ -1577,16 +1587,16 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
           const int kb = two ? g * K + a.korder[k_begin + 2 * p + 1] : ka;
           const uint32_t o0 = offs[ka], e0 = offs[ka + 1];
           const uint32_t o1 = offs[kb], e1 = two ? offs[kb + 1] : o1;
-          const uint32_t n0 = min(e0 - o0, static_cast<uint32_t>(BLOCK_MAX_BYTES));
-          const uint32_t n1 = min(e1 - o1, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+          const uint32_t n0 = min((e0 - o0) << 4, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+          const uint32_t n1 = min((e1 - o1) << 4, static_cast<uint32_t>(BLOCK_MAX_BYTES));
           if (BIG) {
-            dsrc[2 * ds] = e0 - o0 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
-            dsrc[2 * ds + 1] = e1 - o1 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o1 : kFitsSlot;
+            dsrc[2 * ds] = (e0 - o0) << 4 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
+            dsrc[2 * ds + 1] = (e1 - o1) << 4 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o1 : kFitsSlot;
           }
           mbar_expect_tx(bar(W_D_FULL + ds), n0 + n1);
-          bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + o0, n0, bar(W_D_FULL + ds));
+          bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES, a.blocks + blk_bytes(o0), n0, bar(W_D_FULL + ds));
           if (n1)
-            bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES + BLOCK_MAX_BYTES, a.blocks + o1, n1,
+            bulk_g2s(s_d + ds * 2 * BLOCK_MAX_BYTES + BLOCK_MAX_BYTES, a.blocks + blk_bytes(o1), n1,
                      bar(W_D_FULL + ds));
         }
         ++d_it;
@@ -1688,7 +1698,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
               aggregate_stage<TW>(slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
                                   s_a + as * 32768u + half * 16384u, wq, lane, wait_a);
             else if ((wait_a(), true))
-              aggregate_stage_l2<TW>(slot, reinterpret_cast<const uint16_t*>(a.blocks + src + 512),
+              aggregate_stage_l2<TW>(slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512),
                                      s_halo, s_a + as * 32768u + half * 16384u, wq, lane);
           } else {
             wait_a();
@@ -1914,7 +1924,7 @@ __global__ void __launch_bounds__(TM) k_gplan(const int64_t* __restrict__ row_pt
     if (r < K) {
       if (nfix_k[r] + next_k[r] > G_DWORDS) bad = 1;
       blk_size[static_cast<int64_t>(sub) * K + r] =
-          (528u + 4u * static_cast<uint32_t>(nfix_k[r] + next_k[r]) + 15u) & ~15u;
+          (528u + 4u * static_cast<uint32_t>(nfix_k[r] + next_k[r]) + 15u) >> 4;
     }
     __syncthreads();
     if (r == 0) sub_bad[sub] = bad;
@@ -1922,7 +1932,7 @@ __global__ void __launch_bounds__(TM) k_gplan(const int64_t* __restrict__ row_pt
   }
   // FILL: header, zero rows, entries in CSR order, fixup items
   for (int k = 0; k < K; ++k) {
-    uint8_t* b = blocks + blk_off[static_cast<int64_t>(sub) * K + k];
+    uint8_t* b = blocks + blk_bytes(blk_off[static_cast<int64_t>(sub) * K + k]);
     if (r == 0) {
       reinterpret_cast<uint32_t*>(b)[0] = static_cast<uint32_t>(nfix_k[k]);
       reinterpret_cast<uint32_t*>(b)[1] = static_cast<uint32_t>(next_k[k]);
@@ -1939,7 +1949,7 @@ __global__ void __launch_bounds__(TM) k_gplan(const int64_t* __restrict__ row_pt
   for (int64_t e = e0; e < e1; ++e) {
     const int k = static_cast<int>(kk[e]);
     const uint32_t v = inv_perm_cols[col[e]];
-    uint8_t* b = blocks + blk_off[static_cast<int64_t>(sub) * K + k];
+    uint8_t* b = blocks + blk_bytes(blk_off[static_cast<int64_t>(sub) * K + k]);
     const int n = run[k][r]++;
     if (n == 0) reinterpret_cast<uint32_t*>(b + 16)[r] = v;
     else reinterpret_cast<uint32_t*>(b + 528)[xpos[k][r] + n - 1] = v;
@@ -1965,7 +1975,7 @@ static std::unique_ptr<GatherPlan> build_gather_plan(npcg_context* ctx, const in
   P->blk_off.alloc(ctx, nblk + 1);
   uint32_t total = 0;
   exclusive_scan_u32(ctx, blk_size.get(), P->blk_off.get(), nblk + 1, &total);
-  P->blocks.alloc(ctx, total);
+  P->blocks.alloc(ctx, static_cast<int64_t>(blk_bytes(total)));
   launch(ctx, "gplan_fill", k_gplan<true>, dim3(P->n_sub), dim3(TM), 0, row_ptr, col, kk,
          perm_rows, inv_perm_cols, n_rows, K, static_cast<const uint32_t*>(P->blk_off.get()),
          static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), P->blocks.get());
@@ -2116,8 +2126,8 @@ __global__ void __launch_bounds__(G_THREADS, 1)
             const uint32_t ds = d_it % G_NSD;
             mbar_wait(bar(G_D_EMPTY + ds), ((d_it / G_NSD) & 1) ^ 1);
             const uint32_t o0 = offs[g * K + k], o1 = offs[g * K + k + 1];
-            mbar_expect_tx(bar(G_D_FULL + ds), o1 - o0);
-            bulk_g2s(s_d + ds * G_DCAP, a.blocks + o0, o1 - o0, bar(G_D_FULL + ds));
+            mbar_expect_tx(bar(G_D_FULL + ds), (o1 - o0) << 4);
+            bulk_g2s(s_d + ds * G_DCAP, a.blocks + blk_bytes(o0), (o1 - o0) << 4, bar(G_D_FULL + ds));
           }
           ++d_it;
         }
@@ -2569,8 +2579,9 @@ static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
   return p->gbwd.get();
 }
 
-void tc_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                float* fout, int cin, int cout) {
+void tc_forward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
+                const float* fin, float* fout, int cin, int cout) {
+  (void)mode;
   if (use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
     GatherPlan* G = gplan_fwd(ctx, nb);
     TcPlan* p = nb->tc.get();
@@ -2678,8 +2689,10 @@ static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, con
          dim3(256), 0, grad_w, static_cast<const float*>(tmp.get()), nw);
 }
 
-void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
-                 const float* gout, float* grad_in, float* grad_w, int cin, int cout) {
+void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
+                 const float* fin, const float* gout, float* grad_in, float* grad_w, int cin,
+                 int cout, bool fin_unchanged) {
+  (void)mode;
   TcPlan* p = get_plan(ctx, nb);
   const int K = static_cast<int>(nb->n_kernels);
   bool g_converted = false;
@@ -2720,9 +2733,10 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const fl
       wgrad_spill(ctx, nb, P, fin, gout, grad_w, false, cin, cout);
       return;
     }
-    // the bf16 input image saved by the forward on this handle is reused when
-    // the backward is handed the same input (the operator's saved copy)
-    if (fin != p->saved_fin || cin != p->saved_c) {
+    // the bf16 input image made by the forward on this handle is reused when
+    // the caller vouches that the backward's input is that same, unmodified
+    // buffer (NPCG_FLAG_FIN_UNCHANGED: the operator's saved copy)
+    if (!fin_unchanged || fin != p->saved_fin || cin != p->saved_c) {
       convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
       p->saved_fin = fin;
       p->saved_c = cin;

@@ -61,6 +61,12 @@ struct TcPlanDeleter {
 }  // namespace npcg
 
 struct npcg_neighbors {
+  // the stream of the last call that used the handle: destroy synchronises it
+  // before the stream-ordered frees of the cached buffers (which are ordered
+  // on the streams they were allocated on)
+  cudaStream_t last_stream = nullptr;
+  bool used = false;
+  int device = 0;
   int64_t n_out = 0, n_in = 0;
   int64_t t = 0;          // 0: plain radius_search handle (no kernel cells)
   int64_t n_kernels = 1;  // t^3
@@ -80,6 +86,7 @@ struct npcg_neighbors {
   std::vector<int64_t> site_offsets;   // host, n_batches + 1
   npcg::DevBuf<uint8_t> site_fin;      // engine-facing rows saved by the last forward
   int32_t site_fin_dtype = -1;
+  int64_t site_fin_width = 0;          // bytes per saved site row
   // cached plans
   std::unique_ptr<npcg::CsrPlan> tcsr;   // transposed CSR (rows = input points)
   std::unique_ptr<npcg::CellPlan> cells; // (k, i, j)

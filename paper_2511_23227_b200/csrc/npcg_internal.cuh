@@ -157,6 +157,17 @@ class DevBuf {
     return *this;
   }
   void alloc(npcg_context* ctx, int64_t n) {
+    if (p_ && stream_ != ctx->stream) {
+      // the old buffer may still be read by work on the stream it was last
+      // used on: free it on the current stream, ordered after that stream
+      cudaEvent_t e;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) == cudaSuccess) {
+        cudaEventRecord(e, stream_);
+        cudaStreamWaitEvent(ctx->stream, e, 0);
+        cudaEventDestroy(e);
+      }
+      stream_ = ctx->stream;
+    }
     release();
     n_ = n;
     stream_ = ctx->stream;

@@ -183,4 +183,53 @@ void voxel_downsample_impl(npcg_context* ctx, const npcg_cloud* cloud, double vo
   *n_kept = runs;
 }
 
+// ---- upsample (spatial.cpp:154-169): fine row m = coarse row parent[m] ----
+__global__ void k_parent_oob(const int64_t* __restrict__ parent, int64_t n, int64_t bound,
+                             int* __restrict__ flag) {
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x) {
+    const int64_t v = parent[p];
+    if (v < 0 || v >= bound) *flag = 1;
+  }
+}
+
+// one thread per V-sized piece of a fine row (V = 16 B when rows allow it)
+template <typename V>
+__global__ void k_upsample_rows(const int64_t* __restrict__ parent, int64_t n_fine, int64_t pieces,
+                                const V* __restrict__ coarse, V* __restrict__ fine) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= n_fine * pieces) return;
+  const int64_t m = x / pieces, q = x % pieces;
+  fine[x] = __ldg(coarse + parent[m] * pieces + q);
+}
+
+void upsample_impl(npcg_context* ctx, const int64_t* parent, int64_t n_fine, const void* coarse,
+                   int64_t n_coarse, int64_t row_bytes, void* fine) {
+  if (n_fine == 0) return;
+  {
+    DevBuf<int> flag(ctx, 1);
+    NPCG_CUDA(cudaMemsetAsync(flag.get(), 0, sizeof(int), ctx->stream));
+    launch(ctx, "upsample_check", k_parent_oob,
+           dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div(n_fine, 256), 8 * ctx->num_sms))),
+           dim3(256), 0, parent, n_fine, n_coarse, flag.get());
+    int h = 0;
+    NPCG_CUDA(cudaMemcpyAsync(&h, flag.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+    if (h) fail(NPCG_ERR_INDEX, "upsample: parent index outside the coarse rows");
+  }
+  const bool v16 = row_bytes % 16 == 0 && reinterpret_cast<uintptr_t>(coarse) % 16 == 0 &&
+                   reinterpret_cast<uintptr_t>(fine) % 16 == 0;
+  if (v16) {
+    const int64_t pieces = row_bytes / 16;
+    launch(ctx, "upsample", k_upsample_rows<uint4>,
+           dim3(static_cast<unsigned>(ceil_div(n_fine * pieces, 256))), dim3(256), 0, parent, n_fine,
+           pieces, static_cast<const uint4*>(coarse), static_cast<uint4*>(fine));
+  } else {
+    const int64_t pieces = row_bytes / 4;
+    launch(ctx, "upsample", k_upsample_rows<uint32_t>,
+           dim3(static_cast<unsigned>(ceil_div(n_fine * pieces, 256))), dim3(256), 0, parent, n_fine,
+           pieces, static_cast<const uint32_t*>(coarse), static_cast<uint32_t*>(fine));
+  }
+}
+
 }  // namespace npcg

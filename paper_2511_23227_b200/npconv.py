@@ -114,9 +114,10 @@ class Executor(enum.IntEnum):  # engine.hpp:11
 
 
 class Math(enum.IntEnum):  # npcg_math
-    auto = 0
-    exact = 1
-    bf16 = 2
+    auto = 0    # the reference's fp32 contract (rel <= 1e-5): split tensor cores, else exact
+    exact = 1   # CUDA cores in the API dtype
+    bf16 = 2    # opt-in: bf16 operands on the tensor cores (rel ~2e-3, bound 1e-2)
+    f32tc = 3   # split operands on the tensor cores (rel ~4e-6, bound 1e-5)
 
 
 class ConvMode(enum.IntEnum):  # triplets.hpp:34
@@ -133,10 +134,12 @@ class ExecConfig:  # engine.hpp:22-29 (+ math)
     deterministic: bool = False
     workers: int = 0
     math: Math = Math.auto
+    flags: int = 0  # npcg flags (L.FLAG_FIN_UNCHANGED)
 
-    def _c(self):
+    def _c(self, flags: int = 0):
         return L.npcg_exec_config(self.L, self.b_out, self.b_in, int(self.executor),
-                                  int(bool(self.deterministic)), self.workers, int(self.math))
+                                  int(bool(self.deterministic)), self.workers, int(self.math),
+                                  int(self.flags) | flags, 0)
 
 
 @dataclass
@@ -639,10 +642,25 @@ class BackwardResult:
     grad_w: torch.Tensor
 
 
+def _check_layer(nb: Neighbors, weights: torch.Tensor, rows: torch.Tensor, n_rows: int,
+                 width: int, what: str):
+    """The operator's shape checks (conv_op.hpp:129-131, engine.cpp:284-288)
+    before any device work: weight kernel count, feature rows and widths."""
+    if weights.dim() != 4 or weights.shape[0] != nb.n_kernels:
+        raise ShapeError(f"{what}: weight kernel count != geometry t^3")
+    if rows.dim() != 3 or rows.shape[0] != n_rows:
+        raise ShapeError(f"{what}: feature rows != cloud points")
+    if rows.shape[1] != weights.shape[1] or rows.shape[2] != width:
+        raise ShapeError(f"{what}: weight and feature shapes differ")
+    if rows.dtype != weights.dtype:
+        raise ShapeError(f"{what}: weight and feature dtypes differ")
+
+
 def conv_forward(nb: Neighbors, weights: torch.Tensor, fin: torch.Tensor,
                  config: ExecConfig = ExecConfig(), out: torch.Tensor | None = None):
     """npcg_conv_forward over a cached neighbor handle."""
     K, G, cin, cout = weights.shape
+    _check_layer(nb, weights, fin, nb.n_fine, cin, "conv_forward")
     if out is None:
         out = torch.empty((nb.n_out, G, cout), dtype=fin.dtype, device=fin.device)
     cfg = config._c()
@@ -654,13 +672,19 @@ def conv_forward(nb: Neighbors, weights: torch.Tensor, fin: torch.Tensor,
 
 def conv_backward(nb: Neighbors, weights: torch.Tensor, fin: torch.Tensor, gout: torch.Tensor,
                   config: ExecConfig = ExecConfig(), grad_in=None, grad_w=None, need_in=True,
-                  need_w=True):
+                  need_w=True, fin_unchanged: bool = False):
+    """npcg_conv_backward.  fin_unchanged: `fin` is the very buffer the last
+    conv_forward on this handle read, unmodified since (the operator's saved
+    input) -- its device image is then reused (NPCG_FLAG_FIN_UNCHANGED)."""
     K, G, cin, cout = weights.shape
+    if fin is not None:
+        _check_layer(nb, weights, fin, nb.n_fine, cin, "conv_backward")
+    _check_layer(nb, weights, gout, nb.n_out, cout, "conv_backward")
     if need_in and grad_in is None:
         grad_in = torch.empty((nb.n_fine, G, cin), dtype=gout.dtype, device=gout.device)
     if need_w and grad_w is None:
         grad_w = torch.empty((K, G, cout, cin), dtype=gout.dtype, device=gout.device)
-    cfg = config._c()
+    cfg = config._c(L.FLAG_FIN_UNCHANGED if fin_unchanged else 0)
     h = nb.ctx.bind()
     nb.ctx.check(L.lib().npcg_conv_backward(h, nb.h, _dtype_code(gout), _ptr(weights), G, cin, cout,
                                             _ptr(fin), _ptr(gout), C.byref(cfg),
@@ -755,7 +779,10 @@ class PointConvOp:
         if gout.dim() != 3 or gout.shape[0] != self._nb.n_out or gout.shape[1] != G or \
                 gout.shape[2] != cout:
             raise ShapeError("PointConvOp::backward: gout shape mismatch")
-        gi, gw = conv_backward(self._nb, self._w, self._fin, gout.contiguous(), self.config_)
+        # the saved input is the operator's own copy (or, with copy_fin=False,
+        # the caller's promise not to modify it): its device image is reused
+        gi, gw = conv_backward(self._nb, self._w, self._fin, gout.contiguous(), self.config_,
+                               fin_unchanged=True)
         return BackwardResult(gi, gw)
 
 
@@ -789,11 +816,22 @@ def voxel_downsample(cloud: PointCloud, voxel_size: float):
 
 
 def upsample(fine: PointCloud, mp: DownsampleMap, coarse: torch.Tensor) -> torch.Tensor:
+    """spatial.hpp:52-54 (spatial.cpp:154-169) through npcg_upsample: fine row m
+    = coarse row parent_of[m]."""
     if mp.parent_of.numel() != fine.n_points():
         raise ShapeError("upsample: map does not cover the fine cloud")
     if mp.kept_index.numel() != coarse.shape[0]:
         raise ShapeError("upsample: coarse features do not match the map")
-    return coarse.index_select(0, mp.parent_of)
+    c = coarse.contiguous()
+    n = fine.n_points()
+    out = torch.empty((n,) + tuple(c.shape[1:]), dtype=c.dtype, device=c.device)
+    width = int(np.prod(c.shape[1:])) if c.dim() > 1 else 1
+    ctx = context(c.device)
+    h = ctx.bind()
+    par = mp.parent_of.contiguous()
+    ctx.check(L.lib().npcg_upsample(h, _dtype_code(c), _ptr(par), n, _ptr(c), c.shape[0], width,
+                                    _ptr(out)), "upsample")
+    return out
 
 
 @dataclass

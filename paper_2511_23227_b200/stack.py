@@ -36,6 +36,10 @@ class ConvStack:
         for a, b in zip(weights, weights[1:]):
             if a.shape[3] != b.shape[2] or a.shape[0] != b.shape[0] or a.shape[1] != b.shape[1]:
                 raise npc.ShapeError("ConvStack: consecutive layer shapes do not chain")
+        if geometry.mode != npc.ConvMode.native:
+            # layer l >= 1 would see one row per site while the degraded forward
+            # gathers fine rows through kept_index (conv_op.hpp:133-158)
+            raise npc.ShapeError("ConvStack: degraded geometry is not chainable (native only)")
         self.ops = [npc.PointConvOp(w, geometry, config, copy_fin=False) for w in weights]
         self.geometry = geometry
         self.config = config
@@ -70,8 +74,10 @@ class ConvStack:
         g = gout.contiguous()
         gws = [None] * len(self.ops)
         for l in range(len(self.ops) - 1, -1, -1):
+            # activations are the stack's own buffers, unmodified since the forward
             g, gws[l] = npc.conv_backward(self._nb, self.ops[l].weights(), self._acts[l], g,
-                                          self.config, need_in=True, need_w=True)
+                                          self.config, need_in=True, need_w=True,
+                                          fin_unchanged=True)
         return StackGrads(g, gws)
 
     # -- CUDA graph of one forward + backward step ------------------------------

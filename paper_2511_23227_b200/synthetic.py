@@ -1,11 +1,48 @@
 """Synthetic scene generators for BASELINE.json configs 3 and 4, which name
 scene types the reference has no generator for ("builder
 defines"): a LiDAR-like ring scan and a surface-sampled indoor fragment.
-Host-side numpy, seeded; the uniform cube / gaussian clusters of the
-reference's synthetic.cpp live in oracle/ (test infrastructure)."""
+Host-side numpy, seeded.  The reference's own generators (uniform cube,
+features, weights: synthetic.hpp, tensors.hpp:142-150) are exported by
+libnpcg.so as host functions and wrapped here, so product code never needs
+oracle/ (test infrastructure) for its inputs."""
 from __future__ import annotations
 
+import ctypes as C
+
 import numpy as np
+
+from . import _lib as L
+
+
+def _check(st: int, what: str):
+    if st != 0:
+        raise ValueError(f"{what}: {L.STATUS_NAMES.get(st, st)}")
+
+
+def gen_uniform_cube(n: int, extent: float, seed: int) -> np.ndarray:
+    """synthetic.cpp:12-23 (the reference's stream, via npcg_gen_uniform_cube)."""
+    out = np.empty((n, 3), dtype=np.float64)
+    _check(L.lib().npcg_gen_uniform_cube(n, extent, seed, out.ctypes.data_as(C.c_void_p)),
+           "gen_uniform_cube")
+    return out
+
+
+def gen_features(n: int, groups: int, channels: int, seed: int, dtype=np.float32) -> np.ndarray:
+    """synthetic.hpp:33-40: uniform in [-1, 1) (npcg_gen_features)."""
+    out = np.empty((n, groups, channels), dtype=dtype)
+    _check(L.lib().npcg_gen_features(n, groups, channels, seed, 0 if dtype == np.float32 else 1,
+                                     out.ctypes.data_as(C.c_void_p)), "gen_features")
+    return out
+
+
+def make_weights(t: int, groups: int, c_in: int, c_out: int, seed: int,
+                 dtype=np.float32) -> np.ndarray:
+    """tensors.hpp:142-150: uniform in [-s, s), s = (G C_in)^(-1/2) (npcg_make_weights)."""
+    out = np.empty((t ** 3, groups, c_in, c_out), dtype=dtype)
+    _check(L.lib().npcg_make_weights(t, groups, c_in, c_out, seed,
+                                     0 if dtype == np.float32 else 1,
+                                     out.ctypes.data_as(C.c_void_p)), "make_weights")
+    return out
 
 
 def gen_lidar_scan(n: int, seed: int) -> np.ndarray:

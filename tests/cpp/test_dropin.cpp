@@ -264,6 +264,37 @@ int main() {
     write_triplets(dir + "/npcg_dropin_oob.tpl", oob);
     CHECK_THROWS_AS(read_triplets(dir + "/npcg_dropin_oob.tpl"), IOError);
   }
+  // strided_block + upsample (conv_op.hpp:219-225; spatial.cpp:154-169)
+  {
+    const int64_t n = 3000;
+    std::vector<double> xyz(3 * n);
+    orc_gen_uniform_cube(n, 1.0, 21, xyz.data());
+    std::vector<Vec3> pts(n);
+    for (int64_t p = 0; p < n; ++p) pts[p] = {xyz[3 * p], xyz[3 * p + 1], xyz[3 * p + 2]};
+    PointCloud c = make_point_cloud(std::move(pts));
+    const double v = 0.1, r = 1.8 * v;
+    std::vector<double> wv(27 * 4 * 6), fv(n * 4);
+    orc_make_weights_f64(3, 1, 4, 6, 22, wv.data());
+    orc_gen_features_f64(n * 4, 23, fv.data());
+    PointConvOp<double> op(WeightTensor<double>(3, 1, 4, 6, wv), ConvGeometry{r, 3});
+    auto sr = strided_block(op, c, FeatureTensor<double>(n, 1, 4, fv), v);
+    auto [coarse, map] = voxel_downsample(c, v);
+    CHECK(sr.coarse_cloud.n_points() == coarse.n_points() && sr.map.kept_index == map.kept_index);
+    TripletList t = build_triplets_native(coarse, c, ConvGeometry{r, 3});
+    std::vector<double> fo(coarse.n_points() * 6);
+    CHECK(orc_dense_conv(wv.data(), 27, 1, 4, 6, fv.data(), n, t.i.data(), t.j.data(), t.k.data(), t.size(),
+                         coarse.n_points(), nullptr, fo.data(), nullptr, nullptr) == 0);
+    CHECK(rel(sr.coarse_features.values(), fo) <= 1e-12);
+    auto up = upsample(c, sr.map, sr.coarse_features);
+    bool same = up.n() == n;
+    for (int64_t p = 0; same && p < n; ++p)
+      for (int64_t q = 0; q < 6; ++q)
+        same &= up.at(p, 0, q) == sr.coarse_features.at(sr.map.parent_of[p], 0, q);
+    CHECK(same);
+    DownsampleMap bad = sr.map;
+    bad.parent_of.pop_back();
+    CHECK_THROWS_AS(upsample(c, bad, sr.coarse_features), ShapeError);
+  }
   std::printf("drop-in: %d checks, %d failures\n", g_checks, g_fail);
   return g_fail ? 1 : 0;
 }

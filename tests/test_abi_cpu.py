@@ -63,3 +63,19 @@ def test_context_creation_fails_loudly_without_gpu():
     from paper_2511_23227_b200 import npconv
     with pytest.raises(npconv.Error):
         npconv.Context(0)
+
+
+@pytest.mark.parametrize("t,g,ci,co,seed", [(3, 1, 64, 64, 2), (3, 1, 48, 80, 5), (5, 2, 7, 3, 9)])
+def test_synthetic_generators_are_the_reference_streams(ref, t, g, ci, co, seed):
+    """npcg_gen_uniform_cube / npcg_gen_features / npcg_make_weights (host
+    functions of the library, synthetic.hpp:12-40, tensors.hpp:142-150) give
+    the unmodified reference's values bit for bit, so the bench and the drop-in
+    need no oracle/ code for their inputs."""
+    import numpy as np
+    from paper_2511_23227_b200 import synthetic as S
+    for dt in (np.float32, np.float64):
+        assert np.array_equal(S.make_weights(t, g, ci, co, seed, dt), ref.make_weights(t, g, ci, co, seed, dt))
+        assert np.array_equal(S.gen_features(257, g, ci, seed, dt), ref.gen_features(257, g, ci, seed, dt))
+    assert np.array_equal(S.gen_uniform_cube(1000, 2.5, seed), ref.gen_uniform_cube(1000, 2.5, seed))
+    assert L.lib().npcg_gen_uniform_cube(10, 0.0, 1, None) == 7  # DomainError (synthetic.cpp:14)
+    assert L.lib().npcg_make_weights(2, 1, 1, 1, 1, 0, None) == 3  # even t: ShapeError

@@ -48,7 +48,14 @@ def test_fuzz_tensor_core_path(npc, orc, ref, seed):
     res = op.backward(T(go))
     out2 = op.forward(cl, out_cl, T(f)) if strided else op.forward(cl, T(f))
     assert torch.equal(out, out2)
-    ti, tj, tk = op.cached_triplets().numpy()  # the library's own triplets (by_k order)
+    # the library's triplets (by_k order) must be the reference build, sorted
+    # like the reference (triplets.cpp:135-170), before they feed the checks
+    K = t ** 3  # choose_sort_axis (triplets.cpp:172-179)
+    axis = 3 if K <= min(n, n_out) else (1 if n_out <= n else 2)
+    si, sj, sk = orc.sort_triplets(ti, tj, tk, axis, n_out, n, K)
+    li, lj, lk = op.cached_triplets().numpy()
+    assert np.array_equal(li, si) and np.array_equal(lj, sj) and np.array_equal(lk, sk)
+    ti, tj, tk = li, lj, lk
     efo, egi, egw = _emulate_tc(ti, tj, tk, n_out, n, w, f, go)
     assert rel(out.cpu().numpy()[:, 0], efo) <= 2 ** -8
     assert rel(res.grad_in.cpu().numpy()[:, 0], egi) <= 2 ** -8

@@ -451,7 +451,7 @@ def test_c2_bf16_fwd_bwd(npc, orc):
     fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n,
                                 go.astype(np.float64))
     cl = npc.make_point_cloud(xyz)
-    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.auto))
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=npc.Math.bf16))
     out = op.forward(cl, T(f))
     res = op.backward(T(go))
     st = op.neighbors().plan_stats()
