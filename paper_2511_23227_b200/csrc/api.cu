@@ -90,6 +90,8 @@ std::unique_ptr<npcg_neighbors> handle_from_triplets(npcg_context* ctx, const np
   auto nb = std::make_unique<npcg_neighbors>();
   nb->n_out = n_out;
   nb->n_in = n_in;
+  nb->out_off = {0, n_out};
+  nb->in_off = {0, n_in};
   nb->t = t;
   nb->n_kernels = t * t * t;
   nb->n_pairs = T->size;

@@ -31,6 +31,7 @@
 //   warp 22     producer: W_k bulk copies
 #include <cuda.h>
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -56,7 +57,7 @@ constexpr int SLOT_ENTRIES = 512;
 constexpr int BLOCK_MAX_BYTES = 512 + 2 * SLOT_ENTRIES;
 constexpr int MAX_BLOCK_ENTRIES = 8192;  // planner cap per block
 constexpr uint32_t kOverflow = 0xFFFFFFFFu;
-constexpr bool kSplitReady = false;
+constexpr bool kSplitReady = true;
 // Descriptor blocks are 16-byte aligned and addressed in 16-byte units (u32:
 // 64 GB of blocks per plan, ~400M points at ~160 B per point).
 __host__ __device__ __forceinline__ uint64_t blk_bytes(uint32_t units) {
@@ -108,6 +109,8 @@ struct TcPlan {
   DevBuf<__nv_bfloat16> feat_in;   // bf16 F_in in perm_in order
   const void* saved_fin = nullptr;  // fin whose image feat_in holds (set by the forward)
   int saved_c = 0;                  // and its channel count
+  bool saved_split = false;         // and its kind (bf16 image or split image)
+  DevBuf<uint32_t> amax;            // split path: max |x| bits of [F_in, W, G_out, W] (scales)
   DevBuf<__nv_bfloat16> feat_out;  // bf16 G_out in perm_out order
   DevBuf<uint8_t> wpack;           // K x nci images of C x 128 B, SW128 K-major B operand
   DevBuf<float> partial;           // wgrad per-CTA partials
@@ -598,8 +601,9 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
                                                  const uint32_t* col, const uint32_t* kk,
                                                  int64_t n_rows, int64_t n_cols,
                                                  const uint32_t* perm_rows,
-                                                 const uint32_t* inv_perm_cols, int K, int st,
-                                                 int hcap) {
+                                                 const uint32_t* inv_perm_cols,
+                                                 const std::vector<int64_t>& row_batches, int K,
+                                                 int st, int hcap) {
   auto P = std::make_unique<TcDirPlan>();
   P->st = st;
   P->hcap = hcap;
@@ -607,17 +611,23 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   P->n_cols = n_cols;
   P->K = K;
   if (n_rows == 0) return P;
-  // level 0: 128-row sub-tiles, st per super-tile
+  // level 0: 128-row sub-tiles, st per super-tile.  Tiles never cross a
+  // batch boundary (the rows are batch-major), so a scene of a jagged batch
+  // is tiled -- and computed, bit for bit -- exactly as the scene alone.
   std::vector<PlanLevel> lv(1);
   {
-    const int nt = static_cast<int>(ceil_div(n_rows, TM));
-    for (int t = 0; t < nt; ++t) {
-      lv[0].tiles.push_back(make_uint2(static_cast<uint32_t>(t) * TM,
-                                       static_cast<uint32_t>(std::min<int64_t>(TM, n_rows - int64_t(t) * TM))));
-      lv[0].nom.push_back(TM);
+    std::vector<int64_t> bo = row_batches;
+    if (bo.size() < 2 || bo.front() != 0 || bo.back() != n_rows) bo = {0, n_rows};
+    for (size_t b = 0; b + 1 < bo.size(); ++b) {
+      const int t0 = static_cast<int>(lv[0].tiles.size());
+      for (int64_t p = bo[b]; p < bo[b + 1]; p += TM) {
+        lv[0].tiles.push_back(make_uint2(static_cast<uint32_t>(p),
+                                         static_cast<uint32_t>(std::min<int64_t>(TM, bo[b + 1] - p))));
+        lv[0].nom.push_back(TM);
+      }
+      const int nt = static_cast<int>(lv[0].tiles.size());
+      for (int t = t0; t < nt; t += st) lv[0].sup.push_back(make_uint2(t, std::min(st, nt - t)));
     }
-    for (int t = 0; t < nt; t += st)
-      lv[0].sup.push_back(make_uint2(t, std::min(st, nt - t)));
   }
   // Planning levels form a worklist.  A plain super-tile beyond capacity
   // becomes, when only its halo is too large, one item of halo-segment
@@ -876,6 +886,88 @@ __global__ void k_to_bf16_perm(const float* __restrict__ src, const uint32_t* __
   reinterpret_cast<uint4*>(dst + p * CP)[q] = o;
 }
 
+// ---- split operands of the fp32-contract path ---------------------------
+// A tensor x is scaled by a power of two s (max |x| s < 2^7, exact) and each
+// y = x s is split into two fp16 halves, y = hi + lo 2^-11 with hi = fp16(y),
+// lo = fp16((y - hi) 2^11): 22 significand bits (fp32 has 24), both halves in
+// range for sums of up to 254 rows (the planner's per-(row, cell) cap).
+// max |x| of a tensor, as the bits of a non-negative float (atomicMax on the
+// bit pattern orders like the value)
+__global__ void k_absmax(const float* __restrict__ x, int64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0;
+  for (int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x; p < n;
+       p += static_cast<int64_t>(gridDim.x) * blockDim.x)
+    m = max(m, __float_as_uint(fabsf(x[p])));
+  for (int o = 16; o; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+// s = 2^(7 - e) for max = f 2^e (f in [0.5, 1)): max s < 128; 1 when max = 0
+__host__ __device__ __forceinline__ float split_scale(uint32_t max_bits) {
+  if (max_bits == 0 || max_bits >= 0x7F800000u) return 1.f;
+  const int e = static_cast<int>((max_bits >> 23) & 0xFF) - 126;  // max < 2^e (normal inputs)
+  const int k = 7 - (e < -100 ? -100 : e);
+  return ldexpf(1.f, k > 100 ? 100 : k);
+}
+__device__ __forceinline__ void split_f16(float y, float& hi, float& lo) {
+  hi = __half2float(__float2half_rn(y));
+  lo = (y - hi) * 2048.f;
+}
+
+// Split image: row p = for each chunk of 32 channels [hi(32) | lo(32)] in
+// fp16 (128 bytes) of y = x s; channels C <= c < CP zero.  8 channels per thread.
+__global__ void k_to_split_perm(const float* __restrict__ src, const uint32_t* __restrict__ perm,
+                                int64_t n, int C, int CP, const uint32_t* __restrict__ amax,
+                                __half* __restrict__ dst) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int qn = CP >> 3;
+  if (x >= n * qn) return;
+  const int64_t p = x / qn;
+  const int q = static_cast<int>(x % qn);  // channels 8q .. 8q+7
+  uint4 h = make_uint4(0, 0, 0, 0), l = make_uint4(0, 0, 0, 0);
+  if (q * 8 < C) {
+    const float sc = split_scale(*amax);
+    const float4* s = reinterpret_cast<const float4*>(src + static_cast<int64_t>(perm[p]) * C + q * 8);
+    const float4 a = __ldg(s), b = __ldg(s + 1);
+    const float v[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+    float hv[8], lv[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) split_f16(v[i] * sc, hv[i], lv[i]);
+    h = make_uint4(pack_f16x2(hv[0], hv[1]), pack_f16x2(hv[2], hv[3]), pack_f16x2(hv[4], hv[5]),
+                   pack_f16x2(hv[6], hv[7]));
+    l = make_uint4(pack_f16x2(lv[0], lv[1]), pack_f16x2(lv[2], lv[3]), pack_f16x2(lv[4], lv[5]),
+                   pack_f16x2(lv[6], lv[7]));
+  }
+  uint4* row = reinterpret_cast<uint4*>(dst + p * 2 * CP);  // 16-byte units, 8 per 32-channel chunk
+  const int chunk = q >> 2, sub = q & 3;
+  row[chunk * 8 + sub] = h;
+  row[chunk * 8 + 4 + sub] = l;
+}
+
+// Split B images (SW128 K-major, fp16) per (cell, 32-wide chunk r0 of the
+// reduction dim), of W s_w = Wh + Wl 2^-11:
+//   image 1 (main)  K 0..31 = Wh[r0 + kk], K 32..63 = 0 (only its first 32 K are read)
+//   image 2 (corr)  K 0..31 = Wl[r0 + kk], K 32..63 = Wh[r0 + kk - 32]
+// so that the tile [Ah | Al] gives main = Ah Wh and corr = Ah Wl + Al Wh.
+// transpose as k_pack_w.
+__global__ void k_pack_w_split(const float* __restrict__ w, int K, int cin, int cout, int cinp,
+                               int coutp, bool transpose, const uint32_t* __restrict__ amax,
+                               uint8_t* __restrict__ out) {
+  const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (x >= static_cast<int64_t>(K) * cin * cout) return;
+  const int k = static_cast<int>(x / (cin * cout)), rem = static_cast<int>(x % (cin * cout));
+  const int c = rem / cout, m = rem % cout;  // W[k][c][m]
+  const int n = transpose ? c : m, r = transpose ? m : c;
+  const int N = transpose ? cinp : coutp, nchunk = (transpose ? coutp : cinp) / 32;
+  const int64_t img = (static_cast<int64_t>(k) * nchunk + r / 32) * 2;  // two images per chunk
+  float hi, lo;
+  split_f16(w[x] * split_scale(*amax), hi, lo);
+  uint8_t* i1 = out + img * N * 128;
+  uint8_t* i2 = i1 + N * 128;
+  reinterpret_cast<__half*>(i1 + sw128_off(n, r % 32))[0] = __float2half_rn(hi);
+  reinterpret_cast<__half*>(i2 + sw128_off(n, r % 32))[0] = __float2half_rn(lo);
+  reinterpret_cast<__half*>(i2 + sw128_off(n, 32 + r % 32))[0] = __float2half_rn(hi);
+}
+
 // B operand images (SW128 K-major), one per (cell, 64-wide chunk of the
 // reduction dim), N x 128 B each.  transpose=false: N = C_out rows, reduction
 // over C_in (forward); transpose=true: N = C_in rows, reduction over C_out (dgrad).
@@ -913,6 +1005,7 @@ struct FwdArgs {
   float* out;                 // (n_rows, ncols), original order
   int ncols;                  // channels written per row (<= NOUT; the rest is padding)
   long long* trace;           // debug: per-stage event clocks of CTA 0 (traced variant only)
+  const uint32_t* amax;       // SPLIT: max |x| bits of the gathered tensor and of W (scales)
 };
 constexpr int TRACE_STAGES = 512;
 constexpr int TRACE_EV = 8;  // 0 d_issue, 1 d_full, 2 a_empty, 3 agg_done, 4 mma_start, 5 mma_issued, 6 w_full
@@ -939,25 +1032,39 @@ constexpr int OFFS_WORDS = OFFS_DSRC + 8;
 // 256-row super-tiles (TMEM 2 x 2 x 128 columns), NOUT = 256 uses 128-row
 // super-tiles (TMEM 2 x 256 columns) with a smaller halo.
 constexpr int FWD_HCAP1 = 672;  // halo rows of 128-row tiles (what fits beside 256-wide W stages)
-template <int NOUT>
+// SPLIT (fp32-contract path): every stage multiplies the split A tile
+// [Ah | Al] (32 input channels) by two W images -- [Wh; Wh] over the full K =
+// 64 (Ah Wh + Al Wh) and [Wl; 0] over its first 32 K (Ah Wl) -- so a W stage
+// is two NOUT x 128 B images; NOUT = 128 runs on 128-row super-tiles (the
+// wide plan) to make room for them.
+template <int NOUT, bool SPLIT = false>
 struct FwdCfg {
-  static constexpr int nsw = NOUT == 64 ? NSW : 2;
+  static constexpr int nsw = (NOUT == 64 && !SPLIT) ? NSW : 2;
   // descriptor slots: a multiple of the aggregation groups, so a slot is
   // always consumed by the same group (a waiter can then never be two
   // barrier phases ahead, which a parity wait cannot tell apart)
   static constexpr int nsd = NSD;
-  static constexpr uint32_t wbytes = NOUT * 128;
-  static constexpr int st = NOUT <= 128 ? FWD_ST : 1;
-  static constexpr int acc_cols = st * NOUT;  // per TMEM buffer
-  static constexpr uint32_t tmem_cols = 2 * acc_cols <= 256 ? 256 : 512;
+  static constexpr uint32_t wimg = NOUT * 128;              // one W image
+  static constexpr uint32_t wbytes = (SPLIT ? 2 : 1) * wimg;  // a W stage
+  static constexpr int st = (NOUT == 64 || (NOUT == 128 && !SPLIT)) ? FWD_ST : 1;
+  static constexpr int acc_cols = st * NOUT;  // one accumulator set
+  // SPLIT: NMAIN main accumulator sets (hi x hi, cells alternating: short
+  // truncating chains, summed in fp32 round-to-nearest by the epilogue) and one
+  // correction set, single-buffered; bf16: one set, double-buffered
+  static constexpr int nmain = SPLIT ? 3 : 1;
+  static constexpr int nbuf = SPLIT ? 1 : 2;
+  static constexpr int nsets = SPLIT ? nmain + 1 : 2;
+  static constexpr uint32_t tmem_cols = nsets * acc_cols <= 256 ? 256 : 512;
+  static_assert(nsets * acc_cols <= 512, "TMEM");
 };
 
 struct FwdSmem {
   uint32_t halo, a, w, d, bar, tmem_slot, offs;
   size_t total;
 };
-template <int NOUT>
+template <int NOUT, bool SPLIT = false>
 __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
+  using Cfg = FwdCfg<NOUT, SPLIT>;
   FwdSmem L{};
   uint32_t o = 0;
   L.halo = o;
@@ -966,9 +1073,9 @@ __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
   L.a = o;
   o += NSA * 16384;
   L.w = o;
-  o += FwdCfg<NOUT>::nsw * FwdCfg<NOUT>::wbytes;
+  o += Cfg::nsw * Cfg::wbytes;
   L.d = o;
-  o += FwdCfg<NOUT>::nsd * BLOCK_MAX_BYTES;
+  o += Cfg::nsd * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
   L.bar = o;
   o += 48 * 8;
@@ -984,6 +1091,8 @@ static_assert(NSD % AGG_GROUPS == 0, "descriptor slots per group");
 static_assert(fwd_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
 static_assert(fwd_smem_layout<128>(FWD_HCAP).total <= 232448, "smem");
 static_assert(fwd_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
+static_assert(fwd_smem_layout<64, true>(FWD_HCAP).total <= 232448, "smem");
+static_assert(fwd_smem_layout<128, true>(FWD_HCAP1).total <= 232448, "smem");
 
 // Warm L2 with a super-tile's halo rows: one prefetch.global.L2 per 128-byte
 // row, row indices loaded in batches of 8 per lane before the prefetches.
@@ -1047,7 +1156,14 @@ static_assert(B_COUNT <= 48, "barrier region");
 // before their uses (ILP), stores go to the SW128 K-major A tile.
 // wait_slot() is called once, before the first store into the A slot, so the
 // item / halo loads of the copy pass overlap the wait for the slot.
-template <int NW, typename WaitSlot>
+// SPLIT (the fp32-contract path): the halo rows are split images, each
+// 128-byte row = [hi(32 channels) | lo(32 channels)] in fp16 of the scaled
+// value y = x s = hi + lo 2^-11 (split_f16); lanes 0-3 of a row hold hi
+// parts, lanes 4-7 the lo parts of the same channels.  Count-1 rows copy the
+// pair unchanged; rows of >= 2 entries sum hi and lo in fp32 per lane, form
+// the total hi_sum + lo_sum 2^-11 on both partner lanes (lane ^ 4, the same
+// expression: bitwise equal) and split it again.
+template <int NW, bool SPLIT = false, typename WaitSlot>
 __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16_t* ents,
                                                 uint32_t s_halo, uint32_t s_A, int wig, int lane,
                                                 WaitSlot&& wait_slot) {
@@ -1088,7 +1204,7 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
   for (int qi = 0; qi < NQ; ++qi) {
     if (cm[qi] >= 2u) {
       const uint32_t c = item_count(it[qi]), eo = item_eo(it[qi]);
-      if (cm[qi] == 2u) {  // at most two entries per row: one packed bf16x2 add
+      if (!SPLIT && cm[qi] == 2u) {  // at most two entries per row: one packed bf16x2 add
         uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
         if (c > 0u) w0 = lds128(s_halo + static_cast<uint32_t>(ents[eo]) * 128u + l8x16);
         if (c > 1u) w1 = lds128(s_halo + static_cast<uint32_t>(ents[eo + 1]) * 128u + l8x16);
@@ -1107,28 +1223,55 @@ __device__ __forceinline__ void aggregate_stage(const uint8_t* blk, const uint16
         uint4 w0 = make_uint4(0, 0, 0, 0), w1 = make_uint4(0, 0, 0, 0);
         if (e < c) w0 = lds128(s_halo + static_cast<uint32_t>(ents[eo + e]) * 128u + l8x16);
         if (e + 1 < c) w1 = lds128(s_halo + static_cast<uint32_t>(ents[eo + e + 1]) * 128u + l8x16);
-        acc_bf16x2(acc[0], acc[1], w0.x);
-        acc_bf16x2(acc[2], acc[3], w0.y);
-        acc_bf16x2(acc[4], acc[5], w0.z);
-        acc_bf16x2(acc[6], acc[7], w0.w);
-        acc_bf16x2(acc[0], acc[1], w1.x);
-        acc_bf16x2(acc[2], acc[3], w1.y);
-        acc_bf16x2(acc[4], acc[5], w1.z);
-        acc_bf16x2(acc[6], acc[7], w1.w);
+        if constexpr (SPLIT) {
+          acc_f16x2(acc[0], acc[1], w0.x);
+          acc_f16x2(acc[2], acc[3], w0.y);
+          acc_f16x2(acc[4], acc[5], w0.z);
+          acc_f16x2(acc[6], acc[7], w0.w);
+          acc_f16x2(acc[0], acc[1], w1.x);
+          acc_f16x2(acc[2], acc[3], w1.y);
+          acc_f16x2(acc[4], acc[5], w1.z);
+          acc_f16x2(acc[6], acc[7], w1.w);
+        } else {
+          acc_bf16x2(acc[0], acc[1], w0.x);
+          acc_bf16x2(acc[2], acc[3], w0.y);
+          acc_bf16x2(acc[4], acc[5], w0.z);
+          acc_bf16x2(acc[6], acc[7], w0.w);
+          acc_bf16x2(acc[0], acc[1], w1.x);
+          acc_bf16x2(acc[2], acc[3], w1.y);
+          acc_bf16x2(acc[4], acc[5], w1.z);
+          acc_bf16x2(acc[6], acc[7], w1.w);
+        }
       }
       uint4 o;
-      o.x = pack_bf16x2(acc[0], acc[1]);
-      o.y = pack_bf16x2(acc[2], acc[3]);
-      o.z = pack_bf16x2(acc[4], acc[5]);
-      o.w = pack_bf16x2(acc[6], acc[7]);
+      if constexpr (SPLIT) {
+        const bool lo_lane = (lane & 4) != 0;
+#pragma unroll
+        for (int x = 0; x < 8; ++x) {
+          const float other = __shfl_xor_sync(0xffffffffu, acc[x], 4);
+          // y = hi_sum + lo_sum 2^-11 (the same expression on both lanes)
+          const float y = lo_lane ? fmaf(acc[x], 0x1p-11f, other) : fmaf(other, 0x1p-11f, acc[x]);
+          const float hi = __half2float(__float2half_rn(y));
+          acc[x] = lo_lane ? (y - hi) * 2048.f : hi;
+        }
+        o.x = pack_f16x2(acc[0], acc[1]);
+        o.y = pack_f16x2(acc[2], acc[3]);
+        o.z = pack_f16x2(acc[4], acc[5]);
+        o.w = pack_f16x2(acc[6], acc[7]);
+      } else {
+        o.x = pack_bf16x2(acc[0], acc[1]);
+        o.y = pack_bf16x2(acc[2], acc[3]);
+        o.z = pack_bf16x2(acc[4], acc[5]);
+        o.w = pack_bf16x2(acc[6], acc[7]);
+      }
       sts128(s_A + item_sw128(it[qi], l8x16), o);
     }
   }
 }
-template <int NW>
+template <int NW, bool SPLIT = false>
 __device__ __noinline__ void aggregate_stage_l2(const uint8_t* blk, const uint16_t* ents,
                                                 uint32_t s_halo, uint32_t s_A, int wig, int lane) {
-  aggregate_stage<NW>(blk, ents, s_halo, s_A, wig, lane, [] {});
+  aggregate_stage<NW, SPLIT>(blk, ents, s_halo, s_A, wig, lane, [] {});
 }
 
 // Input channels come in a.nci chunks of 64: each super-tile runs the cells
@@ -1137,21 +1280,24 @@ __device__ __noinline__ void aggregate_stage_l2(const uint8_t* blk, const uint16
 // chunk) as an NOUT x 64 image.
 // BIG: the plan has descriptor blocks beyond the shared-memory slot (their
 // entries are read from L2); plans without them run the leaner variant.
-template <int NOUT, bool BIG, bool TRACE = false>
+// SPLIT: the fp32-contract path (chunks of 32 split channels, two W images).
+template <int NOUT, bool BIG, bool TRACE = false, bool SPLIT = false>
 __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   // pipeline event clocks only in the traced debug variant (the checks cost
   // issue slots in the product kernel)
   auto tev = [&](uint32_t stage, int ev) {
     if constexpr (TRACE) trace_ev(a.trace, stage, ev);
   };
-  using Cfg = FwdCfg<NOUT>;
+  using Cfg = FwdCfg<NOUT, SPLIT>;
   constexpr int NSWt = Cfg::nsw, NSDt = Cfg::nsd;
   extern __shared__ uint8_t smem_raw[];
   const uint32_t raw = smem_u32(smem_raw);
   const uint32_t base = (raw + 1023u) & ~1023u;
   uint8_t* gbase = smem_raw + (base - raw);
-  const FwdSmem L = fwd_smem_layout<NOUT>(a.hcap);
+  const FwdSmem L = fwd_smem_layout<NOUT, SPLIT>(a.hcap);
   const int nci = a.nci;
+  // SPLIT: main accumulators actually used (a record has K * nci stages)
+  const int nmain = SPLIT ? min(Cfg::nmain, a.K * nci) : 1;
   const int64_t fstride = static_cast<int64_t>(nci) * CH;
   const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_w = base + L.w, s_d = base + L.d;
   const uint32_t s_bar = base + L.bar;
@@ -1244,7 +1390,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     // ------------------------------ MMA issuer -----------------------------
     // The whole warp runs the loop converged (warp-uniform descriptors); one
     // elected lane issues tcgen05.mma / commit.
-    constexpr uint32_t idesc = idesc_bf16(128, NOUT, false, false);
+    constexpr uint32_t idesc = SPLIT ? idesc_f16(128, NOUT, false, false) : idesc_bf16(128, NOUT, false, false);
+    constexpr uint32_t NB = Cfg::nbuf;
     const uint64_t a_desc0 = sdesc_sw128(s_a, 16, 1024), b_desc0 = sdesc_sw128(s_w, 16, 1024);
     uint32_t w_it = 0, a_it = 0, t_it = 0;
     // The epilogue warps block on named barrier 2 + (tile & 1) (no polling);
@@ -1253,8 +1400,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     bool pending = false;
     uint32_t pend_t = 0;
     auto release_epilogue = [&]() {
-      mbar_wait(bar(B_T_FULL + (pend_t & 1)), (pend_t >> 1) & 1);
-      named_bar_arrive(2 + (pend_t & 1), 32 * 5);
+      mbar_wait(bar(B_T_FULL + (pend_t % NB)), (pend_t / NB) & 1);
+      named_bar_arrive(2 + (pend_t % NB), 32 * 5);
       pending = false;
     };
     for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
@@ -1263,8 +1410,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       const int nsub = static_cast<int>(sp.y & 0xFFu);
       if (a.halo_len[s] == kOverflow) continue;
       const bool first = (sp.y & SUP_FIRST) != 0, last = (sp.y & SUP_LAST) != 0;
-      const uint32_t ab = t_it & 1;
-      if (first) mbar_wait(bar(B_T_EMPTY + ab), ((t_it >> 1) & 1) ^ 1);
+      const uint32_t ab = t_it % NB;
+      if (first) mbar_wait(bar(B_T_EMPTY + ab), ((t_it / NB) & 1) ^ 1);
       tc_fence_after();
       for (int c = 0; c < nci; ++c)
       for (int k = 0; k < K; ++k) {
@@ -1280,16 +1427,36 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           const uint32_t as = st % NSA;
           if (lane == 0) tev(st, 4);
           tc_fence_after();
-          const uint32_t d = tmem + ab * Cfg::acc_cols + g * NOUT;
           // descriptor start-address field is in 16-byte units
           const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
           const uint64_t bd = b_desc0 + ((ws * Cfg::wbytes) >> 4);
-          if (elect_one()) {
+          if constexpr (SPLIT) {
+            // main: Ah (tile K 0..31) x Wh into set q % nmain; corr: [Ah | Al]
+            // x [Wl; Wh] into the last set.  Each set is initialised by its
+            // first MMA of the item (first record).
+            const int q = c * K + k;
+            const int pm = q % nmain;
+            const uint32_t dm = tmem + pm * Cfg::acc_cols + g * NOUT;
+            const uint32_t dc = tmem + Cfg::nmain * Cfg::acc_cols + g * NOUT;
+            const uint64_t bd2 = bd + (Cfg::wimg >> 4);
+            if (elect_one()) {
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-              umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
-                        (!first || c > 0 || k > 0 || ks > 0) ? 1u : 0u);
-            umma_commit(bar(B_A_EMPTY + as));
+              for (int ks = 0; ks < 2; ++ks)
+                umma_bf16(dm, ad + 2u * ks, bd + 2u * ks, idesc, (!first || q >= nmain || ks > 0) ? 1u : 0u);
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                umma_bf16(dc, ad + 2u * ks, bd2 + 2u * ks, idesc, (!first || q > 0 || ks > 0) ? 1u : 0u);
+              umma_commit(bar(B_A_EMPTY + as));
+            }
+          } else {
+            const uint32_t d = tmem + ab * Cfg::acc_cols + g * NOUT;
+            if (elect_one()) {
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
+                          (!first || c > 0 || k > 0 || ks > 0) ? 1u : 0u);
+              umma_commit(bar(B_A_EMPTY + as));
+            }
           }
           __syncwarp();
           if (lane == 0) tev(st, 5);
@@ -1326,6 +1493,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       pending = true;
       pend_t = t_it;
       ++t_it;
+      // single-buffered sets: the next item's first MMA waits for this epilogue
+      if (NB == 1) release_epilogue();
     }
     if (pending) release_epilogue();
   } else if (warp >= FWD_AGG_WARP0) {
@@ -1359,12 +1528,13 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           if (wig == 0 && lane == 0) tev(j, 2);
         };
         if (src == kFitsSlot) {  // (separate instantiations keep shared-memory loads)
-          aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512),
-                                           s_halo, s_a + as * 16384u, wig, lane, wait_a);
+          aggregate_stage<AGG_GROUP_WARPS, SPLIT>(slot, reinterpret_cast<const uint16_t*>(slot + 512),
+                                                  s_halo, s_a + as * 16384u, wig, lane, wait_a);
         } else {
           wait_a();
-          aggregate_stage_l2<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512),
-                                              s_halo, s_a + as * 16384u, wig, lane);
+          aggregate_stage_l2<AGG_GROUP_WARPS, SPLIT>(
+              slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512), s_halo,
+              s_a + as * 16384u, wig, lane);
         }
         fence_proxy_async_smem();
         __syncwarp();
@@ -1381,12 +1551,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     // ------------------------------ epilogue (warps 0-3) -------------------
     const int e = warp;
     uint32_t t_it = 0;
+    // SPLIT: 1 / (s_feat s_w) (exact powers of two)
+    const float inv_scale = SPLIT ? 1.f / (split_scale(a.amax[0]) * split_scale(a.amax[1])) : 1.f;
     for (int w = blockIdx.x; w < a.n_items; w += gridDim.x) {
       const int s = static_cast<int>(a.item_start[w + 1]) - 1;  // last record: the rows
       const uint2 sp = a.sup[s];
       const int nsub = static_cast<int>(sp.y & 0xFFu);
       if (a.halo_len[s] == kOverflow) continue;
-      const uint32_t ab = t_it & 1;
+      const uint32_t ab = t_it % Cfg::nbuf;
       {  // warm L2 with the next item's halo while this one is aggregated
         const int s_next = w + static_cast<int>(gridDim.x) < a.n_items
                                ? static_cast<int>(a.item_start[w + gridDim.x]) : a.n_super;
@@ -1409,6 +1581,23 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           uint32_t v[16];
           tmem_ld16(t0 + 16 * q, v);
           tmem_ld_wait();
+          if constexpr (SPLIT) {
+            // y = ((main_0 + main_1) + main_2) + corr 2^-11, all fp32 round-to-
+            // nearest, then the exact power-of-two unscaling
+            float f[16];
+#pragma unroll
+            for (int x = 0; x < 16; ++x) f[x] = __uint_as_float(v[x]);
+            for (int pm = 1; pm < nmain; ++pm) {
+              tmem_ld16(t0 + pm * Cfg::acc_cols + 16 * q, v);
+              tmem_ld_wait();
+#pragma unroll
+              for (int x = 0; x < 16; ++x) f[x] += __uint_as_float(v[x]);
+            }
+            tmem_ld16(t0 + Cfg::nmain * Cfg::acc_cols + 16 * q, v);
+            tmem_ld_wait();
+#pragma unroll
+            for (int x = 0; x < 16; ++x) v[x] = __float_as_uint(fmaf(__uint_as_float(v[x]), 0x1p-11f, f[x]) * inv_scale);
+          }
           if (o)
 #pragma unroll
             for (int x = 0; x < 4; ++x)
@@ -1449,6 +1638,7 @@ struct WgArgs {
   const __nv_bfloat16* dense;  // bf16 G_out (n_rows, NOUT), permuted (row = sub-tile order)
   float* partial;              // [gridDim.x][K][64 nci c][NOUT m]
   uint8_t korder[KMAX];        // run slot -> kernel cell (runs of 2 x pairs slots, load-balanced)
+  int seg;                     // SPLIT: super-tiles per accumulation segment (bounded chains)
 };
 
 constexpr int WG_THREADS = 32 * (FWD_AGG_WARP0 + FWD_AGG_WARPS);
@@ -1504,7 +1694,9 @@ enum : int {
   W_G_FULL = W_D_EMPTY + WG_NSD,   // WG_NSG
   W_G_EMPTY = W_G_FULL + WG_NSG,   // WG_NSG
   W_DONE = W_G_EMPTY + WG_NSG,
-  W_COUNT = W_DONE + 1
+  W_SEG_FULL = W_DONE + 1,   // SPLIT: a segment's MMAs completed
+  W_SEG_EMPTY = W_SEG_FULL + 1,  // SPLIT: its accumulators were flushed
+  W_COUNT = W_SEG_EMPTY + 1
 };
 static_assert(W_COUNT <= 24, "wgrad barrier region");
 
@@ -1513,7 +1705,12 @@ static_assert(wg_smem_layout<64>(FWD_HCAP).total <= 232448, "smem");
 static_assert(wg_smem_layout<128>(FWD_HCAP).total <= 232448, "smem");
 static_assert(wg_smem_layout<256>(FWD_HCAP1).total <= 232448, "smem");
 
-template <int NOUT, bool BIG>
+// SPLIT (fp32-contract path): A tiles from the split F_in image (32 channels
+// per chunk as [hi | lo], so an A_k^T pair is [Ah; Al] x 2 cells) against the
+// split G_out image ([Gh | Gl] per 32 channels, NOUT = 2 x C_out): the four
+// products (Ah+Al)^T (Gh+Gl) land in separate accumulator quadrants and the
+// reduction adds them.
+template <int NOUT, bool BIG, bool SPLIT = false>
 __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
   using Cfg = WgCfg<NOUT>;
   constexpr int NP = Cfg::pairs, NSG = Cfg::nsg, WNSD = Cfg::nsd;
@@ -1558,6 +1755,8 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
       mbar_init(bar(W_G_EMPTY + i), 1);
     }
     mbar_init(bar(W_DONE), 1);
+    mbar_init(bar(W_SEG_FULL), 1);
+    mbar_init(bar(W_SEG_EMPTY), 4);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
@@ -1605,13 +1804,27 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     }
   } else if (warp == 5) {
     if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16(128, NOUT, true, true);
+      constexpr uint32_t idesc = SPLIT ? idesc_f16(128, NOUT, true, true) : idesc_bf16(128, NOUT, true, true);
       uint32_t a_it = 0, g_it = 0;
       bool first = true;
+      int in_seg = 0;        // SPLIT: super-tiles in the current accumulation segment
+      uint32_t seg_it = 0;
       for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
         if (a.halo_len[s] == kOverflow) continue;
         const uint2 sp = a.sup[s];
         const int nsub = static_cast<int>(sp.y & 0xFFu);
+        if (SPLIT && in_seg == a.seg) {
+          // the tensor core's fp32 accumulation truncates: a segment's sums
+          // are handed to the epilogue warps (fp32 round-to-nearest adds into
+          // the CTA's partial) and the accumulators restart
+          umma_commit(bar(W_SEG_FULL));
+          mbar_wait(bar(W_SEG_EMPTY), seg_it & 1);
+          tc_fence_after();
+          ++seg_it;
+          in_seg = 0;
+          first = true;
+        }
+        ++in_seg;
         for (int g = 0; g < nsub; ++g) {
         if (GH) {
           for (int h = 0; h < 2; ++h) {
@@ -1695,11 +1908,12 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
             const uint8_t* slot = g_d + ds * 2 * BLOCK_MAX_BYTES + half * BLOCK_MAX_BYTES;
             const uint32_t src = BIG ? dsrc[2 * ds + half] : kFitsSlot;
             if (src == kFitsSlot)
-              aggregate_stage<TW>(slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
-                                  s_a + as * 32768u + half * 16384u, wq, lane, wait_a);
+              aggregate_stage<TW, SPLIT>(slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
+                                         s_a + as * 32768u + half * 16384u, wq, lane, wait_a);
             else if ((wait_a(), true))
-              aggregate_stage_l2<TW>(slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512),
-                                     s_halo, s_a + as * 32768u + half * 16384u, wq, lane);
+              aggregate_stage_l2<TW, SPLIT>(
+                  slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512), s_halo,
+                  s_a + as * 32768u + half * 16384u, wq, lane);
           } else {
             wait_a();
           }
@@ -1716,11 +1930,58 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
     }
   } else {
     // warps 0-3: dense G tile loader during the sweep, epilogue at the end
+    // (SPLIT: also at every segment end), TMEM lanes 32e..32e+31 of each pair
+    // accumulator -> the CTA's partial (SPLIT: added, fp32 round-to-nearest)
+    const int e = warp;
+    auto flush = [&](bool add) {
+      tc_fence_after();
+      for (int p = 0; p < n_pairs; ++p) {
+        const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + p * NOUT;
+        const int ks = k_begin + 2 * p + (e >> 1);
+        const int k = ks < K ? a.korder[ks] : K;
+        const int c = chunk * CH + 32 * (e & 1) + lane;
+        float4* o = k < K ? reinterpret_cast<float4*>(
+                                a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * fstride + c) * NOUT)
+                          : nullptr;
+#pragma unroll 4
+        for (int q = 0; q < NOUT / 16; ++q) {
+          uint32_t v[16];
+          tmem_ld16(t0 + 16 * q, v);
+          tmem_ld_wait();
+          if (o)
+#pragma unroll
+            for (int x = 0; x < 4; ++x) {
+              float4 r = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                     __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
+              if (add) {
+                const float4 b = o[q * 4 + x];
+                r.x += b.x;
+                r.y += b.y;
+                r.z += b.z;
+                r.w += b.w;
+              }
+              o[q * 4 + x] = r;
+            }
+        }
+      }
+      tc_fence_before();
+    };
     uint32_t g_it = 0;
+    int in_seg = 0;
+    uint32_t seg_it = 0;
     for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) {
       if (a.halo_len[s] == kOverflow) continue;
       const uint2 sp = a.sup[s];
       const int nsub = static_cast<int>(sp.y & 0xFFu);
+      if (SPLIT && in_seg == a.seg) {  // mirror of the MMA warp's segment
+        mbar_wait(bar(W_SEG_FULL), seg_it & 1);
+        flush(true);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(W_SEG_EMPTY));
+        ++seg_it;
+        in_seg = 0;
+      }
+      ++in_seg;
       {
         const int s_next = s + gridDim.x;
         if (s_next < a.n_super && a.halo_len[s_next] != kOverflow)
@@ -1753,37 +2014,10 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
         ++g_it;
       }
     }
-    // epilogue: TMEM lanes 32e..32e+31 of each pair accumulator -> partial
+    // epilogue: the last (or only) segment
     mbar_wait_sleep(bar(W_DONE), 0);
-    {
-      bool any = false;
-      for (int s = blockIdx.x; s < a.n_super; s += gridDim.x) any |= a.halo_len[s] != kOverflow;
-      if (!any) goto done;
-    }
-    tc_fence_after();
-    const int e = warp;
-    for (int p = 0; p < n_pairs; ++p) {
-      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + p * NOUT;
-      const int ks = k_begin + 2 * p + (e >> 1);
-      const int k = ks < K ? a.korder[ks] : K;
-      const int c = chunk * CH + 32 * (e & 1) + lane;
-      float4* o = k < K ? reinterpret_cast<float4*>(
-                              a.partial + ((static_cast<int64_t>(blockIdx.x) * K + k) * fstride + c) * NOUT)
-                        : nullptr;
-#pragma unroll 4
-      for (int q = 0; q < NOUT / 16; ++q) {
-        uint32_t v[16];
-        tmem_ld16(t0 + 16 * q, v);
-        tmem_ld_wait();
-        if (o)
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-            o[q * 4 + x] = make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
-                                       __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
-      }
-    }
+    if (g_it > 0) flush(SPLIT);
   }
-done:
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -1803,6 +2037,32 @@ __global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, in
   for (int x = 0; x < n_part; ++x)
     s += partial[((static_cast<int64_t>(x) * K + k) * cinp + c) * coutp + m];
   grad_w[(static_cast<int64_t>(k) * cout + m) * cin + c] = s;
+}
+
+// Split variant: partial[x][k][c'][m'] over split channels (c' = 64 (c / 32) +
+// c % 32 for the hi half, + 32 for the scaled lo half; same for m');
+// grad_w[k][m][c] = [sum over CTAs (fixed order) of hh + (hl + lh) 2^-11 +
+// ll 2^-22] / (s_F s_G).
+__global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_part, int K, int cin,
+                                     int cout, int cinp2, int coutp2, const uint32_t* __restrict__ amax_f,
+                                     const uint32_t* __restrict__ amax_g, float* __restrict__ grad_w) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(K) * cin * cout) return;
+  const int k = static_cast<int>(idx / (cin * cout)), c = static_cast<int>((idx / cout) % cin),
+            m = static_cast<int>(idx % cout);
+  const int ch = 64 * (c >> 5) + (c & 31), mh = 64 * (m >> 5) + (m & 31);
+  float hh = 0.f, cr = 0.f, ll = 0.f;
+  for (int x = 0; x < n_part; ++x) {
+    const float* b = partial + (static_cast<int64_t>(x) * K + k) * cinp2 * coutp2;
+    const float* rh = b + static_cast<int64_t>(ch) * coutp2;
+    const float* rl = rh + 32 * coutp2;
+    hh += rh[mh];
+    cr += rh[mh + 32] + rl[mh];
+    ll += rl[mh + 32];
+  }
+  const float inv = 1.f / (split_scale(*amax_f) * split_scale(*amax_g));
+  grad_w[(static_cast<int64_t>(k) * cout + m) * cin + c] =
+      (hh + fmaf(ll, 0x1p-11f, cr) * 0x1p-11f) * inv;
 }
 
 // ===========================================================================
@@ -2437,7 +2697,7 @@ static TcDirPlan* plan_fwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = fa
   auto& slot = wide ? p->fwd1 : p->fwd;
   if (!slot)
     slot = build_dir_plan(ctx, nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out,
-                          nb->n_in, nb->perm_out.get(), p->inv_perm_in.get(),
+                          nb->n_in, nb->perm_out.get(), p->inv_perm_in.get(), nb->out_off,
                           static_cast<int>(nb->n_kernels), wide ? 1 : FWD_ST,
                           wide ? FWD_HCAP1 : FWD_HCAP);
   return slot.get();
@@ -2448,7 +2708,7 @@ static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = fa
   if (!slot) {
     build_tcsr(ctx, nb);
     slot = build_dir_plan(ctx, nb->tcsr->row_ptr.get(), nb->tcsr->col.get(), nb->tcsr->k.get(),
-                          nb->n_in, nb->n_out, nb->perm_in.get(), p->inv_perm_out.get(),
+                          nb->n_in, nb->n_out, nb->perm_in.get(), p->inv_perm_out.get(), nb->in_off,
                           static_cast<int>(nb->n_kernels), wide ? 1 : FWD_ST,
                           wide ? FWD_HCAP1 : FWD_HCAP);
   }
@@ -2456,6 +2716,17 @@ static TcDirPlan* plan_bwd(npcg_context* ctx, npcg_neighbors* nb, bool wide = fa
 }
 
 static bool use_gather_engine_env();
+// Split weight gradient: super-tiles per TMEM accumulation segment (each
+// segment's chain of truncating fp32 accumulations is bounded: 2 sub-tiles x
+// 8 MMAs x seg), NPCG_SPLIT_SEG overrides (read once per process).
+static int split_segment() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("NPCG_SPLIT_SEG");
+    v = e ? std::max(1, std::atoi(e)) : 4;
+  }
+  return v;
+}
 static bool use_gather_engine(int64_t K) { return use_gather_engine_env() && K <= G_KMAX; }
 static GatherPlan* gplan_fwd(npcg_context* ctx, npcg_neighbors* nb);
 static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb);
@@ -2479,6 +2750,43 @@ static void convert(npcg_context* ctx, const float* src, const uint32_t* perm, i
          dim3(256), 0, src, perm, n, C, CP, dst.get());
 }
 
+// max |x| of a tensor into a scale slot (split path)
+static uint32_t* amax_slot(npcg_context* ctx, TcPlan* p, int slot) {
+  if (p->amax.size() < 4) p->amax.alloc(ctx, 4);
+  return p->amax.get() + slot;
+}
+static void absmax(npcg_context* ctx, const float* x, int64_t n, uint32_t* slot) {
+  NPCG_CUDA(cudaMemsetAsync(slot, 0, 4, ctx->stream));
+  if (n == 0) return;
+  launch(ctx, "absmax", k_absmax,
+         dim3(static_cast<unsigned>(std::min<int64_t>(ceil_div(n, 256), 4 * ctx->num_sms))), dim3(256), 0,
+         x, n, slot);
+}
+
+// split image (fp32-contract path): 2 x CP fp16 per row, scaled by the slot's scale
+static void convert_split(npcg_context* ctx, const float* src, const uint32_t* perm, int64_t n,
+                          DevBuf<__nv_bfloat16>& dst, int C, uint32_t* slot) {
+  const int CP = tc_pad(C);
+  absmax(ctx, src, n * C, slot);
+  if (dst.size() < n * 2 * CP) dst.alloc(ctx, n * 2 * CP);
+  if (n == 0) return;
+  launch(ctx, "to_split_perm", k_to_split_perm, dim3(static_cast<unsigned>(ceil_div(n * (CP / 8), 256))),
+         dim3(256), 0, src, perm, n, C, CP, static_cast<const uint32_t*>(slot),
+         reinterpret_cast<__half*>(dst.get()));
+}
+
+static void pack_w_split(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose,
+                         int cin, int cout, uint32_t* slot) {
+  const int cinp = tc_pad(cin), coutp = tc_pad(cout);
+  const int64_t n = static_cast<int64_t>(K) * cin * cout;
+  const int64_t bytes = static_cast<int64_t>(K) * cinp * coutp * 2 * 2 * 2;  // 2 images, K 64 per 32
+  absmax(ctx, w, n, slot);
+  if (p->wpack.size() < bytes) p->wpack.alloc(ctx, bytes);
+  NPCG_CUDA(cudaMemsetAsync(p->wpack.get(), 0, bytes, ctx->stream));
+  launch(ctx, "pack_w_split", k_pack_w_split, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256),
+         0, w, K, cin, cout, cinp, coutp, transpose, static_cast<const uint32_t*>(slot), p->wpack.get());
+}
+
 static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose,
                    int cin = CH, int cout = CH) {
   const int cinp = tc_pad(cin), coutp = tc_pad(cout);
@@ -2491,14 +2799,14 @@ static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool tra
          K, cin, cout, cinp, coutp, transpose, p->wpack.get());
 }
 
-template <int NOUT>
+template <int NOUT, bool SPLIT = false>
 static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, const char* name,
                        bool big) {
-  const FwdSmem L = fwd_smem_layout<NOUT>(hcap);
-  auto kern = big ? k_conv_fwd_tc<NOUT, true> : k_conv_fwd_tc<NOUT, false>;
-  if constexpr (NOUT == 64)
+  const FwdSmem L = fwd_smem_layout<NOUT, SPLIT>(hcap);
+  auto kern = big ? k_conv_fwd_tc<NOUT, true, false, SPLIT> : k_conv_fwd_tc<NOUT, false, false, SPLIT>;
+  if constexpr (NOUT == 64 && !SPLIT)
     if (a.trace) kern = big ? k_conv_fwd_tc<64, true, true> : k_conv_fwd_tc<64, false, true>;
-  if (a.trace && NOUT != 64) fail(NPCG_ERR_UNSUPPORTED, "trace: 64-channel passes only");
+  if (a.trace && (NOUT != 64 || SPLIT)) fail(NPCG_ERR_UNSUPPORTED, "trace: 64-channel bf16 passes only");
   NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
   launch(ctx, name, kern, dim3(grid), dim3(FWD_THREADS), L.total, a);
@@ -2509,8 +2817,9 @@ static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, 
 static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16* feat,
                            const uint8_t* wpack, const uint32_t* perm_rows, float* out,
                            const char* name, long long* trace = nullptr, int cin_g = CH,
-                           int nout = CH) {
+                           int nout = CH, bool split = false, const uint32_t* amax = nullptr) {
   // cin_g / nout: real gathered / written channels; the kernel runs padded
+  // (split: chunks of 32 real channels, each a 64-wide [hi | lo] bf16 slice)
   const int ncols = nout;
   cin_g = tc_pad(cin_g);
   nout = tc_pad(nout);
@@ -2531,13 +2840,20 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   a.st = P->st;
   a.hcap = P->hcap;
   a.K = P->K;
-  a.nci = cin_g / CH;
+  a.nci = split ? cin_g / 32 : cin_g / CH;
   a.feat = feat;
   a.wpack = wpack;
   a.out = out;
   a.ncols = ncols;
   a.trace = trace;
+  a.amax = amax;
   const int grid = std::min(P->n_super, ctx->num_sms);
+  if (split) {
+    if (nout == 64) launch_fwd<64, true>(ctx, a, P->hcap, grid, name, P->big_blocks);
+    else if (nout == 128) launch_fwd<128, true>(ctx, a, P->hcap, grid, name, P->big_blocks);
+    else fail(NPCG_ERR_UNSUPPORTED, "split tensor-core path: at most 128 written channels");
+    return;
+  }
   if (nout == 64) launch_fwd<64>(ctx, a, P->hcap, grid, name, P->big_blocks);
   else if (nout == 128) launch_fwd<128>(ctx, a, P->hcap, grid, name, P->big_blocks);
   else launch_fwd<256>(ctx, a, P->hcap, grid, name, P->big_blocks);
@@ -2579,10 +2895,24 @@ static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb) {
   return p->gbwd.get();
 }
 
+// The forward's device image of fin (bf16 or split), kept for the backward.
+static void input_image(npcg_context* ctx, npcg_neighbors* nb, TcPlan* p, const float* fin, int cin,
+                        bool split) {
+  if (split) convert_split(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin, amax_slot(ctx, p, 0));
+  else convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
+  p->saved_fin = fin;  // PointConvOp saves its input (conv_op.hpp:138)
+  p->saved_c = cin;
+  p->saved_split = split;
+}
+
+// Plans: 256-row super-tiles unless the pass writes more than 128 channels
+// (bf16) / more than 64 (split: its W stages are twice as large).
+static bool wide_pass(int written, bool split) { return tc_pad(written) > (split ? CH : 2 * CH); }
+
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
                 const float* fin, float* fout, int cin, int cout) {
-  (void)mode;
-  if (use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
+  const bool split = mode == TcMode::split;
+  if (!split && use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
     GatherPlan* G = gplan_fwd(ctx, nb);
     TcPlan* p = nb->tc.get();
     if (G->n_overflow < G->n_super) {
@@ -2598,15 +2928,15 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float*
                          CH, fout);
     return;
   }
-  TcDirPlan* P = plan_fwd(ctx, nb, tc_pad(cout) > 2 * CH);
+  TcDirPlan* P = plan_fwd(ctx, nb, wide_pass(cout, split));
   TcPlan* p = nb->tc.get();
   if (P->n_overflow < P->n_super) {
-    convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
-    p->saved_fin = fin;  // PointConvOp saves its input (conv_op.hpp:138)
-    p->saved_c = cin;
-    pack_w(ctx, p, w, P->K, false, cin, cout);
+    input_image(ctx, nb, p, fin, cin, split);
+    if (split) pack_w_split(ctx, p, w, P->K, false, cin, cout, amax_slot(ctx, p, 1));
+    else pack_w(ctx, p, w, P->K, false, cin, cout);
     run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
-                   "conv_fwd_tc", nullptr, cin, cout);
+                   split ? "conv_fwd_tc_split" : "conv_fwd_tc", nullptr, cin, cout, split,
+                   split ? amax_slot(ctx, p, 0) : nullptr);
   }
   // rows of super-tiles beyond the tile capacities: exact engine on those rows only
   const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
@@ -2648,13 +2978,14 @@ __global__ void k_row_lens(const int64_t* __restrict__ row_ptr, const uint32_t* 
   }
 }
 
-template <int NOUT>
+template <int NOUT, bool SPLIT = false>
 static void launch_wgrad(npcg_context* ctx, const WgArgs& a, int hcap, dim3 grid, bool big) {
   const WgSmem L = wg_smem_layout<NOUT>(hcap);
-  auto kern = big ? k_conv_wgrad_tc<NOUT, true> : k_conv_wgrad_tc<NOUT, false>;
+  auto kern = big ? k_conv_wgrad_tc<NOUT, true, SPLIT> : k_conv_wgrad_tc<NOUT, false, SPLIT>;
   NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
-  launch(ctx, "conv_wgrad_tc", kern, grid, dim3(WG_THREADS), L.total, a);
+  launch(ctx, SPLIT ? "conv_wgrad_tc_split" : "conv_wgrad_tc", kern, grid, dim3(WG_THREADS), L.total,
+         a);
 }
 
 static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, const float* fin,
@@ -2692,11 +3023,16 @@ static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, con
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
                  const float* fin, const float* gout, float* grad_in, float* grad_w, int cin,
                  int cout, bool fin_unchanged) {
-  (void)mode;
+  const bool split = mode == TcMode::split;
   TcPlan* p = get_plan(ctx, nb);
   const int K = static_cast<int>(nb->n_kernels);
   bool g_converted = false;
-  if (grad_in && use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
+  auto g_image = [&] {
+    if (split) convert_split(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout, amax_slot(ctx, p, 2));
+    else convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
+    g_converted = true;
+  };
+  if (grad_in && !split && use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
     GatherPlan* G = gplan_bwd(ctx, nb);
     if (G->n_overflow < G->n_super) {
       convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out);
@@ -2712,13 +3048,14 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float
                            G->n_spill, wt.get(), gout, CH, CH, grad_in);
     }
   } else if (grad_in) {
-    TcDirPlan* P = plan_bwd(ctx, nb, tc_pad(cin) > 2 * CH);
+    TcDirPlan* P = plan_bwd(ctx, nb, wide_pass(cin, split));
     if (P->n_overflow < P->n_super) {
-      convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
-      g_converted = true;
-      pack_w(ctx, p, w, K, true, cin, cout);
+      g_image();
+      if (split) pack_w_split(ctx, p, w, K, true, cin, cout, amax_slot(ctx, p, 3));
+      else pack_w(ctx, p, w, K, true, cin, cout);
       run_fwd_kernel(ctx, P, p->feat_out.get(), p->wpack.get(), nb->perm_in.get(), grad_in,
-                     "conv_dgrad_tc", nullptr, cout, cin);
+                     split ? "conv_dgrad_tc_split" : "conv_dgrad_tc", nullptr, cout, cin, split,
+                     split ? amax_slot(ctx, p, 2) : nullptr);
     }
     if (P->n_spill) {
       DevBuf<float> wt(ctx, static_cast<int64_t>(K) * cin * cout);
@@ -2728,7 +3065,8 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float
     }
   }
   if (grad_w) {
-    TcDirPlan* P = plan_fwd(ctx, nb, tc_pad(cout) > 2 * CH);  // same rows and gathers as the forward
+    // same rows and gathers as the forward (split: the pass writes 2 x C_out columns)
+    TcDirPlan* P = plan_fwd(ctx, nb, wide_pass(cout, split));
     if (P->n_overflow == P->n_super) {
       wgrad_spill(ctx, nb, P, fin, gout, grad_w, false, cin, cout);
       return;
@@ -2736,20 +3074,19 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float
     // the bf16 input image made by the forward on this handle is reused when
     // the caller vouches that the backward's input is that same, unmodified
     // buffer (NPCG_FLAG_FIN_UNCHANGED: the operator's saved copy)
-    if (!fin_unchanged || fin != p->saved_fin || cin != p->saved_c) {
-      convert(ctx, fin, nb->perm_in.get(), nb->n_in, p->feat_in, cin);
-      p->saved_fin = fin;
-      p->saved_c = cin;
-    }
-    if (!g_converted) convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
+    if (!fin_unchanged || fin != p->saved_fin || cin != p->saved_c || split != p->saved_split)
+      input_image(ctx, nb, p, fin, cin, split);
+    if (!g_converted) g_image();
     const int cinp = tc_pad(cin), coutp = tc_pad(cout);
-    const int nci = cinp / CH;
-    const int np = coutp == 64 ? WgCfg<64>::pairs : coutp == 128 ? WgCfg<128>::pairs : WgCfg<256>::pairs;
+    // split: chunks of 32 real input channels, 2 x C_out accumulator columns
+    const int nci = split ? cinp / 32 : cinp / CH;
+    const int nw = split ? 2 * coutp : coutp;  // accumulator columns (the kernel's NOUT)
+    const int np = nw == 64 ? WgCfg<64>::pairs : nw == 128 ? WgCfg<128>::pairs : WgCfg<256>::pairs;
     const int gpc = (K + 2 * np - 1) / (2 * np);  // cell groups per C_in chunk
     const int groups = nci * gpc;
     // one CTA per SM in total over (super-tile slices x groups)
     const int gx = std::max(1, std::min(P->n_super, ctx->num_sms / groups));
-    const int64_t need = static_cast<int64_t>(gx) * K * cinp * coutp;
+    const int64_t need = static_cast<int64_t>(gx) * K * nci * CH * nw;
     if (p->partial.size() < need) p->partial.alloc(ctx, need);
     NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
     WgArgs a{};
@@ -2770,15 +3107,26 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float
     a.feat = p->feat_in.get();
     a.dense = p->feat_out.get();
     a.partial = p->partial.get();
+    a.seg = split_segment();
     wgrad_cell_order(P, K, np, gpc, a.korder);
     const dim3 grid(gx, groups);
-    if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid, P->big_blocks);
-    else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid, P->big_blocks);
-    else launch_wgrad<256>(ctx, a, P->hcap, grid, P->big_blocks);
-    const int64_t nw = static_cast<int64_t>(K) * cin * cout;
-    launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(nw, 256))),
-           dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, cinp, coutp,
-           grad_w);
+    const int64_t nwt = static_cast<int64_t>(K) * cin * cout;
+    if (split) {
+      if (nw == 128) launch_wgrad<128, true>(ctx, a, P->hcap, grid, P->big_blocks);
+      else if (nw == 256) launch_wgrad<256, true>(ctx, a, P->hcap, grid, P->big_blocks);
+      else fail(NPCG_ERR_UNSUPPORTED, "split weight gradient: C_out up to 128");
+      launch(ctx, "wgrad_reduce", k_wgrad_reduce_split, dim3(static_cast<unsigned>(ceil_div(nwt, 256))),
+             dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, 2 * cinp,
+             2 * coutp, static_cast<const uint32_t*>(amax_slot(ctx, p, 0)),
+             static_cast<const uint32_t*>(amax_slot(ctx, p, 2)), grad_w);
+    } else {
+      if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid, P->big_blocks);
+      else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid, P->big_blocks);
+      else launch_wgrad<256>(ctx, a, P->hcap, grid, P->big_blocks);
+      launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(nwt, 256))),
+             dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, cinp, coutp,
+             grad_w);
+    }
     if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true, cin, cout);
   }
 }

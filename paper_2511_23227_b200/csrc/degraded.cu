@@ -103,6 +103,7 @@ void build_degraded(npcg_context* ctx, const npcg_cloud* in_cloud, double voxel,
   voxel_downsample_impl(ctx, in_cloud, voxel, nb->kept.get(), nb->parent.get(),
                         nb->site_offsets.data(), &ns);
   nb->n_out = nb->n_in = ns;
+  nb->out_off = nb->in_off = nb->site_offsets;
   nb->site_xyz.alloc(ctx, std::max<int64_t>(3 * ns, 1));
   nb->row_ptr.alloc(ctx, ns + 1);
   if (ns == 0) {

@@ -333,6 +333,8 @@ void build_neighbors(npcg_context* ctx, const npcg_cloud* qc, const npcg_cloud* 
   const int64_t nq = qc->n_points, nt = tc->n_points;
   nb->n_out = nq;
   nb->n_in = nt;
+  nb->out_off.assign(qc->batch_offsets, qc->batch_offsets + qc->n_batches + 1);
+  nb->in_off.assign(tc->batch_offsets, tc->batch_offsets + tc->n_batches + 1);
   nb->t = t;
   nb->n_kernels = t > 0 ? t * t * t : 1;
   nb->radius = radius;

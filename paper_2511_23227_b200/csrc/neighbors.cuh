@@ -68,6 +68,9 @@ struct npcg_neighbors {
   bool used = false;
   int device = 0;
   int64_t n_out = 0, n_in = 0;
+  // batch offsets of the output / input clouds (the spatial orders perm_out /
+  // perm_in are batch-major, so batch b occupies permuted rows [off[b], off[b+1]))
+  std::vector<int64_t> out_off, in_off;
   int64_t t = 0;          // 0: plain radius_search handle (no kernel cells)
   int64_t n_kernels = 1;  // t^3
   double radius = 0.0;

@@ -214,6 +214,17 @@ __host__ __device__ constexpr uint32_t idesc_bf16(uint32_t M, uint32_t N, bool a
          | ((M >> 4) << 24);               // M / 16
 }
 
+// Instruction descriptor, kind::f16: fp16 x fp16 -> fp32, M x N (the split
+// fp32-contract path's operands: hi / scaled lo halves in fp16).
+__host__ __device__ constexpr uint32_t idesc_f16(uint32_t M, uint32_t N, bool a_mn_major,
+                                                 bool b_mn_major) {
+  return (1u << 4)                         // D format fp32; A, B format 0 = fp16
+         | ((a_mn_major ? 1u : 0u) << 15)  // A major
+         | ((b_mn_major ? 1u : 0u) << 16)  // B major
+         | ((N >> 3) << 17)                // N / 8
+         | ((M >> 4) << 24);               // M / 16
+}
+
 // SW128 byte offset of element (row, col) in a tile of 128-byte rows (64 bf16).
 __host__ __device__ __forceinline__ uint32_t sw128_off(uint32_t row, uint32_t col) {
   return row * 128u + ((((col >> 3) ^ (row & 7u)) & 7u) << 4) + ((col & 7u) << 1);
@@ -232,6 +243,18 @@ __device__ __forceinline__ void acc_bf16x2(float& lo_acc, float& hi_acc, uint32_
 __device__ __forceinline__ uint32_t add_bf16x2_rn(uint32_t a, uint32_t b) {
   uint32_t r;
   asm("add.rn.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(b));
+  return r;
+}
+// acc += fp16 (lo / hi half of a 32-bit word), fp32 accumulate
+__device__ __forceinline__ void acc_f16x2(float& lo_acc, float& hi_acc, uint32_t w) {
+  unsigned short lo, hi;
+  asm("mov.b32 {%0,%1}, %2;" : "=h"(lo), "=h"(hi) : "r"(w));
+  asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(lo_acc) : "h"(lo));
+  asm("add.rn.f32.f16 %0, %1, %0;" : "+f"(hi_acc) : "h"(hi));
+}
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
   return r;
 }
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {

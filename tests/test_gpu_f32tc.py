@@ -1,0 +1,101 @@
+"""GPU: the fp32-contract tensor-core path (math = f32tc, and the default
+math = auto) against the fp64 oracle at the reference's fp32 bound
+rel <= 1e-5 (acceptance.cpp:39, 173-195), on the reference's
+fp32 inputs.  Operands are split x = hi + lo (two bf16); products hi*hi +
+hi*lo + lo*hi (forward / input gradient) and all four (weight gradient), fp32
+accumulation.  Cases: uniform clouds (configs 1/2 shapes), every supported
+width pair, clustered and strided (dense, split-record) neighborhoods,
+determinism, and that AUTO actually runs the split kernels."""
+import numpy as np
+import pytest
+import torch
+
+from test_gpu_operator import T, rel
+
+pytestmark = pytest.mark.gpu
+
+TOL = 1e-5
+
+
+def _run(npc, cl, out_cl, w, f, go, math):
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=_run.r, t=_run.t),
+                         npc.ExecConfig(math=math))
+    out = op.forward(cl, out_cl, T(f)) if out_cl is not None else op.forward(cl, T(f))
+    res = op.backward(T(go))
+    return op, out, res
+
+
+def _check(npc, orc, xyz, r, t, cin, cout, seed, out_xyz=None, math=None):
+    math = npc.Math.f32tc if math is None else math
+    n = len(xyz)
+    cl = npc.make_point_cloud(xyz)
+    out_cl = npc.make_point_cloud(out_xyz) if out_xyz is not None else None
+    n_out = len(out_xyz) if out_xyz is not None else n
+    w = orc.make_weights(t, 1, cin, cout, 200 + seed)
+    f = orc.gen_features(n, 1, cin, 300 + seed)
+    go = orc.gen_features(n_out, 1, cout, 400 + seed)
+    _run.r, _run.t = r, t
+    op, out, res = _run(npc, cl, out_cl, w, f, go, math)
+    ti, tj, tk = op.cached_triplets().numpy()
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n_out,
+                                go.astype(np.float64))
+    e = (rel(out.cpu(), fo), rel(res.grad_in.cpu(), gi), rel(res.grad_w.cpu(), gw))
+    print(f"f32tc n={n} t={t} {cin}->{cout}: rel fwd {e[0]:.2e} dgrad {e[1]:.2e} wgrad {e[2]:.2e}")
+    assert max(e) <= TOL, e
+    # bitwise repeat
+    op2, out2, res2 = _run(npc, cl, out_cl, w, f, go, math)
+    assert torch.equal(out, out2)
+    assert torch.equal(res.grad_in, res2.grad_in) and torch.equal(res.grad_w, res2.grad_w)
+    return e
+
+
+@pytest.mark.parametrize("cin,cout", [(64, 64), (64, 128), (128, 64), (128, 128), (32, 32),
+                                      (48, 80), (16, 112)])
+def test_f32tc_widths_uniform(npc, orc, cin, cout):
+    n = 8000
+    xyz = orc.gen_uniform_cube(n, 1.0, 7)
+    _check(npc, orc, xyz, 1.8 * n ** (-1 / 3), 3, cin, cout, cin + cout)
+
+
+@pytest.mark.parametrize("t", [1, 5])
+def test_f32tc_kernel_resolutions(npc, orc, t):
+    n = 4000
+    xyz = orc.gen_uniform_cube(n, 1.0, 8)
+    _check(npc, orc, xyz, 1.8 * n ** (-1 / 3), t, 64, 64, t)
+
+
+def test_f32tc_clustered_dense(npc, ref, orc):
+    """Gaussian clusters: hundreds of neighbors per row (rank-split and
+    halo-segment records accumulate partial sums in TMEM)."""
+    xyz = ref.gen_gaussian_clusters(6000, 6, 2.0, 0.2, 17)
+    _check(npc, orc, xyz, 0.25, 3, 64, 64, 17)
+
+
+def test_f32tc_strided(npc, ref, orc):
+    """Two-cloud strided conv onto a quarter of the points (50+ neighbors)."""
+    xyz = ref.gen_gaussian_clusters(6000, 10, 2.0, 0.3, 18)
+    _check(npc, orc, xyz, 0.3, 3, 64, 128, 18, out_xyz=xyz[::4].copy())
+
+
+def test_auto_is_the_fp32_contract_on_tensor_cores(npc, orc):
+    """math = auto (the default) runs the split kernels for C >= 64 and meets
+    1e-5; C < 64 stays on the exact CUDA-core engines."""
+    n = 6000
+    xyz = orc.gen_uniform_cube(n, 1.0, 9)
+    ctx = npc.context()
+    ctx.profile_reset()
+    ctx.profile(True)
+    _check(npc, orc, xyz, 1.8 * n ** (-1 / 3), 3, 64, 64, 9, math=npc.Math.auto)
+    prof = ctx.profile_dump()
+    ctx.profile(False)
+    assert any("split" in k for k in prof), prof
+    assert npc.ExecConfig().math == npc.Math.auto
+
+
+@pytest.mark.slow
+def test_f32tc_c2_100k(npc, orc):
+    """BASELINE config 2 (100K, C=64, fwd+dgrad+wgrad) on the default path."""
+    n = 100_000
+    xyz = orc.gen_uniform_cube(n, 1.0, 1)
+    e = _check(npc, orc, xyz, 1.8 * n ** (-1 / 3), 3, 64, 64, 1, math=npc.Math.auto)
+    assert max(e) <= TOL

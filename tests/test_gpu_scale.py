@@ -14,7 +14,8 @@
       descriptors, checked bitwise against scenes run alone.
 
 Bounds (metric rel = max|a-b| / max|b|, gradcheck.cpp:11-31): exact fp32
-1e-5 (acceptance.cpp:39), bf16 operands 1e-2."""
+and the default fp32-contract path (auto: split tensor cores) 1e-5
+(acceptance.cpp:39), bf16 operands 1e-2."""
 import os
 
 import numpy as np
@@ -71,7 +72,7 @@ def ns_reference(ns_case, ref):
     return fo, gi, gw
 
 
-@pytest.mark.parametrize("math,tol", [("exact", 1e-5), ("bf16", 1e-2)])
+@pytest.mark.parametrize("math,tol", [("exact", 1e-5), ("bf16", 1e-2), ("auto", 1e-5)])
 def test_ns_conv_vs_reference_fp64(npc, ns_case, ns_reference, math, tol):
     c = ns_case
     cfg = npc.ExecConfig(math=getattr(npc.Math, math))
@@ -101,7 +102,7 @@ def _voxel_for_ratio(npc, cloud, ratio):
     return hi
 
 
-@pytest.mark.parametrize("math,tol", [("exact", 1e-5), ("bf16", 1e-2)])
+@pytest.mark.parametrize("math,tol", [("exact", 1e-5), ("bf16", 1e-2), ("auto", 1e-5)])
 def test_c3_lidar_strided_120k(npc, orc, ref, math, tol):
     """Config 3 at its stated size: 120K-point LiDAR-like scan, downsample ~4x,
     strided 64 -> 128 fwd + bwd, against the reference chain."""
@@ -168,11 +169,22 @@ def _jagged_vs_scenes(npc, n_scenes, n_pts, math, check_scenes, c=64):
 
 def test_c5_batch64_jagged_equals_scenes(npc):
     """Config 5 (64 x 250K) as one jagged 16M-point cloud on one GPU (what a
-    rank runs): every scene bitwise equal to the scene alone; dW = sum over
-    scenes within fp32 tolerance."""
+    rank runs), bf16 operands: every scene's rows bitwise equal to the scene
+    alone (tiles never cross a batch boundary); dW equal to the sum of the
+    per-scene dW within 2e-3 -- the tensor core accumulates in fp32 with
+    truncation (tools/micro/mma_accum.cu), and the bf16 path's per-CTA chains
+    over 16M rows are long; inside its 1e-2 bound."""
     gw, gw_sum, stats, _ = _jagged_vs_scenes(npc, 64, 250_000, "bf16", range(64))
-    assert rel(gw.cpu(), gw_sum.cpu()) <= 1e-5
+    assert rel(gw.cpu(), gw_sum.cpu()) <= 2e-3
     assert all(v["overflow"] == 0 for v in stats.values()), stats
+
+
+def test_c5_batch64_jagged_fp32_contract(npc):
+    """The same 16M-point batch on the default fp32-contract path (split
+    operands; weight-gradient chains bounded by segments): rows bitwise equal
+    to the scenes alone, dW within 1e-5 of the sum of the per-scene dW."""
+    gw, gw_sum, _, _ = _jagged_vs_scenes(npc, 64, 250_000, "auto", range(64))
+    assert rel(gw.cpu(), gw_sum.cpu()) <= 1e-5
 
 
 def test_c5_batch64_exact_subset(npc):
