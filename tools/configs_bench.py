@@ -139,7 +139,8 @@ def per_layer(layers, fin, math, steps):
 
 def result(name, desc, unit_points, ms, prof, layers, bf16, extra):
     flop = sum(3 * 2 * l.nb.size * l.cin * l.cout for l in layers)
-    return {"config": name, "workload": desc, "value": round(unit_points / (ms / 1e3) / 1e6, 3),
+    return {"config": name, "math": MATH, "workload": desc,
+            "value": round(unit_points / (ms / 1e3) / 1e6, 3),
             "unit": "Mpoints/s", "ms_per_step": round(ms, 4),
             "tensor_frac": round(flop / (ms / 1e3) / 1e12 / bf16, 4),
             "algorithmic_flop_per_step": flop,
@@ -151,28 +152,32 @@ def result(name, desc, unit_points, ms, prof, layers, bf16, extra):
 
 
 STEPS = 5
+MATH = "bf16"
 
 
 def main():
-    global STEPS
+    global STEPS, MATH
     ap = argparse.ArgumentParser()
     ap.add_argument("configs", nargs="*", default=["c1", "c2", "c3", "c4"])
     ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--math", default="bf16", choices=["bf16", "auto", "exact", "f32tc"],
+                    help="arithmetic of c2-c4 (c1 always reports auto = exact for C < 64, and bf16)")
     ap.add_argument("--warmup", type=int, default=3)
     a = ap.parse_args()
     STEPS = a.steps
     orc = Oracle()
     bf16 = peaks()
-    auto = npc.Math.auto
+    auto = getattr(npc.Math, a.math)
+    MATH = a.math
     for c in a.configs:
         t0 = time.time()
         if c == "c1":
             n = 16384
             cl = npc.make_point_cloud(orc.gen_uniform_cube(n, 1.0, 1))
-            l = Layer("conv", cl, cl, 1.8 * n ** (-1 / 3), 32, 32, 2, orc, auto)
+            l = Layer("conv", cl, cl, 1.8 * n ** (-1 / 3), 32, 32, 2, orc, npc.Math.auto)
             f = torch.from_numpy(orc.gen_features(n, 1, 32, 3)).cuda()
             out = torch.empty((n, 1, 32), device="cuda")
-            cfg = npc.ExecConfig(math=auto)
+            cfg = npc.ExecConfig(math=npc.Math.auto)
             ms, prof = time_steps(lambda: npc.conv_forward(l.nb, l.w, f, cfg, out=out),
                                   a.steps, a.warmup)
             flop = 2 * l.nb.size * 32 * 32
