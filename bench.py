@@ -520,9 +520,9 @@ def run_ours(args):
     name, (cnt, tot) = top
     per_launch_ms = tot / max(cnt, 1)
     share = tot / max(sum(v[1] for v in prof.values()), 1e-9)
-    # passes per launch: tc kernels fuse (fwd: 1 pass, bwd: 2 passes)
-    passes = 2 if "bwd" in name else 1
-    if "tc" in name or "umma" in name:
+    # passes per launch: the fused backward computes dgrad + wgrad (2 passes)
+    passes = 2 if "bwd_fused" in name else 1
+    if name.startswith("conv_"):  # the tensor-core engines
         achieved = passes * f_pass / (per_launch_ms / 1e3) / 1e12
         # burst peak: the kernel is timed inside a short (tens of ms) region
         roof = {"bound": "tensor", "achieved": round(achieved, 2), "peak": bf16_burst,

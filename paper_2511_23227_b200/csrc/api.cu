@@ -807,7 +807,7 @@ npcg_status npcg_neighbors_prepare(npcg_context* ctx, npcg_neighbors* nb, int32_
       build_cells(ctx, nb);
     }
     if (math != NPCG_MATH_EXACT && tc_supported(1, 64, 64, nb->n_kernels, TcMode::bf16, false))
-      tc_prepare(ctx, nb);
+      tc_prepare(ctx, nb, math == NPCG_MATH_BF16 ? TcMode::bf16 : TcMode::split);
     NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
   });
 }

@@ -38,7 +38,7 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float*
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
                  const float* fin, const float* gout, float* grad_in, float* grad_w, int cin,
                  int cout, bool fin_unchanged);
-void tc_prepare(npcg_context* ctx, npcg_neighbors* nb);
+void tc_prepare(npcg_context* ctx, npcg_neighbors* nb, TcMode mode);
 void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12);
 void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, const float* fin,
                       float* fout, int64_t* trace_host);

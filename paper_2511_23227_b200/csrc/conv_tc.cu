@@ -2066,6 +2066,396 @@ __global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_pa
 }
 
 // ===========================================================================
+// fused backward (bf16 operands, C_in, C_out <= 64, K = 27): the input
+// gradient and the weight gradient from ONE aggregation pass.  Over the
+// transposed plan (rows = input points j, 128-row super-tiles),
+//     B_k[j] = sum_{i : (i, j, k)} G_out[i]
+// is aggregated once per (tile, cell) and feeds both
+//     grad_in[j] += B_k[j] W_k^T          (M128 N64 K64 into a TMEM accumulator)
+//     dW_k       += B_k^T F_in[tile]      (vvor.hpp:79-84: two cells' A slots
+//                                          stacked to M = 128 as an MN-major A
+//                                          operand, the tile's dense F_in rows as
+//                                          the MN-major B operand, K = 128 rows)
+// dW of 27 cells (442 KB fp32) exceeds one SM's TMEM, so the two CTAs of a
+// cluster take the same super-tiles and half of the cells each (14, and 13 + a
+// zero stage, so every pair of stages is two adjacent A slots); each keeps 7
+// pair accumulators (448 columns) + the 64-column input-gradient accumulator.
+// The two halves' input-gradient sums meet in global memory: grad_in is zeroed
+// and each CTA adds its sum once (0 + a + b == 0 + b + a in fp32:
+// deterministic).  Per-pair dW partials are reduced in a fixed order.
+// ===========================================================================
+constexpr int BF_STAGES = 14;      // stages per record and CTA (a half of the 27 cells + padding)
+constexpr uint8_t BF_ZERO = 0xFF;  // the padding stage: a zero A tile
+constexpr int NSF = 2;             // F tiles (16 KB: 128 rows x 64 channels, SW128)
+enum : int { B_F_FULL = B_COUNT, B_F_EMPTY = B_F_FULL + NSF, B_MMA_DONE = B_F_EMPTY + NSF,
+             BF_B_COUNT = B_MMA_DONE + 1 };
+static_assert(BF_B_COUNT <= 48, "barrier region");
+
+struct BfArgs {
+  const uint32_t* halo;
+  const uint32_t* halo_len;
+  const uint32_t* blk_off;
+  const uint8_t* blocks;
+  const uint32_t* perm_rows;  // perm_in: permuted row -> input point
+  const uint2* sup;
+  const uint2* tiles;
+  const uint32_t* item_start;
+  int n_items, hcap, K;
+  const __nv_bfloat16* feat;  // bf16 G_out image (perm_out order): the gathered rows
+  const __nv_bfloat16* fimg;  // bf16 F_in image (perm_in order): the tiles' dense rows
+  const uint8_t* wpack;       // K images of W_k^T (64 x 128 B)
+  float* gin;                 // (n_in, cin) original order, zeroed by the host
+  int gin_cols;               // cin
+  float* partial;             // [pairs][K][64 m][64 c]
+  uint8_t cells[2 * BF_STAGES];  // per half: stage -> cell (BF_ZERO: the zero stage)
+};
+
+struct BfSmem {
+  uint32_t halo, a, w, d, f, bar, tmem_slot, offs;
+  size_t total;
+};
+__host__ __device__ constexpr BfSmem bf_smem_layout(int hcap) {
+  BfSmem L{};
+  uint32_t o = 0;
+  L.halo = o;
+  o += hcap * 128;
+  o = (o + 1023) & ~1023u;
+  L.a = o;
+  o += NSA * 16384;
+  L.f = o;
+  o += NSF * 16384;
+  L.w = o;
+  o += NSW * 8192;
+  L.d = o;
+  o += NSD * BLOCK_MAX_BYTES;
+  o = (o + 7) & ~7u;
+  L.bar = o;
+  o += 48 * 8;
+  L.tmem_slot = o;
+  o += 16;
+  L.offs = o;
+  o += OFFS_WORDS * 4;
+  L.total = o + 1024;
+  return L;
+}
+static_assert(bf_smem_layout(FWD_HCAP1).total <= 232448, "smem");
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+template <bool BIG>
+__global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
+  extern __shared__ uint8_t smem_raw[];
+  const uint32_t raw = smem_u32(smem_raw);
+  const uint32_t base = (raw + 1023u) & ~1023u;
+  uint8_t* gbase = smem_raw + (base - raw);
+  const BfSmem L = bf_smem_layout(a.hcap);
+  const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_w = base + L.w, s_d = base + L.d,
+                 s_f = base + L.f;
+  const uint32_t s_bar = base + L.bar;
+  auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
+  const uint8_t* g_d = gbase + L.d;
+  uint32_t* dsrc = reinterpret_cast<uint32_t*>(gbase + L.offs) + OFFS_DSRC;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int half = static_cast<int>(cluster_ctarank());
+  const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
+  const uint8_t* cells = a.cells + half * BF_STAGES;
+  const int K = a.K;
+  if (threadIdx.x == 0) {
+    mbar_init(bar(B_HALO_FULL), 1);
+    mbar_init(bar(B_HALO_EMPTY), FWD_AGG_WARPS);
+    for (int i = 0; i < NSA; ++i) {
+      mbar_init(bar(B_A_FULL + i), AGG_GROUP_WARPS);
+      mbar_init(bar(B_A_EMPTY + i), 1);
+    }
+    for (int i = 0; i < NSW; ++i) {
+      mbar_init(bar(B_W_FULL + i), 1);
+      mbar_init(bar(B_W_EMPTY + i), 1);
+    }
+    for (int i = 0; i < NSD; ++i) {
+      mbar_init(bar(B_D_FULL + i), 1);
+      mbar_init(bar(B_D_EMPTY + i), AGG_GROUP_WARPS);
+    }
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(bar(B_T_FULL + i), 1);
+      mbar_init(bar(B_T_EMPTY + i), 4);
+    }
+    for (int i = 0; i < NSF; ++i) {
+      mbar_init(bar(B_F_FULL + i), 4);
+      mbar_init(bar(B_F_EMPTY + i), 1);
+    }
+    mbar_init(bar(B_MMA_DONE), 1);
+    fence_barrier_init();
+  }
+  if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------ producer: stage descriptors ---------------------
+    uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
+    uint32_t d_it = 0;
+    for (int w = pair; w < a.n_items; w += npairs)
+      for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+        if (a.halo_len[s] == kOverflow) continue;
+        const uint2 sp = a.sup[s];
+        const int64_t ob = static_cast<int64_t>(sp.x) * K;
+        for (int x = lane; x <= K; x += 32) offs[x] = a.blk_off[ob + x];
+        __syncwarp();
+        for (int ci = 0; ci < BF_STAGES; ++ci) {
+          if (lane == 0) {
+            const uint32_t ds = d_it % NSD;
+            mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
+            const int k = cells[ci] == BF_ZERO ? cells[0] : cells[ci];  // (the zero stage's is unused)
+            const uint32_t o0 = offs[k], o1 = offs[k + 1];
+            const uint32_t nb = min((o1 - o0) << 4, static_cast<uint32_t>(BLOCK_MAX_BYTES));
+            if (BIG) dsrc[ds] = (o1 - o0) << 4 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
+            mbar_expect_tx(bar(B_D_FULL + ds), nb);
+            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + blk_bytes(o0), nb, bar(B_D_FULL + ds));
+          }
+          ++d_it;
+        }
+        __syncwarp();
+      }
+  } else if (warp == FWD_W_WARP) {
+    // ------------------------ producer: W_k^T per record and stage ------------
+    if (lane == 0) {
+      uint32_t w_it = 0;
+      for (int w = pair; w < a.n_items; w += npairs)
+        for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+          if (a.halo_len[s] == kOverflow) continue;
+          for (int ci = 0; ci < BF_STAGES; ++ci) {
+            const int k = cells[ci] == BF_ZERO ? cells[0] : cells[ci];
+            const uint32_t ws = w_it % NSW;
+            mbar_wait_sleep(bar(B_W_EMPTY + ws), ((w_it / NSW) & 1) ^ 1);
+            mbar_expect_tx(bar(B_W_FULL + ws), 8192u);
+            bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u, bar(B_W_FULL + ws));
+            ++w_it;
+          }
+        }
+    }
+    __syncwarp();
+  } else if (warp == 5) {
+    // ------------------------------ MMA issuer --------------------------------
+    constexpr uint32_t idesc_d = idesc_bf16(128, 64, false, false);  // B_k x W_k^T
+    constexpr uint32_t idesc_w = idesc_bf16(128, 64, true, true);    // [B_k; B_k']^T x F
+    const uint64_t a_desc0 = sdesc_sw128(s_a, 16, 1024), b_desc0 = sdesc_sw128(s_w, 16, 1024);
+    uint32_t w_it = 0, a_it = 0, t_it = 0, f_it = 0;
+    bool dw_fresh = true;  // the pair accumulators' first MMA (per CTA)
+    for (int w = pair; w < a.n_items; w += npairs)
+      for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+        const uint2 sp = a.sup[s];
+        if (a.halo_len[s] == kOverflow) continue;
+        const bool first = (sp.y & SUP_FIRST) != 0, last = (sp.y & SUP_LAST) != 0;
+        // single-buffered input-gradient accumulator: the previous item drained
+        if (first) mbar_wait(bar(B_T_EMPTY), (t_it & 1) ^ 1);
+        const uint32_t fs = f_it % NSF;
+        mbar_wait(bar(B_F_FULL + fs), (f_it / NSF) & 1);
+        tc_fence_after();
+        for (int ci = 0; ci < BF_STAGES; ++ci) {
+          const uint32_t ws = w_it % NSW;
+          mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
+          const uint32_t st = a_it + static_cast<uint32_t>(ci);
+          const uint32_t as = st % NSA;
+          mbar_wait(bar(B_A_FULL + as), (st / NSA) & 1);
+          tc_fence_after();
+          const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
+          const uint64_t bd = b_desc0 + ((ws * 8192u) >> 4);
+          if (elect_one()) {
+            if (cells[ci] != BF_ZERO) {
+#pragma unroll
+              for (int ks = 0; ks < 4; ++ks)
+                umma_bf16(tmem, ad + 2u * ks, bd + 2u * ks, idesc_d, (!first || ci > 0 || ks > 0) ? 1u : 0u);
+            }
+            umma_commit(bar(B_W_EMPTY + ws));
+            if (ci & 1) {  // the pair (ci - 1, ci): adjacent A slots, M = 128
+              const uint32_t as0 = as - 1;
+              const uint32_t d = tmem + 64u + 64u * static_cast<uint32_t>(ci >> 1);
+#pragma unroll
+              for (int ks = 0; ks < 8; ++ks) {  // K = tile rows, 16 per step
+                const uint64_t ada = sdesc_sw128(s_a + as0 * 16384u + 2048u * ks, 16384, 1024);
+                const uint64_t bdf = sdesc_sw128(s_f + fs * 16384u + 2048u * ks, 16384, 1024);
+                umma_bf16(d, ada, bdf, idesc_w, (dw_fresh && ks == 0) ? 0u : 1u);
+              }
+              umma_commit(bar(B_A_EMPTY + as0));
+              umma_commit(bar(B_A_EMPTY + as));
+            }
+          }
+          __syncwarp();
+          ++w_it;
+        }
+        a_it += BF_STAGES;
+        dw_fresh = false;
+        if (elect_one()) umma_commit(bar(B_F_EMPTY + fs));
+        __syncwarp();
+        ++f_it;
+        if (!last) continue;
+        if (elect_one()) umma_commit(bar(B_T_FULL));
+        __syncwarp();
+        mbar_wait(bar(B_T_FULL), t_it & 1);
+        named_bar_arrive(2, 32 * 5);  // hand the accumulator to the epilogue
+        ++t_it;
+      }
+    if (elect_one()) umma_commit(bar(B_MMA_DONE));
+    __syncwarp();
+  } else if (warp >= FWD_AGG_WARP0) {
+    // ------------------------------ aggregation --------------------------------
+    const int aw = warp - FWD_AGG_WARP0;
+    const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
+    uint32_t a_it = 0;
+    for (int w = pair; w < a.n_items; w += npairs)
+      for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+        const uint32_t H = a.halo_len[s];
+        if (H == kOverflow) continue;
+        named_bar_sync(1, 32 * FWD_AGG_WARPS);
+        coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat, s_halo,
+                                           32 * aw + lane, CH);
+        named_bar_sync(1, 32 * FWD_AGG_WARPS);
+        const uint32_t first = a_it + ((static_cast<uint32_t>(grp) - a_it) & (AGG_GROUPS - 1));
+        for (uint32_t j = first; j < a_it + BF_STAGES; j += AGG_GROUPS) {
+          const uint32_t ds = j % NSD, as = j % NSA;
+          mbar_wait(bar(B_D_FULL + ds), (j / NSD) & 1);
+          auto wait_a = [&] { mbar_wait(bar(B_A_EMPTY + as), ((j / NSA) & 1) ^ 1); };
+          if (cells[j - a_it] == BF_ZERO) {  // zero A tile (the odd half's padding stage)
+            wait_a();
+            const uint32_t dst = s_a + as * 16384u + static_cast<uint32_t>(wig) * 4096u;
+            for (int x = lane; x < 256; x += 32) sts128(dst + 16u * x, make_uint4(0, 0, 0, 0));
+          } else {
+            const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
+            const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
+            if (src == kFitsSlot) {
+              aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
+                                               s_a + as * 16384u, wig, lane, wait_a);
+            } else {
+              wait_a();
+              aggregate_stage_l2<AGG_GROUP_WARPS>(
+                  slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512), s_halo,
+                  s_a + as * 16384u, wig, lane);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            mbar_arrive(bar(B_A_FULL + as));
+            mbar_arrive(bar(B_D_EMPTY + ds));
+          }
+        }
+        a_it += BF_STAGES;
+      }
+  } else {
+    // ----------------- warps 0-3: F tiles, input-gradient drains, dW dump -------
+    const int e = warp;
+    uint32_t f_it = 0;
+    int pend_s = -1;  // the item (its last record) whose accumulator is to be drained next
+    auto load_f = [&](int s) {
+      const uint32_t fs = f_it % NSF;
+      mbar_wait(bar(B_F_EMPTY + fs), ((f_it / NSF) & 1) ^ 1);
+      const uint2 tl = a.tiles[a.sup[s].x];
+      const uint32_t ft = s_f + fs * 16384u;
+#pragma unroll 8
+      for (int x = lane; x < 32 * 8; x += 32) {  // rows 32e..32e+31, 8 chunks of 16 B
+        const int r = 32 * e + (x >> 3), q = x & 7;
+        const bool in = static_cast<uint32_t>(r) < tl.y;
+        const int64_t row = static_cast<int64_t>(tl.x) + (in ? r : 0);
+        cp_async16_zfill(ft + r * 128 + (((q ^ (r & 7)) & 7) << 4),
+                         reinterpret_cast<const uint4*>(a.fimg + row * CH) + q, in ? 16u : 0u);
+      }
+      cp_async_wait_all();
+      fence_proxy_async_smem();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(B_F_FULL + fs));
+      ++f_it;
+    };
+    auto drain = [&](int s) {
+      named_bar_sync(2, 32 * 5);  // released by the MMA warp once the item's T_FULL landed
+      tc_fence_after();
+      const uint2 tl = a.tiles[a.sup[s].x];
+      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16);
+      const bool in = static_cast<uint32_t>(32 * e + lane) < tl.y;
+      float4* o = in ? reinterpret_cast<float4*>(
+                           a.gin + static_cast<int64_t>(a.perm_rows[static_cast<int64_t>(tl.x) + 32 * e + lane]) *
+                                       a.gin_cols)
+                     : nullptr;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t v[16];
+        tmem_ld16(t0 + 16 * q, v);
+        tmem_ld_wait();
+        if (o && q * 16 < a.gin_cols)
+#pragma unroll
+          for (int x = 0; x < 4; ++x)
+            atomicAdd(o + q * 4 + x, make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                                 __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3])));
+      }
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(B_T_EMPTY));
+    };
+    for (int w = pair; w < a.n_items; w += npairs) {
+      int nrec = 0, last_s = -1;
+      for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
+        if (a.halo_len[s] == kOverflow) continue;
+        if (nrec == 2 && pend_s >= 0) {  // free the accumulator before the F ring blocks
+          drain(pend_s);
+          pend_s = -1;
+        }
+        load_f(s);
+        ++nrec;
+        last_s = s;
+      }
+      if (last_s < 0) continue;
+      if (pend_s >= 0) drain(pend_s);
+      pend_s = last_s;
+    }
+    if (pend_s >= 0) drain(pend_s);
+    // dW: lanes 32e.. of pair p are m rows of cell stages 2p (e < 2) / 2p + 1 (e >= 2)
+    mbar_wait_sleep(bar(B_MMA_DONE), 0);
+    tc_fence_after();
+    const bool none = f_it == 0;  // no records at all: the pair accumulators were never written
+    for (int p = 0; p < BF_STAGES / 2; ++p) {
+      const int k = cells[2 * p + (e >> 1)];
+      if (k == BF_ZERO) continue;
+      const int m = 32 * (e & 1) + lane;
+      float4* o = reinterpret_cast<float4*>(a.partial + ((static_cast<int64_t>(pair) * K + k) * 64 + m) * 64);
+      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + 64u + 64u * p;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t v[16];
+        tmem_ld16(t0 + 16 * q, v);
+        tmem_ld_wait();
+#pragma unroll
+        for (int x = 0; x < 4; ++x)
+          o[q * 4 + x] = none ? make_float4(0.f, 0.f, 0.f, 0.f)
+                              : make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                            __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  if (warp == 5) tmem_free<512>(tmem);
+}
+
+// grad_w[k][m][c] = sum over pairs (fixed order) of partial[x][k][m][c] (64 x 64 padded)
+__global__ void k_wgrad_reduce_mc(const float* __restrict__ partial, int n_part, int K, int cin, int cout,
+                                  float* __restrict__ grad_w) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (idx >= static_cast<int64_t>(K) * cin * cout) return;
+  const int k = static_cast<int>(idx / (cin * cout)), m = static_cast<int>((idx / cin) % cout),
+            c = static_cast<int>(idx % cin);
+  float s = 0.f;
+  for (int x = 0; x < n_part; ++x) s += partial[((static_cast<int64_t>(x) * K + k) * 64 + m) * 64 + c];
+  grad_w[idx] = s;
+}
+
+// ===========================================================================
 // gather engine (forward / dgrad): A tiles assembled by TMA tile::gather4
 // ===========================================================================
 // A stage (128-row sub-tile t, cell k) needs A_k[r] = sum of the bf16 feature
@@ -2731,13 +3121,19 @@ static bool use_gather_engine(int64_t K) { return use_gather_engine_env() && K <
 static GatherPlan* gplan_fwd(npcg_context* ctx, npcg_neighbors* nb);
 static GatherPlan* gplan_bwd(npcg_context* ctx, npcg_neighbors* nb);
 
-void tc_prepare(npcg_context* ctx, npcg_neighbors* nb) {
+static bool fused_bwd_enabled();
+// The plans a 64-channel layer's forward + backward use in `mode`: the
+// forward plan, and the transposed plan of the fused backward (bf16, K = 27:
+// 128-row super-tiles) or of the separate dgrad.
+void tc_prepare(npcg_context* ctx, npcg_neighbors* nb, TcMode mode) {
   if (use_gather_engine(nb->n_kernels)) {
     gplan_fwd(ctx, nb);
     gplan_bwd(ctx, nb);
   }
   plan_fwd(ctx, nb);
-  plan_bwd(ctx, nb);
+  const bool fused = mode == TcMode::bf16 && nb->n_kernels == 27 && fused_bwd_enabled() &&
+                     !use_gather_engine(nb->n_kernels);
+  plan_bwd(ctx, nb, fused);
 }
 
 // bf16 image of C-channel rows, padded with zero channels to CP = tc_pad(C)
@@ -2988,24 +3384,30 @@ static void launch_wgrad(npcg_context* ctx, const WgArgs& a, int hcap, dim3 grid
          a);
 }
 
+// Exact weight gradient of the rows a plan left to the exact engine (vvor
+// over their triplets).  transposed: the plan's rows are input points j (the
+// fused backward's plan over the transposed structure).
 static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, const float* fin,
-                        const float* gout, float* grad_w, bool accumulate, int cin, int cout) {
+                        const float* gout, float* grad_w, bool accumulate, int cin, int cout,
+                        bool transposed = false) {
   const int K = static_cast<int>(nb->n_kernels);
+  const int64_t* rp = transposed ? nb->tcsr->row_ptr.get() : nb->row_ptr.get();
+  const uint32_t* cc = transposed ? nb->tcsr->col.get() : nb->col_j.get();
+  const uint32_t* ck = transposed ? nb->tcsr->k.get() : nb->col_k.get();
+  const uint32_t* perm = transposed ? nb->perm_in.get() : nb->perm_out.get();
   DevBuf<int64_t> len(ctx, P->n_spill + 1), off(ctx, P->n_spill + 1);
   NPCG_CUDA(cudaMemsetAsync(len.get(), 0, (P->n_spill + 1) * 8, ctx->stream));
   launch(ctx, "spill_lens", k_row_lens, dim3(static_cast<unsigned>(ceil_div(P->n_spill, 256))),
-         dim3(256), 0, static_cast<const int64_t*>(nb->row_ptr.get()),
-         static_cast<const uint32_t*>(nb->perm_out.get()),
-         static_cast<const uint32_t*>(P->spill_rows.get()), P->n_spill, len.get());
+         dim3(256), 0, rp, perm, static_cast<const uint32_t*>(P->spill_rows.get()), P->n_spill, len.get());
   int64_t total = 0;
   exclusive_scan_i64(ctx, len.get(), off.get(), P->n_spill + 1, &total);
   DevBuf<uint32_t> ti(ctx, total), tj(ctx, total), tk(ctx, total);
+  // (row, col, k) -> (i, j, k), rows are j when transposed
   launch(ctx, "spill_gather", k_gather_rows_triplets,
-         dim3(static_cast<unsigned>(ceil_div(P->n_spill * 32, 256))), dim3(256), 0,
-         static_cast<const int64_t*>(nb->row_ptr.get()), static_cast<const uint32_t*>(nb->col_j.get()),
-         static_cast<const uint32_t*>(nb->col_k.get()), static_cast<const uint32_t*>(nb->perm_out.get()),
+         dim3(static_cast<unsigned>(ceil_div(P->n_spill * 32, 256))), dim3(256), 0, rp, cc, ck, perm,
          static_cast<const uint32_t*>(P->spill_rows.get()), P->n_spill,
-         static_cast<const int64_t*>(off.get()), ti.get(), tj.get(), tk.get());
+         static_cast<const int64_t*>(off.get()), transposed ? tj.get() : ti.get(),
+         transposed ? ti.get() : tj.get(), tk.get());
   npcg_triplets T{ti.get(), tj.get(), tk.get(), total, nb->n_out, nb->n_in, K, 0};
   CellPlan cells;
   cells_from_triplets(ctx, &T, K, &cells);
@@ -3020,6 +3422,57 @@ static void wgrad_spill(npcg_context* ctx, npcg_neighbors* nb, TcDirPlan* P, con
          dim3(256), 0, grad_w, static_cast<const float*>(tmp.get()), nw);
 }
 
+// The fused backward (one aggregation for dgrad + wgrad) serves the bf16
+// path at K = 27, C_in, C_out <= 64; NPCG_FUSED_BWD=0 disables it (A/B).
+static bool fused_bwd_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = std::getenv("NPCG_FUSED_BWD");
+    v = (e && std::strcmp(e, "0") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+static void run_fused_backward(npcg_context* ctx, npcg_neighbors* nb, TcPlan* p, TcDirPlan* P,
+                               float* grad_in, float* grad_w, int cin, int cout) {
+  const int K = static_cast<int>(nb->n_kernels);
+  const int npairs = std::max(1, std::min(P->n_items, ctx->num_sms / 2));
+  const int64_t need = static_cast<int64_t>(npairs) * K * 64 * 64;
+  if (p->partial.size() < need) p->partial.alloc(ctx, need);
+  NPCG_CUDA(cudaMemsetAsync(grad_in, 0, nb->n_in * cin * sizeof(float), ctx->stream));
+  BfArgs a{};
+  a.halo = P->halo.get();
+  a.halo_len = P->halo_len.get();
+  a.blk_off = P->blk_off.get();
+  a.blocks = P->blocks.get();
+  a.perm_rows = nb->perm_in.get();
+  a.sup = P->sup.get();
+  a.tiles = P->tiles.get();
+  a.item_start = P->item_start.get();
+  a.n_items = P->n_items;
+  a.hcap = P->hcap;
+  a.K = K;
+  a.feat = p->feat_out.get();
+  a.fimg = p->feat_in.get();
+  a.wpack = p->wpack.get();
+  a.gin = grad_in;
+  a.gin_cols = cin;
+  a.partial = p->partial.get();
+  // the two halves of the cells, load-balanced like the weight gradient's runs
+  // (7 pairs each); the 13-cell half is padded with a zero stage
+  uint8_t korder[KMAX];
+  wgrad_cell_order(P, K, BF_STAGES / 2, 2, korder);
+  for (int x = 0; x < 2 * BF_STAGES; ++x) a.cells[x] = x < K ? korder[x] : BF_ZERO;
+  const BfSmem L = bf_smem_layout(P->hcap);
+  auto kern = P->big_blocks ? k_conv_bwd_fused<true> : k_conv_bwd_fused<false>;
+  NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(L.total)));
+  launch_cluster(ctx, "conv_bwd_fused", kern, dim3(2 * npairs), dim3(FWD_THREADS), L.total, 2, a);
+  const int64_t nw = static_cast<int64_t>(K) * cin * cout;
+  launch(ctx, "wgrad_reduce", k_wgrad_reduce_mc, dim3(static_cast<unsigned>(ceil_div(nw, 256))), dim3(256),
+         0, static_cast<const float*>(p->partial.get()), npairs, K, cin, cout, grad_w);
+}
+
 void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
                  const float* fin, const float* gout, float* grad_in, float* grad_w, int cin,
                  int cout, bool fin_unchanged) {
@@ -3032,6 +3485,28 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float
     else convert(ctx, gout, nb->perm_out.get(), nb->n_out, p->feat_out, cout);
     g_converted = true;
   };
+  if (!split && grad_in && grad_w && K == 27 && tc_pad(cin) == CH && tc_pad(cout) == CH &&
+      fused_bwd_enabled() && !use_gather_engine(nb->n_kernels)) {
+    // one aggregation pass feeds both gradients (over 128-row super-tiles)
+    TcDirPlan* P = plan_bwd(ctx, nb, true);
+    if (!fin_unchanged || fin != p->saved_fin || cin != p->saved_c || p->saved_split)
+      input_image(ctx, nb, p, fin, cin, false);
+    g_image();
+    pack_w(ctx, p, w, K, true, cin, cout);
+    if (P->n_overflow < P->n_super) {
+      run_fused_backward(ctx, nb, p, P, grad_in, grad_w, cin, cout);
+    } else {
+      NPCG_CUDA(cudaMemsetAsync(grad_w, 0, static_cast<int64_t>(K) * cin * cout * 4, ctx->stream));
+    }
+    if (P->n_spill) {  // rows beyond the tile capacities: exact engines on those rows
+      DevBuf<float> wt(ctx, static_cast<int64_t>(K) * cin * cout);
+      transpose_w<float>(ctx, w, K, cin, cout, wt.get());
+      mvmr_rows_subset_f32(ctx, nb->tcsr->view(), nb->perm_in.get(), P->spill_rows.get(), P->n_spill,
+                           wt.get(), gout, cout, cin, grad_in);
+      wgrad_spill(ctx, nb, P, fin, gout, grad_w, true, cin, cout, true);
+    }
+    return;
+  }
   if (grad_in && !split && use_gather_engine(nb->n_kernels) && cin == CH && cout == CH) {
     GatherPlan* G = gplan_bwd(ctx, nb);
     if (G->n_overflow < G->n_super) {
@@ -3191,9 +3666,14 @@ void tc_trace_forward(npcg_context* ctx, npcg_neighbors* nb, const float* w, con
 
 // plan statistics for the bench / tests: [n_super, n_overflow, max_halo, mean_halo*100] x 3 dirs
 void tc_plan_stats(npcg_context* ctx, npcg_neighbors* nb, int64_t* out12) {
-  tc_prepare(ctx, nb);
+  // the plans of the 64-channel bf16 passes: forward, and dgrad / wgrad (the
+  // fused backward's 128-row transposed plan at K = 27, else the transposed
+  // plan of the dgrad and the forward plan of the wgrad)
+  tc_prepare(ctx, nb, TcMode::bf16);
   TcPlan* p = nb->tc.get();
-  const TcDirPlan* ds[3] = {p->fwd.get(), p->bwd.get(), p->fwd.get()};  // wgrad runs on the forward plan
+  const bool fused = p->bwd1 && nb->n_kernels == 27 && fused_bwd_enabled();
+  const TcDirPlan* ds[3] = {p->fwd.get(), fused ? p->bwd1.get() : p->bwd.get(),
+                            fused ? p->bwd1.get() : p->fwd.get()};  // wgrad runs on the forward plan
   for (int i = 0; i < 3; ++i) {
     out12[4 * i + 0] = ds[i]->n_super;
     out12[4 * i + 1] = ds[i]->n_spill;

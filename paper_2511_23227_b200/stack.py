@@ -30,7 +30,10 @@ class ConvStack:
     """Layers l = 0..L-1 with weights (K, G, C_l, C_{l+1}) sharing one geometry."""
 
     def __init__(self, weights: list[torch.Tensor], geometry: npc.ConvGeometry,
-                 config: npc.ExecConfig = npc.ExecConfig()):
+                 config: npc.ExecConfig = npc.ExecConfig(), comm=None):
+        """comm: a shard.DwComm (data-parallel training over whole clouds,
+        SURVEY.md §8e): each layer's weight gradient is summed over ranks on a
+        side stream while the next (lower) layer's backward runs."""
         if not weights:
             raise npc.ShapeError("ConvStack: no layers")
         for a, b in zip(weights, weights[1:]):
@@ -47,6 +50,8 @@ class ConvStack:
         self._key = None
         self._acts: list[torch.Tensor] = []
         self._graph = None
+        self.comm = comm
+        self._comm_stream = None
 
     # -- shared cache (conv_op.hpp:106-127, one build for all layers) ----------
     def neighbors(self, cloud: npc.PointCloud) -> npc.Neighbors:
@@ -73,11 +78,25 @@ class ConvStack:
             raise npc.StateError("ConvStack::backward: no cached forward inputs")
         g = gout.contiguous()
         gws = [None] * len(self.ops)
+        main = torch.cuda.current_stream()
+        if self.comm is not None and self._comm_stream is None:
+            self._comm_stream = torch.cuda.Stream(device=main.device)
         for l in range(len(self.ops) - 1, -1, -1):
             # activations are the stack's own buffers, unmodified since the forward
             g, gws[l] = npc.conv_backward(self._nb, self.ops[l].weights(), self._acts[l], g,
                                           self.config, need_in=True, need_w=True,
                                           fin_unchanged=True)
+            if self.comm is not None:
+                # layer l's dW all-reduce overlaps layer l-1's backward (the one
+                # exchange of data-parallel training)
+                side = self._comm_stream
+                side.wait_stream(main)
+                gws[l].record_stream(side)
+                with torch.cuda.stream(side):
+                    self.comm.allreduce(gws[l])
+        if self.comm is not None:
+            main.wait_stream(self._comm_stream)
+            npc.context(main.device).bind()  # the library context back on this stream
         return StackGrads(g, gws)
 
     # -- CUDA graph of one forward + backward step ------------------------------

@@ -156,8 +156,21 @@ def _emulate_tc(ti, tj, tk, n_out, n_in, w, f, g):
     np.add.at(B, (tj[o], tk[o]), gb[ti[o]])
     B = _bf16(B.reshape(-1, co)).reshape(n_in, K, co).astype(np.float64)
     gin = np.einsum("nkm,kcm->nc", B, wb)
-    gw = np.einsum("nm,nkc->kmc", gb.astype(np.float64), A)
+    if _fused_backward(K, ci, co):
+        # the fused backward (one aggregation for both gradients): dW_k =
+        # sum_j bf16(B_k[j]) (x) bf16(F_in[j])  (vvor.hpp:79-84)
+        gw = np.einsum("nkm,nc->kmc", B, fb.astype(np.float64))
+    else:
+        gw = np.einsum("nm,nkc->kmc", gb.astype(np.float64), A)
     return fout, gin, gw
+
+
+def _fused_backward(K, ci, co):
+    """Whether the library's bf16 backward runs the fused kernel (both
+    gradients, K = 27, C_in, C_out <= 64; NPCG_FUSED_BWD=0 turns it off)."""
+    import os
+    return (K == 27 and ci <= 64 and co <= 64 and os.environ.get("NPCG_FUSED_BWD", "1") != "0"
+            and os.environ.get("NPCG_TC_ENGINE", "halo") != "gather")
 
 
 def _bf16_case(npc, orc, n, seed=1):
