@@ -1116,14 +1116,28 @@ __device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t 
 }
 // Cooperative halo load by the aggregation warps: 16-byte cp.async per lane,
 // 8 lanes per 128-byte row (coalesced within runs of consecutive rows).
+// The row indices of a batch are loaded first (independent loads in flight),
+// then the batch's copies are issued.
 template <int NT>
 __device__ __forceinline__ void coop_load_halo(const uint32_t* rows, uint32_t H,
                                                const __nv_bfloat16* feat, uint32_t s_halo,
                                                int t, int64_t stride = CH) {
+  constexpr uint32_t STEP = NT / 8, B = 8;
   const uint32_t q = static_cast<uint32_t>(t & 7);
-  for (uint32_t h = static_cast<uint32_t>(t) >> 3; h < H; h += NT / 8)
-    cp_async16(s_halo + h * 128u + q * 16u,
-               reinterpret_cast<const uint8_t*>(feat + static_cast<int64_t>(rows[h]) * stride) + q * 16u);
+  const uint8_t* base = reinterpret_cast<const uint8_t*>(feat) + q * 16u;
+  for (uint32_t h0 = static_cast<uint32_t>(t) >> 3; h0 < H; h0 += B * STEP) {
+    uint32_t r[B];
+#pragma unroll
+    for (uint32_t x = 0; x < B; ++x) {
+      const uint32_t h = h0 + x * STEP;
+      r[x] = h < H ? __ldg(rows + h) : 0u;
+    }
+#pragma unroll
+    for (uint32_t x = 0; x < B; ++x) {
+      const uint32_t h = h0 + x * STEP;
+      if (h < H) cp_async16(s_halo + h * 128u + q * 16u, base + static_cast<int64_t>(r[x]) * stride * 2);
+    }
+  }
   cp_async_wait_all();
 }
 // Entries of a staged block are in the slot, or in global memory (L2) when
@@ -2076,16 +2090,19 @@ __global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_pa
 //                                          stacked to M = 128 as an MN-major A
 //                                          operand, the tile's dense F_in rows as
 //                                          the MN-major B operand, K = 128 rows)
-// dW of 27 cells (442 KB fp32) exceeds one SM's TMEM, so the two CTAs of a
-// cluster take the same super-tiles and half of the cells each (14, and 13 + a
-// zero stage, so every pair of stages is two adjacent A slots); each keeps 7
-// pair accumulators (448 columns) + the 64-column input-gradient accumulator.
+// (the weight-gradient MMA is M = 64: its accumulator takes lanes 0-15 of each
+// 32-lane TMEM quadrant, or lanes 16-31 with a lane offset of 16 in the D
+// address -- tools/micro/mma_m64.cu -- so two cells share 64 columns and every
+// stage's MMAs release its A slot at once).  dW of 27 cells (442 KB fp32)
+// exceeds one SM's TMEM, so the two CTAs of a cluster take the same
+// super-tiles and half of the cells each (14 / 13); each keeps 7 column blocks
+// of two cells (448 columns) + the 64-column input-gradient accumulator.
 // The two halves' input-gradient sums meet in global memory: grad_in is zeroed
 // and each CTA adds its sum once (0 + a + b == 0 + b + a in fp32:
 // deterministic).  Per-pair dW partials are reduced in a fixed order.
 // ===========================================================================
-constexpr int BF_STAGES = 14;      // stages per record and CTA (a half of the 27 cells + padding)
-constexpr uint8_t BF_ZERO = 0xFF;  // the padding stage: a zero A tile
+constexpr int BF_STAGES = 14;      // at most this many stages (cells) per record and CTA
+constexpr uint8_t BF_ZERO = 0xFF;  // no cell (the 13-cell half's 14th entry)
 constexpr int NSF = 2;             // F tiles (16 KB: 128 rows x 64 channels, SW128)
 enum : int { B_F_FULL = B_COUNT, B_F_EMPTY = B_F_FULL + NSF, B_MMA_DONE = B_F_EMPTY + NSF,
              BF_B_COUNT = B_MMA_DONE + 1 };
@@ -2107,7 +2124,7 @@ struct BfArgs {
   float* gin;                 // (n_in, cin) original order, zeroed by the host
   int gin_cols;               // cin
   float* partial;             // [pairs][K][64 m][64 c]
-  uint8_t cells[2 * BF_STAGES];  // per half: stage -> cell (BF_ZERO: the zero stage)
+  uint8_t cells[2 * BF_STAGES];  // per half: stage -> cell (BF_ZERO: none)
 };
 
 struct BfSmem {
@@ -2164,6 +2181,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
   const int half = static_cast<int>(cluster_ctarank());
   const int pair = blockIdx.x >> 1, npairs = gridDim.x >> 1;
   const uint8_t* cells = a.cells + half * BF_STAGES;
+  int nst = 0;  // stages per record of this half
+  while (nst < BF_STAGES && cells[nst] != BF_ZERO) ++nst;
   const int K = a.K;
   if (threadIdx.x == 0) {
     mbar_init(bar(B_HALO_FULL), 1);
@@ -2208,11 +2227,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         const int64_t ob = static_cast<int64_t>(sp.x) * K;
         for (int x = lane; x <= K; x += 32) offs[x] = a.blk_off[ob + x];
         __syncwarp();
-        for (int ci = 0; ci < BF_STAGES; ++ci) {
+        for (int ci = 0; ci < nst; ++ci) {
           if (lane == 0) {
             const uint32_t ds = d_it % NSD;
             mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
-            const int k = cells[ci] == BF_ZERO ? cells[0] : cells[ci];  // (the zero stage's is unused)
+            const int k = cells[ci];
             const uint32_t o0 = offs[k], o1 = offs[k + 1];
             const uint32_t nb = min((o1 - o0) << 4, static_cast<uint32_t>(BLOCK_MAX_BYTES));
             if (BIG) dsrc[ds] = (o1 - o0) << 4 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
@@ -2230,8 +2249,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
       for (int w = pair; w < a.n_items; w += npairs)
         for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
           if (a.halo_len[s] == kOverflow) continue;
-          for (int ci = 0; ci < BF_STAGES; ++ci) {
-            const int k = cells[ci] == BF_ZERO ? cells[0] : cells[ci];
+          for (int ci = 0; ci < nst; ++ci) {
+            const int k = cells[ci];
             const uint32_t ws = w_it % NSW;
             mbar_wait_sleep(bar(B_W_EMPTY + ws), ((w_it / NSW) & 1) ^ 1);
             mbar_expect_tx(bar(B_W_FULL + ws), 8192u);
@@ -2244,7 +2263,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
   } else if (warp == 5) {
     // ------------------------------ MMA issuer --------------------------------
     constexpr uint32_t idesc_d = idesc_bf16(128, 64, false, false);  // B_k x W_k^T
-    constexpr uint32_t idesc_w = idesc_bf16(128, 64, true, true);    // [B_k; B_k']^T x F
+    constexpr uint32_t idesc_w = idesc_bf16(64, 64, true, true);     // B_k^T x F (M = 64)
     const uint64_t a_desc0 = sdesc_sw128(s_a, 16, 1024), b_desc0 = sdesc_sw128(s_w, 16, 1024);
     uint32_t w_it = 0, a_it = 0, t_it = 0, f_it = 0;
     bool dw_fresh = true;  // the pair accumulators' first MMA (per CTA)
@@ -2258,7 +2277,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         const uint32_t fs = f_it % NSF;
         mbar_wait(bar(B_F_FULL + fs), (f_it / NSF) & 1);
         tc_fence_after();
-        for (int ci = 0; ci < BF_STAGES; ++ci) {
+        for (int ci = 0; ci < nst; ++ci) {
           const uint32_t ws = w_it % NSW;
           mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
           const uint32_t st = a_it + static_cast<uint32_t>(ci);
@@ -2267,30 +2286,25 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
           tc_fence_after();
           const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
           const uint64_t bd = b_desc0 + ((ws * 8192u) >> 4);
+          // cell stage ci: column block ci / 2, lanes 0-15 / 16-31 of each quadrant
+          const uint32_t dw = tmem + 64u + 64u * static_cast<uint32_t>(ci >> 1) + ((ci & 1) ? (16u << 16) : 0u);
           if (elect_one()) {
-            if (cells[ci] != BF_ZERO) {
 #pragma unroll
-              for (int ks = 0; ks < 4; ++ks)
-                umma_bf16(tmem, ad + 2u * ks, bd + 2u * ks, idesc_d, (!first || ci > 0 || ks > 0) ? 1u : 0u);
-            }
+            for (int ks = 0; ks < 4; ++ks)
+              umma_bf16(tmem, ad + 2u * ks, bd + 2u * ks, idesc_d, (!first || ci > 0 || ks > 0) ? 1u : 0u);
             umma_commit(bar(B_W_EMPTY + ws));
-            if (ci & 1) {  // the pair (ci - 1, ci): adjacent A slots, M = 128
-              const uint32_t as0 = as - 1;
-              const uint32_t d = tmem + 64u + 64u * static_cast<uint32_t>(ci >> 1);
 #pragma unroll
-              for (int ks = 0; ks < 8; ++ks) {  // K = tile rows, 16 per step
-                const uint64_t ada = sdesc_sw128(s_a + as0 * 16384u + 2048u * ks, 16384, 1024);
-                const uint64_t bdf = sdesc_sw128(s_f + fs * 16384u + 2048u * ks, 16384, 1024);
-                umma_bf16(d, ada, bdf, idesc_w, (dw_fresh && ks == 0) ? 0u : 1u);
-              }
-              umma_commit(bar(B_A_EMPTY + as0));
-              umma_commit(bar(B_A_EMPTY + as));
+            for (int ks = 0; ks < 8; ++ks) {  // K = tile rows, 16 per step
+              const uint64_t ada = sdesc_sw128(s_a + as * 16384u + 2048u * ks, 16384, 1024);
+              const uint64_t bdf = sdesc_sw128(s_f + fs * 16384u + 2048u * ks, 16384, 1024);
+              umma_bf16(dw, ada, bdf, idesc_w, (dw_fresh && ks == 0) ? 0u : 1u);
             }
+            umma_commit(bar(B_A_EMPTY + as));
           }
           __syncwarp();
           ++w_it;
         }
-        a_it += BF_STAGES;
+        a_it += static_cast<uint32_t>(nst);
         dw_fresh = false;
         if (elect_one()) umma_commit(bar(B_F_EMPTY + fs));
         __syncwarp();
@@ -2318,26 +2332,20 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
                                            32 * aw + lane, CH);
         named_bar_sync(1, 32 * FWD_AGG_WARPS);
         const uint32_t first = a_it + ((static_cast<uint32_t>(grp) - a_it) & (AGG_GROUPS - 1));
-        for (uint32_t j = first; j < a_it + BF_STAGES; j += AGG_GROUPS) {
+        for (uint32_t j = first; j < a_it + static_cast<uint32_t>(nst); j += AGG_GROUPS) {
           const uint32_t ds = j % NSD, as = j % NSA;
           mbar_wait(bar(B_D_FULL + ds), (j / NSD) & 1);
           auto wait_a = [&] { mbar_wait(bar(B_A_EMPTY + as), ((j / NSA) & 1) ^ 1); };
-          if (cells[j - a_it] == BF_ZERO) {  // zero A tile (the odd half's padding stage)
-            wait_a();
-            const uint32_t dst = s_a + as * 16384u + static_cast<uint32_t>(wig) * 4096u;
-            for (int x = lane; x < 256; x += 32) sts128(dst + 16u * x, make_uint4(0, 0, 0, 0));
+          const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
+          const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
+          if (src == kFitsSlot) {
+            aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
+                                             s_a + as * 16384u, wig, lane, wait_a);
           } else {
-            const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
-            const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
-            if (src == kFitsSlot) {
-              aggregate_stage<AGG_GROUP_WARPS>(slot, reinterpret_cast<const uint16_t*>(slot + 512), s_halo,
-                                               s_a + as * 16384u, wig, lane, wait_a);
-            } else {
-              wait_a();
-              aggregate_stage_l2<AGG_GROUP_WARPS>(
-                  slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512), s_halo,
-                  s_a + as * 16384u, wig, lane);
-            }
+            wait_a();
+            aggregate_stage_l2<AGG_GROUP_WARPS>(
+                slot, reinterpret_cast<const uint16_t*>(a.blocks + blk_bytes(src) + 512), s_halo,
+                s_a + as * 16384u, wig, lane);
           }
           fence_proxy_async_smem();
           __syncwarp();
@@ -2346,7 +2354,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
             mbar_arrive(bar(B_D_EMPTY + ds));
           }
         }
-        a_it += BF_STAGES;
+        a_it += static_cast<uint32_t>(nst);
       }
   } else {
     // ----------------- warps 0-3: F tiles, input-gradient drains, dW dump -------
@@ -2398,6 +2406,12 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
       if (lane == 0) mbar_arrive(bar(B_T_EMPTY));
     };
     for (int w = pair; w < a.n_items; w += npairs) {
+      {  // warm L2 with the next item's halo while this one is aggregated
+        const int s_next = w + npairs < a.n_items ? static_cast<int>(a.item_start[w + npairs]) : -1;
+        if (s_next >= 0 && a.halo_len[s_next] != kOverflow)
+          prefetch_halo_l2<128>(a.halo + static_cast<int64_t>(s_next) * a.hcap, a.halo_len[s_next], a.feat,
+                                32 * e + lane, CH, 1);
+      }
       int nrec = 0, last_s = -1;
       for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
         if (a.halo_len[s] == kOverflow) continue;
@@ -2414,26 +2428,30 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
       pend_s = last_s;
     }
     if (pend_s >= 0) drain(pend_s);
-    // dW: lanes 32e.. of pair p are m rows of cell stages 2p (e < 2) / 2p + 1 (e >= 2)
+    // dW: column block b holds cell stages 2b (lanes 0-15 of each quadrant) and
+    // 2b + 1 (lanes 16-31); quadrant e holds rows m = 16e .. 16e + 15
     mbar_wait_sleep(bar(B_MMA_DONE), 0);
     tc_fence_after();
-    const bool none = f_it == 0;  // no records at all: the pair accumulators were never written
-    for (int p = 0; p < BF_STAGES / 2; ++p) {
-      const int k = cells[2 * p + (e >> 1)];
-      if (k == BF_ZERO) continue;
-      const int m = 32 * (e & 1) + lane;
-      float4* o = reinterpret_cast<float4*>(a.partial + ((static_cast<int64_t>(pair) * K + k) * 64 + m) * 64);
-      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + 64u + 64u * p;
+    const bool none = f_it == 0;  // no records at all: the accumulators were never written
+    for (int b = 0; b < BF_STAGES / 2; ++b) {
+      const int ci = 2 * b + (lane >> 4);
+      const int k = cells[ci];  // (ci < BF_STAGES)
+      const int m = 16 * e + (lane & 15);
+      float4* o = k != BF_ZERO
+                      ? reinterpret_cast<float4*>(a.partial + ((static_cast<int64_t>(pair) * K + k) * 64 + m) * 64)
+                      : nullptr;
+      const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + 64u + 64u * b;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
         uint32_t v[16];
         tmem_ld16(t0 + 16 * q, v);
         tmem_ld_wait();
+        if (o)
 #pragma unroll
-        for (int x = 0; x < 4; ++x)
-          o[q * 4 + x] = none ? make_float4(0.f, 0.f, 0.f, 0.f)
-                              : make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
-                                            __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
+          for (int x = 0; x < 4; ++x)
+            o[q * 4 + x] = none ? make_float4(0.f, 0.f, 0.f, 0.f)
+                                : make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
+                                              __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3]));
       }
     }
   }
