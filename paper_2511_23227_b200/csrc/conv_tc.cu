@@ -2104,9 +2104,36 @@ __global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_pa
 constexpr int BF_STAGES = 14;      // at most this many stages (cells) per record and CTA
 constexpr uint8_t BF_ZERO = 0xFF;  // no cell (the 13-cell half's 14th entry)
 constexpr int NSF = 2;             // F tiles (16 KB: 128 rows x 64 channels, SW128)
-enum : int { B_F_FULL = B_COUNT, B_F_EMPTY = B_F_FULL + NSF, B_MMA_DONE = B_F_EMPTY + NSF,
-             BF_B_COUNT = B_MMA_DONE + 1 };
-static_assert(BF_B_COUNT <= 48, "barrier region");
+// Slot counts of the fused kernel (the M = 64 weight-gradient MMAs need no
+// slot pairing; -DBF_NSA_=.. etc. for A/B builds).
+#ifndef BF_NSA_
+#define BF_NSA_ 4
+#endif
+#ifndef BF_NSW_
+#define BF_NSW_ 3
+#endif
+#ifndef BF_NSD_
+#define BF_NSD_ 8
+#endif
+constexpr int BF_NSA = BF_NSA_, BF_NSW = BF_NSW_, BF_NSD = BF_NSD_;
+static_assert(BF_NSD % AGG_GROUPS == 0, "descriptor slots per group");
+enum : int {
+  BB_HALO_FULL = 0,
+  BB_HALO_EMPTY = 1,
+  BB_A_FULL = 2,
+  BB_A_EMPTY = BB_A_FULL + BF_NSA,
+  BB_W_FULL = BB_A_EMPTY + BF_NSA,
+  BB_W_EMPTY = BB_W_FULL + BF_NSW,
+  BB_D_FULL = BB_W_EMPTY + BF_NSW,
+  BB_D_EMPTY = BB_D_FULL + BF_NSD,
+  BB_T_FULL = BB_D_EMPTY + BF_NSD,
+  BB_T_EMPTY = BB_T_FULL + 1,
+  BB_F_FULL = BB_T_EMPTY + 1,
+  BB_F_EMPTY = BB_F_FULL + NSF,
+  BB_MMA_DONE = BB_F_EMPTY + NSF,
+  BB_COUNT = BB_MMA_DONE + 1
+};
+static_assert(BB_COUNT <= 48, "barrier region");
 
 struct BfArgs {
   const uint32_t* halo;
@@ -2138,13 +2165,13 @@ __host__ __device__ constexpr BfSmem bf_smem_layout(int hcap) {
   o += hcap * 128;
   o = (o + 1023) & ~1023u;
   L.a = o;
-  o += NSA * 16384;
+  o += BF_NSA * 16384;
   L.f = o;
   o += NSF * 16384;
   L.w = o;
-  o += NSW * 8192;
+  o += BF_NSW * 8192;
   L.d = o;
-  o += NSD * BLOCK_MAX_BYTES;
+  o += BF_NSD * BLOCK_MAX_BYTES;
   o = (o + 7) & ~7u;
   L.bar = o;
   o += 48 * 8;
@@ -2185,29 +2212,27 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
   while (nst < BF_STAGES && cells[nst] != BF_ZERO) ++nst;
   const int K = a.K;
   if (threadIdx.x == 0) {
-    mbar_init(bar(B_HALO_FULL), 1);
-    mbar_init(bar(B_HALO_EMPTY), FWD_AGG_WARPS);
-    for (int i = 0; i < NSA; ++i) {
-      mbar_init(bar(B_A_FULL + i), AGG_GROUP_WARPS);
-      mbar_init(bar(B_A_EMPTY + i), 1);
+    mbar_init(bar(BB_HALO_FULL), 1);
+    mbar_init(bar(BB_HALO_EMPTY), FWD_AGG_WARPS);
+    for (int i = 0; i < BF_NSA; ++i) {
+      mbar_init(bar(BB_A_FULL + i), AGG_GROUP_WARPS);
+      mbar_init(bar(BB_A_EMPTY + i), 1);
     }
-    for (int i = 0; i < NSW; ++i) {
-      mbar_init(bar(B_W_FULL + i), 1);
-      mbar_init(bar(B_W_EMPTY + i), 1);
+    for (int i = 0; i < BF_NSW; ++i) {
+      mbar_init(bar(BB_W_FULL + i), 1);
+      mbar_init(bar(BB_W_EMPTY + i), 1);
     }
-    for (int i = 0; i < NSD; ++i) {
-      mbar_init(bar(B_D_FULL + i), 1);
-      mbar_init(bar(B_D_EMPTY + i), AGG_GROUP_WARPS);
+    for (int i = 0; i < BF_NSD; ++i) {
+      mbar_init(bar(BB_D_FULL + i), 1);
+      mbar_init(bar(BB_D_EMPTY + i), AGG_GROUP_WARPS);
     }
-    for (int i = 0; i < 2; ++i) {
-      mbar_init(bar(B_T_FULL + i), 1);
-      mbar_init(bar(B_T_EMPTY + i), 4);
-    }
+    mbar_init(bar(BB_T_FULL), 1);
+    mbar_init(bar(BB_T_EMPTY), 4);
     for (int i = 0; i < NSF; ++i) {
-      mbar_init(bar(B_F_FULL + i), 4);
-      mbar_init(bar(B_F_EMPTY + i), 1);
+      mbar_init(bar(BB_F_FULL + i), 4);
+      mbar_init(bar(BB_F_EMPTY + i), 1);
     }
-    mbar_init(bar(B_MMA_DONE), 1);
+    mbar_init(bar(BB_MMA_DONE), 1);
     fence_barrier_init();
   }
   if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
@@ -2229,14 +2254,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         __syncwarp();
         for (int ci = 0; ci < nst; ++ci) {
           if (lane == 0) {
-            const uint32_t ds = d_it % NSD;
-            mbar_wait(bar(B_D_EMPTY + ds), ((d_it / NSD) & 1) ^ 1);
+            const uint32_t ds = d_it % BF_NSD;
+            mbar_wait(bar(BB_D_EMPTY + ds), ((d_it / BF_NSD) & 1) ^ 1);
             const int k = cells[ci];
             const uint32_t o0 = offs[k], o1 = offs[k + 1];
             const uint32_t nb = min((o1 - o0) << 4, static_cast<uint32_t>(BLOCK_MAX_BYTES));
             if (BIG) dsrc[ds] = (o1 - o0) << 4 > static_cast<uint32_t>(BLOCK_MAX_BYTES) ? o0 : kFitsSlot;
-            mbar_expect_tx(bar(B_D_FULL + ds), nb);
-            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + blk_bytes(o0), nb, bar(B_D_FULL + ds));
+            mbar_expect_tx(bar(BB_D_FULL + ds), nb);
+            bulk_g2s(s_d + ds * BLOCK_MAX_BYTES, a.blocks + blk_bytes(o0), nb, bar(BB_D_FULL + ds));
           }
           ++d_it;
         }
@@ -2251,10 +2276,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
           if (a.halo_len[s] == kOverflow) continue;
           for (int ci = 0; ci < nst; ++ci) {
             const int k = cells[ci];
-            const uint32_t ws = w_it % NSW;
-            mbar_wait_sleep(bar(B_W_EMPTY + ws), ((w_it / NSW) & 1) ^ 1);
-            mbar_expect_tx(bar(B_W_FULL + ws), 8192u);
-            bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u, bar(B_W_FULL + ws));
+            const uint32_t ws = w_it % BF_NSW;
+            mbar_wait_sleep(bar(BB_W_EMPTY + ws), ((w_it / BF_NSW) & 1) ^ 1);
+            mbar_expect_tx(bar(BB_W_FULL + ws), 8192u);
+            bulk_g2s(s_w + ws * 8192u, a.wpack + static_cast<int64_t>(k) * 8192, 8192u, bar(BB_W_FULL + ws));
             ++w_it;
           }
         }
@@ -2273,16 +2298,16 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         if (a.halo_len[s] == kOverflow) continue;
         const bool first = (sp.y & SUP_FIRST) != 0, last = (sp.y & SUP_LAST) != 0;
         // single-buffered input-gradient accumulator: the previous item drained
-        if (first) mbar_wait(bar(B_T_EMPTY), (t_it & 1) ^ 1);
+        if (first) mbar_wait(bar(BB_T_EMPTY), (t_it & 1) ^ 1);
         const uint32_t fs = f_it % NSF;
-        mbar_wait(bar(B_F_FULL + fs), (f_it / NSF) & 1);
+        mbar_wait(bar(BB_F_FULL + fs), (f_it / NSF) & 1);
         tc_fence_after();
         for (int ci = 0; ci < nst; ++ci) {
-          const uint32_t ws = w_it % NSW;
-          mbar_wait(bar(B_W_FULL + ws), (w_it / NSW) & 1);
+          const uint32_t ws = w_it % BF_NSW;
+          mbar_wait(bar(BB_W_FULL + ws), (w_it / BF_NSW) & 1);
           const uint32_t st = a_it + static_cast<uint32_t>(ci);
-          const uint32_t as = st % NSA;
-          mbar_wait(bar(B_A_FULL + as), (st / NSA) & 1);
+          const uint32_t as = st % BF_NSA;
+          mbar_wait(bar(BB_A_FULL + as), (st / BF_NSA) & 1);
           tc_fence_after();
           const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
           const uint64_t bd = b_desc0 + ((ws * 8192u) >> 4);
@@ -2292,31 +2317,31 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
               umma_bf16(tmem, ad + 2u * ks, bd + 2u * ks, idesc_d, (!first || ci > 0 || ks > 0) ? 1u : 0u);
-            umma_commit(bar(B_W_EMPTY + ws));
+            umma_commit(bar(BB_W_EMPTY + ws));
 #pragma unroll
             for (int ks = 0; ks < 8; ++ks) {  // K = tile rows, 16 per step
               const uint64_t ada = sdesc_sw128(s_a + as * 16384u + 2048u * ks, 16384, 1024);
               const uint64_t bdf = sdesc_sw128(s_f + fs * 16384u + 2048u * ks, 16384, 1024);
               umma_bf16(dw, ada, bdf, idesc_w, (dw_fresh && ks == 0) ? 0u : 1u);
             }
-            umma_commit(bar(B_A_EMPTY + as));
+            umma_commit(bar(BB_A_EMPTY + as));
           }
           __syncwarp();
           ++w_it;
         }
         a_it += static_cast<uint32_t>(nst);
         dw_fresh = false;
-        if (elect_one()) umma_commit(bar(B_F_EMPTY + fs));
+        if (elect_one()) umma_commit(bar(BB_F_EMPTY + fs));
         __syncwarp();
         ++f_it;
         if (!last) continue;
-        if (elect_one()) umma_commit(bar(B_T_FULL));
+        if (elect_one()) umma_commit(bar(BB_T_FULL));
         __syncwarp();
-        mbar_wait(bar(B_T_FULL), t_it & 1);
+        mbar_wait(bar(BB_T_FULL), t_it & 1);
         named_bar_arrive(2, 32 * 5);  // hand the accumulator to the epilogue
         ++t_it;
       }
-    if (elect_one()) umma_commit(bar(B_MMA_DONE));
+    if (elect_one()) umma_commit(bar(BB_MMA_DONE));
     __syncwarp();
   } else if (warp >= FWD_AGG_WARP0) {
     // ------------------------------ aggregation --------------------------------
@@ -2333,9 +2358,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         named_bar_sync(1, 32 * FWD_AGG_WARPS);
         const uint32_t first = a_it + ((static_cast<uint32_t>(grp) - a_it) & (AGG_GROUPS - 1));
         for (uint32_t j = first; j < a_it + static_cast<uint32_t>(nst); j += AGG_GROUPS) {
-          const uint32_t ds = j % NSD, as = j % NSA;
-          mbar_wait(bar(B_D_FULL + ds), (j / NSD) & 1);
-          auto wait_a = [&] { mbar_wait(bar(B_A_EMPTY + as), ((j / NSA) & 1) ^ 1); };
+          const uint32_t ds = j % BF_NSD, as = j % BF_NSA;
+          mbar_wait(bar(BB_D_FULL + ds), (j / BF_NSD) & 1);
+          auto wait_a = [&] { mbar_wait(bar(BB_A_EMPTY + as), ((j / BF_NSA) & 1) ^ 1); };
           const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
           const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
           if (src == kFitsSlot) {
@@ -2350,8 +2375,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            mbar_arrive(bar(B_A_FULL + as));
-            mbar_arrive(bar(B_D_EMPTY + ds));
+            mbar_arrive(bar(BB_A_FULL + as));
+            mbar_arrive(bar(BB_D_EMPTY + ds));
           }
         }
         a_it += static_cast<uint32_t>(nst);
@@ -2363,7 +2388,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
     int pend_s = -1;  // the item (its last record) whose accumulator is to be drained next
     auto load_f = [&](int s) {
       const uint32_t fs = f_it % NSF;
-      mbar_wait(bar(B_F_EMPTY + fs), ((f_it / NSF) & 1) ^ 1);
+      mbar_wait(bar(BB_F_EMPTY + fs), ((f_it / NSF) & 1) ^ 1);
       const uint2 tl = a.tiles[a.sup[s].x];
       const uint32_t ft = s_f + fs * 16384u;
 #pragma unroll 8
@@ -2377,7 +2402,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
       cp_async_wait_all();
       fence_proxy_async_smem();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar(B_F_FULL + fs));
+      if (lane == 0) mbar_arrive(bar(BB_F_FULL + fs));
       ++f_it;
     };
     auto drain = [&](int s) {
@@ -2403,7 +2428,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
       }
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar(B_T_EMPTY));
+      if (lane == 0) mbar_arrive(bar(BB_T_EMPTY));
     };
     for (int w = pair; w < a.n_items; w += npairs) {
       {  // warm L2 with the next item's halo while this one is aggregated
@@ -2430,7 +2455,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
     if (pend_s >= 0) drain(pend_s);
     // dW: column block b holds cell stages 2b (lanes 0-15 of each quadrant) and
     // 2b + 1 (lanes 16-31); quadrant e holds rows m = 16e .. 16e + 15
-    mbar_wait_sleep(bar(B_MMA_DONE), 0);
+    mbar_wait_sleep(bar(BB_MMA_DONE), 0);
     tc_fence_after();
     const bool none = f_it == 0;  // no records at all: the accumulators were never written
     for (int b = 0; b < BF_STAGES / 2; ++b) {
