@@ -50,6 +50,8 @@ constexpr int CH = 64;
 constexpr int KMAX = 128;   // kernel cells (t^3 <= 125: t = 1, 3, 5)
 constexpr int G_KMAX = 32;  // the gather engine's planner keeps per-cell arrays in static smem
 constexpr int MAXE_ST = 16384;         // entries per super-tile the planner sorts in smem
+// (128-row super-tiles: half, so more planner CTAs fit an SM)
+__host__ __device__ constexpr int maxe_of(int st) { return st == 1 ? MAXE_ST / 2 : MAXE_ST; }
 // A (sub-tile, cell) descriptor block: u32 item[128] | u16 entry[E].  Its
 // first BLOCK_MAX_BYTES (items + up to 512 entries) are staged in a shared-
 // memory slot; the entries of larger blocks are read from L2 (global).
@@ -210,7 +212,23 @@ __global__ void __launch_bounds__(TM) k_plan_counts(const int64_t* __restrict__ 
   const uint2 tl = tiles[blockIdx.x];
   const EntryFilter f = EntryFilter::from(tfilter[blockIdx.x]);
   const bool colf = !(f.clo == 0 && f.chi == 0xFFFFFFFFu);
-  if (static_cast<uint32_t>(r) < tl.y) {
+  if (f.all()) {
+    // no filter: every entry counts; a warp walks a row's entries in parallel
+    // (the row / cell counts are u16 pairs updated with 32-bit atomics)
+    const int lane = r & 31, warp = r >> 5;
+    for (int rr = warp; rr < static_cast<int>(tl.y); rr += TM / 32) {
+      const uint32_t i = perm_rows[tl.x + rr];
+      const int64_t e0 = row_ptr[i], e1 = row_ptr[i + 1];
+      for (int64_t e = e0 + lane; e < e1; e += 32) {
+        const uint32_t k = kk[e];
+        const int idx = rr * K + static_cast<int>(k);
+        atomicAdd(reinterpret_cast<unsigned*>(rc) + (idx >> 1), 1u << (16 * (idx & 1)));
+        atomicAdd(&cnt[k], 1u);
+      }
+    }
+    __syncthreads();
+    for (int k = 0; k < K; ++k) inc[r * K + k] = rc[r * K + k];
+  } else if (static_cast<uint32_t>(r) < tl.y) {
     const uint32_t i = perm_rows[tl.x + r];
     for (int64_t e = row_ptr[i]; e < row_ptr[i + 1]; ++e) {
       if (colf) {
@@ -290,8 +308,9 @@ __global__ void __launch_bounds__(512) k_plan_super(
     uint32_t* __restrict__ halo_len, uint32_t* __restrict__ seg,
     uint8_t* __restrict__ blocks) {
   extern __shared__ __align__(16) uint8_t sm[];
-  uint32_t* buf = reinterpret_cast<uint32_t*>(sm);                          // MAXE_ST
-  uint16_t* cnt = reinterpret_cast<uint16_t*>(buf + MAXE_ST);               // st*K*TM
+  const int maxe = maxe_of(st);
+  uint32_t* buf = reinterpret_cast<uint32_t*>(sm);                          // maxe
+  uint16_t* cnt = reinterpret_cast<uint16_t*>(buf + maxe);                  // st*K*TM
   uint16_t* eoff = cnt + st * K * TM;                                        // st*K*TM
   int* rowoff = reinterpret_cast<int*>(eoff + st * K * TM);                  // st*TM + 1
   __shared__ int s_total, s_bad, s_H;
@@ -348,8 +367,19 @@ __global__ void __launch_bounds__(512) k_plan_super(
   __syncthreads();
   const int my_off = incl - len + wsum[warp];
   if (tid < R) rowoff[tid] = my_off;
+  if (tid == 0) rowoff[R] = s_total;
   const int E = s_total;
-  if (E > MAXE_ST) {
+  // records without entry filters (all but the rank / halo-segment splits):
+  // the per-entry passes run warp-cooperatively, a row's entries in parallel
+  __shared__ int s_plain;
+  if (tid == 0) {
+    int pl = 1;
+    for (int g = 0; g < nsub; ++g) pl &= EntryFilter::from(tfilter[sub0 + g]).all() ? 1 : 0;
+    s_plain = pl;
+  }
+  const int nwarps = static_cast<int>(blockDim.x) >> 5;
+  const unsigned lt_mask = (1u << lane) - 1u;
+  if (E > maxe) {
     if (tid == 0) {
       halo_len[s] = kOverflow;
       seg[static_cast<int64_t>(s) * (MAXSEG + 1)] = 0;
@@ -357,7 +387,22 @@ __global__ void __launch_bounds__(512) k_plan_super(
     return;
   }
   // 2. permuted neighbor ids + per-(sub, cell, row) counts
-  if (tid < R && len > 0) {
+  __syncthreads();
+  const bool plain = s_plain != 0;
+  if (plain) {
+    for (int rr = warp; rr < R; rr += nwarps) {
+      const int g = rr / TM, r = rr % TM;
+      const int off = rowoff[rr], n = rowoff[rr + 1] - off;
+      if (n == 0) continue;
+      const int64_t e0 = row_ptr[perm_rows[tiles[sub0 + g].x + r]];
+      for (int b = lane; b < n; b += 32) {
+        const int64_t e = e0 + b;
+        const int idx = (g * K + static_cast<int>(kk[e])) * TM + r;
+        buf[off + b] = inv_perm_cols[col[e]];
+        atomicAdd(reinterpret_cast<unsigned*>(cnt) + (idx >> 1), 1u << (16 * (idx & 1)));
+      }
+    }
+  } else if (tid < R && len > 0) {
     const int g = tid / TM, r = tid % TM;
     int q = 0;
     for_row_entries(row_ptr, kk, col, inv_perm_cols, row_i, filt, [&](int64_t e, int k) {
@@ -365,57 +410,98 @@ __global__ void __launch_bounds__(512) k_plan_super(
       cnt[(g * K + k) * TM + r]++;
     });
   }
-  int P = 1;
-  while (P < E) P <<= 1;
-  for (int x = E + tid; x < P; x += blockDim.x) buf[x] = 0xFFFFFFFFu;
   __syncthreads();
-  // 3. bitonic sort buf[0, P)
-  for (int size = 2; size <= P; size <<= 1) {
-    for (int stride = size >> 1; stride > 0; stride >>= 1) {
-      for (int x = tid; x < (P >> 1); x += blockDim.x) {
-        const int lo = 2 * stride * (x / stride) + (x % stride);
-        const int hi = lo + stride;
-        const bool up = (lo & size) == 0;
-        const uint32_t a = buf[lo], b = buf[hi];
-        if ((a > b) == up) {
-          buf[lo] = b;
-          buf[hi] = a;
+  // bitonic sort of buf[0, P) (P a power of two, padded with 0xFFFFFFFF)
+  auto bitonic = [&](int P) {
+    for (int size = 2; size <= P; size <<= 1) {
+      for (int stride = size >> 1; stride > 0; stride >>= 1) {
+        for (int x = tid; x < (P >> 1); x += blockDim.x) {
+          const int lo = 2 * stride * (x / stride) + (x % stride);
+          const int hi = lo + stride;
+          const bool up = (lo & size) == 0;
+          const uint32_t a = buf[lo], b = buf[hi];
+          if ((a > b) == up) {
+            buf[lo] = b;
+            buf[hi] = a;
+          }
         }
+        __syncthreads();
       }
-      __syncthreads();
     }
-  }
-  // 4. unique (compaction in place, chunked per thread)
-  const int per = (P + blockDim.x - 1) / blockDim.x;
-  const int c0 = tid * per, c1 = min(P, c0 + per);
-  int local = 0;
-  for (int x = c0; x < c1; ++x) {
+  };
+  // 3. the distinct rows, sorted, into buf[0, H).  Fast path: a shared hash
+  //    set of the entries' rows; when at most HS_MAX rows are distinct (every
+  //    super-tile whose halo can fit), only those are sorted.  Otherwise all
+  //    entries are sorted and compacted.
+  constexpr int HS_SIZE = 2048, HS_MAX = 1024;  // (inserts stop past HS_MAX: <= 1536 used)
+  __shared__ uint32_t hset[HS_SIZE];
+  __shared__ int s_n, s_c;
+  for (int x = tid; x < HS_SIZE; x += blockDim.x) hset[x] = 0xFFFFFFFFu;
+  if (tid == 0) s_n = s_c = 0;
+  __syncthreads();
+  for (int x = tid; x < E; x += blockDim.x) {
+    if (*reinterpret_cast<volatile int*>(&s_n) > HS_MAX) break;
     const uint32_t v = buf[x];
-    if (v != 0xFFFFFFFFu && (x == 0 || buf[x - 1] != v)) ++local;
-  }
-  int li = local;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int n = __shfl_up_sync(0xffffffffu, li, o);
-    if (lane >= o) li += n;
-  }
-  __syncthreads();
-  if (lane == 31) wsum[warp] = li;
-  __syncthreads();
-  if (tid == 0) {
-    int acc = 0;
-    for (int w = 0; w < 16; ++w) {
-      const int v = wsum[w];
-      wsum[w] = acc;
-      acc += v;
+    uint32_t h = (v * 2654435761u) >> 21;
+    while (true) {
+      const uint32_t old = atomicCAS(&hset[h], 0xFFFFFFFFu, v);
+      if (old == 0xFFFFFFFFu) {
+        atomicAdd(&s_n, 1);
+        break;
+      }
+      if (old == v) break;
+      h = (h + 1) & (HS_SIZE - 1);
     }
-    s_H = acc;
   }
   __syncthreads();
-  const int H = s_H;
-  const bool over = H > hcap;
-  // gather my unique values into registers-by-chunk, then write compacted
-  {
+  if (s_n <= HS_MAX) {
+    for (int x = tid; x < HS_SIZE; x += blockDim.x) {
+      const uint32_t v = hset[x];
+      if (v != 0xFFFFFFFFu) buf[atomicAdd(&s_c, 1)] = v;
+    }
+    __syncthreads();
+    const int Hn = s_n;
+    int P = 1;
+    while (P < Hn) P <<= 1;
+    for (int x = Hn + tid; x < P; x += blockDim.x) buf[x] = 0xFFFFFFFFu;
+    __syncthreads();
+    bitonic(P);
+    if (tid == 0) s_H = Hn;
+    __syncthreads();
+  } else {
+    int P = 1;
+    while (P < E) P <<= 1;
+    for (int x = E + tid; x < P; x += blockDim.x) buf[x] = 0xFFFFFFFFu;
+    __syncthreads();
+    bitonic(P);
+    // unique (compaction in place, chunked per thread)
+    const int per = (P + blockDim.x - 1) / blockDim.x;
+    const int c0 = tid * per, c1 = min(P, c0 + per);
+    int local = 0;
+    for (int x = c0; x < c1; ++x) {
+      const uint32_t v = buf[x];
+      if (v != 0xFFFFFFFFu && (x == 0 || buf[x - 1] != v)) ++local;
+    }
+    int li = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int n = __shfl_up_sync(0xffffffffu, li, o);
+      if (lane >= o) li += n;
+    }
+    __syncthreads();
+    if (lane == 31) wsum[warp] = li;
+    __syncthreads();
+    if (tid == 0) {
+      int acc = 0;
+      for (int w = 0; w < 16; ++w) {
+        const int v = wsum[w];
+        wsum[w] = acc;
+        acc += v;
+      }
+      s_H = acc;
+    }
+    __syncthreads();
+    // gather my unique values into registers-by-chunk, then write compacted
     int w0 = li - local + wsum[warp];
     uint32_t vals[32];
     int nv = 0;
@@ -424,11 +510,13 @@ __global__ void __launch_bounds__(512) k_plan_super(
       if (v != 0xFFFFFFFFu && (x == 0 || buf[x - 1] != v)) vals[nv++] = v;
     }
     __syncthreads();
-    for (int q = 0; q < nv; ++q) {
-      buf[w0 + q] = vals[q];
-      if (!over) halo_out[static_cast<int64_t>(s) * hcap + w0 + q] = vals[q];
-    }
+    for (int q = 0; q < nv; ++q) buf[w0 + q] = vals[q];
+    __syncthreads();
   }
+  const int H = s_H;
+  const bool over = H > hcap;
+  if (!over)
+    for (int x = tid; x < H; x += blockDim.x) halo_out[static_cast<int64_t>(s) * hcap + x] = buf[x];
   __syncthreads();
   if (over) {
     // beyond the halo cap: report the split of the halo into <= hcap-row
@@ -476,7 +564,41 @@ __global__ void __launch_bounds__(512) k_plan_super(
   for (int x = tid; x < st * K * TM; x += blockDim.x) cnt[x] = 0;
   __syncthreads();
   // 6. entries: halo index of each neighbor, written at its item's offset
-  if (tid < R && len > 0) {
+  //    (in CSR order within each (row, cell))
+  if (plain) {
+    for (int rr = warp; rr < R; rr += nwarps) {
+      const int g = rr / TM, r = rr % TM;
+      const int n = rowoff[rr + 1] - rowoff[rr];
+      if (n == 0) continue;
+      const int64_t e0 = row_ptr[perm_rows[tiles[sub0 + g].x + r]];
+      for (int b = 0; b < n; b += 32) {
+        const bool act = b + lane < n;
+        int k = -1, lo = 0;
+        if (act) {
+          const int64_t e = e0 + b + lane;
+          k = static_cast<int>(kk[e]);
+          const uint32_t pj = inv_perm_cols[col[e]];
+          int hi = H;
+          while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (buf[mid] < pj) lo = mid + 1;
+            else hi = mid;
+          }
+        }
+        const unsigned same = __match_any_sync(0xffffffffu, k);
+        const int rank = __popc(same & lt_mask);
+        const int idx = (g * K + (act ? k : 0)) * TM + r;
+        if (act) {
+          const int pos = eoff[idx] + cnt[idx] + rank;
+          const uint64_t boff = blk_bytes(blk_off[static_cast<int64_t>(sub0 + g) * K + k]);
+          reinterpret_cast<uint16_t*>(blocks + boff + 512)[pos] = static_cast<uint16_t>(lo);
+        }
+        __syncwarp();
+        if (act && rank == __popc(same) - 1) cnt[idx] = static_cast<uint16_t>(cnt[idx] + __popc(same));
+        __syncwarp();
+      }
+    }
+  } else if (tid < R && len > 0) {
     const int g = tid / TM, r = tid % TM;
     for_row_entries(row_ptr, kk, col, inv_perm_cols, row_i, filt, [&](int64_t e, int k) {
       const uint32_t pj = inv_perm_cols[col[e]];
@@ -560,7 +682,7 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   L.blocks.alloc(ctx, static_cast<int64_t>(blk_bytes(L.block_units)));
   L.halo.alloc(ctx, static_cast<int64_t>(ns) * hcap);
   L.halo_len.alloc(ctx, ns);
-  const size_t smem = MAXE_ST * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
+  const size_t smem = maxe_of(st) * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
   NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   launch(ctx, "plan_super", k_plan_super, dim3(ns), dim3(512), smem, row_ptr, col, kk, perm_rows,
