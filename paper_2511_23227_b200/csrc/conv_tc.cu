@@ -2545,8 +2545,10 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         if (o && q * 16 < a.gin_cols)
 #pragma unroll
           for (int x = 0; x < 4; ++x)
-            atomicAdd(o + q * 4 + x, make_float4(__uint_as_float(v[4 * x]), __uint_as_float(v[4 * x + 1]),
-                                                 __uint_as_float(v[4 * x + 2]), __uint_as_float(v[4 * x + 3])));
+            asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(o + q * 4 + x),
+                         "f"(__uint_as_float(v[4 * x])), "f"(__uint_as_float(v[4 * x + 1])),
+                         "f"(__uint_as_float(v[4 * x + 2])), "f"(__uint_as_float(v[4 * x + 3]))
+                         : "memory");
       }
       tc_fence_before();
       __syncwarp();
