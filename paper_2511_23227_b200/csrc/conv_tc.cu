@@ -113,6 +113,8 @@ struct TcPlan {
   int saved_c = 0;                  // and its channel count
   bool saved_split = false;         // and its kind (bf16 image or split image)
   DevBuf<uint32_t> amax;            // split path: max |x| bits of [F_in, W, G_out, W] (scales)
+  DevBuf<uint32_t> bf_flags;        // fused backward: per (item, quadrant) "half 0 stored" flags
+  uint32_t bf_gen = 0;              // and the value of the last launch
   DevBuf<__nv_bfloat16> feat_out;  // bf16 G_out in perm_out order
   DevBuf<uint8_t> wpack;           // K x nci images of C x 128 B, SW128 K-major B operand
   DevBuf<float> partial;           // wgrad per-CTA partials
@@ -2219,9 +2221,11 @@ __global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_pa
 // exceeds one SM's TMEM, so the two CTAs of a cluster take the same
 // super-tiles and half of the cells each (14 / 13); each keeps 7 column blocks
 // of two cells (448 columns) + the 64-column input-gradient accumulator.
-// The two halves' input-gradient sums meet in global memory: grad_in is zeroed
-// and each CTA adds its sum once (0 + a + b == 0 + b + a in fp32:
-// deterministic).  Per-pair dW partials are reduced in a fixed order.
+// The two halves' input-gradient sums meet in global memory: the half-0 CTA
+// stores its sum, publishes a per-(item, quadrant) flag (release), and the
+// half-1 CTA, once it sees the flag (acquire), adds its sum with
+// red.global.add (a + b in fp32: deterministic; no zero fill of grad_in).
+// Per-pair dW partials are reduced in a fixed order.
 // ===========================================================================
 constexpr int BF_STAGES = 14;      // at most this many stages (cells) per record and CTA
 constexpr uint8_t BF_ZERO = 0xFF;  // no cell (the 13-cell half's 14th entry)
@@ -2238,6 +2242,9 @@ constexpr int NSF = 2;             // F tiles (16 KB: 128 rows x 64 channels, SW
 #define BF_NSD_ 8
 #endif
 constexpr int BF_NSA = BF_NSA_, BF_NSW = BF_NSW_, BF_NSD = BF_NSD_;
+#ifndef BF_FLAGS
+#define BF_FLAGS 0  // 1: half 0 stores, half 1 adds after its flag (A/B: slower); 0: grad_in zeroed, both add
+#endif
 static_assert(BF_NSD % AGG_GROUPS == 0, "descriptor slots per group");
 enum : int {
   BB_HALO_FULL = 0,
@@ -2270,8 +2277,10 @@ struct BfArgs {
   const __nv_bfloat16* feat;  // bf16 G_out image (perm_out order): the gathered rows
   const __nv_bfloat16* fimg;  // bf16 F_in image (perm_in order): the tiles' dense rows
   const uint8_t* wpack;       // K images of W_k^T (64 x 128 B)
-  float* gin;                 // (n_in, cin) original order, zeroed by the host
+  float* gin;                 // (n_in, cin) original order
   int gin_cols;               // cin
+  uint32_t* item_flag;        // [n_items][4]: the half-0 CTA stored the item's rows (quadrant e)
+  uint32_t gen;               // this launch's flag value (flags are never reset)
   float* partial;             // [pairs][K][64 m][64 c]
   uint8_t cells[2 * BF_STAGES];  // per half: stage -> cell (BF_ZERO: none)
 };
@@ -2527,7 +2536,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
       if (lane == 0) mbar_arrive(bar(BB_F_FULL + fs));
       ++f_it;
     };
-    auto drain = [&](int s) {
+    auto drain = [&](int s, int w) {
       named_bar_sync(2, 32 * 5);  // released by the MMA warp once the item's T_FULL landed
       tc_fence_after();
       const uint2 tl = a.tiles[a.sup[s].x];
@@ -2537,23 +2546,49 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
                            a.gin + static_cast<int64_t>(a.perm_rows[static_cast<int64_t>(tl.x) + 32 * e + lane]) *
                                        a.gin_cols)
                      : nullptr;
+      uint32_t* flag = a.item_flag + static_cast<int64_t>(w) * 4 + e;
+      uint32_t v[4][16];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        uint32_t v[16];
-        tmem_ld16(t0 + 16 * q, v);
-        tmem_ld_wait();
-        if (o && q * 16 < a.gin_cols)
-#pragma unroll
-          for (int x = 0; x < 4; ++x)
-            asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(o + q * 4 + x),
-                         "f"(__uint_as_float(v[4 * x])), "f"(__uint_as_float(v[4 * x + 1])),
-                         "f"(__uint_as_float(v[4 * x + 2])), "f"(__uint_as_float(v[4 * x + 3]))
-                         : "memory");
-      }
+      for (int q = 0; q < 4; ++q) tmem_ld16(t0 + 16 * q, v[q]);
+      tmem_ld_wait();
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(bar(BB_T_EMPTY));
+      if (lane == 0) mbar_arrive(bar(BB_T_EMPTY));  // the accumulator is free again
+      if (BF_FLAGS && half == 0) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (o && q * 16 < a.gin_cols)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              o[q * 4 + x] = make_float4(__uint_as_float(v[q][4 * x]), __uint_as_float(v[q][4 * x + 1]),
+                                         __uint_as_float(v[q][4 * x + 2]), __uint_as_float(v[q][4 * x + 3]));
+        __syncwarp();
+        if (lane == 0) {
+          __threadfence();
+          asm volatile("st.release.gpu.global.u32 [%0], %1;" ::"l"(flag), "r"(a.gen) : "memory");
+        }
+      } else {
+        if (BF_FLAGS && lane == 0) {
+          uint32_t f = 0;
+          while (true) {
+            asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(f) : "l"(flag) : "memory");
+            if (f == a.gen) break;
+            __nanosleep(64);
+          }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+          if (o && q * 16 < a.gin_cols)
+#pragma unroll
+            for (int x = 0; x < 4; ++x)
+              asm volatile("red.relaxed.gpu.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(o + q * 4 + x),
+                           "f"(__uint_as_float(v[q][4 * x])), "f"(__uint_as_float(v[q][4 * x + 1])),
+                           "f"(__uint_as_float(v[q][4 * x + 2])), "f"(__uint_as_float(v[q][4 * x + 3]))
+                           : "memory");
+      }
     };
+    int pend_w = -1;
     for (int w = pair; w < a.n_items; w += npairs) {
       {  // warm L2 with the next item's halo while this one is aggregated
         const int s_next = w + npairs < a.n_items ? static_cast<int>(a.item_start[w + npairs]) : -1;
@@ -2565,7 +2600,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
       for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
         if (a.halo_len[s] == kOverflow) continue;
         if (nrec == 2 && pend_s >= 0) {  // free the accumulator before the F ring blocks
-          drain(pend_s);
+          drain(pend_s, pend_w);
           pend_s = -1;
         }
         load_f(s);
@@ -2573,10 +2608,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         last_s = s;
       }
       if (last_s < 0) continue;
-      if (pend_s >= 0) drain(pend_s);
+      if (pend_s >= 0) drain(pend_s, pend_w);
       pend_s = last_s;
+      pend_w = w;
     }
-    if (pend_s >= 0) drain(pend_s);
+    if (pend_s >= 0) drain(pend_s, pend_w);
     // dW: column block b holds cell stages 2b (lanes 0-15 of each quadrant) and
     // 2b + 1 (lanes 16-31); quadrant e holds rows m = 16e .. 16e + 15
     mbar_wait_sleep(bar(BB_MMA_DONE), 0);
@@ -3606,8 +3642,19 @@ static void run_fused_backward(npcg_context* ctx, npcg_neighbors* nb, TcPlan* p,
   const int npairs = std::max(1, std::min(P->n_items, ctx->num_sms / 2));
   const int64_t need = static_cast<int64_t>(npairs) * K * 64 * 64;
   if (p->partial.size() < need) p->partial.alloc(ctx, need);
-  NPCG_CUDA(cudaMemsetAsync(grad_in, 0, nb->n_in * cin * sizeof(float), ctx->stream));
+  if (!BF_FLAGS) NPCG_CUDA(cudaMemsetAsync(grad_in, 0, nb->n_in * cin * sizeof(float), ctx->stream));
+  if (p->bf_flags.size() < static_cast<int64_t>(P->n_items) * 4) {
+    p->bf_flags.alloc(ctx, static_cast<int64_t>(P->n_items) * 4);
+    NPCG_CUDA(cudaMemsetAsync(p->bf_flags.get(), 0, P->n_items * 16, ctx->stream));
+    p->bf_gen = 0;
+  }
+  if (++p->bf_gen == 0) {  // wrapped: flags of a previous launch could match
+    NPCG_CUDA(cudaMemsetAsync(p->bf_flags.get(), 0, p->bf_flags.size() * 4, ctx->stream));
+    p->bf_gen = 1;
+  }
   BfArgs a{};
+  a.item_flag = p->bf_flags.get();
+  a.gen = p->bf_gen;
   a.halo = P->halo.get();
   a.halo_len = P->halo_len.get();
   a.blk_off = P->blk_off.get();
