@@ -1132,9 +1132,16 @@ struct FwdArgs {
   const uint32_t* amax;       // SPLIT: max |x| bits of the gathered tensor and of W (scales)
 };
 constexpr int TRACE_STAGES = 512;
-constexpr int TRACE_EV = 8;  // 0 d_issue, 1 d_full, 2 a_empty, 3 agg_done, 4 mma_start, 5 mma_issued, 6 w_full
+constexpr int TRACE_EV = 16;  // 0 d_issue, 1 d_full, 2 a_empty, 3 agg_done, 4 mma_start, 5 mma_issued, 6 w_full,
+                              // 7 grp_done, 8 cell top, 10 fence done, 11 mma block done, 12 cell end
 __device__ __forceinline__ void trace_ev(long long* tr, uint32_t stage, int ev) {
   if (tr && blockIdx.x == 0 && stage < TRACE_STAGES) tr[stage * TRACE_EV + ev] = clock64();
+}
+// the latest of several warps' clocks (ev 7: the group's last aggregation warp done)
+__device__ __forceinline__ void trace_max(long long* tr, uint32_t stage, int ev) {
+  if (tr && blockIdx.x == 0 && stage < TRACE_STAGES)
+    atomicMax(reinterpret_cast<unsigned long long*>(tr) + stage * TRACE_EV + ev,
+              static_cast<unsigned long long>(clock64()));
 }
 
 constexpr int FWD_AGG_WARP0 = 6;
@@ -1553,6 +1560,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       tc_fence_after();
       for (int c = 0; c < nci; ++c)
       for (int k = 0; k < K; ++k) {
+        if (lane == 0) tev(a_it, 8);
         if (pending && (c > 0 || k == 1 || !first)) release_epilogue();
         const uint32_t ws = w_it % NSWt;
         mbar_wait(bar(B_W_FULL + ws), (w_it / NSWt) & 1);
@@ -1565,6 +1573,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
           const uint32_t as = st % NSA;
           if (lane == 0) tev(st, 4);
           tc_fence_after();
+          if (lane == 0) tev(st, 10);
           // descriptor start-address field is in 16-byte units
           const uint64_t ad = a_desc0 + ((as * 16384u) >> 4);
           const uint64_t bd = b_desc0 + ((ws * Cfg::wbytes) >> 4);
@@ -1593,6 +1602,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
               for (int ks = 0; ks < 4; ++ks)
                 umma_bf16(d, ad + 2u * ks, bd + 2u * ks, idesc,
                           (!first || c > 0 || k > 0 || ks > 0) ? 1u : 0u);
+              tev(st, 11);
               umma_commit(bar(B_A_EMPTY + as));
             }
           }
@@ -1606,7 +1616,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             for (int g = 0; g < 2; ++g) {
               const uint32_t st = a_it + static_cast<uint32_t>(g);
               if ((todo >> g) & 1u)
-                if (__shfl_sync(0xffffffffu, mbar_test(bar(B_A_FULL + st % NSA), (st / NSA) & 1), 0)) {
+                if (__any_sync(0xffffffffu, mbar_test(bar(B_A_FULL + st % NSA), (st / NSA) & 1))) {
                   issue(g);
                   todo &= ~(1u << g);
                 }
@@ -1622,6 +1632,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         a_it += static_cast<uint32_t>(nsub);
         if (elect_one()) umma_commit(bar(B_W_EMPTY + ws));
         __syncwarp();
+        if (lane == 0) tev(a_it - nsub, 12);
         ++w_it;
       }
       if (!last) continue;  // the next record of this item accumulates on
@@ -1677,6 +1688,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         fence_proxy_async_smem();
         __syncwarp();
         if (wig == 0 && lane == 0) tev(j, 3);
+        if constexpr (TRACE) if (lane == 0) trace_max(a.trace, j, 7);
         if (lane == 0) {
           mbar_arrive(bar(B_A_FULL + as));
           mbar_arrive(bar(B_D_EMPTY + ds));
@@ -3402,10 +3414,10 @@ template <int NOUT, bool SPLIT = false>
 static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, const char* name,
                        bool big) {
   const FwdSmem L = fwd_smem_layout<NOUT, SPLIT>(hcap);
+  if (a.trace && (NOUT != 64 || SPLIT)) fail(NPCG_ERR_UNSUPPORTED, "trace: 64-channel bf16 passes only");
   auto kern = big ? k_conv_fwd_tc<NOUT, true, false, SPLIT> : k_conv_fwd_tc<NOUT, false, false, SPLIT>;
   if constexpr (NOUT == 64 && !SPLIT)
     if (a.trace) kern = big ? k_conv_fwd_tc<64, true, true> : k_conv_fwd_tc<64, false, true>;
-  if (a.trace && (NOUT != 64 || SPLIT)) fail(NPCG_ERR_UNSUPPORTED, "trace: 64-channel bf16 passes only");
   NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
   launch(ctx, name, kern, dim3(grid), dim3(FWD_THREADS), L.total, a);
