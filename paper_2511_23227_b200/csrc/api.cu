@@ -74,7 +74,7 @@ TcMode use_tc(const npcg_exec_config* cfg, npcg_dtype dtype, int64_t G, int64_t 
       if (dtype != NPCG_F32) fail(NPCG_ERR_UNSUPPORTED, "f32tc math requires F32 tensors");
       if (!tc_supported(G, cin, cout, K, TcMode::split, true))
         fail(NPCG_ERR_UNSUPPORTED,
-             "split tensor-core path needs G=1, C_in, C_out multiples of 16 up to 128, K<=128");
+             "split tensor-core path needs G=1, C_in, C_out multiples of 16 up to 256, K<=128");
       return TcMode::split;
     default:
       return dtype == NPCG_F32 && tc_supported(G, cin, cout, K, TcMode::split, false)

@@ -134,7 +134,7 @@ static int tc_pad(int c) { return c <= 64 ? 64 : c <= 128 ? 128 : 256; }
 bool tc_supported(int64_t G, int64_t cin, int64_t cout, int64_t K, TcMode mode, bool forced) {
   if (mode == TcMode::none) return false;
   if (mode == TcMode::split && !kSplitReady) return false;
-  const int64_t cmax = mode == TcMode::split ? 128 : 256;
+  const int64_t cmax = 256;  // (split: passes wider than 128 run in 128-column halves)
   return G == 1 && tc_width(cin, cmax, forced) && tc_width(cout, cmax, forced) && K >= 1 &&
          K <= KMAX;
 }
@@ -1073,15 +1073,16 @@ __global__ void k_to_split_perm(const float* __restrict__ src, const uint32_t* _
 //   image 2 (corr)  K 0..31 = Wl[r0 + kk], K 32..63 = Wh[r0 + kk - 32]
 // so that the tile [Ah | Al] gives main = Ah Wh and corr = Ah Wl + Al Wh.
 // transpose as k_pack_w.
-__global__ void k_pack_w_split(const float* __restrict__ w, int K, int cin, int cout, int cinp,
-                               int coutp, bool transpose, const uint32_t* __restrict__ amax,
+// Only B rows [n0, n0 + N) are packed (a 128-column half of a wider pass).
+__global__ void k_pack_w_split(const float* __restrict__ w, int K, int cin, int cout, int N, int nchunk,
+                               int n0, bool transpose, const uint32_t* __restrict__ amax,
                                uint8_t* __restrict__ out) {
   const int64_t x = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (x >= static_cast<int64_t>(K) * cin * cout) return;
   const int k = static_cast<int>(x / (cin * cout)), rem = static_cast<int>(x % (cin * cout));
   const int c = rem / cout, m = rem % cout;  // W[k][c][m]
-  const int n = transpose ? c : m, r = transpose ? m : c;
-  const int N = transpose ? cinp : coutp, nchunk = (transpose ? coutp : cinp) / 32;
+  const int n = (transpose ? c : m) - n0, r = transpose ? m : c;
+  if (n < 0 || n >= N) return;
   const int64_t img = (static_cast<int64_t>(k) * nchunk + r / 32) * 2;  // two images per chunk
   float hi, lo;
   split_f16(w[x] * split_scale(*amax), hi, lo);
@@ -1128,6 +1129,7 @@ struct FwdArgs {
   const uint8_t* wpack;       // (K x nci) images of NOUT x 128 B
   float* out;                 // (n_rows, ncols), original order
   int ncols;                  // channels written per row (<= NOUT; the rest is padding)
+  int out_stride, out_col0;   // output row stride and first written column (128-column halves)
   long long* trace;           // debug: per-stage event clocks of CTA 0 (traced variant only)
   const uint32_t* amax;       // SPLIT: max |x| bits of the gathered tensor and of W (scales)
 };
@@ -1723,7 +1725,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         const uint2 tl = a.tiles[sp.x + g];
         const int64_t row = static_cast<int64_t>(tl.x) + 32 * e + lane;
         float4* o = static_cast<uint32_t>(32 * e + lane) < tl.y
-                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * a.ncols)
+                        ? reinterpret_cast<float4*>(a.out + static_cast<int64_t>(a.perm_rows[row]) * a.out_stride +
+                                                    a.out_col0)
                         : nullptr;
 #pragma unroll 4
         for (int q = 0; q < NOUT / 16; ++q) {
@@ -1786,6 +1789,7 @@ struct WgArgs {
   int nci, gpc;                // C_in chunks; cell groups per chunk (blockIdx.y = c * gpc + group)
   const __nv_bfloat16* feat;   // bf16 F_in (n_cols, 64 nci), permuted
   const __nv_bfloat16* dense;  // bf16 G_out (n_rows, NOUT), permuted (row = sub-tile order)
+  int dense_stride;            // elements per dense row (NOUT, or the whole width for a half)
   float* partial;              // [gridDim.x][K][64 nci c][NOUT m]
   uint8_t korder[KMAX];        // run slot -> kernel cell (runs of 2 x pairs slots, load-balanced)
   int seg;                     // SPLIT: super-tiles per accumulation segment (bounded chains)
@@ -2155,7 +2159,7 @@ __global__ void __launch_bounds__(WG_THREADS, 1) k_conv_wgrad_tc(WgArgs a) {
           const bool in = static_cast<uint32_t>(r) < tl.y;
           const int64_t row = static_cast<int64_t>(tl.x) + (in ? r : 0);
           cp_async16_zfill(gt + j * 16384 + r * 128 + (((q ^ (r & 7)) & 7) << 4),
-                           reinterpret_cast<const uint4*>(a.dense + row * NOUT) + j * 8 + q, in ? 16u : 0u);
+                           reinterpret_cast<const uint4*>(a.dense + row * a.dense_stride) + j * 8 + q, in ? 16u : 0u);
         }
         cp_async_wait_all();
         fence_proxy_async_smem();
@@ -2193,9 +2197,11 @@ __global__ void k_wgrad_reduce(const float* __restrict__ partial, int n_part, in
 // c % 32 for the hi half, + 32 for the scaled lo half; same for m');
 // grad_w[k][m][c] = [sum over CTAs (fixed order) of hh + (hl + lh) 2^-11 +
 // ll 2^-22] / (s_F s_G).
+// (m0, cout_all: this partial holds output channels [m0, m0 + cout) of cout_all)
 __global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_part, int K, int cin,
                                      int cout, int cinp2, int coutp2, const uint32_t* __restrict__ amax_f,
-                                     const uint32_t* __restrict__ amax_g, float* __restrict__ grad_w) {
+                                     const uint32_t* __restrict__ amax_g, float* __restrict__ grad_w,
+                                     int m0, int cout_all) {
   const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (idx >= static_cast<int64_t>(K) * cin * cout) return;
   const int k = static_cast<int>(idx / (cin * cout)), c = static_cast<int>((idx / cout) % cin),
@@ -2211,7 +2217,7 @@ __global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_pa
     ll += rl[mh + 32];
   }
   const float inv = 1.f / (split_scale(*amax_f) * split_scale(*amax_g));
-  grad_w[(static_cast<int64_t>(k) * cout + m) * cin + c] =
+  grad_w[(static_cast<int64_t>(k) * cout_all + m0 + m) * cin + c] =
       (hh + fmaf(ll, 0x1p-11f, cr) * 0x1p-11f) * inv;
 }
 
@@ -3386,16 +3392,19 @@ static void convert_split(npcg_context* ctx, const float* src, const uint32_t* p
          reinterpret_cast<__half*>(dst.get()));
 }
 
+// Written channels [n0, n0 + nn) of the pass (C_out forward, C_in dgrad);
+// the scale slot is filled from the whole tensor when n0 == 0.
 static void pack_w_split(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose,
-                         int cin, int cout, uint32_t* slot) {
-  const int cinp = tc_pad(cin), coutp = tc_pad(cout);
+                         int cin, int cout, uint32_t* slot, int n0 = 0, int nn = -1) {
+  if (nn < 0) nn = transpose ? cin : cout;
+  const int N = tc_pad(nn), R = tc_pad(transpose ? cout : cin);
   const int64_t n = static_cast<int64_t>(K) * cin * cout;
-  const int64_t bytes = static_cast<int64_t>(K) * cinp * coutp * 2 * 2 * 2;  // 2 images, K 64 per 32
-  absmax(ctx, w, n, slot);
+  const int64_t bytes = static_cast<int64_t>(K) * R * N * 2 * 2 * 2;  // 2 images, K 64 per 32
+  if (n0 == 0) absmax(ctx, w, n, slot);
   if (p->wpack.size() < bytes) p->wpack.alloc(ctx, bytes);
   NPCG_CUDA(cudaMemsetAsync(p->wpack.get(), 0, bytes, ctx->stream));
   launch(ctx, "pack_w_split", k_pack_w_split, dim3(static_cast<unsigned>(ceil_div(n, 256))), dim3(256),
-         0, w, K, cin, cout, cinp, coutp, transpose, static_cast<const uint32_t*>(slot), p->wpack.get());
+         0, w, K, cin, cout, N, R / 32, n0, transpose, static_cast<const uint32_t*>(slot), p->wpack.get());
 }
 
 static void pack_w(npcg_context* ctx, TcPlan* p, const float* w, int K, bool transpose,
@@ -3428,7 +3437,8 @@ static void launch_fwd(npcg_context* ctx, const FwdArgs& a, int hcap, int grid, 
 static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16* feat,
                            const uint8_t* wpack, const uint32_t* perm_rows, float* out,
                            const char* name, long long* trace = nullptr, int cin_g = CH,
-                           int nout = CH, bool split = false, const uint32_t* amax = nullptr) {
+                           int nout = CH, bool split = false, const uint32_t* amax = nullptr,
+                           int col0 = 0, int out_stride = -1) {
   // cin_g / nout: real gathered / written channels; the kernel runs padded
   // (split: chunks of 32 real channels, each a 64-wide [hi | lo] bf16 slice)
   const int ncols = nout;
@@ -3456,6 +3466,8 @@ static void run_fwd_kernel(npcg_context* ctx, TcDirPlan* P, const __nv_bfloat16*
   a.wpack = wpack;
   a.out = out;
   a.ncols = ncols;
+  a.out_stride = out_stride < 0 ? ncols : out_stride;
+  a.out_col0 = col0;
   a.trace = trace;
   a.amax = amax;
   const int grid = std::min(P->n_super, ctx->num_sms);
@@ -3520,6 +3532,23 @@ static void input_image(npcg_context* ctx, npcg_neighbors* nb, TcPlan* p, const 
 // (bf16) / more than 64 (split: its W stages are twice as large).
 static bool wide_pass(int written, bool split) { return tc_pad(written) > (split ? CH : 2 * CH); }
 
+// A split (fp32-contract) gather pass: the split kernels hold at most 128
+// written channels in TMEM (3 main + 1 correction accumulator sets), so a
+// wider pass runs as 128-column halves, each with its own W images and the
+// output row stride of the whole width.  transpose: the dgrad pass (gathers
+// C_out, writes C_in).
+static void split_passes(npcg_context* ctx, TcPlan* p, TcDirPlan* P, const float* w, bool transpose,
+                         int cin, int cout, const __nv_bfloat16* feat, const uint32_t* perm_rows,
+                         float* out, const char* name, uint32_t* amax_feat, uint32_t* amax_w) {
+  const int gathered = transpose ? cout : cin, written = transpose ? cin : cout;
+  for (int n0 = 0; n0 < written; n0 += 128) {
+    const int nn = std::min(128, written - n0);
+    pack_w_split(ctx, p, w, P->K, transpose, cin, cout, amax_w, n0, nn);
+    run_fwd_kernel(ctx, P, feat, p->wpack.get(), perm_rows, out, name, nullptr, gathered, nn, true, amax_feat,
+                   n0, written);
+  }
+}
+
 void tc_forward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float* w,
                 const float* fin, float* fout, int cin, int cout) {
   const bool split = mode == TcMode::split;
@@ -3543,11 +3572,14 @@ void tc_forward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float*
   TcPlan* p = nb->tc.get();
   if (P->n_overflow < P->n_super) {
     input_image(ctx, nb, p, fin, cin, split);
-    if (split) pack_w_split(ctx, p, w, P->K, false, cin, cout, amax_slot(ctx, p, 1));
-    else pack_w(ctx, p, w, P->K, false, cin, cout);
-    run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout,
-                   split ? "conv_fwd_tc_split" : "conv_fwd_tc", nullptr, cin, cout, split,
-                   split ? amax_slot(ctx, p, 0) : nullptr);
+    if (split) {
+      split_passes(ctx, p, P, w, false, cin, cout, p->feat_in.get(), nb->perm_out.get(), fout,
+                   "conv_fwd_tc_split", amax_slot(ctx, p, 0), amax_slot(ctx, p, 1));
+    } else {
+      pack_w(ctx, p, w, P->K, false, cin, cout);
+      run_fwd_kernel(ctx, P, p->feat_in.get(), p->wpack.get(), nb->perm_out.get(), fout, "conv_fwd_tc",
+                     nullptr, cin, cout);
+    }
   }
   // rows of super-tiles beyond the tile capacities: exact engine on those rows only
   const CsrView v{nb->row_ptr.get(), nb->col_j.get(), nb->col_k.get(), nb->n_out, nb->n_pairs};
@@ -3752,11 +3784,14 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float
     TcDirPlan* P = plan_bwd(ctx, nb, wide_pass(cin, split));
     if (P->n_overflow < P->n_super) {
       g_image();
-      if (split) pack_w_split(ctx, p, w, K, true, cin, cout, amax_slot(ctx, p, 3));
-      else pack_w(ctx, p, w, K, true, cin, cout);
-      run_fwd_kernel(ctx, P, p->feat_out.get(), p->wpack.get(), nb->perm_in.get(), grad_in,
-                     split ? "conv_dgrad_tc_split" : "conv_dgrad_tc", nullptr, cout, cin, split,
-                     split ? amax_slot(ctx, p, 2) : nullptr);
+      if (split) {
+        split_passes(ctx, p, P, w, true, cin, cout, p->feat_out.get(), nb->perm_in.get(), grad_in,
+                     "conv_dgrad_tc_split", amax_slot(ctx, p, 2), amax_slot(ctx, p, 3));
+      } else {
+        pack_w(ctx, p, w, K, true, cin, cout);
+        run_fwd_kernel(ctx, P, p->feat_out.get(), p->wpack.get(), nb->perm_in.get(), grad_in,
+                       "conv_dgrad_tc", nullptr, cout, cin);
+      }
     }
     if (P->n_spill) {
       DevBuf<float> wt(ctx, static_cast<int64_t>(K) * cin * cout);
@@ -3779,54 +3814,60 @@ void tc_backward(npcg_context* ctx, npcg_neighbors* nb, TcMode mode, const float
       input_image(ctx, nb, p, fin, cin, split);
     if (!g_converted) g_image();
     const int cinp = tc_pad(cin), coutp = tc_pad(cout);
-    // split: chunks of 32 real input channels, 2 x C_out accumulator columns
+    // split: chunks of 32 real input channels, 2 x C_out accumulator columns;
+    // C_out > 128 runs as 128-channel halves of the G image (the kernel holds
+    // at most 256 accumulator columns)
     const int nci = split ? cinp / 32 : cinp / CH;
-    const int nw = split ? 2 * coutp : coutp;  // accumulator columns (the kernel's NOUT)
-    const int np = nw == 64 ? WgCfg<64>::pairs : nw == 128 ? WgCfg<128>::pairs : WgCfg<256>::pairs;
-    const int gpc = (K + 2 * np - 1) / (2 * np);  // cell groups per C_in chunk
-    const int groups = nci * gpc;
-    // one CTA per SM in total over (super-tile slices x groups)
-    const int gx = std::max(1, std::min(P->n_super, ctx->num_sms / groups));
-    const int64_t need = static_cast<int64_t>(gx) * K * nci * CH * nw;
-    if (p->partial.size() < need) p->partial.alloc(ctx, need);
-    NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
-    WgArgs a{};
-    a.halo = P->halo.get();
-    a.halo_len = P->halo_len.get();
-    a.blk_off = P->blk_off.get();
-    a.blocks = P->blocks.get();
-    a.sup = P->sup.get();
-    a.tiles = P->tiles.get();
-    a.n_rows = P->n_rows;
-    a.n_sub = P->n_sub;
-    a.n_super = P->n_super;
-    a.st = P->st;
-    a.hcap = P->hcap;
-    a.K = K;
-    a.nci = nci;
-    a.gpc = gpc;
-    a.feat = p->feat_in.get();
-    a.dense = p->feat_out.get();
-    a.partial = p->partial.get();
-    a.seg = split_segment();
-    wgrad_cell_order(P, K, np, gpc, a.korder);
-    const dim3 grid(gx, groups);
-    const int64_t nwt = static_cast<int64_t>(K) * cin * cout;
-    if (split) {
-      if (nw == 128) launch_wgrad<128, true>(ctx, a, P->hcap, grid, P->big_blocks);
-      else if (nw == 256) launch_wgrad<256, true>(ctx, a, P->hcap, grid, P->big_blocks);
-      else fail(NPCG_ERR_UNSUPPORTED, "split weight gradient: C_out up to 128");
-      launch(ctx, "wgrad_reduce", k_wgrad_reduce_split, dim3(static_cast<unsigned>(ceil_div(nwt, 256))),
-             dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, 2 * cinp,
-             2 * coutp, static_cast<const uint32_t*>(amax_slot(ctx, p, 0)),
-             static_cast<const uint32_t*>(amax_slot(ctx, p, 2)), grad_w);
-    } else {
-      if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid, P->big_blocks);
-      else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid, P->big_blocks);
-      else launch_wgrad<256>(ctx, a, P->hcap, grid, P->big_blocks);
-      launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(nwt, 256))),
-             dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, cinp, coutp,
-             grad_w);
+    for (int m0 = 0; m0 < cout; m0 += split ? 128 : cout) {
+      const int mc = split ? std::min(128, cout - m0) : cout;  // output channels of this pass
+      const int mcp = tc_pad(mc);
+      const int nw = split ? 2 * mcp : coutp;  // accumulator columns (the kernel's NOUT)
+      const int np = nw == 64 ? WgCfg<64>::pairs : nw == 128 ? WgCfg<128>::pairs : WgCfg<256>::pairs;
+      const int gpc = (K + 2 * np - 1) / (2 * np);  // cell groups per C_in chunk
+      const int groups = nci * gpc;
+      // one CTA per SM in total over (super-tile slices x groups)
+      const int gx = std::max(1, std::min(P->n_super, ctx->num_sms / groups));
+      const int64_t need = static_cast<int64_t>(gx) * K * nci * CH * nw;
+      if (p->partial.size() < need) p->partial.alloc(ctx, need);
+      NPCG_CUDA(cudaMemsetAsync(p->partial.get(), 0, need * 4, ctx->stream));
+      WgArgs a{};
+      a.halo = P->halo.get();
+      a.halo_len = P->halo_len.get();
+      a.blk_off = P->blk_off.get();
+      a.blocks = P->blocks.get();
+      a.sup = P->sup.get();
+      a.tiles = P->tiles.get();
+      a.n_rows = P->n_rows;
+      a.n_sub = P->n_sub;
+      a.n_super = P->n_super;
+      a.st = P->st;
+      a.hcap = P->hcap;
+      a.K = K;
+      a.nci = nci;
+      a.gpc = gpc;
+      a.feat = p->feat_in.get();
+      a.dense = p->feat_out.get() + (split ? 2 * m0 : 0);
+      a.dense_stride = split ? 2 * coutp : coutp;
+      a.partial = p->partial.get();
+      a.seg = split_segment();
+      wgrad_cell_order(P, K, np, gpc, a.korder);
+      const dim3 grid(gx, groups);
+      const int64_t nwt = static_cast<int64_t>(K) * cin * mc;
+      if (split) {
+        if (nw == 128) launch_wgrad<128, true>(ctx, a, P->hcap, grid, P->big_blocks);
+        else launch_wgrad<256, true>(ctx, a, P->hcap, grid, P->big_blocks);
+        launch(ctx, "wgrad_reduce", k_wgrad_reduce_split, dim3(static_cast<unsigned>(ceil_div(nwt, 256))),
+               dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, mc, 2 * cinp, nw,
+               static_cast<const uint32_t*>(amax_slot(ctx, p, 0)),
+               static_cast<const uint32_t*>(amax_slot(ctx, p, 2)), grad_w, m0, cout);
+      } else {
+        if (coutp == 64) launch_wgrad<64>(ctx, a, P->hcap, grid, P->big_blocks);
+        else if (coutp == 128) launch_wgrad<128>(ctx, a, P->hcap, grid, P->big_blocks);
+        else launch_wgrad<256>(ctx, a, P->hcap, grid, P->big_blocks);
+        launch(ctx, "wgrad_reduce", k_wgrad_reduce, dim3(static_cast<unsigned>(ceil_div(nwt, 256))),
+               dim3(256), 0, static_cast<const float*>(p->partial.get()), gx, K, cin, cout, cinp, coutp,
+               grad_w);
+      }
     }
     if (P->n_spill) wgrad_spill(ctx, nb, P, fin, gout, grad_w, true, cin, cout);
   }

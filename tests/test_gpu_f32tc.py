@@ -4,7 +4,7 @@ rel <= 1e-5 (acceptance.cpp:39, 173-195), on the reference's
 fp32 inputs.  Operands are split x = hi + lo (two bf16); products hi*hi +
 hi*lo + lo*hi (forward / input gradient) and all four (weight gradient), fp32
 accumulation.  Cases: uniform clouds (configs 1/2 shapes), every supported
-width pair, clustered and strided (dense, split-record) neighborhoods,
+width pair (beyond 128 written channels as 128-column halves), clustered and strided (dense, split-record) neighborhoods,
 determinism, and that AUTO actually runs the split kernels."""
 import numpy as np
 import pytest
@@ -50,7 +50,9 @@ def _check(npc, orc, xyz, r, t, cin, cout, seed, out_xyz=None, math=None):
 
 
 @pytest.mark.parametrize("cin,cout", [(64, 64), (64, 128), (128, 64), (128, 128), (32, 32),
-                                      (48, 80), (16, 112)])
+                                      (48, 80), (16, 112),
+                                      # wider than 128: passes in 128-column halves
+                                      (128, 256), (256, 128), (256, 256), (64, 192), (208, 48)])
 def test_f32tc_widths_uniform(npc, orc, cin, cout):
     n = 8000
     xyz = orc.gen_uniform_cube(n, 1.0, 7)
