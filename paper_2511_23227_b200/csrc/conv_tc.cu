@@ -664,6 +664,8 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   DevBuf<uint32_t> d_seg(ctx, static_cast<int64_t>(ns) * (MAXSEG + 1));
   DevBuf<uint32_t> d_maxc(ctx, nt), d_maxblk(ctx, 1);
   NPCG_CUDA(cudaMemsetAsync(d_maxblk.get(), 0, 4, ctx->stream));
+  // (records write only their used segment bounds; the whole array is read back)
+  NPCG_CUDA(cudaMemsetAsync(d_seg.get(), 0, static_cast<size_t>(ns) * (MAXSEG + 1) * 4, ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(d_sup.get(), L.sup.data(), ns * sizeof(uint2), cudaMemcpyHostToDevice,
                             ctx->stream));
   NPCG_CUDA(cudaMemcpyAsync(d_tiles.get(), L.tiles.data(), nt * sizeof(uint2),
