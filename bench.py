@@ -551,6 +551,7 @@ def run_ours(args):
              "algorithmic_bytes_per_step": layer_bytes, "algorithmic_flop_per_step": layer_flops}
 
     cpu = None if (args.no_cpu_baseline or world > 1) else cpu_baseline_sample(n_unit)
+    e2e_cpp = None if (args.no_e2e or world > 1 or args.workload != "ns") else e2e_cpp_dropin(args)
     dtype = {"auto": "f32 contract: split bf16x3 operands on tcgen05 where supported, else f32",
              "exact": "f32", "bf16": "bf16-operand/fp32-accumulate (tcgen05), the opt-in variant",
              "f32tc": "split bf16x3 operands, fp32 accumulate (tcgen05)"}[args.math]
@@ -584,6 +585,7 @@ def run_ours(args):
         "cpu_baseline": cpu,
         "fp32_variant": fp32v,
         "e2e": e2e,
+        "e2e_cpp_dropin": e2e_cpp,
     }
     print(json.dumps(out))
     if args.profile_out:
@@ -591,6 +593,24 @@ def run_ours(args):
             json.dump(out, fh, indent=1)
     if world > 1:
         dist.destroy_process_group()
+
+
+def e2e_cpp_dropin(args):
+    """The same layer step through the torch-free C++ drop-in (include/npcg/npconv.hpp,
+    PointConvOp<float> on host std::vector-backed tensors; tools/cpp/bench_dropin):
+    the boundary a reference caller uses, copies and host results inside the
+    timed region.  Runs after the timed region, in its own process."""
+    exe = os.path.join(ROOT, "tools", "cpp", "bench_dropin")
+    if not os.path.exists(exe):
+        return {"unavailable": "tools/cpp/bench_dropin not built (__graft_entry__.build())"}
+    math = {"f32tc": "auto"}.get(args.math, args.math)
+    try:
+        r = subprocess.run([exe, str(1_000_000), str(max(3, min(args.steps, 10))), "3", math],
+                           capture_output=True, text=True, timeout=600)
+        line = [x for x in r.stdout.splitlines() if x.startswith("{")]
+        return json.loads(line[-1]) if line else {"unavailable": (r.stderr or r.stdout)[-300:]}
+    except Exception as e:  # noqa: BLE001 (reported, not fatal for the bench line)
+        return {"unavailable": repr(e)[:300]}
 
 
 def main():

@@ -33,14 +33,18 @@
 #include <cmath>
 #include <cstdint>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <fstream>
+#include <map>
 #include <memory>
+#include <mutex>
 #include <sstream>
 #include <span>
 #include <stdexcept>
 #include <string>
 #include <thread>
+#include <unordered_map>
 #include <utility>
 #include <vector>
 
@@ -108,6 +112,98 @@ inline void cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw DeviceError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+// Tensor storage on the host: a process-wide cache of PINNED blocks for large
+// tensors (>= 1 MiB), so a result returned by value lands by DMA straight into
+// already-mapped memory (no page faults, no staging copy) and an input built
+// once is uploaded the same way.  Freed blocks are kept for reuse up to
+// NPCG_HOST_CACHE_MB (default 4096) and are never handed back to the OS
+// before exit.  Falls back to malloc when pinned memory is unavailable.
+class PinnedPool {
+ public:
+  static PinnedPool& get() {
+    static PinnedPool* p = new PinnedPool();  // (leaked: no CUDA calls during static destruction)
+    return *p;
+  }
+  void* take(size_t bytes) {
+    std::lock_guard<std::mutex> g(m_);
+    auto it = free_.lower_bound(bytes);
+    if (it != free_.end() && it->first <= bytes + bytes / 4) {
+      void* p = it->second;
+      cached_ -= it->first;
+      free_.erase(it);
+      return p;
+    }
+    void* p = nullptr;
+    if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
+      (void)cudaGetLastError();
+      return nullptr;
+    }
+    size_[p] = bytes;
+    return p;
+  }
+  bool give(void* p) {
+    std::lock_guard<std::mutex> g(m_);
+    const auto it = size_.find(p);
+    if (it == size_.end()) return false;
+    free_.emplace(it->second, p);
+    cached_ += it->second;
+    while (cached_ > limit_ && !free_.empty()) {  // drop the largest cached blocks first
+      auto last = std::prev(free_.end());
+      cached_ -= last->first;
+      size_.erase(last->second);
+      cudaFreeHost(last->second);
+      free_.erase(last);
+    }
+    return true;
+  }
+  bool owns(const void* p) {
+    std::lock_guard<std::mutex> g(m_);
+    return size_.count(const_cast<void*>(p)) != 0;
+  }
+
+ private:
+  PinnedPool() {
+    const char* e = std::getenv("NPCG_HOST_CACHE_MB");
+    limit_ = (e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : size_t(4096)) << 20;
+  }
+  std::mutex m_;
+  std::multimap<size_t, void*> free_;
+  std::unordered_map<void*, size_t> size_;
+  size_t cached_ = 0, limit_ = 0;
+};
+
+// std::vector allocator over PinnedPool; elements are default-initialised
+// (a buffer that a copy fills is not zeroed first).
+template <typename T>
+struct HostAlloc {
+  using value_type = T;
+  static constexpr size_t kPinnedMin = size_t(1) << 20;
+  HostAlloc() = default;
+  template <typename U>
+  HostAlloc(const HostAlloc<U>&) {}
+  T* allocate(size_t n) {
+    const size_t b = n * sizeof(T);
+    if (b >= kPinnedMin)
+      if (void* p = PinnedPool::get().take(b)) return static_cast<T*>(p);
+    void* p = std::malloc(b ? b : 1);
+    if (!p) throw std::bad_alloc();
+    return static_cast<T*>(p);
+  }
+  void deallocate(T* p, size_t n) {
+    if (n * sizeof(T) < kPinnedMin || !PinnedPool::get().give(p)) std::free(p);
+  }
+  template <typename U, typename... A>
+  void construct(U* p, A&&... a) {
+    if constexpr (sizeof...(A) == 0) ::new (static_cast<void*>(p)) U;
+    else ::new (static_cast<void*>(p)) U(std::forward<A>(a)...);
+  }
+  friend bool operator==(const HostAlloc&, const HostAlloc&) { return true; }
+};
+template <typename T>
+using HostVec = std::vector<T, HostAlloc<T>>;
+struct trusted_t {};  // results the library produced: no finiteness re-scan
+inline constexpr trusted_t trusted{};
+
 // Host <-> device copies of the reference's std::vector containers (pageable
 // memory): through two pinned staging chunks, the CPU side of a chunk copied by
 // several threads while the other chunk's DMA runs, so a transfer goes at
@@ -119,6 +215,12 @@ class Stager {
     return s;
   }
   void h2d(void* dst, const void* src, size_t bytes) {
+    if (bytes >= kSmall && PinnedPool::get().owns(src)) {  // pinned tensor storage: one DMA
+      init();
+      cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, stream_), "H2D");
+      cuda(cudaStreamSynchronize(stream_), "H2D sync");
+      return;
+    }
     if (bytes < kSmall) {
       cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyHostToDevice), "H2D");
       return;
@@ -134,6 +236,12 @@ class Stager {
     cuda(cudaStreamSynchronize(stream_), "H2D sync");
   }
   void d2h(void* dst, const void* src, size_t bytes) {
+    if (bytes >= kSmall && PinnedPool::get().owns(dst)) {
+      init();
+      cuda(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, stream_), "D2H");
+      cuda(cudaStreamSynchronize(stream_), "D2H sync");
+      return;
+    }
     if (bytes < kSmall) {
       cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "D2H");
       return;
@@ -231,6 +339,15 @@ class Dev {
     }
     return v;
   }
+  // into pooled pinned storage (tensor results)
+  HostVec<T> host_vec(size_t n) const {
+    HostVec<T> v(n);
+    if (n) {
+      check(npcg_context_synchronize(ctx()), "sync");
+      Stager::get().d2h(v.data(), p_, n * sizeof(T));
+    }
+    return v;
+  }
 
  private:
   T* p_ = nullptr;
@@ -255,15 +372,18 @@ class FeatureTensor {
       throw ShapeError("FeatureTensor: need n >= 0, groups >= 1, channels >= 1");
     v_.assign(static_cast<size_t>(n * g * c), T(0));
   }
-  FeatureTensor(int64_t n, int64_t g, int64_t c, std::vector<T> values)
-      : n_(n), g_(g), c_(c), v_(std::move(values)) {
+  FeatureTensor(int64_t n, int64_t g, int64_t c, const std::vector<T>& values) : n_(n), g_(g), c_(c) {
     if (n < 0 || g < 1 || c < 1)
       throw ShapeError("FeatureTensor: need n >= 0, groups >= 1, channels >= 1");
-    if (static_cast<int64_t>(v_.size()) != n * g * c)
+    if (static_cast<int64_t>(values.size()) != n * g * c)
       throw ShapeError("FeatureTensor: value count does not match (n, groups, channels)");
-    for (T x : v_)
+    for (T x : values)
       if (!std::isfinite(static_cast<double>(x))) throw NonFiniteError("FeatureTensor: non-finite value");
+    v_.assign(values.begin(), values.end());  // into pooled pinned storage
   }
+  // a result of the library's own kernels (shape known, values not re-scanned)
+  FeatureTensor(detail::trusted_t, int64_t n, int64_t g, int64_t c, detail::HostVec<T>&& values)
+      : n_(n), g_(g), c_(c), v_(std::move(values)) {}
   int64_t n() const { return n_; }
   int64_t groups() const { return g_; }
   int64_t channels() const { return c_; }
@@ -277,7 +397,7 @@ class FeatureTensor {
 
  private:
   int64_t n_ = 0, g_ = 1, c_ = 1;
-  std::vector<T> v_;
+  detail::HostVec<T> v_;
 };
 
 template <typename T>
@@ -597,7 +717,7 @@ MvmrResult<T> mvmr(const WeightTensor<T>& w, const FeatureTensor<T>& fin, const 
   detail::check(npcg_mvmr(detail::ctx(), detail::dtype_of<T>(), dw.get(), w.t(), w.groups(), w.c_in(), w.c_out(),
                           df.get(), fin.n(), &d.view, n_out, &c, out.get()),
                 "mvmr");
-  return {FeatureTensor<T>(n_out, w.groups(), w.c_out(), out.host()), {}, 0};
+  return {FeatureTensor<T>(detail::trusted, n_out, w.groups(), w.c_out(), out.host_vec(out.size())), {}, 0};
 }
 
 template <typename T>
@@ -612,7 +732,7 @@ MvmrResult<T> mvmr_transposed(const WeightTensor<T>& w, const FeatureTensor<T>& 
   detail::check(npcg_mvmr_transposed(detail::ctx(), detail::dtype_of<T>(), dw.get(), w.t(), w.groups(), w.c_in(),
                                      w.c_out(), dg.get(), gout.n(), &d.view, n_in, &c, out.get()),
                 "mvmr_transposed");
-  return {FeatureTensor<T>(n_in, w.groups(), w.c_in(), out.host()), {}, 0};
+  return {FeatureTensor<T>(detail::trusted, n_in, w.groups(), w.c_in(), out.host_vec(out.size())), {}, 0};
 }
 
 template <typename T>
@@ -697,7 +817,7 @@ class PointConvOp {
                   "PointConvOp::forward");
     n_in_ = fin.n();
     has_forward_ = true;
-    return FeatureTensor<T>(n_out_, w_.groups(), w_.c_out(), dout_.host(n_o));
+    return FeatureTensor<T>(detail::trusted, n_out_, w_.groups(), w_.c_out(), dout_.host_vec(n_o));
   }
 
   BackwardResult<T> backward(const FeatureTensor<T>& gout) {
@@ -715,7 +835,7 @@ class PointConvOp {
     detail::check(npcg_conv_backward(detail::ctx(), nb_->h, detail::dtype_of<T>(), dw_.get(), w_.groups(), w_.c_in(),
                                      w_.c_out(), dfin_.get(), dg_.get(), &c, dgi_.get(), dgw_.get()),
                   "PointConvOp::backward");
-    BackwardResult<T> r{FeatureTensor<T>(n_in_, w_.groups(), w_.c_in(), dgi_.host(n_gi)),
+    BackwardResult<T> r{FeatureTensor<T>(detail::trusted, n_in_, w_.groups(), w_.c_in(), dgi_.host_vec(n_gi)),
                         WeightGradient<T>(w_.kernels(), w_.groups(), w_.c_out(), w_.c_in())};
     const auto h = dgw_.host(n_gw);
     std::copy(h.begin(), h.end(), r.grad_w.values_mut().begin());
@@ -772,7 +892,7 @@ FeatureTensor<T> upsample(const PointCloud& fine, const DownsampleMap& map, cons
   detail::Dev<T> out(static_cast<size_t>(n * w));
   detail::check(npcg_upsample(detail::ctx(), detail::dtype_of<T>(), par.get(), n, dc.get(), coarse.n(), w, out.get()),
                 "upsample");
-  return FeatureTensor<T>(n, coarse.groups(), coarse.channels(), out.host());
+  return FeatureTensor<T>(detail::trusted, n, coarse.groups(), coarse.channels(), out.host_vec(out.size()));
 }
 
 template <typename T>

@@ -87,5 +87,23 @@ def build_cpp_tests(verbose: bool = True) -> str:
     return out
 
 
+def build_cpp_bench(verbose: bool = True) -> str:
+    """Builds tools/cpp/bench_dropin (end-to-end timing through the C++ drop-in
+    header, linked against libnpcg.so only: no torch, no oracle)."""
+    src = os.path.join(ROOT, "tools", "cpp", "bench_dropin.cpp")
+    out = os.path.join(ROOT, "tools", "cpp", "bench_dropin")
+    deps = [src, LIB, os.path.join(ROOT, "include", "npcg", "npconv.hpp")]
+    if os.path.exists(out) and os.path.getmtime(out) > max(os.path.getmtime(d) for d in deps):
+        return out
+    cmd = [NVCC, "-std=c++20", "-O2", "-I" + os.path.join(ROOT, "include"), src, "-o", out,
+           "-L" + HERE, "-lnpcg", "-Xlinker", "-rpath", "-Xlinker", "$ORIGIN/../../paper_2511_23227_b200"]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"C++ drop-in bench build failed:\n{r.stderr}")
+    if verbose:
+        print(f"built {out}")
+    return out
+
+
 if __name__ == "__main__":
     build(force="--force" in sys.argv)
