@@ -34,6 +34,7 @@
 #include <cuda_fp16.h>
 
 #include <algorithm>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -308,7 +309,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
     const uint32_t* __restrict__ blk_off, const uint32_t* __restrict__ sub_bad,
     uint32_t* __restrict__ halo_out,
     uint32_t* __restrict__ halo_len, uint32_t* __restrict__ seg,
-    uint8_t* __restrict__ blocks) {
+    uint8_t* __restrict__ blocks, int packed, unsigned long long* __restrict__ pdbg) {
   extern __shared__ __align__(16) uint8_t sm[];
   const int maxe = maxe_of(st);
   uint32_t* buf = reinterpret_cast<uint32_t*>(sm);                          // maxe
@@ -316,9 +317,16 @@ __global__ void __launch_bounds__(512) k_plan_super(
   uint16_t* eoff = cnt + st * K * TM;                                        // st*K*TM
   int* rowoff = reinterpret_cast<int*>(eoff + st * K * TM);                  // st*TM + 1
   __shared__ int s_total, s_bad, s_H;
+  // packed (plain records, column ids < 2^25): phase 2 keeps each entry as
+  // (permuted column << 7 | cell) in buf, phase 6 reads them back from there
+  // (no second pass over global memory); the halo goes to hal[]
+  __shared__ int64_t rowe0[512];
+  __shared__ uint32_t hal[1024];
+  __shared__ uint64_t s_boff[2 * KMAX];
   __shared__ int wsum[16];
 
   const int s = blockIdx.x;
+  if (pdbg && threadIdx.x == 0) pdbg[s * 8 + 6] = clock64();
   const int sub0 = static_cast<int>(sup[s].x);
   const int nsub = static_cast<int>(sup[s].y & 0xFFu);
   const int R = nsub * TM;
@@ -345,7 +353,8 @@ __global__ void __launch_bounds__(512) k_plan_super(
     filt = EntryFilter::from(tfilter[sub0 + tid / TM]);
     if (static_cast<uint32_t>(tid % TM) < tl.y) {
       row_i = perm_rows[tl.x + tid % TM];
-      if (filt.all()) len = static_cast<int>(row_ptr[row_i + 1] - row_ptr[row_i]);
+      rowe0[tid] = row_ptr[row_i];
+      if (filt.all()) len = static_cast<int>(row_ptr[row_i + 1] - rowe0[tid]);
       else for_row_entries(row_ptr, kk, col, inv_perm_cols, row_i, filt, [&](int64_t, int) { ++len; });
     }
   }
@@ -388,10 +397,52 @@ __global__ void __launch_bounds__(512) k_plan_super(
     }
     return;
   }
+  if (pdbg && tid == 0) pdbg[s * 8 + 0] = clock64();  // (planner profile: phase clocks)
   // 2. permuted neighbor ids + per-(sub, cell, row) counts
   __syncthreads();
   const bool plain = s_plain != 0;
-  if (plain) {
+  const bool pk = plain && packed != 0;
+  if (pk) {
+    // flattened over the super-tile's entries, four per thread in flight
+    auto row_of = [&](int x) {  // last rr with rowoff[rr] <= x
+      int lo = 0, hi = R;
+      while (hi - lo > 1) {
+        const int mid = (lo + hi) >> 1;
+        if (rowoff[mid] <= x) lo = mid;
+        else hi = mid;
+      }
+      return lo;
+    };
+    const int step = static_cast<int>(blockDim.x);
+    for (int x0 = tid; x0 < E; x0 += 4 * step) {
+      int rr[4];
+      int64_t e[4];
+      uint32_t c[4], k[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = x0 + u * step;
+        rr[u] = x < E ? row_of(x) : 0;
+        e[u] = x < E ? rowe0[rr[u]] + (x - rowoff[rr[u]]) : -1;
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e[u] >= 0) {
+          c[u] = col[e[u]];
+          k[u] = kk[e[u]];
+        }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e[u] >= 0) c[u] = inv_perm_cols[c[u]];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (e[u] >= 0) {
+          const int g = rr[u] / TM, r = rr[u] % TM;
+          buf[x0 + u * step] = (c[u] << 7) | k[u];
+          const int idx = (g * K + static_cast<int>(k[u])) * TM + r;
+          atomicAdd(reinterpret_cast<unsigned*>(cnt) + (idx >> 1), 1u << (16 * (idx & 1)));
+        }
+    }
+  } else if (plain) {
     for (int rr = warp; rr < R; rr += nwarps) {
       const int g = rr / TM, r = rr % TM;
       const int off = rowoff[rr], n = rowoff[rr + 1] - off;
@@ -414,23 +465,24 @@ __global__ void __launch_bounds__(512) k_plan_super(
   }
   __syncthreads();
   // bitonic sort of buf[0, P) (P a power of two, padded with 0xFFFFFFFF)
-  auto bitonic = [&](int P) {
+  auto bitonic = [&](uint32_t* v, int P) {
     for (int size = 2; size <= P; size <<= 1) {
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
         for (int x = tid; x < (P >> 1); x += blockDim.x) {
           const int lo = 2 * stride * (x / stride) + (x % stride);
           const int hi = lo + stride;
           const bool up = (lo & size) == 0;
-          const uint32_t a = buf[lo], b = buf[hi];
+          const uint32_t a = v[lo], b = v[hi];
           if ((a > b) == up) {
-            buf[lo] = b;
-            buf[hi] = a;
+            v[lo] = b;
+            v[hi] = a;
           }
         }
         __syncthreads();
       }
     }
   };
+  if (pdbg && tid == 0) pdbg[s * 8 + 1] = clock64();
   // 3. the distinct rows, sorted, into buf[0, H).  Fast path: a shared hash
   //    set of the entries' rows; when at most HS_MAX rows are distinct (every
   //    super-tile whose halo can fit), only those are sorted.  Otherwise all
@@ -443,7 +495,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
   __syncthreads();
   for (int x = tid; x < E; x += blockDim.x) {
     if (*reinterpret_cast<volatile int*>(&s_n) > HS_MAX) break;
-    const uint32_t v = buf[x];
+    const uint32_t v = pk ? buf[x] >> 7 : buf[x];
     uint32_t h = (v * 2654435761u) >> 21;
     while (true) {
       const uint32_t old = atomicCAS(&hset[h], 0xFFFFFFFFu, v);
@@ -456,26 +508,34 @@ __global__ void __launch_bounds__(512) k_plan_super(
     }
   }
   __syncthreads();
+  // the halo (sorted distinct rows): hal[] on the hash path (buf keeps the
+  // entries), buf itself on the full-sort path (whose halo never fits)
+  uint32_t* halo = buf;
   if (s_n <= HS_MAX) {
+    halo = hal;
     for (int x = tid; x < HS_SIZE; x += blockDim.x) {
       const uint32_t v = hset[x];
-      if (v != 0xFFFFFFFFu) buf[atomicAdd(&s_c, 1)] = v;
+      if (v != 0xFFFFFFFFu) hal[atomicAdd(&s_c, 1)] = v;
     }
     __syncthreads();
     const int Hn = s_n;
     int P = 1;
     while (P < Hn) P <<= 1;
-    for (int x = Hn + tid; x < P; x += blockDim.x) buf[x] = 0xFFFFFFFFu;
+    for (int x = Hn + tid; x < P; x += blockDim.x) hal[x] = 0xFFFFFFFFu;
     __syncthreads();
-    bitonic(P);
+    bitonic(hal, P);
     if (tid == 0) s_H = Hn;
     __syncthreads();
   } else {
+    if (pk) {
+      for (int x = tid; x < E; x += blockDim.x) buf[x] >>= 7;
+      __syncthreads();
+    }
     int P = 1;
     while (P < E) P <<= 1;
     for (int x = E + tid; x < P; x += blockDim.x) buf[x] = 0xFFFFFFFFu;
     __syncthreads();
-    bitonic(P);
+    bitonic(buf, P);
     // unique (compaction in place, chunked per thread)
     const int per = (P + blockDim.x - 1) / blockDim.x;
     const int c0 = tid * per, c1 = min(P, c0 + per);
@@ -518,7 +578,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
   const int H = s_H;
   const bool over = H > hcap;
   if (!over)
-    for (int x = tid; x < H; x += blockDim.x) halo_out[static_cast<int64_t>(s) * hcap + x] = buf[x];
+    for (int x = tid; x < H; x += blockDim.x) halo_out[static_cast<int64_t>(s) * hcap + x] = halo[x];
   __syncthreads();
   if (over) {
     // beyond the halo cap: report the split of the halo into <= hcap-row
@@ -530,10 +590,11 @@ __global__ void __launch_bounds__(512) k_plan_super(
       uint32_t* sg = seg + static_cast<int64_t>(s) * (MAXSEG + 1);
       sg[0] = nseg <= MAXSEG ? static_cast<uint32_t>(nseg) : 0u;
       if (nseg <= MAXSEG)
-        for (int q = 1; q < nseg; ++q) sg[q] = buf[static_cast<int64_t>(q) * H / nseg];
+        for (int q = 1; q < nseg; ++q) sg[q] = halo[static_cast<int64_t>(q) * H / nseg];
     }
     return;
   }
+  if (pdbg && tid == 0) pdbg[s * 8 + 2] = clock64();
   // 5. items per (sub, cell) block: rows by count descending (stable in r)
   const unsigned lt = (1u << lane) - 1u;
   for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
@@ -564,10 +625,44 @@ __global__ void __launch_bounds__(512) k_plan_super(
   }
   __syncthreads();
   for (int x = tid; x < st * K * TM; x += blockDim.x) cnt[x] = 0;
+  for (int x = tid; x < nsub * K; x += blockDim.x)
+    s_boff[x] = blk_bytes(blk_off[static_cast<int64_t>(sub0 + x / K) * K + x % K]);
   __syncthreads();
+  if (pdbg && tid == 0) pdbg[s * 8 + 3] = clock64();
   // 6. entries: halo index of each neighbor, written at its item's offset
   //    (in CSR order within each (row, cell))
-  if (plain) {
+  if (pk) {
+    // flattened: each thread places its entries independently (all reads from
+    // shared memory); the rank of an entry within its (row, cell) is the
+    // number of earlier entries of the row with the same cell (CSR order)
+    const int step = static_cast<int>(blockDim.x);
+    for (int x0 = tid; x0 < E; x0 += 2 * step) {
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int x = x0 + u * step;
+        if (x >= E) break;
+        int lo = 0, hi = R;
+        while (hi - lo > 1) {
+          const int mid = (lo + hi) >> 1;
+          if (rowoff[mid] <= x) lo = mid;
+          else hi = mid;
+        }
+        const int rr = lo, g = rr / TM, r = rr % TM;
+        const uint32_t v = buf[x];
+        const uint32_t k = v & 127u, pj = v >> 7;
+        int rank = 0;
+        for (int y = rowoff[rr]; y < x; ++y) rank += (buf[y] & 127u) == k;
+        int a = 0, b = H;
+        while (a < b) {
+          const int mid = (a + b) >> 1;
+          if (hal[mid] < pj) a = mid + 1;
+          else b = mid;
+        }
+        const int idx = (g * K + static_cast<int>(k)) * TM + r;
+        reinterpret_cast<uint16_t*>(blocks + s_boff[g * K + k] + 512)[eoff[idx] + rank] = static_cast<uint16_t>(a);
+      }
+    }
+  } else if (plain) {
     for (int rr = warp; rr < R; rr += nwarps) {
       const int g = rr / TM, r = rr % TM;
       const int n = rowoff[rr + 1] - rowoff[rr];
@@ -583,7 +678,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
           int hi = H;
           while (lo < hi) {
             const int mid = (lo + hi) >> 1;
-            if (buf[mid] < pj) lo = mid + 1;
+            if (halo[mid] < pj) lo = mid + 1;
             else hi = mid;
           }
         }
@@ -607,7 +702,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
       int lo = 0, hi = H;
       while (lo < hi) {
         const int mid = (lo + hi) >> 1;
-        if (buf[mid] < pj) lo = mid + 1;
+        if (halo[mid] < pj) lo = mid + 1;
         else hi = mid;
       }
       const int idx = (g * K + k) * TM + r;
@@ -617,6 +712,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
     });
   }
   __syncthreads();
+  if (pdbg && tid == 0) pdbg[s * 8 + 4] = clock64();
   // 7. in quads whose rows have at most one entry (the copy pass), a row's
   //    item carries its entry's halo index instead of the entry offset
   for (int b = warp; b < nsub * K; b += blockDim.x / 32) {
@@ -631,6 +727,10 @@ __global__ void __launch_bounds__(512) k_plan_super(
     }
   }
   if (tid == 0) halo_len[s] = static_cast<uint32_t>(H);
+  if (pdbg) {
+    __syncthreads();
+    if (tid == 0) pdbg[s * 8 + 5] = clock64();
+  }
 }
 
 __global__ void k_add_u32(uint32_t* __restrict__ p, int64_t n, uint32_t add) {
@@ -656,7 +756,7 @@ struct PlanLevel {
 
 static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, const uint32_t* col,
                        const uint32_t* kk, const uint32_t* perm_rows, const uint32_t* inv_perm_cols,
-                       int K, int st, int hcap) {
+                       int K, int st, int hcap, bool packed) {
   const int ns = static_cast<int>(L.sup.size()), nt = static_cast<int>(L.tiles.size());
   if (L.tfilter.empty()) L.tfilter.assign(nt, no_filter());
   DevBuf<uint2> d_sup(ctx, ns), d_tiles(ctx, nt);
@@ -687,6 +787,13 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   L.halo.alloc(ctx, static_cast<int64_t>(ns) * hcap);
   L.halo_len.alloc(ctx, ns);
   const size_t smem = maxe_of(st) * 4 + 2 * static_cast<size_t>(st) * K * TM * 2 + (st * TM + 1) * 4;
+  // NPCG_PLAN_PROFILE=1: per-phase clocks of k_plan_super (stderr, mean over records)
+  static const bool prof = std::getenv("NPCG_PLAN_PROFILE") != nullptr;
+  DevBuf<unsigned long long> pdbg;
+  if (prof) {
+    pdbg.alloc(ctx, static_cast<int64_t>(ns) * 8);
+    NPCG_CUDA(cudaMemsetAsync(pdbg.get(), 0, static_cast<size_t>(ns) * 64, ctx->stream));
+  }
   NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
   launch(ctx, "plan_super", k_plan_super, dim3(ns), dim3(512), smem, row_ptr, col, kk, perm_rows,
@@ -694,7 +801,7 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
          static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K, st,
          hcap,
          static_cast<const uint32_t*>(L.blk_off.get()), static_cast<const uint32_t*>(sub_bad.get()),
-         L.halo.get(), L.halo_len.get(), d_seg.get(), L.blocks.get());
+         L.halo.get(), L.halo_len.get(), d_seg.get(), L.blocks.get(), packed ? 1 : 0, pdbg.get());
   L.hl.resize(ns);
   L.maxc.resize(nt);
   NPCG_CUDA(cudaMemcpyAsync(L.hl.data(), L.halo_len.get(), ns * 4, cudaMemcpyDeviceToHost,
@@ -706,6 +813,23 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   NPCG_CUDA(cudaMemcpyAsync(L.seg.data(), d_seg.get(), L.seg.size() * 4, cudaMemcpyDeviceToHost,
                             ctx->stream));
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (prof && ns) {
+    std::vector<unsigned long long> h(static_cast<size_t>(ns) * 8);
+    NPCG_CUDA(cudaMemcpy(h.data(), pdbg.get(), h.size() * 8, cudaMemcpyDeviceToHost));
+    double acc[6] = {0, 0, 0, 0, 0, 0};
+    int m = 0;
+    for (int x = 0; x < ns; ++x) {
+      const unsigned long long* c = &h[static_cast<size_t>(x) * 8];
+      if (!c[5] || !c[6]) continue;  // (overflowed records return early)
+      const unsigned long long v[6] = {c[6], c[0], c[1], c[2], c[3], c[4]};
+      for (int q = 0; q < 5; ++q) acc[q] += static_cast<double>(v[q + 1] - v[q]);
+      acc[5] += static_cast<double>(c[5] - c[4]);
+      ++m;
+    }
+    std::fprintf(stderr, "[npcg plan profile] st %d records %d (complete %d), mean cycles: rows %.0f ids %.0f "
+                 "halo %.0f items %.0f entries %.0f copyfix %.0f\n", st, ns, m, acc[0] / m, acc[1] / m,
+                 acc[2] / m, acc[3] / m, acc[4] / m, acc[5] / m);
+  }
 }
 
 // entries per kernel cell: shared-memory histogram of the structure's cells
@@ -731,6 +855,9 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
                                                  const std::vector<int64_t>& row_batches, int K,
                                                  int st, int hcap) {
   auto P = std::make_unique<TcDirPlan>();
+  static const bool hprof = std::getenv("NPCG_PLAN_PROFILE") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  auto hms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(); };
   P->st = st;
   P->hcap = hcap;
   P->n_rows = n_rows;
@@ -786,7 +913,11 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
     NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
   };
   for (size_t li = 0; li < lv.size(); ++li) {
-    plan_level(ctx, lv[li], row_ptr, col, kk, perm_rows, inv_perm_cols, K, st, hcap);
+    // entries packed as (column << 7 | cell) in the planner's smem when they fit
+    if (hprof) std::fprintf(stderr, "[npcg plan host] %.3f ms: level %zu start\n", hms(), li);
+    plan_level(ctx, lv[li], row_ptr, col, kk, perm_rows, inv_perm_cols, K, st, hcap,
+               n_cols <= (int64_t(1) << 25) && K <= 128);
+    if (hprof) std::fprintf(stderr, "[npcg plan host] %.3f ms: level %zu planned\n", hms(), li);
     PlanLevel seg_items, halves, ranks;
     seg_items.kind = 2;
     ranks.kind = 1;
@@ -983,6 +1114,7 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
   P->k_count.assign(K, 0);
   NPCG_CUDA(cudaMemcpyAsync(P->k_count.data(), kc.get(), K * 8, cudaMemcpyDeviceToHost, ctx->stream));
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));  // host vectors go out of scope
+  if (hprof) std::fprintf(stderr, "[npcg plan host] %.3f ms: plan done (%d records)\n", hms(), P->n_super);
   return P;
 }
 

@@ -22,6 +22,9 @@
 
 #include "neighbors.cuh"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace npcg {
 
 constexpr uint32_t kEmpty = 0xFFFFFFFFu;
@@ -534,9 +537,67 @@ void csr_from_triplets(npcg_context* ctx, const npcg_triplets* T, bool transpose
   csr_build(ctx, transpose ? T->j : T->i, transpose ? T->i : T->j, T->k, T->size, n_rows, out);
 }
 
+// Same-cloud handles: the radius relation is symmetric (d2 is computed from
+// coordinate differences whose negation is exact, and the probe covers the same
+// 27 cells), so row j of the transposed structure lists exactly row j's
+// neighbours, i ascending: the forward arrays themselves.  Only the cells
+// differ (k belongs to the pair (i, j): j relative to centre i), found by a
+// binary search of j in forward row i.  A warp per row, rows in spatial order
+// (neighbouring rows share most of their rows i: L2 hits).
+__global__ void k_tcsr_cells(const int64_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                             const uint32_t* __restrict__ kk, const uint32_t* __restrict__ perm,
+                             int64_t n, uint32_t* __restrict__ out_k, int* __restrict__ missing) {
+  const int64_t w = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= n) return;
+  const uint32_t j = perm[w];
+  const int64_t e0 = row_ptr[j], e1 = row_ptr[j + 1];
+  for (int64_t e = e0 + lane; e < e1; e += 32) {
+    const uint32_t i = col[e];
+    int64_t lo = row_ptr[i], hi = row_ptr[i + 1];
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (col[mid] < j) lo = mid + 1;
+      else hi = mid;
+    }
+    if (lo < row_ptr[i + 1] && col[lo] == j) out_k[e] = kk[lo];
+    else *missing = 1;
+  }
+}
+
+static bool tcsr_sort_forced() {
+  const char* e = std::getenv("NPCG_TCSR_SORT");  // (A/B and tests: the radix-sort build)
+  return e && std::strcmp(e, "1") == 0;
+}
+
 void build_tcsr(npcg_context* ctx, npcg_neighbors* nb) {
   if (nb->tcsr) return;
   auto p = std::make_unique<CsrPlan>();
+  if (nb->same_cloud && !nb->degraded && nb->t > 0 && !tcsr_sort_forced()) {
+    const int64_t n = nb->n_out, nnz = nb->n_pairs;
+    p->n_rows = n;
+    p->nnz = nnz;
+    p->row_ptr.alloc(ctx, n + 1);
+    p->col.alloc(ctx, nnz);
+    p->k.alloc(ctx, nnz);
+    NPCG_CUDA(cudaMemcpyAsync(p->row_ptr.get(), nb->row_ptr.get(), (n + 1) * 8, cudaMemcpyDeviceToDevice,
+                              ctx->stream));
+    if (nnz) {
+      NPCG_CUDA(cudaMemcpyAsync(p->col.get(), nb->col_j.get(), nnz * 4, cudaMemcpyDeviceToDevice, ctx->stream));
+      DevBuf<int> missing(ctx, 1);
+      NPCG_CUDA(cudaMemsetAsync(missing.get(), 0, 4, ctx->stream));
+      launch(ctx, "tcsr_cells", k_tcsr_cells, dim3(static_cast<unsigned>(ceil_div(n * 32, 256))), dim3(256), 0,
+             static_cast<const int64_t*>(nb->row_ptr.get()), static_cast<const uint32_t*>(nb->col_j.get()),
+             static_cast<const uint32_t*>(nb->col_k.get()), static_cast<const uint32_t*>(nb->perm_out.get()), n,
+             p->k.get(), missing.get());
+      int h = 0;
+      NPCG_CUDA(cudaMemcpyAsync(&h, missing.get(), 4, cudaMemcpyDeviceToHost, ctx->stream));
+      NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+      if (h) fail(NPCG_ERR_STATE, "transposed structure: asymmetric same-cloud neighbor relation");
+    }
+    nb->tcsr = std::move(p);
+    return;
+  }
   DevBuf<uint32_t> ei(ctx, nb->n_pairs);
   if (nb->n_pairs) expand_rows_u32(ctx, nb->row_ptr.get(), nb->n_out, ei.get());
   // stable by j over the (i, j)-ordered list -> rows over j with i ascending
