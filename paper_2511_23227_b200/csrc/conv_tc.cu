@@ -293,6 +293,21 @@ __device__ __forceinline__ void for_row_entries(const int64_t* row_ptr, const ui
   }
 }
 
+// Lockstep branchless searches for U keys at once (the same trip count for
+// every key, so their shared-memory loads are in flight together): the last
+// index i in [0, n) with a[i] <= key[u] (a sorted ascending, a[0] <= key).
+template <int U, typename T, typename K>
+__device__ __forceinline__ void last_le(const T* a, int n, const K (&key)[U], int (&out)[U]) {
+#pragma unroll
+  for (int u = 0; u < U; ++u) out[u] = 0;
+  while (n > 1) {
+    const int half = n >> 1;
+#pragma unroll
+    for (int u = 0; u < U; ++u) out[u] = static_cast<K>(a[out[u] + half]) <= key[u] ? out[u] + half : out[u];
+    n -= half;
+  }
+}
+
 // Per super-tile: halo (sorted unique permuted neighbor rows), per-(sub-tile,
 // cell) item lists (rows ordered by entry count, descending) and u16 halo
 // indices of the entries.  Block layout: u32 item[128] | u16 entry[E] (pad 16 B)
@@ -404,25 +419,25 @@ __global__ void __launch_bounds__(512) k_plan_super(
   const bool pk = plain && packed != 0;
   if (pk) {
     // flattened over the super-tile's entries, four per thread in flight
-    auto row_of = [&](int x) {  // last rr with rowoff[rr] <= x
-      int lo = 0, hi = R;
-      while (hi - lo > 1) {
-        const int mid = (lo + hi) >> 1;
-        if (rowoff[mid] <= x) lo = mid;
-        else hi = mid;
-      }
-      return lo;
-    };
-    const int step = static_cast<int>(blockDim.x);
-    for (int x0 = tid; x0 < E; x0 += 4 * step) {
-      int rr[4];
+    // warp-contiguous chunks of 32 entries (coalesced CSR reads), four chunks
+    // per warp in flight; a lane's row from its chunk's first row (searched in
+    // lockstep) and a short forward step
+    for (int cb0 = 32 * warp; cb0 < E; cb0 += 4 * 32 * nwarps) {
+      int cbs[4], r0[4], rr[4];
       int64_t e[4];
       uint32_t c[4], k[4];
 #pragma unroll
+      for (int u = 0; u < 4; ++u) cbs[u] = min(cb0 + u * 32 * nwarps, E - 1);
+      last_le<4>(rowoff, R, cbs, r0);
+#pragma unroll
       for (int u = 0; u < 4; ++u) {
-        const int x = x0 + u * step;
-        rr[u] = x < E ? row_of(x) : 0;
-        e[u] = x < E ? rowe0[rr[u]] + (x - rowoff[rr[u]]) : -1;
+        const int x = cb0 + u * 32 * nwarps + lane;
+        rr[u] = r0[u];
+        e[u] = -1;
+        if (x < E) {
+          while (rowoff[rr[u] + 1] <= x) ++rr[u];
+          e[u] = rowe0[rr[u]] + (x - rowoff[rr[u]]);
+        }
       }
 #pragma unroll
       for (int u = 0; u < 4; ++u)
@@ -437,7 +452,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
       for (int u = 0; u < 4; ++u)
         if (e[u] >= 0) {
           const int g = rr[u] / TM, r = rr[u] % TM;
-          buf[x0 + u * step] = (c[u] << 7) | k[u];
+          buf[cb0 + u * 32 * nwarps + lane] = (c[u] << 7) | k[u];
           const int idx = (g * K + static_cast<int>(k[u])) * TM + r;
           atomicAdd(reinterpret_cast<unsigned*>(cnt) + (idx >> 1), 1u << (16 * (idx & 1)));
         }
@@ -469,7 +484,7 @@ __global__ void __launch_bounds__(512) k_plan_super(
     for (int size = 2; size <= P; size <<= 1) {
       for (int stride = size >> 1; stride > 0; stride >>= 1) {
         for (int x = tid; x < (P >> 1); x += blockDim.x) {
-          const int lo = 2 * stride * (x / stride) + (x % stride);
+          const int lo = ((x & ~(stride - 1)) << 1) | (x & (stride - 1));  // (stride: a power of two)
           const int hi = lo + stride;
           const bool up = (lo & size) == 0;
           const uint32_t a = v[lo], b = v[hi];
@@ -632,34 +647,39 @@ __global__ void __launch_bounds__(512) k_plan_super(
   // 6. entries: halo index of each neighbor, written at its item's offset
   //    (in CSR order within each (row, cell))
   if (pk) {
-    // flattened: each thread places its entries independently (all reads from
-    // shared memory); the rank of an entry within its (row, cell) is the
-    // number of earlier entries of the row with the same cell (CSR order)
-    const int step = static_cast<int>(blockDim.x);
-    for (int x0 = tid; x0 < E; x0 += 2 * step) {
+    // warp-contiguous chunks of 32 entries (all reads from shared memory, two
+    // chunks per warp with their searches in lockstep): the rank of an entry
+    // within its (row, cell) -- CSR order -- is its rank among the chunk's
+    // entries of the same (row, cell) plus the row's entries of that cell
+    // before the chunk
+    for (int cb0 = 32 * warp; cb0 < E; cb0 += 2 * 32 * nwarps) {
+      int cbs[2], r0[2], rr[2], hx[2];
+      uint32_t v[2], pj[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) cbs[u] = min(cb0 + u * 32 * nwarps, E - 1);
+      last_le<2>(rowoff, R, cbs, r0);
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const int x = x0 + u * step;
-        if (x >= E) break;
-        int lo = 0, hi = R;
-        while (hi - lo > 1) {
-          const int mid = (lo + hi) >> 1;
-          if (rowoff[mid] <= x) lo = mid;
-          else hi = mid;
-        }
-        const int rr = lo, g = rr / TM, r = rr % TM;
-        const uint32_t v = buf[x];
-        const uint32_t k = v & 127u, pj = v >> 7;
-        int rank = 0;
-        for (int y = rowoff[rr]; y < x; ++y) rank += (buf[y] & 127u) == k;
-        int a = 0, b = H;
-        while (a < b) {
-          const int mid = (a + b) >> 1;
-          if (hal[mid] < pj) a = mid + 1;
-          else b = mid;
-        }
+        const int x = min(cb0 + u * 32 * nwarps + lane, E - 1);
+        rr[u] = r0[u];
+        while (rowoff[rr[u] + 1] <= x) ++rr[u];
+        v[u] = buf[x];
+        pj[u] = v[u] >> 7;
+      }
+      last_le<2>(hal, H, pj, hx);  // the entries' halo indices (their rows are in the halo)
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int cb = cb0 + u * 32 * nwarps, x = cb + lane;
+        const bool act = x < E;
+        const uint32_t k = v[u] & 127u;
+        const unsigned same = __match_any_sync(0xffffffffu, act ? static_cast<int>(rr[u] * 128 + k) : -1);
+        if (!act) continue;
+        int rank = __popc(same & lt_mask);
+        for (int y = rowoff[rr[u]]; y < cb; ++y) rank += (buf[y] & 127u) == k;
+        const int g = rr[u] / TM, r = rr[u] % TM;
         const int idx = (g * K + static_cast<int>(k)) * TM + r;
-        reinterpret_cast<uint16_t*>(blocks + s_boff[g * K + k] + 512)[eoff[idx] + rank] = static_cast<uint16_t>(a);
+        reinterpret_cast<uint16_t*>(blocks + s_boff[g * K + k] + 512)[eoff[idx] + rank] =
+            static_cast<uint16_t>(hx[u]);
       }
     }
   } else if (plain) {
@@ -758,6 +778,10 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
                        const uint32_t* kk, const uint32_t* perm_rows, const uint32_t* inv_perm_cols,
                        int K, int st, int hcap, bool packed) {
   const int ns = static_cast<int>(L.sup.size()), nt = static_cast<int>(L.tiles.size());
+  static const bool hprof = std::getenv("NPCG_PLAN_PROFILE") != nullptr;
+  const auto h0 = std::chrono::steady_clock::now();
+  auto hms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count(); };
+  double tm[6] = {0, 0, 0, 0, 0, 0};
   if (L.tfilter.empty()) L.tfilter.assign(nt, no_filter());
   DevBuf<uint2> d_sup(ctx, ns), d_tiles(ctx, nt);
   DevBuf<uint4> d_filt(ctx, nt);
@@ -782,7 +806,9 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
          perm_rows, static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K,
          blk_size.get(), sub_bad.get(), d_maxc.get(), d_maxblk.get());
   L.blk_off.alloc(ctx, nblk + 1);
+  if (hprof) tm[0] = hms();
   exclusive_scan_u32(ctx, blk_size.get(), L.blk_off.get(), nblk + 1, &L.block_units);
+  if (hprof) tm[1] = hms();
   L.blocks.alloc(ctx, static_cast<int64_t>(blk_bytes(L.block_units)));
   L.halo.alloc(ctx, static_cast<int64_t>(ns) * hcap);
   L.halo_len.alloc(ctx, ns);
@@ -796,6 +822,7 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   }
   NPCG_CUDA(cudaFuncSetAttribute(k_plan_super, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(smem)));
+  if (hprof) tm[2] = hms();
   launch(ctx, "plan_super", k_plan_super, dim3(ns), dim3(512), smem, row_ptr, col, kk, perm_rows,
          inv_perm_cols, static_cast<const uint2*>(d_sup.get()),
          static_cast<const uint2*>(d_tiles.get()), static_cast<const uint4*>(d_filt.get()), K, st,
@@ -812,7 +839,11 @@ static void plan_level(npcg_context* ctx, PlanLevel& L, const int64_t* row_ptr, 
   L.seg.resize(static_cast<size_t>(ns) * (MAXSEG + 1));
   NPCG_CUDA(cudaMemcpyAsync(L.seg.data(), d_seg.get(), L.seg.size() * 4, cudaMemcpyDeviceToHost,
                             ctx->stream));
+  if (hprof) tm[3] = hms();
   NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+  if (hprof)
+    std::fprintf(stderr, "[npcg plan host] level: counts issued %.3f, scan synced %.3f, super issued %.3f, "
+                 "readback issued %.3f, synced %.3f ms\n", tm[0], tm[1], tm[2], tm[3], hms());
   if (prof && ns) {
     std::vector<unsigned long long> h(static_cast<size_t>(ns) * 8);
     NPCG_CUDA(cudaMemcpy(h.data(), pdbg.get(), h.size() * 8, cudaMemcpyDeviceToHost));
@@ -954,7 +985,10 @@ static std::unique_ptr<TcDirPlan> build_dir_plan(npcg_context* ctx, const int64_
       const uint32_t nom = L.nom[sp.x];
       if (L.kind == 0) {
         const uint32_t* sg = &L.seg[x * (MAXSEG + 1)];
-        if (sg[0] >= 2) {  // halo too large only: one item of segment records
+        // halo too large only: a super-tile of several sub-tiles is re-tiled
+        // first (halves: half the stages of segment records, and planned on
+        // the plain path); a single tile becomes one item of segment records
+        if (sg[0] >= 2 && (nsub == 1 || std::getenv("NPCG_PLAN_SEGMENTS_FIRST"))) {
           const uint32_t nseg = sg[0];
           for (uint32_t q = 0; q < nseg; ++q) {
             const uint32_t fl = (q == 0 ? SUP_FIRST : 0u) | (q + 1 == nseg ? SUP_LAST : 0u);
