@@ -140,6 +140,17 @@ __global__ void k_cell_scatter(const uint32_t* __restrict__ cell_of_pt, int64_t 
   cell_pts[cell_start[h] + atomicAdd(&cell_fill[h], 1u)] = static_cast<uint32_t>(p);
 }
 
+// target coordinates in cell order (a cell's candidates are contiguous: the
+// probe loop reads them without the index indirection)
+__global__ void k_gather_xyz(const uint32_t* __restrict__ cell_pts, const double* __restrict__ xyz, int64_t n,
+                             double* __restrict__ sxyz) {
+  const int64_t q = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  if (q >= n) return;
+  const int64_t p = cell_pts[q];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) sxyz[3 * q + a] = xyz[3 * p + a];
+}
+
 __device__ __forceinline__ int64_t find_cell(const longlong4& probe,
                                              const uint32_t* __restrict__ slots, uint64_t mask,
                                              const longlong4* __restrict__ keys) {
@@ -153,14 +164,23 @@ __device__ __forceinline__ int64_t find_cell(const longlong4& probe,
 }
 
 // triplets.cpp:30-51 -- exact fp64 recipe, no contraction.
+// The IEEE quotient is only needed when x / cell lies within rounding distance
+// of an integer (floor could differ); elsewhere floor of x * (1 / cell) is the
+// same integer (relative error < 2^-50 on |u| <= t + 1, margin 2^-30).
+__device__ __forceinline__ double cell_floor(double x, double cell, double inv_cell) {
+  const double q = __dmul_rn(x, inv_cell);
+  const double f = floor(q);
+  if (q - f > 0x1p-30 && f + 1.0 - q > 0x1p-30) return f;
+  return floor(__ddiv_rn(x, cell));
+}
 __device__ __forceinline__ int64_t kernel_cell(const double* __restrict__ center,
                                                const double* __restrict__ nbr, double radius,
-                                               int64_t t, double cell) {
+                                               int64_t t, double cell, double inv_cell) {
   int64_t idx[3];
 #pragma unroll
   for (int a = 0; a < 3; ++a) {
-    const double u = __ddiv_rn(__dadd_rn(__dsub_rn(nbr[a], center[a]), radius), cell);
-    int64_t c = static_cast<int64_t>(floor(u));
+    const double u = cell_floor(__dadd_rn(__dsub_rn(nbr[a], center[a]), radius), cell, inv_cell);
+    int64_t c = static_cast<int64_t>(u);
     c = c < 0 ? 0 : (c > t - 1 ? t - 1 : c);
     idx[a] = c;
   }
@@ -174,6 +194,7 @@ struct Grid {
   const uint32_t* cell_start;
   const uint32_t* cell_cnt;
   const uint32_t* cell_pts;
+  const double* sxyz;  // target coordinates in cell_pts order
 };
 
 // Count (FILL=false) or fill (FILL=true) the neighbors of each query.
@@ -186,7 +207,10 @@ __global__ void __launch_bounds__(256) k_query(const double* __restrict__ qxyz,
                                                int64_t* __restrict__ counts,
                                                const int64_t* __restrict__ row_ptr,
                                                uint32_t* __restrict__ out_j,
-                                               uint32_t* __restrict__ out_k) {
+                                               uint32_t* __restrict__ out_k,
+                                               uint32_t* __restrict__ scr_j,
+                                               uint32_t* __restrict__ scr_k, int cap,
+                                               int* __restrict__ scr_over) {
   const int64_t s = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (s >= nq) return;
   const int64_t i = qorder ? qorder[s] : s;
@@ -196,6 +220,7 @@ __global__ void __launch_bounds__(256) k_query(const double* __restrict__ qxyz,
   const int64_t cx = cell_of(q[0], radius), cy = cell_of(q[1], radius),
                 cz = cell_of(q[2], radius);
   const double kcell = t > 0 ? __ddiv_rn(__dmul_rn(2.0, radius), static_cast<double>(t)) : 1.0;
+  const double kinv = __drcp_rn(kcell);
   int64_t pos = 0;
   if (FILL) pos = row_ptr[i];
   int64_t cnt = 0;
@@ -207,32 +232,45 @@ __global__ void __launch_bounds__(256) k_query(const double* __restrict__ qxyz,
         if (h < 0) continue;
         const uint32_t s0 = g.cell_start[h], n0 = g.cell_cnt[h];
         for (uint32_t e = 0; e < n0; ++e) {
-          const uint32_t p = g.cell_pts[s0 + e];
-          const double* tp = txyz + 3 * static_cast<int64_t>(p);
+          const double* tp = g.sxyz + 3 * static_cast<int64_t>(s0 + e);
           const double ddx = __dsub_rn(q[0], tp[0]);
           const double ddy = __dsub_rn(q[1], tp[1]);
           const double ddz = __dsub_rn(q[2], tp[2]);
           const double d2 = __fma_rn(ddz, ddz, __fma_rn(ddx, ddx, __dmul_rn(ddy, ddy)));
           if (r2 >= d2) {
+            const uint32_t p = g.cell_pts[s0 + e];
             if (FILL) {
               out_j[pos + cnt] = p;
-              if (t > 0) out_k[pos + cnt] = static_cast<uint32_t>(kernel_cell(q, tp, radius, t, kcell));
+              if (t > 0) out_k[pos + cnt] = static_cast<uint32_t>(kernel_cell(q, tp, radius, t, kcell, kinv));
+            } else if (scr_j && cnt < cap) {  // one-pass build: the hits of row i at i * cap
+              scr_j[i * cap + cnt] = p;
+              if (t > 0) scr_k[i * cap + cnt] = static_cast<uint32_t>(kernel_cell(q, tp, radius, t, kcell, kinv));
             }
             ++cnt;
           }
         }
       }
-  if (!FILL) counts[i] = cnt;
+  if (!FILL) {
+    counts[i] = cnt;
+    if (scr_over && cnt > cap) *scr_over = 1;
+  }
 }
 
 // Rank-sort each row by j (j values are unique within a row).
+// (in_stride > 0: row r's input entries start at r * in_stride -- the one-pass
+// build's per-row scratch -- instead of at its CSR position)
 __global__ void k_sort_rows(const int64_t* __restrict__ row_ptr, int64_t n_rows,
                             const uint32_t* __restrict__ in_j, const uint32_t* __restrict__ in_k,
-                            uint32_t* __restrict__ out_j, uint32_t* __restrict__ out_k) {
+                            uint32_t* __restrict__ out_j, uint32_t* __restrict__ out_k,
+                            int64_t in_stride) {
   const int64_t row = (static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (row >= n_rows) return;
   const int64_t s = row_ptr[row], len = row_ptr[row + 1] - s;
+  if (in_stride) {  // shift the inputs so that in_j[s + x] is the row's x-th scratch entry
+    in_j += row * in_stride - s;
+    if (in_k) in_k += row * in_stride - s;
+  }
   if (len <= 32) {
     const uint32_t mine = lane < len ? in_j[s + lane] : 0xFFFFFFFFu;
     uint32_t rank = 0;
@@ -382,15 +420,33 @@ void build_neighbors(npcg_context* ctx, const npcg_cloud* qc, const npcg_cloud* 
   launch(ctx, "cell_scatter", k_cell_scatter, dim3(tb), dim3(256), 0,
          static_cast<const uint32_t*>(cell_of_pt.get()), nt,
          static_cast<const uint32_t*>(cell_start.get()), cell_fill.get(), cell_pts.get());
-  Grid g{slots.get(), hsize - 1, keys.get(), cell_start.get(), cell_cnt.get(), cell_pts.get()};
+  DevBuf<double> sxyz(ctx, nt * 3);
+  launch(ctx, "gather_xyz", k_gather_xyz, dim3(tb), dim3(256), 0, static_cast<const uint32_t*>(cell_pts.get()),
+         tc->xyz, nt, sxyz.get());
+  Grid g{slots.get(), hsize - 1, keys.get(), cell_start.get(), cell_cnt.get(), cell_pts.get(), sxyz.get()};
 
-  // 3: count
+  // 3: count (and, when the scratch fits, keep the hits: one-pass build)
   DevBuf<int64_t> counts(ctx, nq);
   const unsigned qb = static_cast<unsigned>(ceil_div(nq, 256));
+  constexpr int kCap = 64;  // hits kept per query (more: the two-pass fill below)
+  const bool one_pass = static_cast<uint64_t>(nq) * kCap * 8 <= (uint64_t(4) << 30);
+  DevBuf<uint32_t> scr_j, scr_k;
+  DevBuf<int> scr_over;
+  int h_over = 1;
+  if (one_pass) {
+    scr_j.alloc(ctx, nq * kCap);
+    if (t > 0) scr_k.alloc(ctx, nq * kCap);
+    scr_over.alloc(ctx, 1);
+    NPCG_CUDA(cudaMemsetAsync(scr_over.get(), 0, sizeof(int), ctx->stream));
+  }
   launch(ctx, "radius_count", k_query<false>, dim3(qb), dim3(256), 0, qc->xyz,
          static_cast<const uint32_t*>(qbid.get()), static_cast<const uint32_t*>(nb->perm_out.get()),
          nq, tc->xyz, g, radius, t, counts.get(), static_cast<const int64_t*>(nullptr),
-         static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr));
+         static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), scr_j.get(),
+         t > 0 ? scr_k.get() : static_cast<uint32_t*>(nullptr), kCap,
+         one_pass ? scr_over.get() : static_cast<int*>(nullptr));
+  if (one_pass)
+    NPCG_CUDA(cudaMemcpyAsync(&h_over, scr_over.get(), sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
   int64_t total = 0;
   exclusive_scan_i64(ctx, counts.get(), nb->row_ptr.get(), nq, &total);
   NPCG_CUDA(cudaMemcpyAsync(nb->row_ptr.get() + nq, &total, sizeof(int64_t),
@@ -398,19 +454,28 @@ void build_neighbors(npcg_context* ctx, const npcg_cloud* qc, const npcg_cloud* 
   nb->n_pairs = total;
   if (total > 0xFFFFFFFFll * 64) fail(NPCG_ERR_SHAPE, "radius_search: pair count too large");
 
+  nb->col_j.alloc(ctx, total);
+  if (t > 0) nb->col_k.alloc(ctx, total);
+  if (one_pass && h_over == 0) {  // every row's hits are in the scratch: rank them by j
+    launch(ctx, "sort_rows", k_sort_rows, dim3(static_cast<unsigned>(ceil_div(nq * 32, 256))), dim3(256), 0,
+           static_cast<const int64_t*>(nb->row_ptr.get()), nq, static_cast<const uint32_t*>(scr_j.get()),
+           t > 0 ? static_cast<const uint32_t*>(scr_k.get()) : static_cast<const uint32_t*>(nullptr),
+           nb->col_j.get(), t > 0 ? nb->col_k.get() : static_cast<uint32_t*>(nullptr),
+           static_cast<int64_t>(kCap));
+    return;
+  }
   // 4: fill (j, k) in probe order, 5: rank rows by j
   DevBuf<uint32_t> tmp_j(ctx, total), tmp_k(ctx, t > 0 ? total : 0);
   launch(ctx, "radius_fill", k_query<true>, dim3(qb), dim3(256), 0, qc->xyz,
          static_cast<const uint32_t*>(qbid.get()), static_cast<const uint32_t*>(nb->perm_out.get()),
          nq, tc->xyz, g, radius, t, static_cast<int64_t*>(nullptr),
-         static_cast<const int64_t*>(nb->row_ptr.get()), tmp_j.get(), tmp_k.get());
-  nb->col_j.alloc(ctx, total);
-  if (t > 0) nb->col_k.alloc(ctx, total);
+         static_cast<const int64_t*>(nb->row_ptr.get()), tmp_j.get(), tmp_k.get(),
+         static_cast<uint32_t*>(nullptr), static_cast<uint32_t*>(nullptr), 0, static_cast<int*>(nullptr));
   launch(ctx, "sort_rows", k_sort_rows, dim3(static_cast<unsigned>(ceil_div(nq * 32, 256))),
          dim3(256), 0, static_cast<const int64_t*>(nb->row_ptr.get()), nq,
          static_cast<const uint32_t*>(tmp_j.get()),
          t > 0 ? static_cast<const uint32_t*>(tmp_k.get()) : static_cast<const uint32_t*>(nullptr),
-         nb->col_j.get(), t > 0 ? nb->col_k.get() : static_cast<uint32_t*>(nullptr));
+         nb->col_j.get(), t > 0 ? nb->col_k.get() : static_cast<uint32_t*>(nullptr), static_cast<int64_t>(0));
 }
 
 // ---------------------------------------------------------------------------
@@ -421,7 +486,7 @@ __global__ void k_kernel_index(const double* __restrict__ c, const double* __res
   const int64_t p = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
   if (p >= n) return;
   const double cell = __ddiv_rn(__dmul_rn(2.0, radius), static_cast<double>(t));
-  k[p] = kernel_cell(c + 3 * p, nbr + 3 * p, radius, t, cell);
+  k[p] = kernel_cell(c + 3 * p, nbr + 3 * p, radius, t, cell, __drcp_rn(cell));
 }
 void kernel_index_batch(npcg_context* ctx, const double* c, const double* nbr, int64_t n,
                         double radius, int64_t t, int64_t* k) {
