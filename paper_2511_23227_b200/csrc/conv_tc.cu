@@ -2407,11 +2407,12 @@ __global__ void k_wgrad_reduce_split(const float* __restrict__ partial, int n_pa
 // exceeds one SM's TMEM, so the two CTAs of a cluster take the same
 // super-tiles and half of the cells each (14 / 13); each keeps 7 column blocks
 // of two cells (448 columns) + the 64-column input-gradient accumulator.
-// The two halves' input-gradient sums meet in global memory: the half-0 CTA
-// stores its sum, publishes a per-(item, quadrant) flag (release), and the
-// half-1 CTA, once it sees the flag (acquire), adds its sum with
-// red.global.add (a + b in fp32: deterministic; no zero fill of grad_in).
-// Per-pair dW partials are reduced in a fixed order.
+// The two halves' input-gradient sums meet in global memory: grad_in is zeroed
+// and each CTA adds its sum once with red.global.add.v4.f32 (0 + a + b equals
+// 0 + b + a in fp32: deterministic).  (BF_FLAGS=1: the half-0 CTA stores its
+// sum and publishes a per-(item, quadrant) flag, the half-1 CTA adds after
+// seeing it -- no zero fill, but measured slower: the halves wait on each
+// other.)  Per-pair dW partials are reduced in a fixed order.
 // ===========================================================================
 constexpr int BF_STAGES = 14;      // at most this many stages (cells) per record and CTA
 constexpr uint8_t BF_ZERO = 0xFF;  // no cell (the 13-cell half's 14th entry)
@@ -2788,7 +2789,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
                            a.gin + static_cast<int64_t>(a.perm_rows[static_cast<int64_t>(tl.x) + 32 * e + lane]) *
                                        a.gin_cols)
                      : nullptr;
-      uint32_t* flag = a.item_flag + static_cast<int64_t>(w) * 4 + e;
+      uint32_t* flag = BF_FLAGS ? a.item_flag + static_cast<int64_t>(w) * 4 + e : nullptr;
       uint32_t v[4][16];
 #pragma unroll
       for (int q = 0; q < 4; ++q) tmem_ld16(t0 + 16 * q, v[q]);
@@ -3912,14 +3913,16 @@ static void run_fused_backward(npcg_context* ctx, npcg_neighbors* nb, TcPlan* p,
   const int64_t need = static_cast<int64_t>(npairs) * K * 64 * 64;
   if (p->partial.size() < need) p->partial.alloc(ctx, need);
   if (!BF_FLAGS) NPCG_CUDA(cudaMemsetAsync(grad_in, 0, nb->n_in * cin * sizeof(float), ctx->stream));
-  if (p->bf_flags.size() < static_cast<int64_t>(P->n_items) * 4) {
-    p->bf_flags.alloc(ctx, static_cast<int64_t>(P->n_items) * 4);
-    NPCG_CUDA(cudaMemsetAsync(p->bf_flags.get(), 0, P->n_items * 16, ctx->stream));
-    p->bf_gen = 0;
-  }
-  if (++p->bf_gen == 0) {  // wrapped: flags of a previous launch could match
-    NPCG_CUDA(cudaMemsetAsync(p->bf_flags.get(), 0, p->bf_flags.size() * 4, ctx->stream));
-    p->bf_gen = 1;
+  if (BF_FLAGS) {
+    if (p->bf_flags.size() < static_cast<int64_t>(P->n_items) * 4) {
+      p->bf_flags.alloc(ctx, static_cast<int64_t>(P->n_items) * 4);
+      NPCG_CUDA(cudaMemsetAsync(p->bf_flags.get(), 0, P->n_items * 16, ctx->stream));
+      p->bf_gen = 0;
+    }
+    if (++p->bf_gen == 0) {  // wrapped: flags of a previous launch could match
+      NPCG_CUDA(cudaMemsetAsync(p->bf_flags.get(), 0, p->bf_flags.size() * 4, ctx->stream));
+      p->bf_gen = 1;
+    }
   }
   BfArgs a{};
   a.item_flag = p->bf_flags.get();
