@@ -1321,6 +1321,9 @@ constexpr int AGG_GROUP_WARPS = FWD_AGG_WARPS / AGG_GROUPS;
 constexpr int FWD_W_WARP = FWD_AGG_WARP0 + FWD_AGG_WARPS;
 constexpr int FWD_THREADS = 32 * (FWD_W_WARP + 1);
 constexpr int FWD_ST = 2, FWD_HCAP = 928;  // 256-row super-tiles, halo <= 928 rows (116 KB)
+#ifndef FWD_NMAIN
+#define FWD_NMAIN 3  // split path: main accumulator sets (A/B)
+#endif
 constexpr int NSA = 4;  // A stages (16 KB)
 constexpr int NSW = 3;  // W stages (NOUT x 128 B; 2 for NOUT = 256)
 constexpr int NSD = 8;  // stage-descriptor slots (a multiple of AGG_GROUPS)
@@ -1352,9 +1355,11 @@ struct FwdCfg {
   // SPLIT: NMAIN main accumulator sets (hi x hi, cells alternating: short
   // truncating chains, summed in fp32 round-to-nearest by the epilogue) and one
   // correction set, single-buffered; bf16: one set, double-buffered
-  static constexpr int nmain = SPLIT ? 3 : 1;
-  static constexpr int nbuf = SPLIT ? 1 : 2;
-  static constexpr int nsets = SPLIT ? nmain + 1 : 2;
+  static constexpr int nmain = SPLIT ? FWD_NMAIN : 1;
+  static constexpr int bsets = SPLIT ? nmain + 1 : 1;       // accumulator sets per buffer
+  static constexpr int nbuf = 2 * bsets * acc_cols <= 512 ? 2 : 1;
+  static constexpr int nsets = nbuf * bsets;
+  static constexpr uint32_t bstride = bsets * acc_cols;     // TMEM columns per buffer
   static constexpr uint32_t tmem_cols = nsets * acc_cols <= 256 ? 256 : 512;
   static_assert(nsets * acc_cols <= 512, "TMEM");
 };
@@ -1753,8 +1758,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
             // first MMA of the item (first record).
             const int q = c * K + k;
             const int pm = q % nmain;
-            const uint32_t dm = tmem + pm * Cfg::acc_cols + g * NOUT;
-            const uint32_t dc = tmem + Cfg::nmain * Cfg::acc_cols + g * NOUT;
+            const uint32_t dm = tmem + ab * Cfg::bstride + pm * Cfg::acc_cols + g * NOUT;
+            const uint32_t dc = tmem + ab * Cfg::bstride + Cfg::nmain * Cfg::acc_cols + g * NOUT;
             const uint64_t bd2 = bd + (Cfg::wimg >> 4);
             if (elect_one()) {
 #pragma unroll
@@ -1889,7 +1894,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       named_bar_sync(2 + ab, 32 * 5);  // released by the MMA warp once T_FULL(tile) landed
       tc_fence_after();
       for (int g = 0; g < nsub; ++g) {
-        const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * Cfg::acc_cols + g * NOUT;
+        const uint32_t t0 = tmem + (static_cast<uint32_t>(32 * e) << 16) + ab * Cfg::bstride + g * NOUT;
         const uint2 tl = a.tiles[sp.x + g];
         const int64_t row = static_cast<int64_t>(tl.x) + 32 * e + lane;
         float4* o = static_cast<uint32_t>(32 * e + lane) < tl.y
