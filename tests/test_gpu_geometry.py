@@ -152,6 +152,33 @@ def test_matches_reference_directly(npc, ref):
         assert _eq(tl.numpy(), ref.build_triplets(xyz, xyz, r, 3, axis=0))
 
 
+@pytest.mark.parametrize("case", ["sparse", "dense", "mixed"])
+def test_one_pass_build_and_dense_fallback(npc, orc, case):
+    """The neighbor build keeps up to 64 hits per query from its probe pass
+    and ranks them straight from there; a cloud with a longer row takes the
+    two-pass fill.  Both must give the reference's bytes."""
+    rng = np.random.default_rng(7)
+    if case == "sparse":  # ~25 neighbors per row: one pass
+        xyz = orc.gen_uniform_cube(4000, 1.0, 71)
+        r = 1.8 * 4000 ** (-1 / 3)
+    elif case == "dense":  # 100-300 per row: fallback
+        xyz = rng.normal(size=(2500, 3)) * 0.2
+        r = 0.12
+    else:  # mostly sparse plus one dense knot
+        xyz = np.concatenate([orc.gen_uniform_cube(3000, 1.0, 72), 0.5 + rng.normal(size=(200, 3)) * 0.01])
+        r = 1.8 * 3000 ** (-1 / 3)
+    off = np.array([0, len(xyz) // 3, len(xyz)], dtype=np.int64)
+    cl = _cloud(npc, xyz, off)
+    tl = npc.build_triplets_native(cl, cl, npc.ConvGeometry(radius=r, t=3))
+    want = orc.build_triplets(xyz, xyz, r, 3, off, off)
+    assert _eq(tl.numpy(), want), case
+    rows = np.bincount(want[0], minlength=len(xyz))
+    if case == "sparse":
+        assert rows.max() <= 64
+    else:
+        assert rows.max() > 64
+
+
 def test_complete_graph_and_large_rows(npc, orc):
     xyz = orc.gen_uniform_cube(60, 1.0, 35)
     cl = _cloud(npc, xyz)
