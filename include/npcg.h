@@ -89,15 +89,16 @@ typedef enum npcg_sort_axis {
 typedef enum npcg_math {
   NPCG_MATH_AUTO = 0,  /* fp32 contract (rel <= 1e-5): F32 tensors run on the split tensor-core
                           path (F32TC) where it applies (G=1, K<=128, C_in and C_out multiples of
-                          16 in [64, 128]), everything else (fp64, narrow or wide layers) on EXACT */
+                          16 up to 256), everything else (fp64, G>1, other widths) on EXACT */
   NPCG_MATH_EXACT = 1, /* CUDA cores in the API dtype (fp32 / fp64 FMA, fp32 accumulate for F32) */
   NPCG_MATH_BF16 = 2,  /* opt-in: tcgen05 tensor cores, bf16 operands, fp32 accumulate (F32 API
                           only; C_in and C_out multiples of 16 up to 256, zero-padded inside);
                           rel ~2e-3, bound 1e-2 */
-  NPCG_MATH_F32TC = 3  /* tcgen05 with split operands: every fp32 operand x = hi + lo (two bf16),
-                          products hi*hi + hi*lo + lo*hi (+ lo*lo for the weight gradient), fp32
-                          accumulate; rel ~4e-6 (bound 1e-5, the reference's fp32 bound).
-                          C_in, C_out multiples of 16 up to 128 */
+  NPCG_MATH_F32TC = 3  /* tcgen05 with split operands: every fp32 operand, scaled by a power of
+                          two, x s = hi + lo 2^-11 (two fp16), products hi*hi + hi*lo + lo*hi
+                          (+ lo*lo for the weight gradient), fp32 accumulation in short chains;
+                          rel ~1e-6 (bound 1e-5, the reference's fp32 bound).  C_in, C_out
+                          multiples of 16 up to 256 (wider than 128: 128-column halves) */
 } npcg_math;
 
 /* npcg_exec_config.flags */

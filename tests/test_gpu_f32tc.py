@@ -80,8 +80,8 @@ def test_f32tc_strided(npc, ref, orc):
 
 
 def test_auto_is_the_fp32_contract_on_tensor_cores(npc, orc):
-    """math = auto (the default) runs the split kernels for C >= 64 and meets
-    1e-5; C < 64 stays on the exact CUDA-core engines."""
+    """math = auto (the default) runs the split kernels (every multiple of 16
+    up to 256 channels, narrow layers included) and meets 1e-5."""
     n = 6000
     xyz = orc.gen_uniform_cube(n, 1.0, 9)
     ctx = npc.context()

@@ -91,9 +91,10 @@ def test_strided_two_cloud_forward(npc, orc, ref):
     assert up.shape[0] == 6000
 
 
-def test_c1_forward_parity(npc, orc):
-    """BASELINE config 1: 16K points, C=32, fp32 exact vs the fp64 oracle (the
-    automatic engine choice keeps C < 64 on the CUDA cores)."""
+@pytest.mark.parametrize("math", ["auto", "exact"])
+def test_c1_forward_parity(npc, orc, math):
+    """BASELINE config 1: 16K points, C=32, the default fp32 contract (the
+    split tensor-core path) and the exact CUDA-core engine vs the fp64 oracle."""
     n = 16384
     xyz = orc.gen_uniform_cube(n, 1.0, 1)
     r = 1.8 * n ** (-1 / 3)
@@ -102,7 +103,7 @@ def test_c1_forward_parity(npc, orc):
     ti, tj, tk = orc.build_triplets(xyz, xyz, r, 3)
     assert len(ti) == 385924
     fo, _, _ = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, n)
-    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3))
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=getattr(npc.Math, math)))
     out = op.forward(npc.make_point_cloud(xyz), T(f))
     assert rel(out.cpu(), fo) <= 1e-5
 
@@ -263,7 +264,7 @@ def test_bf16_wide_channels(npc, orc, cin, cout):
     output columns per tile; the weight gradient pairs (cell, C_in chunk) A
     tiles against G tiles of C_out columns.  Other multiples of 16 are
     zero-padded to 64 / 128 / 256 (math = bf16 forces narrow widths onto the
-    tensor cores; the automatic choice keeps C < 64 on the exact engines)."""
+    tensor cores; the automatic choice runs them on the split fp32-contract path)."""
     n = 6000
     xyz = orc.gen_uniform_cube(n, 1.0, 31)
     r = 1.8 * n ** (-1 / 3)
