@@ -379,7 +379,10 @@ void build_neighbors(npcg_context* ctx, const npcg_cloud* qc, const npcg_cloud* 
   nb->t = t;
   nb->n_kernels = t > 0 ? t * t * t : 1;
   nb->radius = radius;
-  nb->same_cloud = (qc->xyz == tc->xyz && nq == nt && qc->n_batches == tc->n_batches);
+  // same points and the same batches: the radius relation is symmetric (the
+  // transposed structure and the input spatial order come from the forward's)
+  nb->same_cloud = (qc->xyz == tc->xyz && nq == nt && qc->n_batches == tc->n_batches &&
+                    std::equal(qc->batch_offsets, qc->batch_offsets + qc->n_batches + 1, tc->batch_offsets));
   nb->row_ptr.alloc(ctx, nq + 1);
   NPCG_CUDA(cudaMemsetAsync(nb->row_ptr.get(), 0, (nq + 1) * sizeof(int64_t), ctx->stream));
 
