@@ -1362,10 +1362,13 @@ struct FwdCfg {
   static constexpr uint32_t bstride = bsets * acc_cols;     // TMEM columns per buffer
   static constexpr uint32_t tmem_cols = nsets * acc_cols <= 256 ? 256 : 512;
   static_assert(nsets * acc_cols <= 512, "TMEM");
+  // the halo row list staged in smem by the descriptor producer (room only
+  // beside the 64-column W stages)
+  static constexpr bool hidx = NOUT == 64 && !SPLIT;
 };
 
 struct FwdSmem {
-  uint32_t halo, a, w, d, bar, tmem_slot, offs;
+  uint32_t halo, a, w, d, bar, tmem_slot, offs, hidx;
   size_t total;
 };
 template <int NOUT, bool SPLIT = false>
@@ -1389,6 +1392,9 @@ __host__ __device__ constexpr FwdSmem fwd_smem_layout(int hcap) {
   o += 16;
   L.offs = o;
   o += OFFS_WORDS * 4;  // block offsets of the super-tile, then the slot sources
+  o = (o + 15) & ~15u;
+  L.hidx = o;           // the record's halo row list (bulk-copied ahead by the descriptor producer)
+  if (Cfg::hidx) o += ((hcap * 4 + 15) & ~15);
   L.total = o + 1024;   // alignment slack
   return L;
 }
@@ -1424,7 +1430,7 @@ __device__ __forceinline__ void prefetch_halo_l2(const uint32_t* rows, uint32_t 
 // 8 lanes per 128-byte row (coalesced within runs of consecutive rows).
 // The row indices of a batch are loaded first (independent loads in flight),
 // then the batch's copies are issued.
-template <int NT>
+template <int NT, bool SMEM_ROWS = false>
 __device__ __forceinline__ void coop_load_halo(const uint32_t* rows, uint32_t H,
                                                const __nv_bfloat16* feat, uint32_t s_halo,
                                                int t, int64_t stride = CH) {
@@ -1436,7 +1442,7 @@ __device__ __forceinline__ void coop_load_halo(const uint32_t* rows, uint32_t H,
 #pragma unroll
     for (uint32_t x = 0; x < B; ++x) {
       const uint32_t h = h0 + x * STEP;
-      r[x] = h < H ? __ldg(rows + h) : 0u;
+      r[x] = h < H ? (SMEM_ROWS ? rows[h] : __ldg(rows + h)) : 0u;
     }
 #pragma unroll
     for (uint32_t x = 0; x < B; ++x) {
@@ -1620,6 +1626,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   const int nmain = SPLIT ? min(Cfg::nmain, a.K * nci) : 1;
   const int64_t fstride = static_cast<int64_t>(nci) * CH;
   const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_w = base + L.w, s_d = base + L.d;
+  const uint32_t s_hidx = base + L.hidx;
   const uint32_t s_bar = base + L.bar;
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
@@ -1658,12 +1665,19 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
   if (warp == 4) {
     // ------------------------ producer: halo + descriptors -----------------
     uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
-    uint32_t d_it = 0;
+    uint32_t d_it = 0, h_it = 0;
     for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
     for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
       const uint2 sp = a.sup[s];
       const int nsub = static_cast<int>(sp.y & 0xFFu);
       if (a.halo_len[s] == kOverflow) continue;
+      if (Cfg::hidx && lane == 0) {  // the record's halo row list into shared memory (agg warps release it)
+        const uint32_t hb = (a.halo_len[s] * 4u + 15u) & ~15u;
+        mbar_wait(bar(B_HALO_EMPTY), (h_it & 1) ^ 1);
+        mbar_expect_tx(bar(B_HALO_FULL), hb);
+        bulk_g2s(s_hidx, a.halo + static_cast<int64_t>(s) * a.hcap, hb, bar(B_HALO_FULL));
+      }
+      ++h_it;
       // stage this super-tile's descriptor offsets in smem
       const int64_t ob = static_cast<int64_t>(sp.x) * K;
       for (int x = lane; x <= nsub * K; x += 32) offs[x] = a.blk_off[ob + x];
@@ -1826,6 +1840,8 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
     const int aw = warp - FWD_AGG_WARP0;
     const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
     uint32_t a_it = 0;  // pipeline position of the current (record, chunk)'s first stage
+    uint32_t h_it = 0;
+    const uint32_t* hidx = reinterpret_cast<const uint32_t*>(gbase + L.hidx);
     for (int w = blockIdx.x; w < a.n_items; w += gridDim.x)
     for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
       const uint2 sp = a.sup[s];
@@ -1834,8 +1850,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
       if (H == kOverflow) continue;
       for (int c = 0; c < nci; ++c) {
       named_bar_sync(1, 32 * FWD_AGG_WARPS);  // all aggregation warps done with the previous halo
-      coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat + c * CH,
-                                         s_halo, 32 * aw + lane, fstride);
+      if (Cfg::hidx) {
+        if (c == 0) mbar_wait(bar(B_HALO_FULL), h_it & 1);  // the record's row list is in smem
+        coop_load_halo<32 * FWD_AGG_WARPS, true>(hidx, H, a.feat + c * CH, s_halo, 32 * aw + lane, fstride);
+      } else {
+        coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat + c * CH,
+                                           s_halo, 32 * aw + lane, fstride);
+      }
+      if (Cfg::hidx && c == nci - 1) {  // (all chunks loaded: the producer may fetch the next list)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(B_HALO_EMPTY));
+        ++h_it;
+      }
       named_bar_sync(1, 32 * FWD_AGG_WARPS);
       // this group's stages of the (record, chunk): every AGG_GROUPS-th one
       // (stage index = pipeline position; slot / parity derive from it)
