@@ -2507,7 +2507,7 @@ struct BfArgs {
 };
 
 struct BfSmem {
-  uint32_t halo, a, w, d, f, bar, tmem_slot, offs;
+  uint32_t halo, a, w, d, f, bar, tmem_slot, offs, hidx;
   size_t total;
 };
 __host__ __device__ constexpr BfSmem bf_smem_layout(int hcap) {
@@ -2531,6 +2531,9 @@ __host__ __device__ constexpr BfSmem bf_smem_layout(int hcap) {
   o += 16;
   L.offs = o;
   o += OFFS_WORDS * 4;
+  o = (o + 15) & ~15u;
+  L.hidx = o;  // the record's halo row list (bulk-copied ahead by the descriptor producer)
+  o += ((hcap * 4 + 15) & ~15);
   L.total = o + 1024;
   return L;
 }
@@ -2550,7 +2553,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
   uint8_t* gbase = smem_raw + (base - raw);
   const BfSmem L = bf_smem_layout(a.hcap);
   const uint32_t s_halo = base + L.halo, s_a = base + L.a, s_w = base + L.w, s_d = base + L.d,
-                 s_f = base + L.f;
+                 s_f = base + L.f, s_hidx = base + L.hidx;
   const uint32_t s_bar = base + L.bar;
   auto bar = [&](int i) { return s_bar + 8u * static_cast<uint32_t>(i); };
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(gbase + L.tmem_slot);
@@ -2599,10 +2602,17 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
   if (warp == 4) {
     // ------------------------ producer: stage descriptors ---------------------
     uint32_t* offs = reinterpret_cast<uint32_t*>(gbase + L.offs);
-    uint32_t d_it = 0;
+    uint32_t d_it = 0, h_it = 0;
     for (int w = pair; w < a.n_items; w += npairs)
       for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
         if (a.halo_len[s] == kOverflow) continue;
+        if (lane == 0) {  // the record's halo row list into shared memory (agg warps release it)
+          const uint32_t hb = (a.halo_len[s] * 4u + 15u) & ~15u;
+          mbar_wait(bar(BB_HALO_EMPTY), (h_it & 1) ^ 1);
+          mbar_expect_tx(bar(BB_HALO_FULL), hb);
+          bulk_g2s(s_hidx, a.halo + static_cast<int64_t>(s) * a.hcap, hb, bar(BB_HALO_FULL));
+        }
+        ++h_it;
         const uint2 sp = a.sup[s];
         const int64_t ob = static_cast<int64_t>(sp.x) * K;
         for (int x = lane; x <= K; x += 32) offs[x] = a.blk_off[ob + x];
@@ -2743,14 +2753,18 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
     // ------------------------------ aggregation --------------------------------
     const int aw = warp - FWD_AGG_WARP0;
     const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
-    uint32_t a_it = 0, d_it = 0;
+    uint32_t a_it = 0, d_it = 0, h_it = 0;
     for (int w = pair; w < a.n_items; w += npairs)
       for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
         const uint32_t H = a.halo_len[s];
         if (H == kOverflow) continue;
         named_bar_sync(1, 32 * FWD_AGG_WARPS);
-        coop_load_halo<32 * FWD_AGG_WARPS>(a.halo + static_cast<int64_t>(s) * a.hcap, H, a.feat, s_halo,
-                                           32 * aw + lane, CH);
+        mbar_wait(bar(BB_HALO_FULL), h_it & 1);  // the record's row list is in smem
+        coop_load_halo<32 * FWD_AGG_WARPS, true>(reinterpret_cast<const uint32_t*>(gbase + L.hidx), H, a.feat,
+                                                 s_halo, 32 * aw + lane, CH);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(bar(BB_HALO_EMPTY));
+        ++h_it;
         named_bar_sync(1, 32 * FWD_AGG_WARPS);
         const uint32_t first = a_it + ((static_cast<uint32_t>(grp) - a_it) & (AGG_GROUPS - 1));
         for (uint32_t j = first; j < a_it + static_cast<uint32_t>(nsp); j += AGG_GROUPS) {
