@@ -2460,9 +2460,6 @@ constexpr int NSF = 2;             // F tiles (16 KB: 128 rows x 64 channels, SW
 #define BF_NSD_ 8
 #endif
 constexpr int BF_NSA = BF_NSA_, BF_NSW = BF_NSW_, BF_NSD = BF_NSD_;
-#ifndef BF_PAIR
-#define BF_PAIR 0  // 1: weight-gradient MMAs per cell pair (M = 128 over two adjacent A slots)
-#endif
 #ifndef BF_FLAGS
 #define BF_FLAGS 0  // 1: half 0 stores, half 1 adds after its flag (A/B: slower); 0: grad_in zeroed, both add
 #endif
@@ -2565,9 +2562,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
   const uint8_t* cells = a.cells + half * BF_STAGES;
   int nst = 0;  // stages per record of this half
   while (nst < BF_STAGES && cells[nst] != BF_ZERO) ++nst;
-  // BF_PAIR: A-slot stages per record padded to an even count (a phantom
-  // stage fills the odd half's last pair: arrive / release only)
-  const int nsp = BF_PAIR ? nst + (nst & 1) : nst;
   const int K = a.K;
   if (threadIdx.x == 0) {
     mbar_init(bar(BB_HALO_FULL), 1);
@@ -2667,46 +2661,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         const uint32_t fs = f_it % NSF;
         mbar_wait(bar(BB_F_FULL + fs), (f_it / NSF) & 1);
         tc_fence_after();
-#if BF_PAIR
-        constexpr uint32_t idesc_p = idesc_bf16(128, 64, true, true);  // [B_k1; B_k2]^T x F (M = 128)
-        for (int ci = 0; ci < nsp; ci += 2) {
-          const uint32_t st = a_it + static_cast<uint32_t>(ci);
-          const uint32_t as = st % BF_NSA;  // (even: the pair's slots as, as + 1 are adjacent)
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            const uint32_t sh = st + h, ash = sh % BF_NSA;
-            mbar_wait(bar(BB_A_FULL + ash), (sh / BF_NSA) & 1);
-            if (ci + h >= nst) continue;  // phantom stage
-            const uint32_t ws = w_it % BF_NSW;
-            mbar_wait(bar(BB_W_FULL + ws), (w_it / BF_NSW) & 1);
-            tc_fence_after();
-            const uint64_t ad = a_desc0 + ((ash * 16384u) >> 4);
-            const uint64_t bd = b_desc0 + ((ws * 8192u) >> 4);
-            if (elect_one()) {
-#pragma unroll
-              for (int ks = 0; ks < 4; ++ks)
-                umma_bf16(tmem, ad + 2u * ks, bd + 2u * ks, idesc_d, (!first || ci + h > 0 || ks > 0) ? 1u : 0u);
-              umma_commit(bar(BB_W_EMPTY + ws));
-            }
-            __syncwarp();
-            ++w_it;
-          }
-          tc_fence_after();
-          const uint32_t dw = tmem + 64u + 32u * static_cast<uint32_t>(ci);  // pair block ci / 2
-          if (elect_one()) {
-#pragma unroll
-            for (int ks = 0; ks < 8; ++ks) {  // K = tile rows, 16 per step
-              const uint64_t ada = sdesc_sw128(s_a + as * 16384u + 2048u * ks, 16384, 1024);
-              const uint64_t bdf = sdesc_sw128(s_f + fs * 16384u + 2048u * ks, 16384, 1024);
-              umma_bf16(dw, ada, bdf, idesc_p, (dw_fresh && ks == 0) ? 0u : 1u);
-            }
-            umma_commit(bar(BB_A_EMPTY + as));
-            umma_commit(bar(BB_A_EMPTY + (as + 1) % BF_NSA));
-          }
-          __syncwarp();
-        }
-        a_it += static_cast<uint32_t>(nsp);
-#else
         for (int ci = 0; ci < nst; ++ci) {
           const uint32_t ws = w_it % BF_NSW;
           mbar_wait(bar(BB_W_FULL + ws), (w_it / BF_NSW) & 1);
@@ -2735,7 +2689,6 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
           ++w_it;
         }
         a_it += static_cast<uint32_t>(nst);
-#endif
         dw_fresh = false;
         if (elect_one()) umma_commit(bar(BB_F_EMPTY + fs));
         __syncwarp();
@@ -2753,7 +2706,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
     // ------------------------------ aggregation --------------------------------
     const int aw = warp - FWD_AGG_WARP0;
     const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
-    uint32_t a_it = 0, d_it = 0, h_it = 0;
+    uint32_t a_it = 0, h_it = 0;
     for (int w = pair; w < a.n_items; w += npairs)
       for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
         const uint32_t H = a.halo_len[s];
@@ -2767,17 +2720,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         ++h_it;
         named_bar_sync(1, 32 * FWD_AGG_WARPS);
         const uint32_t first = a_it + ((static_cast<uint32_t>(grp) - a_it) & (AGG_GROUPS - 1));
-        for (uint32_t j = first; j < a_it + static_cast<uint32_t>(nsp); j += AGG_GROUPS) {
-          // descriptor slots count real stages (BF_PAIR: no phantom fills)
-          const uint32_t jr = BF_PAIR ? d_it + (j - a_it) : j;
-          const uint32_t ds = jr % BF_NSD, as = j % BF_NSA;
-          if (BF_PAIR && static_cast<int>(j - a_it) >= nst) {  // phantom: hand the slot through
-            mbar_wait(bar(BB_A_EMPTY + as), ((j / BF_NSA) & 1) ^ 1);
-            __syncwarp();
-            if (lane == 0) mbar_arrive(bar(BB_A_FULL + as));
-            continue;
-          }
-          mbar_wait(bar(BB_D_FULL + ds), (jr / BF_NSD) & 1);
+        for (uint32_t j = first; j < a_it + static_cast<uint32_t>(nst); j += AGG_GROUPS) {
+          const uint32_t ds = j % BF_NSD, as = j % BF_NSA;
+          mbar_wait(bar(BB_D_FULL + ds), (j / BF_NSD) & 1);
           auto wait_a = [&] { mbar_wait(bar(BB_A_EMPTY + as), ((j / BF_NSA) & 1) ^ 1); };
           const uint8_t* slot = g_d + ds * BLOCK_MAX_BYTES;
           const uint32_t src = BIG ? dsrc[ds] : kFitsSlot;
@@ -2797,8 +2742,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
             mbar_arrive(bar(BB_D_EMPTY + ds));
           }
         }
-        a_it += static_cast<uint32_t>(nsp);
-        d_it += static_cast<uint32_t>(nst);
+        a_it += static_cast<uint32_t>(nst);
       }
   } else {
     // ----------------- warps 0-3: F tiles, input-gradient drains, dW dump -------
@@ -2907,10 +2851,9 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
     tc_fence_after();
     const bool none = f_it == 0;  // no records at all: the accumulators were never written
     for (int b = 0; b < BF_STAGES / 2; ++b) {
-      // BF_PAIR: pair block b is M = 128: rows 0-63 cell stage 2b, 64-127 stage 2b + 1 (lane = row)
-      const int ci = BF_PAIR ? 2 * b + (e >> 1) : 2 * b + (lane >> 4);
+      const int ci = 2 * b + (lane >> 4);
       const int k = cells[ci];  // (ci < BF_STAGES)
-      const int m = BF_PAIR ? 32 * (e & 1) + lane : 16 * e + (lane & 15);
+      const int m = 16 * e + (lane & 15);
       float4* o = k != BF_ZERO
                       ? reinterpret_cast<float4*>(a.partial + ((static_cast<int64_t>(pair) * K + k) * 64 + m) * 64)
                       : nullptr;
