@@ -2500,6 +2500,7 @@ struct BfArgs {
   uint32_t* item_flag;        // [n_items][4]: the half-0 CTA stored the item's rows (quadrant e)
   uint32_t gen;               // this launch's flag value (flags are never reset)
   float* partial;             // [pairs][K][64 m][64 c]
+  long long* prof;            // NPCG_BF_PROFILE: per CTA {halo-boundary clocks, aggregation-loop clocks}
   uint8_t cells[2 * BF_STAGES];  // per half: stage -> cell (BF_ZERO: none)
 };
 
@@ -2707,11 +2708,14 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
     const int aw = warp - FWD_AGG_WARP0;
     const int grp = aw / AGG_GROUP_WARPS, wig = aw % AGG_GROUP_WARPS;
     uint32_t a_it = 0, h_it = 0;
+    long long p_bnd = 0, p_wait = 0, p_t0 = a.prof ? clock64() : 0;
     for (int w = pair; w < a.n_items; w += npairs)
       for (int s = static_cast<int>(a.item_start[w]); s < static_cast<int>(a.item_start[w + 1]); ++s) {
         const uint32_t H = a.halo_len[s];
         if (H == kOverflow) continue;
+        const long long p_b0 = a.prof ? clock64() : 0;
         named_bar_sync(1, 32 * FWD_AGG_WARPS);
+        if (a.prof) p_wait += clock64() - p_b0;
         mbar_wait(bar(BB_HALO_FULL), h_it & 1);  // the record's row list is in smem
         coop_load_halo<32 * FWD_AGG_WARPS, true>(reinterpret_cast<const uint32_t*>(gbase + L.hidx), H, a.feat,
                                                  s_halo, 32 * aw + lane, CH);
@@ -2719,6 +2723,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         if (lane == 0) mbar_arrive(bar(BB_HALO_EMPTY));
         ++h_it;
         named_bar_sync(1, 32 * FWD_AGG_WARPS);
+        if (a.prof) p_bnd += clock64() - p_b0;
         const uint32_t first = a_it + ((static_cast<uint32_t>(grp) - a_it) & (AGG_GROUPS - 1));
         for (uint32_t j = first; j < a_it + static_cast<uint32_t>(nst); j += AGG_GROUPS) {
           const uint32_t ds = j % BF_NSD, as = j % BF_NSA;
@@ -2744,6 +2749,11 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
         }
         a_it += static_cast<uint32_t>(nst);
       }
+    if (a.prof && aw == 0 && lane == 0) {
+      a.prof[3 * blockIdx.x] = p_bnd;
+      a.prof[3 * blockIdx.x + 1] = clock64() - p_t0;
+      a.prof[3 * blockIdx.x + 2] = p_wait;
+    }
   } else {
     // ----------------- warps 0-3: F tiles, input-gradient drains, dW dump -------
     const int e = warp;
@@ -3941,7 +3951,27 @@ static void run_fused_backward(npcg_context* ctx, npcg_neighbors* nb, TcPlan* p,
   auto kern = P->big_blocks ? k_conv_bwd_fused<true> : k_conv_bwd_fused<false>;
   NPCG_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  static_cast<int>(L.total)));
+  static const bool bprof = std::getenv("NPCG_BF_PROFILE") != nullptr;
+  DevBuf<long long> prof;
+  if (bprof) {
+    prof.alloc(ctx, 6 * npairs);
+    NPCG_CUDA(cudaMemsetAsync(prof.get(), 0, 48 * npairs, ctx->stream));
+    a.prof = prof.get();
+  }
   launch_cluster(ctx, "conv_bwd_fused", kern, dim3(2 * npairs), dim3(FWD_THREADS), L.total, 2, a);
+  if (bprof) {  // (debug: synchronises)
+    std::vector<long long> h(6 * npairs);
+    NPCG_CUDA(cudaMemcpy(h.data(), prof.get(), h.size() * 8, cudaMemcpyDeviceToHost));
+    double bnd = 0, tot = 0, wt = 0;
+    for (int x = 0; x < 2 * npairs; ++x) {
+      bnd += static_cast<double>(h[3 * x]);
+      tot += static_cast<double>(h[3 * x + 1]);
+      wt += static_cast<double>(h[3 * x + 2]);
+    }
+    std::fprintf(stderr, "[npcg fused profile] halo boundaries %.1f %% of the aggregation loop (of which %.1f %% "
+                 "waiting for the last group of the record; %.0f clocks per CTA)\n",
+                 100.0 * bnd / std::max(tot, 1.0), 100.0 * wt / std::max(tot, 1.0), tot / (2 * npairs));
+  }
   const int64_t nw = static_cast<int64_t>(K) * cin * cout;
   launch(ctx, "wgrad_reduce", k_wgrad_reduce_mc, dim3(static_cast<unsigned>(ceil_div(nw, 256))), dim3(256),
          0, static_cast<const float*>(p->partial.get()), npairs, K, cin, cout, grad_w);
