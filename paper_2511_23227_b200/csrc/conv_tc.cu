@@ -1675,7 +1675,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_fwd_tc(FwdArgs a) {
         const uint32_t hb = (a.halo_len[s] * 4u + 15u) & ~15u;
         mbar_wait(bar(B_HALO_EMPTY), (h_it & 1) ^ 1);
         mbar_expect_tx(bar(B_HALO_FULL), hb);
-        bulk_g2s(s_hidx, a.halo + static_cast<int64_t>(s) * a.hcap, hb, bar(B_HALO_FULL));
+        if (hb) bulk_g2s(s_hidx, a.halo + static_cast<int64_t>(s) * a.hcap, hb, bar(B_HALO_FULL));  // (H = 0: arrival alone)
       }
       ++h_it;
       // stage this super-tile's descriptor offsets in smem
@@ -2605,7 +2605,7 @@ __global__ void __launch_bounds__(FWD_THREADS, 1) k_conv_bwd_fused(BfArgs a) {
           const uint32_t hb = (a.halo_len[s] * 4u + 15u) & ~15u;
           mbar_wait(bar(BB_HALO_EMPTY), (h_it & 1) ^ 1);
           mbar_expect_tx(bar(BB_HALO_FULL), hb);
-          bulk_g2s(s_hidx, a.halo + static_cast<int64_t>(s) * a.hcap, hb, bar(BB_HALO_FULL));
+          if (hb) bulk_g2s(s_hidx, a.halo + static_cast<int64_t>(s) * a.hcap, hb, bar(BB_HALO_FULL));
         }
         ++h_it;
         const uint2 sp = a.sup[s];

@@ -504,3 +504,29 @@ def test_gather_engine_parity():
                        timeout=900)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
     assert " passed" in r.stdout
+
+
+@pytest.mark.parametrize("math", ["bf16", "auto"])
+def test_output_tiles_without_neighbors(npc, orc, math):
+    """A two-cloud layer whose output cloud has whole tiles of points with no
+    input neighbour (empty halos): those rows are exactly zero, the others
+    match the oracle, and the backward's empty rows / gradients too."""
+    rng = np.random.default_rng(3)
+    xin = orc.gen_uniform_cube(3000, 1.0, 5)
+    near = xin[rng.choice(3000, 200, replace=False)] + rng.normal(0, 0.01, (200, 3))
+    far = rng.random((400, 3)) + 10.0  # > 128 consecutive rows with no neighbours
+    xout = np.concatenate([near, far])
+    r = 1.8 * 3000 ** (-1 / 3)
+    w = orc.make_weights(3, 1, 64, 64, 7)
+    f = orc.gen_features(3000, 1, 64, 8)
+    go = orc.gen_features(len(xout), 1, 64, 9)
+    op = npc.PointConvOp(T(w), npc.ConvGeometry(radius=r, t=3), npc.ExecConfig(math=getattr(npc.Math, math)))
+    out = op.forward(npc.make_point_cloud(xin), npc.make_point_cloud(xout), T(f))
+    res = op.backward(T(go))
+    ti, tj, tk = orc.build_triplets(xout, xin, r, 3)
+    fo, gi, gw = orc.dense_conv(w.astype(np.float64), f.astype(np.float64), ti, tj, tk, len(xout),
+                                go.astype(np.float64))
+    tol = 1e-2 if math == "bf16" else 1e-5
+    assert torch.count_nonzero(out[200:]) == 0
+    assert rel(out.cpu(), fo) <= tol
+    assert rel(res.grad_in.cpu(), gi) <= tol and rel(res.grad_w.cpu(), gw) <= tol
