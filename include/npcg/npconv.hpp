@@ -116,8 +116,9 @@ inline void cuda(cudaError_t e, const char* what) {
 // tensors (>= 1 MiB), so a result returned by value lands by DMA straight into
 // already-mapped memory (no page faults, no staging copy) and an input built
 // once is uploaded the same way.  Freed blocks are kept for reuse up to
-// NPCG_HOST_CACHE_MB (default 4096) and are never handed back to the OS
-// before exit.  Falls back to malloc when pinned memory is unavailable.
+// NPCG_HOST_CACHE_MB (default 4096); all page-locked blocks together (live and
+// cached) stay under NPCG_HOST_PINNED_MAX_MB (default 16384), beyond which --
+// or when pinned memory is unavailable -- tensors use pageable malloc memory.
 class PinnedPool {
  public:
   static PinnedPool& get() {
@@ -133,12 +134,17 @@ class PinnedPool {
       free_.erase(it);
       return p;
     }
+    // bounded page-locked footprint (live + cached): make room from the cache,
+    // else the caller falls back to pageable memory
+    while (pinned_ + bytes > max_ && !free_.empty()) evict_largest();
+    if (pinned_ + bytes > max_) return nullptr;
     void* p = nullptr;
     if (cudaHostAlloc(&p, bytes, cudaHostAllocDefault) != cudaSuccess) {
       (void)cudaGetLastError();
       return nullptr;
     }
     size_[p] = bytes;
+    pinned_ += bytes;
     return p;
   }
   bool give(void* p) {
@@ -147,13 +153,7 @@ class PinnedPool {
     if (it == size_.end()) return false;
     free_.emplace(it->second, p);
     cached_ += it->second;
-    while (cached_ > limit_ && !free_.empty()) {  // drop the largest cached blocks first
-      auto last = std::prev(free_.end());
-      cached_ -= last->first;
-      size_.erase(last->second);
-      cudaFreeHost(last->second);
-      free_.erase(last);
-    }
+    while (cached_ > limit_ && !free_.empty()) evict_largest();  // the largest cached blocks first
     return true;
   }
   bool owns(const void* p) {
@@ -165,11 +165,21 @@ class PinnedPool {
   PinnedPool() {
     const char* e = std::getenv("NPCG_HOST_CACHE_MB");
     limit_ = (e ? static_cast<size_t>(std::strtoull(e, nullptr, 10)) : size_t(4096)) << 20;
+    const char* m = std::getenv("NPCG_HOST_PINNED_MAX_MB");
+    max_ = (m ? static_cast<size_t>(std::strtoull(m, nullptr, 10)) : size_t(16384)) << 20;
+  }
+  void evict_largest() {  // (m_ held)
+    auto last = std::prev(free_.end());
+    cached_ -= last->first;
+    pinned_ -= last->first;
+    size_.erase(last->second);
+    cudaFreeHost(last->second);
+    free_.erase(last);
   }
   std::mutex m_;
   std::multimap<size_t, void*> free_;
   std::unordered_map<void*, size_t> size_;
-  size_t cached_ = 0, limit_ = 0;
+  size_t cached_ = 0, limit_ = 0, pinned_ = 0, max_ = 0;
 };
 
 // std::vector allocator over PinnedPool; elements are default-initialised
