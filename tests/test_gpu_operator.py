@@ -474,13 +474,19 @@ def test_c2_bf16_fwd_bwd(npc, orc):
     assert max(e) <= 1e-2, e
 
 
-def test_cpp_dropin_header(npc):
-    """The C++ drop-in (include/npcg/npconv.hpp) passes reference-style cases."""
+@pytest.mark.parametrize("pinned_mb", [None, "0"])
+def test_cpp_dropin_header(npc, pinned_mb):
+    """The C++ drop-in (include/npcg/npconv.hpp) passes reference-style cases,
+    with its pinned tensor storage and with all tensors pageable
+    (NPCG_HOST_PINNED_MAX_MB=0: the staged copy path)."""
     import os
     import subprocess
     exe = os.path.join(os.path.dirname(os.path.abspath(__file__)), "cpp", "test_dropin")
     assert os.path.exists(exe), "run __graft_entry__.build() first"
-    r = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    env = dict(os.environ)
+    if pinned_mb is not None:
+        env["NPCG_HOST_PINNED_MAX_MB"] = pinned_mb
+    r = subprocess.run([exe], capture_output=True, text=True, timeout=300, env=env)
     print(r.stdout)
     assert r.returncode == 0, r.stdout + r.stderr
     assert "0 failures" in r.stdout
