@@ -536,3 +536,23 @@ def test_output_tiles_without_neighbors(npc, orc, math):
     assert torch.count_nonzero(out[200:]) == 0
     assert rel(out.cpu(), fo) <= tol
     assert rel(res.grad_in.cpu(), gi) <= tol and rel(res.grad_w.cpu(), gw) <= tol
+
+
+def test_cpp_dropin_large_tensors_pinned_equals_pageable(npc):
+    """tools/cpp/bench_dropin at 200K points (51 MB tensors): results through
+    the pinned tensor storage (one DMA per tensor) are bitwise those through
+    pageable storage (staged copies) -- same checksum of out, grad_in, grad_w."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools", "cpp", "bench_dropin")
+    assert os.path.exists(exe), "run __graft_entry__.build() first"
+    sums = []
+    for mb in (None, "0"):
+        env = dict(os.environ)
+        if mb is not None:
+            env["NPCG_HOST_PINNED_MAX_MB"] = mb
+        r = subprocess.run([exe, "200000", "2", "1", "auto"], capture_output=True, text=True, timeout=300, env=env)
+        assert r.returncode == 0, r.stdout + r.stderr
+        sums.append(json.loads(r.stdout.strip().splitlines()[-1])["checksum"])
+    assert sums[0] == sums[1], sums

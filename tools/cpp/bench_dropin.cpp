@@ -81,6 +81,16 @@ int main(int argc, char** argv) {
     v_ms += std::chrono::duration<double, std::milli>(g - e).count() / 3;
     check += out.values()[0] + r.grad_in.values()[0];
   }
+  // a full checksum of one more step's results (outside the timed region)
+  {
+    const FeatureTensor<float> out = op.forward(cloud, fin);
+    const BackwardResult<float> r = op.backward(gout);
+    double cs = 0;
+    for (float v : out.values()) cs += v;
+    for (float v : r.grad_in.values()) cs += 2.0 * v;
+    for (float v : r.grad_w.values()) cs += 3.0 * v;
+    check = cs;
+  }
   // per step: fin + gout up; out, grad_in, grad_w down (the weights stay resident)
   const int64_t h2d = 2 * n * c * 4, d2h = 2 * n * c * 4 + t * t * t * c * c * 4;
   std::printf(
@@ -89,7 +99,7 @@ int main(int argc, char** argv) {
       "\"n_points\": %lld, \"channels\": %lld, \"h2d_bytes_per_step\": %lld, \"d2h_bytes_per_step\": %lld, "
       "\"forward_ms\": %.3f, \"backward_ms\": %.3f, \"pageable_vector_first_touch_ms\": %.3f, "
       "\"first_steps_s\": %.3f, \"timer\": \"host wall clock (std::chrono), results in host vectors\", "
-      "\"checksum\": %.6g}\n",
+      "\"checksum\": %.17g}\n",
       n / (ms * 1e3), ms, steps, warmup, math.c_str(), static_cast<long long>(n), static_cast<long long>(c),
       static_cast<long long>(h2d), static_cast<long long>(d2h), f_ms, b_ms, v_ms, warm_s, check);
   return std::isfinite(check) ? 0 : 1;
