@@ -101,3 +101,13 @@ def test_f32tc_c2_100k(npc, orc):
     xyz = orc.gen_uniform_cube(n, 1.0, 1)
     e = _check(npc, orc, xyz, 1.8 * n ** (-1 / 3), 3, 64, 64, 1, math=npc.Math.auto)
     assert max(e) <= TOL
+
+
+@pytest.mark.parametrize("n", [1, 2, 5, 33, 129, 300])
+@pytest.mark.parametrize("c", [16, 32, 64])
+def test_auto_tiny_clouds(npc, orc, n, c):
+    """The default (AUTO) path on tiny clouds and narrow layers -- one point,
+    partial tiles, a single super-tile -- meets the fp32 bound."""
+    xyz = orc.gen_uniform_cube(n, 1.0, 40 + n)
+    r = 0.6 if n < 10 else 1.8 * n ** (-1 / 3)
+    _check(npc, orc, xyz, r, 3, c, c, n + c, math=npc.Math.auto)
