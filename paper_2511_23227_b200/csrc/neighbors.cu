@@ -658,10 +658,12 @@ void build_tcsr(npcg_context* ctx, npcg_neighbors* nb) {
              static_cast<const int64_t*>(nb->row_ptr.get()), static_cast<const uint32_t*>(nb->col_j.get()),
              static_cast<const uint32_t*>(nb->col_k.get()), static_cast<const uint32_t*>(nb->perm_out.get()), n,
              p->k.get(), missing.get());
-      int h = 0;
-      NPCG_CUDA(cudaMemcpyAsync(&h, missing.get(), 4, cudaMemcpyDeviceToHost, ctx->stream));
-      NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
-      if (h) fail(NPCG_ERR_STATE, "transposed structure: asymmetric same-cloud neighbor relation");
+      if (std::getenv("NPCG_PLAN_DEBUG")) {  // (the relation is symmetric by construction: checked on request)
+        int h = 0;
+        NPCG_CUDA(cudaMemcpyAsync(&h, missing.get(), 4, cudaMemcpyDeviceToHost, ctx->stream));
+        NPCG_CUDA(cudaStreamSynchronize(ctx->stream));
+        if (h) fail(NPCG_ERR_STATE, "transposed structure: asymmetric same-cloud neighbor relation");
+      }
     }
     nb->tcsr = std::move(p);
     return;
